@@ -1,0 +1,240 @@
+/*
+ * mtsph_b200.h -- C ABI of the B200-native multi-rate SPH hot path.
+ *
+ * Shared library: paper_2309_04010_b200/libmtsph_b200.so (sm_100a).
+ * Plain pointers and sizes only; no torch types.  All functions return an
+ * mtsph_status (0 = ok); on failure mtsph_last_error() holds a message and
+ * mtsph_last_error_ids() the offending particle ids (original numbering),
+ * mirroring the reference's error classes (errors.py).
+ *
+ * Two layers:
+ *
+ *  1. Drop-in replacements for the reference's compiled particle loops
+ *     (/root/reference/pkg/src/mtsph/_accel.py).  Same argument meaning and
+ *     array layout as the numba kernels (numpy C order, int64 CSR), HOST
+ *     pointers; each call stages to HBM, runs the sm_100a kernel and copies
+ *     the result back.  These are what a ctypes shim for `mtsph._accel`
+ *     binds.
+ *
+ *  2. Device-resident problems (neighbourhood, necking solid, porous
+ *     membrane) whose state stays in HBM for the whole run; one call runs
+ *     a complete inner relaxation loop (scenarios.py relax_step repeated
+ *     under stepping.py:347's kinetic-energy criterion) without host
+ *     round trips.  These back the drop-in Problem objects of the Python
+ *     package (paper_2309_04010_b200.scenarios).
+ */
+#ifndef MTSPH_B200_H
+#define MTSPH_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MTSPH_ABI_VERSION 1
+
+typedef int mtsph_status;
+enum {
+    MTSPH_OK = 0,
+    MTSPH_ERR_ARG = 1,          /* bad argument / unsupported dimension      */
+    MTSPH_ERR_CUDA = 2,         /* CUDA runtime failure or no device         */
+    MTSPH_ERR_GEOMETRY = 3,     /* errors.py:266 GeometryError               */
+    MTSPH_ERR_SINGULAR = 4,     /* errors.py:270 SingularMomentMatrixError   */
+    MTSPH_ERR_INVERSION = 5,    /* errors.py:283 ElementInversionError       */
+    MTSPH_ERR_RETURN_MAP = 6,   /* errors.py:295 ReturnMapError              */
+    MTSPH_ERR_NONFINITE = 7,    /* errors.py:308 SimulationError             */
+};
+
+int mtsph_abi_version(void);
+const char *mtsph_last_error(void);
+/* copies up to cap ids of the last failure; returns how many there were */
+int64_t mtsph_last_error_ids(int64_t *ids, int64_t cap);
+/* number of CUDA devices visible (0 on a CPU-only host) */
+int mtsph_device_count(void);
+
+/* ------------------------------------------------------------------ */
+/* Layer 1: _accel.py drop-ins (host pointers, reference layout)       */
+/* ------------------------------------------------------------------ */
+
+/* _accel.py:16  out[a] = sum_b vol[b] (src[b]-src[a]) (x) grad_ab        */
+mtsph_status mtsph_velocity_gradient_gather(
+    int64_t n, int d, const double *src, const int64_t *indptr,
+    const int64_t *idx, const double *grad, const double *vol, double *out);
+
+/* _accel.py:34  out[a] = sum_b vol[b] (tens[a]+tens[b]) . grad_ab        */
+mtsph_status mtsph_pair_tensor_divergence(
+    int64_t n, int d, const double *tens, const int64_t *indptr,
+    const int64_t *idx, const double *grad, const double *vol, double *out);
+
+/* _accel.py:52  out[a] += sum_b vol[b] (tens[a]+tens[b]) . (amap[a] grad) */
+mtsph_status mtsph_pair_tensor_divergence_mapped(
+    int64_t n, int d, const double *tens, const double *amap,
+    const int64_t *indptr, const int64_t *idx, const double *grad,
+    const double *vol, double *out);
+
+/* _accel.py:76  out[a] = coeff[a] sum_b vol[b] (sat[a]-sat[b]) (amap[a] grad) */
+mtsph_status mtsph_scalar_difference_flux(
+    int64_t n, int d, const double *sat, const double *coeff,
+    const double *amap, const int64_t *indptr, const int64_t *idx,
+    const double *vol, const double *grad, double *out);
+
+/* _accel.py:171 sequential pairwise implicit damping sweep, in place.
+ * Reproduces the reference's serial group order exactly (level-scheduled
+ * on the GPU: groups in one level touch disjoint particles).  The group
+ * size limit is the reference's (64 pairs).                             */
+mtsph_status mtsph_damping_sweep(
+    int64_t n, int d, double *vel, int64_t npairs, const int64_t *pair_i,
+    const int64_t *pair_j, const double *pair_damp, const double *inv_mass_i,
+    const double *inv_mass_j, int64_t ngroups, const int64_t *group_ptr,
+    double eta, double dt);
+
+/* _accel.py:210 antisymmetric flux-divergence mass rate                  */
+mtsph_status mtsph_conservative_mass_rate(
+    int64_t n, int d, const double *flux, const double *amap, int64_t npairs,
+    const int64_t *pair_i, const int64_t *pair_j, const double *pair_grad,
+    const double *vol, double *out);
+
+/* _accel.py:240 fused mixture-stress momentum RHS                        */
+mtsph_status mtsph_porous_stress_rhs(
+    int64_t n, int d, const double *def_grad, const double *pressure,
+    const double *corr, const int64_t *indptr, const int64_t *idx,
+    const double *grad0, const double *vol0, double mu, double lam,
+    double *tbuf, double *out_j, double *out_rate);
+
+/* ------------------------------------------------------------------ */
+/* Layer 2: device-resident neighbourhoods and problems                */
+/* ------------------------------------------------------------------ */
+
+/* damping-sweep ordering */
+enum {
+    MTSPH_SWEEP_NONE = 0,      /* no pair schedule (no damping)             */
+    MTSPH_SWEEP_SERIAL = 1,    /* the reference's exact serial group order  */
+    MTSPH_SWEEP_COLOURED = 2,  /* B200: 3^d-coloured midpoint-cell sweep    */
+};
+
+typedef struct mtsph_nbh mtsph_nbh;
+
+/* neighbors.py:59 + :232.  Builds the fixed reference-configuration
+ * neighbourhood on the GPU (cell lists, Morton particle order, SELL-32
+ * neighbour table, correction matrices, damping pair schedule).          */
+mtsph_status mtsph_nbh_create(int64_t n, int d, const double *pos,
+                              const double *vol, const double *h_axes,
+                              int sweep, mtsph_nbh **out);
+mtsph_status mtsph_nbh_destroy(mtsph_nbh *nb);
+/* sizes in the reference's layout (directed CSR entries, unique pairs,
+ * damping groups, colours or levels of the sweep schedule)              */
+mtsph_status mtsph_nbh_sizes(const mtsph_nbh *nb, int64_t *nnz, int64_t *npairs,
+                             int64_t *ngroups, int64_t *nphases);
+/* export in the reference layout and numbering (NULL outputs skipped).
+ * pair arrays follow the schedule order of the chosen sweep.           */
+mtsph_status mtsph_nbh_export(const mtsph_nbh *nb, int64_t *indptr, int64_t *idx,
+                              double *grad0, int64_t *pair_i, int64_t *pair_j,
+                              double *pair_damp, double *pair_grad,
+                              int64_t *pair_group, double *corr);
+/* internal (Morton) order: perm[k] = original id of internal particle k  */
+mtsph_status mtsph_nbh_permutation(const mtsph_nbh *nb, int64_t *perm);
+
+/* --- necking solid (scenarios.py:41 NeckingProblem) --- */
+
+typedef struct {
+    int64_t n;
+    int d;
+    const double *pos;          /* (n,d) reference positions               */
+    const double *vol;          /* (n,)                                     */
+    const double *rho0;         /* (n,)                                     */
+    const uint8_t *constrained; /* (n,) 1 = velocity prescribed             */
+    const int8_t *side;         /* (n,) -1 left clamp, +1 right clamp, 0    */
+    const uint8_t *mid_mask;    /* (n,) mid-span section (neck radius)      */
+    double h_axes[3];
+    double shear_modulus, bulk_modulus;
+    int plastic;                /* 0: Neo-Hookean only (solids.py:394)      */
+    int hardening_law;          /* 0: reference saturation+linear (plasticity.py:64)
+                                   1: power law s0 (1 + a/e0)^m             */
+    double hard[4];             /* law 0: s0, sinf, delta, H; law 1: s0, e0, m, - */
+    double rm_tol;              /* return-map tolerance (<=0: 1e-8 s0)     */
+    int rm_max_iter;            /* 50 in the reference                      */
+    int sweep;                  /* MTSPH_SWEEP_*                            */
+} mtsph_solid_desc;
+
+typedef struct mtsph_solid mtsph_solid;
+
+typedef struct {
+    double eta;            /* damping viscosity                           */
+    double cfl;            /* 0.6                                          */
+    double criterion;      /* absolute kinetic-energy threshold           */
+    double dt_outer;       /* for the default cap 10*ceil(dt_outer/dt)   */
+    int64_t max_inner;     /* 0 = default cap                              */
+    int64_t min_inner;     /* >= 1                                         */
+} mtsph_inner_params;
+
+typedef struct {
+    int64_t n_inner;       /* relaxation steps taken                      */
+    int cap_hit;           /* loop ended on the safety cap                */
+    double ek;             /* last pre-damping kinetic energy             */
+    double min_dt;         /* smallest inner step used                    */
+    double last_dt;
+} mtsph_inner_result;
+
+mtsph_status mtsph_solid_create(const mtsph_solid_desc *desc, mtsph_solid **out);
+mtsph_status mtsph_solid_destroy(mtsph_solid *s);
+/* NeckingProblem.advance_slow: arm the boundary ramp of one outer step  */
+mtsph_status mtsph_solid_set_ramp(mtsph_solid *s, double end_disp, int64_t ramp_steps,
+                                  int64_t ramp_left);
+mtsph_status mtsph_solid_ramp_left(const mtsph_solid *s, int64_t *ramp_left);
+/* solids.py:433 stable step                                              */
+mtsph_status mtsph_solid_stable_dt(mtsph_solid *s, double cfl, double *dt);
+/* one relax_step at a host-chosen dt; returns the pre-damping E_k        */
+mtsph_status mtsph_solid_relax_step(mtsph_solid *s, double dt, double eta, double *ek);
+/* the whole inner loop on the device (graph-captured chunks)            */
+mtsph_status mtsph_solid_relax(mtsph_solid *s, const mtsph_inner_params *p,
+                               mtsph_inner_result *r);
+/* observables: reaction_force, neck radius, max alpha, min mid alpha,
+ * all-finite flag (1/0)                                                 */
+mtsph_status mtsph_solid_measure(mtsph_solid *s, double out[5]);
+/* field access in original numbering.  field names: "pos","vel","F",
+ * "accel","cp_inv","alpha","ref_pos"                                    */
+mtsph_status mtsph_solid_get(mtsph_solid *s, const char *field, double *host);
+mtsph_status mtsph_solid_set(mtsph_solid *s, const char *field, const double *host);
+/* launches of this library's kernels since creation (bench evidence)    */
+mtsph_status mtsph_solid_launches(const mtsph_solid *s, int64_t *count);
+
+/* --- porous membrane (scenarios.py:171 PorousProblem) --- */
+
+typedef struct {
+    int64_t n;
+    int d;
+    const double *pos, *vol;
+    const uint8_t *constrained;
+    const uint8_t *contact;     /* droplet contact region                   */
+    double h_axes[3];
+    double density0, diffusivity, pressure_coeff, shear_modulus, lame_lambda,
+           bulk_modulus, porosity, fluid_density0, initial_saturation;
+    double contact_time, evaporation_rate;
+    int sweep;
+} mtsph_porous_desc;
+
+typedef struct mtsph_porous mtsph_porous;
+
+mtsph_status mtsph_porous_create(const mtsph_porous_desc *desc, mtsph_porous **out);
+mtsph_status mtsph_porous_destroy(mtsph_porous *p);
+/* PorousProblem.advance_slow: one explicit diffusion update; returns the
+ * number of clamped particles                                           */
+mtsph_status mtsph_porous_advance_slow(mtsph_porous *p, double dt_outer, double t,
+                                       int64_t *clamped);
+mtsph_status mtsph_porous_stable_dt(mtsph_porous *p, double cfl, double *dt);
+mtsph_status mtsph_porous_relax_step(mtsph_porous *p, double dt, double eta, double *ek);
+mtsph_status mtsph_porous_relax(mtsph_porous *p, const mtsph_inner_params *ip,
+                                mtsph_inner_result *r);
+/* PorousProblem.measure's velocity refresh (split_velocities)           */
+mtsph_status mtsph_porous_refresh_velocities(mtsph_porous *p);
+/* fields: "pos","ref_pos","F","momentum","vel_solid","vel_fluid",
+ * "fluid_mass","flux","saturation","pressure"                           */
+mtsph_status mtsph_porous_get(mtsph_porous *p, const char *field, double *host);
+mtsph_status mtsph_porous_set(mtsph_porous *p, const char *field, const double *host);
+mtsph_status mtsph_porous_launches(const mtsph_porous *p, int64_t *count);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MTSPH_B200_H */

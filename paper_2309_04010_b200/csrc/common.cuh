@@ -1,0 +1,235 @@
+// common.cuh -- shared device helpers for the mtsph B200 kernels.
+//
+// Everything here is header-only and compiled into one translation unit
+// (mtsph_b200.cu).  fp64 throughout: the reference state is fp64 and the
+// parity bar is 1e-10 relative per step.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace mtsph {
+
+// ---------------------------------------------------------------- errors
+
+struct Error : std::runtime_error {
+    int code;
+    std::vector<int64_t> ids;
+    Error(int c, const std::string &m, std::vector<int64_t> i = {})
+        : std::runtime_error(m), code(c), ids(std::move(i)) {}
+};
+
+#define MT_CUDA(expr)                                                          \
+    do {                                                                       \
+        cudaError_t _e = (expr);                                               \
+        if (_e != cudaSuccess)                                                 \
+            throw ::mtsph::Error(2, std::string(#expr) + ": " +                \
+                                        cudaGetErrorString(_e));               \
+    } while (0)
+
+#define MT_LAUNCH_CHECK() MT_CUDA(cudaGetLastError())
+
+constexpr int kThreads = 256;
+inline unsigned blocks_for(int64_t n, int t = kThreads) {
+    int64_t b = (n + t - 1) / t;
+    return (unsigned)(b < 1 ? 1 : b);
+}
+
+// device buffer with RAII
+template <class T> struct DBuf {
+    T *p = nullptr;
+    size_t n = 0;
+    DBuf() = default;
+    explicit DBuf(size_t cnt) { alloc(cnt); }
+    DBuf(const DBuf &) = delete;
+    DBuf &operator=(const DBuf &) = delete;
+    DBuf(DBuf &&o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    DBuf &operator=(DBuf &&o) noexcept {
+        if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+        return *this;
+    }
+    ~DBuf() { release(); }
+    void alloc(size_t cnt) {
+        release();
+        n = cnt;
+        if (cnt) MT_CUDA(cudaMalloc(&p, cnt * sizeof(T)));
+    }
+    void zero(cudaStream_t s = 0) {
+        if (n) MT_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s));
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    void upload(const T *h, size_t cnt, cudaStream_t s = 0) {
+        if (cnt > n) alloc(cnt);
+        if (cnt) MT_CUDA(cudaMemcpyAsync(p, h, cnt * sizeof(T), cudaMemcpyHostToDevice, s));
+    }
+    void download(T *h, size_t cnt, cudaStream_t s = 0) const {
+        if (cnt) MT_CUDA(cudaMemcpyAsync(h, p, cnt * sizeof(T), cudaMemcpyDeviceToHost, s));
+    }
+    T *get() const { return p; }
+};
+
+// ---------------------------------------------------------------- kernel
+
+// Anisotropic Wendland C2 kernel, support 2h (kernels.py:91-129).  Scaled
+// separation u_k = r_k / h_k, q = |u|:
+//   w(q) = (1 - q/2)^4 (1 + 2q),  dw/dq = -5 q (1 - q/2)^3
+//   grad_k = pref * dw/dq / q * u_k / h_k = pref * (-5 (1-q/2)^3) u_k / h_k
+struct KSpec {
+    double h[3];
+    double inv_h[3];
+    double pref;   // sigma_d / prod(h)
+    double h_min;
+};
+
+template <int D>
+__device__ __forceinline__ void grad_w(const double *rel, const KSpec &ks, double *g) {
+    double u[D];
+    double q2 = 0.0;
+#pragma unroll
+    for (int k = 0; k < D; ++k) { u[k] = rel[k] * ks.inv_h[k]; q2 += u[k] * u[k]; }
+    const double q = sqrt(q2);
+    const double t = 1.0 - 0.5 * q;
+    const double mag = (q < 2.0) ? ks.pref * (-5.0 * t * t * t) : 0.0;
+#pragma unroll
+    for (int k = 0; k < D; ++k) g[k] = mag * (u[k] * ks.inv_h[k]);
+}
+
+// read-only 32 B load through the non-coherent path (two LDG.128)
+__device__ __forceinline__ double4 ldg4(const double4 *p) {
+    const double2 *q = reinterpret_cast<const double2 *>(p);
+    const double2 a = __ldg(q), b = __ldg(q + 1);
+    return make_double4(a.x, a.y, b.x, b.y);
+}
+
+// ------------------------------------------------------ small tensors
+
+template <int D> __device__ __forceinline__ double det_d(const double *t) {
+    if (D == 1) return t[0];
+    if (D == 2) return t[0] * t[3] - t[1] * t[2];
+    return t[0] * (t[4] * t[8] - t[5] * t[7]) - t[1] * (t[3] * t[8] - t[5] * t[6]) +
+           t[2] * (t[3] * t[7] - t[4] * t[6]);
+}
+
+// adjugate / det, reference tensors.py:170 layout
+template <int D> __device__ __forceinline__ void inv_d(const double *t, double j, double *o) {
+    if (D == 1) { o[0] = 1.0 / j; return; }
+    if (D == 2) {
+        o[0] = t[3] / j; o[1] = -t[1] / j; o[2] = -t[2] / j; o[3] = t[0] / j;
+        return;
+    }
+    o[0] = (t[4] * t[8] - t[5] * t[7]) / j;
+    o[1] = (t[2] * t[7] - t[1] * t[8]) / j;
+    o[2] = (t[1] * t[5] - t[2] * t[4]) / j;
+    o[3] = (t[5] * t[6] - t[3] * t[8]) / j;
+    o[4] = (t[0] * t[8] - t[2] * t[6]) / j;
+    o[5] = (t[2] * t[3] - t[0] * t[5]) / j;
+    o[6] = (t[3] * t[7] - t[4] * t[6]) / j;
+    o[7] = (t[1] * t[6] - t[0] * t[7]) / j;
+    o[8] = (t[0] * t[4] - t[1] * t[3]) / j;
+}
+
+template <int D> __device__ __forceinline__ void mm(const double *a, const double *b, double *o) {
+#pragma unroll
+    for (int r = 0; r < D; ++r)
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+            double s = 0.0;
+#pragma unroll
+            for (int k = 0; k < D; ++k) s += a[r * D + k] * b[k * D + c];
+            o[r * D + c] = s;
+        }
+}
+
+// a @ b^T
+template <int D> __device__ __forceinline__ void mmt(const double *a, const double *b, double *o) {
+#pragma unroll
+    for (int r = 0; r < D; ++r)
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+            double s = 0.0;
+#pragma unroll
+            for (int k = 0; k < D; ++k) s += a[r * D + k] * b[c * D + k];
+            o[r * D + c] = s;
+        }
+}
+
+// det^(-1/d) without pow for d = 2, 3
+template <int D> __device__ __forceinline__ double det_pow_minus_inv_d(double j) {
+    if (D == 1) return 1.0 / j;
+    if (D == 2) return rsqrt(j);
+    return rcbrt(j);
+}
+
+// --------------------------------------------------- reductions (fixed order)
+
+// block-level sum/max with a fixed tree shape: deterministic for a fixed
+// launch configuration.
+template <int BT> __device__ __forceinline__ double block_sum(double v, double *sh) {
+    const int t = threadIdx.x;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if ((t & 31) == 0) sh[t >> 5] = v;
+    __syncthreads();
+    double r = 0.0;
+    if (t < 32) {
+        r = (t < BT / 32) ? sh[t] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) r += __shfl_down_sync(0xffffffffu, r, o);
+    }
+    __syncthreads();
+    return r;  // valid in thread 0
+}
+
+template <int BT> __device__ __forceinline__ double block_max(double v, double *sh) {
+    const int t = threadIdx.x;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_down_sync(0xffffffffu, v, o));
+    if ((t & 31) == 0) sh[t >> 5] = v;
+    __syncthreads();
+    double r = 0.0;
+    if (t < 32) {
+        r = (t < BT / 32) ? sh[t] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) r = fmax(r, __shfl_down_sync(0xffffffffu, r, o));
+    }
+    __syncthreads();
+    return r;
+}
+
+// ordered uint64 key of a double (for radix sorts that mimic np.lexsort);
+// +0.0 and -0.0 map to the same key, as numpy compares them equal.
+__device__ __forceinline__ uint64_t dkey(double x) {
+    uint64_t b = (uint64_t)__double_as_longlong(x);
+    if ((b << 1) == 0) b = 0;  // -0.0 -> +0.0
+    return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
+}
+
+__host__ __device__ __forceinline__ uint64_t spread3(uint64_t v) {  // 21 bits -> every 3rd
+    v &= 0x1fffffull;
+    v = (v | v << 32) & 0x1f00000000ffffull;
+    v = (v | v << 16) & 0x1f0000ff0000ffull;
+    v = (v | v << 8) & 0x100f00f00f00f00full;
+    v = (v | v << 4) & 0x10c30c30c30c30c3ull;
+    v = (v | v << 2) & 0x1249249249249249ull;
+    return v;
+}
+__host__ __device__ __forceinline__ uint64_t spread2(uint64_t v) {  // 32 bits -> every 2nd
+    v &= 0xffffffffull;
+    v = (v | v << 16) & 0x0000ffff0000ffffull;
+    v = (v | v << 8) & 0x00ff00ff00ff00ffull;
+    v = (v | v << 4) & 0x0f0f0f0f0f0f0f0full;
+    v = (v | v << 2) & 0x3333333333333333ull;
+    v = (v | v << 1) & 0x5555555555555555ull;
+    return v;
+}
+
+}  // namespace mtsph

@@ -1,0 +1,224 @@
+// damping.cuh -- pairwise implicit viscous damping sweeps (paper Eq. 24-25,
+// §4.3 pairwise splitting; reference _accel.py:97-206).
+//
+// Every group of pairs is solved with backward Euler in closed form (one
+// pair) or by a small Gaussian elimination (mirror-image pairs that share
+// particles, solved simultaneously as in the reference).  The sweep visits
+// all groups forward then in reverse, half the step each.
+//
+//  * serial  : the reference's exact group sequence, level-scheduled; the
+//              groups of one level touch disjoint particles, so running a
+//              level in parallel performs exactly the serial operations.
+//              One CTA walks all levels (__syncthreads between levels).
+//  * coloured: groups bucketed into midpoint-cell tasks of 3^d colours;
+//              one kernel per colour and direction, one thread per task,
+//              groups of a task in the reference's within-task order.
+//
+// The damping coefficient 2 V_i V_j (-e.gradW)/r of each pair
+// (neighbors.py:137-144) is recomputed from the reference positions in the
+// kernel instead of being streamed from HBM.
+#pragma once
+
+#include "common.cuh"
+#include "nbh.cuh"
+
+namespace mtsph {
+
+struct Ctrl {
+    double dt, eta, cfl, criterion, dt_outer;
+    double ek, vmax2, amax2, min_dt, last_dt;
+    double ramp_disp, h, sound;
+    double vol_movable;   // porous energy density normaliser
+    long long n_inner, min_inner, max_inner, ramp_left;
+    int done, cap_hit, mode, pad;
+    unsigned long long err_inv, err_rm;  // min original id per error class
+};
+
+template <int D> struct VT;
+template <> struct VT<2> { using T = double2; };
+template <> struct VT<3> { using T = double4; };
+
+__device__ __forceinline__ void vget(const double2 &v, double *o) { o[0] = v.x; o[1] = v.y; }
+__device__ __forceinline__ void vget(const double4 &v, double *o) { o[0] = v.x; o[1] = v.y; o[2] = v.z; }
+__device__ __forceinline__ void vset(double2 &v, const double *o) { v.x = o[0]; v.y = o[1]; }
+__device__ __forceinline__ void vset(double4 &v, const double *o) { v.x = o[0]; v.y = o[1]; v.z = o[2]; v.w = 0.0; }
+
+template <int D> __device__ __forceinline__ void xget(const double4 &xv, double *x) {
+    x[0] = xv.x; x[1] = xv.y;
+    if (D == 3) x[2] = xv.z;
+}
+template <int D> __device__ __forceinline__ double volof(const double4 &xv) { return D == 3 ? xv.w : xv.z; }
+
+// neighbors.py:137-144: 2 V_i V_j (-(e . grad W_ij)) / |r_ij|, r = X_j - X_i
+template <int D>
+__device__ __forceinline__ double pair_damp(const double4 &xi, const double4 &xj, const KSpec &ks) {
+    double a[3], b[3], rel[D], g[D];
+    xget<D>(xi, a);
+    xget<D>(xj, b);
+    double r2 = 0.0;
+#pragma unroll
+    for (int k = 0; k < D; ++k) { rel[k] = b[k] - a[k]; r2 += rel[k] * rel[k]; }
+    const double r = sqrt(r2);
+    grad_w<D>(rel, ks, g);
+    double radial = 0.0;
+#pragma unroll
+    for (int k = 0; k < D; ++k) radial -= (rel[k] / r) * g[k];
+    return 2.0 * volof<D>(xi) * volof<D>(xj) * radial / r;
+}
+
+struct SweepArgs {
+    const int32_t *pi, *pj;
+    const int64_t *gptr, *gscr;
+    double *scratch;
+    const double4 *XV;
+    const double *inv_m;
+    void *V;
+    KSpec ks;
+};
+
+template <int D>
+__device__ __forceinline__ void visit_group(const SweepArgs &A, int64_t g, double half) {
+    using V_t = typename VT<D>::T;
+    V_t *V = reinterpret_cast<V_t *>(A.V);
+    const int64_t lo = A.gptr[g], hi = A.gptr[g + 1];
+    if (hi - lo == 1) {
+        const int32_t i = A.pi[lo], j = A.pj[lo];
+        const double c = half * pair_damp<D>(A.XV[i], A.XV[j], A.ks);
+        const double ca = c * A.inv_m[i], cb = c * A.inv_m[j];
+        const double den = 1.0 + ca + cb;
+        V_t vi = V[i], vj = V[j];
+        double a[3], b[3];
+        vget(vi, a);
+        vget(vj, b);
+#pragma unroll
+        for (int m = 0; m < D; ++m) {
+            const double u = (a[m] - b[m]) / den;
+            a[m] -= ca * u;
+            b[m] += cb * u;
+        }
+        vset(vi, a);
+        vset(vj, b);
+        V[i] = vi;
+        V[j] = vj;
+        return;
+    }
+    // simultaneous solve (_accel.py:107), scratch: A[nb*nb] rhs[nb*3] loc[nb]
+    double *S = A.scratch + A.gscr[g];
+    const int nbmax = (int)(2 * (hi - lo));
+    double *Am = S;
+    double *rhs = S + nbmax * nbmax;
+    long long *loc = reinterpret_cast<long long *>(rhs + 3 * nbmax);
+    int nb = 0;
+    for (int64_t k = lo; k < hi; ++k) {
+        const int32_t e[2] = {A.pi[k], A.pj[k]};
+        for (int s = 0; s < 2; ++s) {
+            bool found = false;
+            for (int t = 0; t < nb; ++t) if (loc[t] == e[s]) { found = true; break; }
+            if (!found) loc[nb++] = e[s];
+        }
+    }
+    for (int r = 0; r < nb; ++r) {
+        for (int c = 0; c < nb; ++c) Am[r * nb + c] = (r == c) ? 1.0 : 0.0;
+        double v[3];
+        vget(V[loc[r]], v);
+        for (int m = 0; m < D; ++m) rhs[r * 3 + m] = v[m];
+    }
+    for (int64_t k = lo; k < hi; ++k) {
+        const int32_t i = A.pi[k], j = A.pj[k];
+        const double c = half * pair_damp<D>(A.XV[i], A.XV[j], A.ks);
+        int ia = 0, ib = 0;
+        for (int t = 0; t < nb; ++t) {
+            if (loc[t] == i) ia = t;
+            if (loc[t] == j) ib = t;
+        }
+        const double ca = c * A.inv_m[i], cb = c * A.inv_m[j];
+        Am[ia * nb + ia] += ca;
+        Am[ia * nb + ib] -= ca;
+        Am[ib * nb + ib] += cb;
+        Am[ib * nb + ia] -= cb;
+    }
+    for (int col = 0; col < nb - 1; ++col) {
+        const double piv = Am[col * nb + col];
+        for (int r = col + 1; r < nb; ++r) {
+            const double f = Am[r * nb + col] / piv;
+            if (f != 0.0) {
+                for (int c = col; c < nb; ++c) Am[r * nb + c] -= f * Am[col * nb + c];
+                for (int m = 0; m < D; ++m) rhs[r * 3 + m] -= f * rhs[col * 3 + m];
+            }
+        }
+    }
+    for (int r = nb - 1; r >= 0; --r)
+        for (int m = 0; m < D; ++m) {
+            double s = rhs[r * 3 + m];
+            for (int c = r + 1; c < nb; ++c) s -= Am[r * nb + c] * rhs[c * 3 + m];
+            rhs[r * 3 + m] = s / Am[r * nb + r];
+        }
+    for (int t = 0; t < nb; ++t) {
+        double v[3] = {rhs[t * 3], rhs[t * 3 + 1], rhs[t * 3 + 2]};
+        V_t w;
+        vset(w, v);
+        V[loc[t]] = w;
+    }
+}
+
+// exact serial order: one CTA walks the levels forward, then backward
+template <int D>
+__global__ void __launch_bounds__(1024) k_sweep_serial(SweepArgs A, const int64_t *__restrict__ level_ptr,
+                                                       int64_t nlevels, const int64_t *__restrict__ level_groups,
+                                                       const Ctrl *ctrl) {
+    if (ctrl->done) return;
+    const double half = 0.5 * ctrl->dt * ctrl->eta;
+    for (int64_t L = 0; L < nlevels; ++L) {
+        for (int64_t k = level_ptr[L] + threadIdx.x; k < level_ptr[L + 1]; k += blockDim.x)
+            visit_group<D>(A, level_groups[k], half);
+        __syncthreads();
+    }
+    for (int64_t L = nlevels - 1; L >= 0; --L) {
+        for (int64_t k = level_ptr[L] + threadIdx.x; k < level_ptr[L + 1]; k += blockDim.x)
+            visit_group<D>(A, level_groups[k], half);
+        __syncthreads();
+    }
+}
+
+// one colour phase: thread per task, groups in task order (dir>0) or
+// reversed (dir<0)
+template <int D>
+__global__ void __launch_bounds__(128) k_sweep_colour(SweepArgs A, int64_t t0, int64_t t1, int dir,
+                                                      const int64_t *__restrict__ task_ptr,
+                                                      const Ctrl *ctrl) {
+    const int64_t t = t0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= t1 || ctrl->done) return;
+    const double half = 0.5 * ctrl->dt * ctrl->eta;
+    const int64_t g0 = task_ptr[t], g1 = task_ptr[t + 1];
+    if (dir > 0)
+        for (int64_t g = g0; g < g1; ++g) visit_group<D>(A, g, half);
+    else
+        for (int64_t g = g1 - 1; g >= g0; --g) visit_group<D>(A, g, half);
+}
+
+// launch one full sweep on stream s; returns the number of kernel launches
+template <int D>
+int launch_sweep(const NbhDev &nb, const SweepArgs &A, const int64_t *level_ptr_d, const Ctrl *ctrl,
+                 cudaStream_t s) {
+    if (nb.npairs == 0) return 0;
+    if (nb.sweep == 1) {
+        k_sweep_serial<D><<<1, 1024, 0, s>>>(A, level_ptr_d, nb.nlevels, nb.level_groups.p, ctrl);
+        MT_LAUNCH_CHECK();
+        return 1;
+    }
+    int launches = 0;
+    const int nc = (int)nb.colour_task_ptr.size() - 1;
+    for (int pass = 0; pass < 2; ++pass)
+        for (int q = 0; q < nc; ++q) {
+            const int c = pass == 0 ? q : nc - 1 - q;
+            const int64_t t0 = nb.colour_task_ptr[c], t1 = nb.colour_task_ptr[c + 1];
+            if (t1 <= t0) continue;
+            k_sweep_colour<D><<<blocks_for(t1 - t0, 128), 128, 0, s>>>(A, t0, t1, pass == 0 ? 1 : -1,
+                                                                        nb.task_ptr.p, ctrl);
+            MT_LAUNCH_CHECK();
+            ++launches;
+        }
+    return launches;
+}
+
+}  // namespace mtsph

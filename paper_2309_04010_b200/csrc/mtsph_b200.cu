@@ -1,0 +1,558 @@
+// mtsph_b200.cu -- the C ABI (include/mtsph_b200.h) over the sm_100a kernels.
+//
+// Host runtime in C++: owns device memory, one stream per problem, CUDA
+// graphs for the device-side inner loop, error translation to the
+// reference's error classes.  Compiled with
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -shared
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/mtsph_b200.h"
+#include "common.cuh"
+#include "damping.cuh"
+#include "nbh.cuh"
+#include "porous.cuh"
+#include "solid.cuh"
+#include "layer1.cuh"
+
+using namespace mtsph;
+
+// ------------------------------------------------------------- errors
+
+static thread_local std::string g_err;
+static thread_local std::vector<int64_t> g_err_ids;
+
+static int fail(int code, const std::string &msg, std::vector<int64_t> ids = {}) {
+    g_err = msg;
+    g_err_ids = std::move(ids);
+    return code;
+}
+
+#define API_BEGIN try {
+#define API_END                                                                \
+    }                                                                          \
+    catch (const mtsph::Error &e) { return fail(e.code, e.what(), e.ids); }    \
+    catch (const std::exception &e) { return fail(MTSPH_ERR_CUDA, e.what()); } \
+    return MTSPH_OK;
+
+extern "C" int mtsph_abi_version(void) { return MTSPH_ABI_VERSION; }
+extern "C" const char *mtsph_last_error(void) { return g_err.c_str(); }
+extern "C" int64_t mtsph_last_error_ids(int64_t *ids, int64_t cap) {
+    int64_t n = (int64_t)g_err_ids.size();
+    for (int64_t k = 0; k < n && k < cap; ++k) ids[k] = g_err_ids[k];
+    return n;
+}
+extern "C" int mtsph_device_count(void) {
+    int c = 0;
+    if (cudaGetDeviceCount(&c) != cudaSuccess) { cudaGetLastError(); return 0; }
+    return c;
+}
+
+static void require_device() {
+    if (mtsph_device_count() <= 0) throw Error(MTSPH_ERR_CUDA, "no CUDA device available");
+}
+
+// ------------------------------------------------------------- neighbourhood
+
+struct mtsph_nbh {
+    NbhDev nb;
+    cudaStream_t s = nullptr;
+    ~mtsph_nbh() { if (s) cudaStreamDestroy(s); }
+};
+
+extern "C" mtsph_status mtsph_nbh_create(int64_t n, int d, const double *pos, const double *vol,
+                                         const double *h_axes, int sweep, mtsph_nbh **out) {
+    API_BEGIN
+    require_device();
+    auto h = std::make_unique<mtsph_nbh>();
+    MT_CUDA(cudaStreamCreateWithFlags(&h->s, cudaStreamNonBlocking));
+    build_nbh(h->nb, n, d, pos, vol, h_axes, sweep, h->s);
+    *out = h.release();
+    API_END
+}
+
+extern "C" mtsph_status mtsph_nbh_destroy(mtsph_nbh *nb) {
+    delete nb;
+    return MTSPH_OK;
+}
+
+extern "C" mtsph_status mtsph_nbh_sizes(const mtsph_nbh *h, int64_t *nnz, int64_t *npairs, int64_t *ngroups,
+                                        int64_t *nphases) {
+    const NbhDev &nb = h->nb;
+    if (nnz) *nnz = nb.nnz;
+    if (npairs) *npairs = nb.npairs;
+    if (ngroups) *ngroups = nb.ngroups;
+    if (nphases) {
+        if (nb.sweep == 1) *nphases = nb.nlevels;
+        else if (nb.sweep == 2) {
+            int64_t c = 0;
+            for (size_t k = 0; k + 1 < nb.colour_task_ptr.size(); ++k)
+                c += nb.colour_task_ptr[k + 1] > nb.colour_task_ptr[k];
+            *nphases = c;
+        } else *nphases = 0;
+    }
+    return MTSPH_OK;
+}
+
+extern "C" mtsph_status mtsph_nbh_permutation(const mtsph_nbh *h, int64_t *perm) {
+    API_BEGIN
+    h->nb.perm.download(perm, h->nb.n, h->s);
+    MT_CUDA(cudaStreamSynchronize(h->s));
+    API_END
+}
+
+// host-side kernel gradient identical to the device grad_w
+static void grad_host(int d, const double *rel, const KSpec &ks, double *g) {
+    double u[3], q2 = 0.0;
+    for (int k = 0; k < d; ++k) { u[k] = rel[k] * ks.inv_h[k]; q2 += u[k] * u[k]; }
+    const double q = std::sqrt(q2), t = 1.0 - 0.5 * q;
+    const double mag = q < 2.0 ? ks.pref * (-5.0 * t * t * t) : 0.0;
+    for (int k = 0; k < d; ++k) g[k] = mag * (u[k] * ks.inv_h[k]);
+}
+
+extern "C" mtsph_status mtsph_nbh_export(const mtsph_nbh *h, int64_t *indptr, int64_t *idx, double *grad0,
+                                         int64_t *pair_i, int64_t *pair_j, double *pair_damp,
+                                         double *pair_grad, int64_t *pair_group, double *corr) {
+    API_BEGIN
+    const NbhDev &nb = h->nb;
+    const int64_t n = nb.n;
+    const int d = nb.d;
+    cudaStream_t s = h->s;
+    std::vector<int64_t> perm(n), iptr(n + 1);
+    std::vector<int32_t> csr(std::max<int64_t>(nb.nnz, 1));
+    std::vector<double4> XV(n);
+    nb.perm.download(perm.data(), n, s);
+    nb.indptr.download(iptr.data(), n + 1, s);
+    nb.csr.download(csr.data(), nb.nnz, s);
+    nb.XV.download(XV.data(), n, s);
+    MT_CUDA(cudaStreamSynchronize(s));
+    auto X = [&](int64_t k, int c) {
+        const double4 &q = XV[k];
+        return c == 0 ? q.x : (c == 1 ? q.y : q.z);
+    };
+    auto Vol = [&](int64_t k) { return d == 3 ? XV[k].w : XV[k].z; };
+    // reference CSR: rows in original order, neighbours ascending original id
+    std::vector<int64_t> iperm(n);
+    for (int64_t k = 0; k < n; ++k) iperm[perm[k]] = k;
+    int64_t w = 0;
+    if (indptr) indptr[0] = 0;
+    std::vector<std::pair<int64_t, int32_t>> row;
+    for (int64_t o = 0; o < n; ++o) {
+        const int64_t a = iperm[o];
+        row.clear();
+        for (int64_t k = iptr[a]; k < iptr[a + 1]; ++k) row.emplace_back(perm[csr[k]], csr[k]);
+        std::sort(row.begin(), row.end());
+        for (auto &e : row) {
+            if (idx) idx[w] = e.first;
+            if (grad0) {
+                double rel[3];
+                for (int c = 0; c < d; ++c) rel[c] = X(e.second, c) - X(a, c);
+                grad_host(d, rel, nb.ks, grad0 + w * d);
+            }
+            ++w;
+        }
+        if (indptr) indptr[o + 1] = w;
+    }
+    if (corr) {
+        std::vector<double> B((size_t)n * d * d);
+        nb.B.download(B.data(), B.size(), s);
+        MT_CUDA(cudaStreamSynchronize(s));
+        for (int64_t k = 0; k < n; ++k)
+            for (int q = 0; q < d * d; ++q) corr[perm[k] * d * d + q] = B[(size_t)q * n + k];
+    }
+    if (nb.sweep && nb.npairs) {
+        std::vector<int32_t> pi(nb.npairs), pj(nb.npairs);
+        std::vector<int64_t> gp(nb.ngroups + 1);
+        nb.pi.download(pi.data(), nb.npairs, s);
+        nb.pj.download(pj.data(), nb.npairs, s);
+        nb.gptr.download(gp.data(), nb.ngroups + 1, s);
+        MT_CUDA(cudaStreamSynchronize(s));
+        // export in execution order: SERIAL = reference order; COLOURED =
+        // colour-major, task order
+        for (int64_t k = 0; k < nb.npairs; ++k) {
+            if (pair_i) pair_i[k] = perm[pi[k]];
+            if (pair_j) pair_j[k] = perm[pj[k]];
+            double rel[3], g[3], r2 = 0.0;
+            for (int c = 0; c < d; ++c) { rel[c] = X(pj[k], c) - X(pi[k], c); r2 += rel[c] * rel[c]; }
+            grad_host(d, rel, nb.ks, g);
+            if (pair_grad) for (int c = 0; c < d; ++c) pair_grad[k * d + c] = g[c];
+            if (pair_damp) {
+                const double r = std::sqrt(r2);
+                double radial = 0.0;
+                for (int c = 0; c < d; ++c) radial -= (rel[c] / r) * g[c];
+                pair_damp[k] = 2.0 * Vol(pi[k]) * Vol(pj[k]) * radial / r;
+            }
+        }
+        if (pair_group) for (int64_t g = 0; g <= nb.ngroups; ++g) pair_group[g] = gp[g];
+    } else if (pair_group) {
+        pair_group[0] = 0;
+    }
+    API_END
+}
+
+// ------------------------------------------------------------- solid
+
+struct mtsph_solid {
+    NbhDev nb;
+    int d = 0;
+    int64_t n = 0;
+    cudaStream_t s = nullptr;
+    DBuf<unsigned char> V;
+    DBuf<double> x, a, F, cp, alpha, T, mass, rho0, inv_m, part, meas;
+    DBuf<uint8_t> flags;
+    DBuf<Ctrl> ctrl;
+    DBuf<int64_t> level_ptr;
+    Ctrl *hc = nullptr;  // pinned mirror
+    Mat mat{};
+    int nblk = 0;
+    int64_t launches = 0;
+    int per_step_launches = 0;
+    cudaGraphExec_t graphs[3] = {nullptr, nullptr, nullptr};
+    int graph_steps[3] = {4, 32, 128};
+    ~mtsph_solid() {
+        for (auto &g : graphs) if (g) cudaGraphExecDestroy(g);
+        if (hc) cudaFreeHost(hc);
+        if (s) cudaStreamDestroy(s);
+    }
+    SolidArgs args() {
+        SolidArgs A{};
+        A.n = n;
+        A.XV = nb.XV.p;
+        A.V = V.p;
+        A.x = x.p; A.a = a.p; A.F = F.p; A.cp = cp.p; A.alpha = alpha.p; A.T = T.p;
+        A.B = nb.B.p; A.mass = mass.p; A.rho0 = rho0.p; A.flags = flags.p;
+        A.slice_ptr = nb.slice_ptr.p; A.slice_w = nb.slice_w.p; A.nbr = nb.nbr.p;
+        A.perm = nb.perm.p;
+        A.part = part.p;
+        A.nblk = nblk;
+        A.ctrl = ctrl.p;
+        A.ks = nb.ks;
+        A.mat = mat;
+        return A;
+    }
+    SweepArgs sweep_args() {
+        SweepArgs S{};
+        S.pi = nb.pi.p; S.pj = nb.pj.p; S.gptr = nb.gptr.p; S.gscr = nb.gscr.p;
+        S.scratch = nb.scratch.p; S.XV = nb.XV.p; S.inv_m = inv_m.p; S.V = V.p; S.ks = nb.ks;
+        return S;
+    }
+    void pull_ctrl() {
+        MT_CUDA(cudaMemcpyAsync(hc, ctrl.p, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
+        MT_CUDA(cudaStreamSynchronize(s));
+    }
+    void push_ctrl() {
+        MT_CUDA(cudaMemcpyAsync(ctrl.p, hc, sizeof(Ctrl), cudaMemcpyHostToDevice, s));
+        MT_CUDA(cudaStreamSynchronize(s));
+    }
+};
+
+template <int D> static int solid_step(mtsph_solid *S, int ctrl_mode) {
+    SolidArgs A = S->args();
+    const unsigned nb = blocks_for(S->n);
+    k_solid_kick_drift<D><<<nb, 256, 0, S->s>>>(A);
+    k_solid_stress<D><<<nb, 256, 0, S->s>>>(A);
+    k_solid_accel<D><<<nb, 256, 0, S->s>>>(A);
+    MT_LAUNCH_CHECK();
+    int l = 3 + launch_sweep<D>(S->nb, S->sweep_args(), S->level_ptr.p, S->ctrl.p, S->s);
+    k_solid_vmax<D><<<nb, 256, 0, S->s>>>(A, 0);
+    k_ctrl<<<1, 256, 0, S->s>>>(S->ctrl.p, S->part.p, S->nblk, ctrl_mode);
+    MT_LAUNCH_CHECK();
+    return l + 2;
+}
+
+static int solid_step_any(mtsph_solid *S, int mode) {
+    return S->d == 2 ? solid_step<2>(S, mode) : solid_step<3>(S, mode);
+}
+
+template <int D> static void solid_init_dt(mtsph_solid *S) {
+    SolidArgs A = S->args();
+    k_solid_vmax<D><<<blocks_for(S->n), 256, 0, S->s>>>(A, 1);
+    k_ctrl<<<1, 256, 0, S->s>>>(S->ctrl.p, S->part.p, S->nblk, CTRL_INIT);
+    MT_LAUNCH_CHECK();
+    S->launches += 2;
+}
+
+static void check_solid_errors(mtsph_solid *S) {
+    if (S->hc->err_inv != ~0ull)
+        throw Error(MTSPH_ERR_INVERSION, "non-positive deformation determinant (first id " +
+                                             std::to_string(S->hc->err_inv) + ")",
+                    {(int64_t)S->hc->err_inv});
+    if (S->hc->err_rm != ~0ull)
+        throw Error(MTSPH_ERR_RETURN_MAP, "return mapping did not converge (first id " +
+                                              std::to_string(S->hc->err_rm) + ")",
+                    {(int64_t)S->hc->err_rm});
+}
+
+extern "C" mtsph_status mtsph_solid_create(const mtsph_solid_desc *dsc, mtsph_solid **out) {
+    API_BEGIN
+    require_device();
+    const int64_t n = dsc->n;
+    const int d = dsc->d;
+    if (d != 2 && d != 3) throw Error(MTSPH_ERR_ARG, "solid problems support d = 2 or 3");
+    auto S = std::make_unique<mtsph_solid>();
+    S->n = n;
+    S->d = d;
+    MT_CUDA(cudaStreamCreateWithFlags(&S->s, cudaStreamNonBlocking));
+    build_nbh(S->nb, n, d, dsc->pos, dsc->vol, dsc->h_axes, dsc->sweep, S->s);
+    std::vector<int64_t> perm(n);
+    S->nb.perm.download(perm.data(), n, S->s);
+    MT_CUDA(cudaStreamSynchronize(S->s));
+    const int dd = d * d;
+    std::vector<double> x((size_t)d * n), F((size_t)dd * n, 0.0), mass(n), rho0(n), inv_m(n);
+    std::vector<uint8_t> flags(n);
+    for (int64_t k = 0; k < n; ++k) {
+        const int64_t o = perm[k];
+        for (int c = 0; c < d; ++c) x[(size_t)c * n + k] = dsc->pos[o * d + c];
+        for (int c = 0; c < d; ++c) F[(size_t)(c * d + c) * n + k] = 1.0;
+        rho0[k] = dsc->rho0[o];
+        mass[k] = dsc->rho0[o] * dsc->vol[o];
+        const bool movable = !dsc->constrained[o];
+        inv_m[k] = movable ? 1.0 / mass[k] : 0.0;
+        uint8_t f = movable ? FL_MOVABLE : 0;
+        if (dsc->side && dsc->side[o] < 0) f |= FL_LEFT;
+        if (dsc->side && dsc->side[o] > 0) f |= FL_RIGHT;
+        if (dsc->mid_mask && dsc->mid_mask[o]) f |= FL_MID;
+        flags[k] = f;
+    }
+    const size_t vbytes = (size_t)n * (d == 3 ? sizeof(double4) : sizeof(double2));
+    S->V.alloc(vbytes);
+    S->V.zero(S->s);
+    S->x.upload(x.data(), x.size(), S->s);
+    S->a.alloc((size_t)d * n);
+    S->a.zero(S->s);
+    S->F.upload(F.data(), F.size(), S->s);
+    S->cp.upload(F.data(), F.size(), S->s);
+    S->alpha.alloc(n);
+    S->alpha.zero(S->s);
+    S->T.alloc((size_t)n * (d == 3 ? 12 : 4));
+    S->T.zero(S->s);
+    S->mass.upload(mass.data(), n, S->s);
+    S->rho0.upload(rho0.data(), n, S->s);
+    S->inv_m.upload(inv_m.data(), n, S->s);
+    S->flags.upload(flags.data(), n, S->s);
+    S->nblk = (int)blocks_for(n);
+    S->part.alloc((size_t)3 * S->nblk);
+    S->part.zero(S->s);
+    S->meas.alloc((size_t)5 * S->nblk);
+    if (S->nb.sweep == 1) S->level_ptr.upload(S->nb.level_ptr_h.data(), S->nb.level_ptr_h.size(), S->s);
+    Mat &m = S->mat;
+    m.mu = dsc->shear_modulus;
+    m.K = dsc->bulk_modulus;
+    for (int k = 0; k < 4; ++k) m.p[k] = dsc->hard[k];
+    m.law = dsc->hardening_law;
+    m.plastic = dsc->plastic ? 1 : 0;
+    m.tol = dsc->rm_tol > 0 ? dsc->rm_tol : 1e-8 * dsc->hard[0];
+    m.max_iter = dsc->rm_max_iter > 0 ? dsc->rm_max_iter : 50;
+    MT_CUDA(cudaMallocHost(&S->hc, sizeof(Ctrl)));
+    std::memset(S->hc, 0, sizeof(Ctrl));
+    S->hc->h = S->nb.ks.h_min;
+    S->hc->sound = std::sqrt(dsc->bulk_modulus / dsc->rho0[0]);
+    S->hc->cfl = 0.6;
+    S->hc->min_dt = INFINITY;
+    S->hc->err_inv = S->hc->err_rm = ~0ull;
+    S->hc->vol_movable = 0.0;
+    S->ctrl.alloc(1);
+    S->push_ctrl();
+    *out = S.release();
+    API_END
+}
+
+extern "C" mtsph_status mtsph_solid_destroy(mtsph_solid *s) {
+    delete s;
+    return MTSPH_OK;
+}
+
+extern "C" mtsph_status mtsph_solid_set_ramp(mtsph_solid *S, double end_disp, int64_t ramp_steps,
+                                             int64_t ramp_left) {
+    API_BEGIN
+    S->pull_ctrl();
+    S->hc->ramp_disp = end_disp / (double)(ramp_steps > 0 ? ramp_steps : 1);
+    S->hc->ramp_left = ramp_left;
+    S->push_ctrl();
+    API_END
+}
+
+extern "C" mtsph_status mtsph_solid_ramp_left(const mtsph_solid *S, int64_t *ramp_left) {
+    API_BEGIN
+    const_cast<mtsph_solid *>(S)->pull_ctrl();
+    *ramp_left = S->hc->ramp_left;
+    API_END
+}
+
+extern "C" mtsph_status mtsph_solid_stable_dt(mtsph_solid *S, double cfl, double *dt) {
+    API_BEGIN
+    S->pull_ctrl();
+    S->hc->cfl = cfl;
+    S->push_ctrl();
+    if (S->d == 2) solid_init_dt<2>(S); else solid_init_dt<3>(S);
+    S->pull_ctrl();
+    *dt = S->hc->dt;
+    API_END
+}
+
+extern "C" mtsph_status mtsph_solid_relax_step(mtsph_solid *S, double dt, double eta, double *ek) {
+    API_BEGIN
+    S->pull_ctrl();
+    S->hc->dt = dt;
+    S->hc->eta = eta;
+    S->hc->done = 0;
+    S->push_ctrl();
+    S->launches += solid_step_any(S, CTRL_SINGLE);
+    S->pull_ctrl();
+    check_solid_errors(S);
+    *ek = S->hc->ek;
+    API_END
+}
+
+static cudaGraphExec_t solid_graph(mtsph_solid *S, int which) {
+    if (S->graphs[which]) return S->graphs[which];
+    cudaGraph_t g;
+    MT_CUDA(cudaStreamBeginCapture(S->s, cudaStreamCaptureModeThreadLocal));
+    int l = 0;
+    for (int k = 0; k < S->graph_steps[which]; ++k) l = solid_step_any(S, CTRL_STEP);
+    MT_CUDA(cudaStreamEndCapture(S->s, &g));
+    MT_CUDA(cudaGraphInstantiate(&S->graphs[which], g, 0));
+    cudaGraphDestroy(g);
+    S->per_step_launches = l;
+    return S->graphs[which];
+}
+
+extern "C" mtsph_status mtsph_solid_relax(mtsph_solid *S, const mtsph_inner_params *p, mtsph_inner_result *r) {
+    API_BEGIN
+    S->pull_ctrl();
+    Ctrl *c = S->hc;
+    c->eta = p->eta;
+    c->cfl = p->cfl;
+    c->criterion = p->criterion;
+    c->dt_outer = p->dt_outer;
+    c->max_inner = p->max_inner;
+    c->min_inner = p->min_inner < 1 ? 1 : p->min_inner;
+    c->n_inner = 0;
+    c->done = 0;
+    c->cap_hit = 0;
+    c->min_dt = INFINITY;
+    c->err_inv = c->err_rm = ~0ull;
+    S->push_ctrl();
+    if (S->d == 2) solid_init_dt<2>(S); else solid_init_dt<3>(S);
+    int which = 0;
+    while (true) {
+        cudaGraphExec_t g = solid_graph(S, which);
+        MT_CUDA(cudaGraphLaunch(g, S->s));
+        S->launches += (int64_t)S->graph_steps[which] * S->per_step_launches;
+        S->pull_ctrl();
+        if (c->done) break;
+        if (which < 2) ++which;
+    }
+    check_solid_errors(S);
+    r->n_inner = c->n_inner;
+    r->cap_hit = c->cap_hit;
+    r->ek = c->ek;
+    r->min_dt = c->min_dt;
+    r->last_dt = c->last_dt;
+    API_END
+}
+
+extern "C" mtsph_status mtsph_solid_measure(mtsph_solid *S, double out[5]) {
+    API_BEGIN
+    SolidArgs A = S->args();
+    const int nb = S->nblk;
+    if (S->d == 2) k_solid_measure<2><<<nb, 256, 0, S->s>>>(A, S->meas.p);
+    else k_solid_measure<3><<<nb, 256, 0, S->s>>>(A, S->meas.p);
+    MT_LAUNCH_CHECK();
+    S->launches += 1;
+    std::vector<double> h((size_t)5 * nb);
+    S->meas.download(h.data(), h.size(), S->s);
+    MT_CUDA(cudaStreamSynchronize(S->s));
+    double fx = 0.0, rad = 0.0, amax = 0.0, amin = 1e308, bad = 0.0;
+    for (int b = 0; b < nb; ++b) {
+        fx += h[b];
+        rad = std::max(rad, h[nb + b]);
+        amax = std::max(amax, h[2 * nb + b]);
+        amin = std::min(amin, h[3 * nb + b]);
+        bad = std::max(bad, h[4 * nb + b]);
+    }
+    out[0] = -fx;
+    out[1] = rad;
+    out[2] = S->mat.plastic ? amax : 0.0;
+    out[3] = S->mat.plastic ? amin : 0.0;
+    out[4] = bad > 0 ? 0.0 : 1.0;
+    API_END
+}
+
+enum FieldKind { FK_SOA_VEC, FK_SOA_TEN, FK_SCALAR, FK_VEL, FK_REF };
+
+extern "C" mtsph_status mtsph_solid_get(mtsph_solid *S, const char *field, double *host) {
+    API_BEGIN
+    const int64_t n = S->n;
+    const int d = S->d;
+    std::vector<int64_t> perm(n);
+    S->nb.perm.download(perm.data(), n, S->s);
+    std::string f(field);
+    std::vector<double> buf;
+    auto soa = [&](const DBuf<double> &src, int comps) {
+        buf.resize((size_t)comps * n);
+        src.download(buf.data(), buf.size(), S->s);
+        MT_CUDA(cudaStreamSynchronize(S->s));
+        for (int64_t k = 0; k < n; ++k)
+            for (int c = 0; c < comps; ++c) host[perm[k] * comps + c] = buf[(size_t)c * n + k];
+    };
+    if (f == "pos") soa(S->x, d);
+    else if (f == "accel") soa(S->a, d);
+    else if (f == "F") soa(S->F, d * d);
+    else if (f == "cp_inv") soa(S->cp, d * d);
+    else if (f == "alpha") soa(S->alpha, 1);
+    else if (f == "vel" || f == "ref_pos") {
+        const int stride = (f == "ref_pos" || d == 3) ? 4 : 2;
+        buf.resize((size_t)stride * n);
+        if (f == "vel") MT_CUDA(cudaMemcpyAsync(buf.data(), S->V.p, buf.size() * 8, cudaMemcpyDeviceToHost, S->s));
+        else MT_CUDA(cudaMemcpyAsync(buf.data(), S->nb.XV.p, buf.size() * 8, cudaMemcpyDeviceToHost, S->s));
+        MT_CUDA(cudaStreamSynchronize(S->s));
+        for (int64_t k = 0; k < n; ++k)
+            for (int c = 0; c < d; ++c) host[perm[k] * d + c] = buf[(size_t)k * stride + c];
+    } else throw Error(MTSPH_ERR_ARG, "unknown solid field " + f);
+    API_END
+}
+
+extern "C" mtsph_status mtsph_solid_set(mtsph_solid *S, const char *field, const double *host) {
+    API_BEGIN
+    const int64_t n = S->n;
+    const int d = S->d;
+    std::vector<int64_t> perm(n);
+    S->nb.perm.download(perm.data(), n, S->s);
+    MT_CUDA(cudaStreamSynchronize(S->s));
+    std::string f(field);
+    std::vector<double> buf;
+    auto soa = [&](DBuf<double> &dst, int comps) {
+        buf.resize((size_t)comps * n);
+        for (int64_t k = 0; k < n; ++k)
+            for (int c = 0; c < comps; ++c) buf[(size_t)c * n + k] = host[perm[k] * comps + c];
+        dst.upload(buf.data(), buf.size(), S->s);
+    };
+    if (f == "pos") soa(S->x, d);
+    else if (f == "accel") soa(S->a, d);
+    else if (f == "F") soa(S->F, d * d);
+    else if (f == "cp_inv") soa(S->cp, d * d);
+    else if (f == "alpha") soa(S->alpha, 1);
+    else if (f == "vel") {
+        const int stride = d == 3 ? 4 : 2;
+        buf.assign((size_t)stride * n, 0.0);
+        for (int64_t k = 0; k < n; ++k)
+            for (int c = 0; c < d; ++c) buf[(size_t)k * stride + c] = host[perm[k] * d + c];
+        MT_CUDA(cudaMemcpyAsync(S->V.p, buf.data(), buf.size() * 8, cudaMemcpyHostToDevice, S->s));
+    } else throw Error(MTSPH_ERR_ARG, "unknown or read-only solid field " + f);
+    MT_CUDA(cudaStreamSynchronize(S->s));
+    API_END
+}
+
+extern "C" mtsph_status mtsph_solid_launches(const mtsph_solid *S, int64_t *count) {
+    *count = S->launches;
+    return MTSPH_OK;
+}
+
+#include "porous_api.cuh"
+#include "layer1_api.cuh"

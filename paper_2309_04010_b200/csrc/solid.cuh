@@ -1,0 +1,478 @@
+// solid.cuh -- total-Lagrangian elastoplastic inner relaxation on the GPU.
+//
+// One inner step = NeckingProblem.relax_step (scenarios.py:113) + the
+// stepping.py:347 bookkeeping, as five kernels plus the damping sweep:
+//
+//   k_solid_kick_drift : v += dt/2 a (free), boundary ramp / clamps, x += dt v
+//   k_solid_stress     : SELL gather dF/dt = (sum_b V_b (v_b - v_a) (x) gradW) B
+//                        (solids.py:364), F += dt dF/dt, J2 return map or
+//                        Neo-Hookean stress (plasticity.py:118, solids.py:394),
+//                        T = P B stored for the divergence
+//   k_solid_accel      : SELL gather a = 1/rho0 sum_b V_b (T_a + T_b) gradW
+//                        (solids.py:416), v += dt/2 a, E_k and |a|max partials
+//   sweep              : damping (damping.cuh)
+//   k_solid_vmax       : |v|max partial after damping
+//   k_solid_ctrl       : 1 block: fixed-order reductions, convergence test,
+//                        counters, next dt (solids.py:433) -- all on device
+//
+// State lives in HBM in the Morton order of the neighbourhood: own-access
+// fields SoA (coalesced), gathered fields AoS (X|vol and v as one 32 B
+// sector, T as 3 x 32 B rows), so a neighbour costs whole sectors.
+#pragma once
+
+#include "damping.cuh"
+#include "nbh.cuh"
+
+namespace mtsph {
+
+enum { FL_MOVABLE = 1, FL_LEFT = 2, FL_RIGHT = 4, FL_MID = 8 };
+
+struct Mat {
+    double mu, K;
+    double p[4];   // law 0: s0, sinf, delta, H ; law 1: s0, e0, m, -
+    double tol;
+    int max_iter;
+    int law;
+    int plastic;
+};
+
+__device__ __forceinline__ double hard_k(const Mat &m, double a) {
+    if (m.law == 1) return m.p[0] * pow(1.0 + a / m.p[1], m.p[2]);
+    return m.p[0] + (m.p[1] - m.p[0]) * (1.0 - exp(-m.p[2] * a)) + m.p[3] * a;
+}
+__device__ __forceinline__ double hard_kp(const Mat &m, double a) {
+    if (m.law == 1) return m.p[0] * m.p[2] / m.p[1] * pow(1.0 + a / m.p[1], m.p[2] - 1.0);
+    return (m.p[1] - m.p[0]) * m.p[2] * exp(-m.p[2] * a) + m.p[3];
+}
+
+#define SQ23_D 0.81649658092772603273
+
+// plasticity.py:118 for one particle.  Returns 0, 1 (det F <= 0),
+// 2 (no convergence), 3 (plastic tensor inverted).
+template <int D>
+__device__ __forceinline__ int return_map_dev(const double *F, double *cp, double &alpha, const Mat &m,
+                                              double *P) {
+    const double j = det_d<D>(F);
+    if (!(j > 0.0)) return 1;
+    const double sc = det_pow_minus_inv_d<D>(j);
+    double fb[D * D], be[D * D], s[D * D];
+#pragma unroll
+    for (int k = 0; k < D * D; ++k) fb[k] = F[k] * sc;
+    if (m.plastic) {
+        double tmp[D * D];
+        mm<D>(fb, cp, tmp);
+        mmt<D>(tmp, fb, be);
+#pragma unroll
+        for (int r = 0; r < D; ++r)
+#pragma unroll
+            for (int c = r + 1; c < D; ++c) {
+                const double v = 0.5 * (be[r * D + c] + be[c * D + r]);
+                be[r * D + c] = v;
+                be[c * D + r] = v;
+            }
+    } else {
+        mmt<D>(fb, fb, be);
+    }
+    double tr = 0.0;
+#pragma unroll
+    for (int r = 0; r < D; ++r) tr += be[r * D + r];
+#pragma unroll
+    for (int k = 0; k < D * D; ++k) s[k] = m.mu * be[k];
+#pragma unroll
+    for (int r = 0; r < D; ++r) s[r * D + r] = m.mu * (be[r * D + r] - tr / D);
+    if (m.plastic) {
+        double sn2 = 0.0;
+#pragma unroll
+        for (int k = 0; k < D * D; ++k) sn2 += s[k] * s[k];
+        const double sn = sqrt(sn2);
+        const double fpre = sn - SQ23_D * hard_k(m, alpha);
+        if (fpre > 0.0) {
+            const double mue = (tr / D) * m.mu;
+            double x = 0.0, lo = 0.0, hi = sn / (2.0 * mue);
+            for (int it = 0; it < m.max_iter; ++it) {
+                const double at = alpha + SQ23_D * x;
+                const double g = sn - 2.0 * mue * x - SQ23_D * hard_k(m, at);
+                if (!(fabs(g) > m.tol)) break;
+                if (g > 0.0) lo = x;
+                if (g < 0.0) hi = x;
+                const double gp = -2.0 * mue - (2.0 / 3.0) * hard_kp(m, at);
+                const double nw = x - g / gp;
+                x = (nw > lo && nw < hi) ? nw : 0.5 * (lo + hi);
+            }
+            const double gf = sn - 2.0 * mue * x - SQ23_D * hard_k(m, alpha + SQ23_D * x);
+            if (fabs(gf) > m.tol) return 2;
+            const double dg = x > 0.0 ? x : 0.0;
+            const double scale = 1.0 - 2.0 * mue * dg / sn;
+#pragma unroll
+            for (int k = 0; k < D * D; ++k) s[k] *= scale;
+            alpha += SQ23_D * dg;
+            double bn[D * D], fbi[D * D], tmp[D * D];
+#pragma unroll
+            for (int k = 0; k < D * D; ++k) bn[k] = s[k] / m.mu;
+#pragma unroll
+            for (int r = 0; r < D; ++r) bn[r * D + r] += tr / D;
+            inv_d<D>(fb, det_d<D>(fb), fbi);
+            mm<D>(fbi, bn, tmp);
+            mmt<D>(tmp, fbi, cp);
+#pragma unroll
+            for (int r = 0; r < D; ++r)
+#pragma unroll
+                for (int c = r + 1; c < D; ++c) {
+                    const double v = 0.5 * (cp[r * D + c] + cp[c * D + r]);
+                    cp[r * D + c] = v;
+                    cp[c * D + r] = v;
+                }
+            const double jc = det_d<D>(cp);
+            if (!(jc > 0.0)) return 3;
+            const double cs = det_pow_minus_inv_d<D>(jc);
+#pragma unroll
+            for (int k = 0; k < D * D; ++k) cp[k] *= cs;
+        }
+    }
+    const double vol = 0.5 * m.K * (j * j - 1.0);
+#pragma unroll
+    for (int r = 0; r < D; ++r) s[r * D + r] += vol;
+    double fi[D * D];
+    inv_d<D>(F, j, fi);
+    mmt<D>(s, fi, P);
+    return 0;
+}
+
+template <int D> struct TS { static constexpr int n = D == 3 ? 12 : 4; };
+
+template <int D> __device__ __forceinline__ void tload(const double *Tp, int64_t a, double *t) {
+    const double4 *r = reinterpret_cast<const double4 *>(Tp + a * TS<D>::n);
+    if (D == 2) {
+        double4 q = r[0];
+        t[0] = q.x; t[1] = q.y; t[2] = q.z; t[3] = q.w;
+    } else {
+#pragma unroll
+        for (int row = 0; row < 3; ++row) {
+            double4 q = r[row];
+            t[row * 3] = q.x; t[row * 3 + 1] = q.y; t[row * 3 + 2] = q.z;
+        }
+    }
+}
+template <int D> __device__ __forceinline__ void tstore(double *Tp, int64_t a, const double *t) {
+    double4 *r = reinterpret_cast<double4 *>(Tp + a * TS<D>::n);
+    if (D == 2) {
+        r[0] = make_double4(t[0], t[1], t[2], t[3]);
+    } else {
+#pragma unroll
+        for (int row = 0; row < 3; ++row) r[row] = make_double4(t[row * 3], t[row * 3 + 1], t[row * 3 + 2], 0.0);
+    }
+}
+
+struct SolidArgs {
+    int64_t n;
+    const double4 *XV;
+    void *V;
+    double *x, *a, *F, *cp, *alpha, *T;
+    const double *B, *mass, *rho0;
+    const uint8_t *flags;
+    const int64_t *slice_ptr;
+    const int32_t *slice_w, *nbr;
+    const int64_t *perm;
+    double *part;    // [3][nblk]: ek, amax2, vmax2
+    int nblk;
+    Ctrl *ctrl;
+    KSpec ks;
+    Mat mat;
+};
+
+template <int D>
+__global__ void __launch_bounds__(256) k_solid_kick_drift(SolidArgs A) {
+    using V_t = typename VT<D>::T;
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= A.n) return;
+    const Ctrl *c = A.ctrl;
+    if (c->done) return;
+    const double dt = c->dt;
+    V_t *V = reinterpret_cast<V_t *>(A.V);
+    double v[3];
+    vget(V[i], v);
+    const uint8_t f = A.flags[i];
+    if (f & FL_MOVABLE) {
+#pragma unroll
+        for (int k = 0; k < D; ++k) v[k] += 0.5 * dt * A.a[(int64_t)k * A.n + i];
+    }
+    if (c->ramp_left > 0) {
+        if (f & (FL_LEFT | FL_RIGHT)) {
+            const double vbc = c->ramp_disp / dt;
+#pragma unroll
+            for (int k = 0; k < D; ++k) v[k] = 0.0;
+            v[0] = (f & FL_LEFT) ? -vbc : vbc;
+        }
+    } else if (!(f & FL_MOVABLE)) {
+#pragma unroll
+        for (int k = 0; k < D; ++k) v[k] = 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < D; ++k) A.x[(int64_t)k * A.n + i] += dt * v[k];
+    V_t w;
+    vset(w, v);
+    V[i] = w;
+}
+
+template <int D>
+__global__ void __launch_bounds__(256) k_solid_stress(SolidArgs A) {
+    using V_t = typename VT<D>::T;
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= A.n) return;
+    Ctrl *c = A.ctrl;
+    if (c->done) return;
+    const double dt = c->dt;
+    const int64_t n = A.n;
+    const V_t *V = reinterpret_cast<const V_t *>(A.V);
+    double xa[3], va[3];
+    xget<D>(A.XV[i], xa);
+    vget(V[i], va);
+    double acc[D * D];
+#pragma unroll
+    for (int k = 0; k < D * D; ++k) acc[k] = 0.0;
+    const int64_t s = i >> 5;
+    const int lane = (int)(i & 31);
+    const int64_t base = A.slice_ptr[s] + lane;
+    const int w = A.slice_w[s];
+    for (int m = 0; m < w; ++m) {
+        const int32_t b = __ldg(A.nbr + base + (int64_t)m * 32);
+        const double4 xvb = ldg4(A.XV + b);
+        double xb[3], vb[3], rel[D], g[D];
+        xget<D>(xvb, xb);
+        vget(V[b], vb);
+#pragma unroll
+        for (int k = 0; k < D; ++k) rel[k] = xb[k] - xa[k];
+        grad_w<D>(rel, A.ks, g);
+        const double volb = volof<D>(xvb);
+#pragma unroll
+        for (int r = 0; r < D; ++r) {
+            const double dv = volb * (vb[r] - va[r]);
+#pragma unroll
+            for (int cc = 0; cc < D; ++cc) acc[r * D + cc] += dv * g[cc];
+        }
+    }
+    double Bm[D * D], F[D * D], L[D * D];
+#pragma unroll
+    for (int k = 0; k < D * D; ++k) {
+        Bm[k] = A.B[(int64_t)k * n + i];
+        F[k] = A.F[(int64_t)k * n + i];
+    }
+    mm<D>(acc, Bm, L);
+#pragma unroll
+    for (int k = 0; k < D * D; ++k) F[k] += dt * L[k];
+    double cp[D * D];
+    double alpha = 0.0;
+    if (A.mat.plastic) {
+#pragma unroll
+        for (int k = 0; k < D * D; ++k) cp[k] = A.cp[(int64_t)k * n + i];
+        alpha = A.alpha[i];
+    }
+    double P[D * D];
+    const int rc = return_map_dev<D>(F, cp, alpha, A.mat, P);
+#pragma unroll
+    for (int k = 0; k < D * D; ++k) A.F[(int64_t)k * n + i] = F[k];
+    if (rc) {
+        const unsigned long long id = (unsigned long long)A.perm[i];
+        if (rc == 1) atomicMin(&c->err_inv, id);
+        else atomicMin(&c->err_rm, id);
+#pragma unroll
+        for (int k = 0; k < D * D; ++k) P[k] = 0.0;
+    } else if (A.mat.plastic) {
+#pragma unroll
+        for (int k = 0; k < D * D; ++k) A.cp[(int64_t)k * n + i] = cp[k];
+        A.alpha[i] = alpha;
+    }
+    double Tm[D * D];
+    mm<D>(P, Bm, Tm);
+    tstore<D>(A.T, i, Tm);
+}
+
+template <int D>
+__global__ void __launch_bounds__(256) k_solid_accel(SolidArgs A) {
+    using V_t = typename VT<D>::T;
+    __shared__ double sh[32];
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const Ctrl *c = A.ctrl;
+    if (c->done) return;  // uniform across the grid
+    double ek = 0.0, a2m = 0.0;
+    if (i < A.n) {
+        const double dt = c->dt;
+        double xa[3], Ta[D * D];
+        xget<D>(A.XV[i], xa);
+        tload<D>(A.T, i, Ta);
+        double acc[D];
+#pragma unroll
+        for (int k = 0; k < D; ++k) acc[k] = 0.0;
+        const int64_t s = i >> 5;
+        const int lane = (int)(i & 31);
+        const int64_t base = A.slice_ptr[s] + lane;
+        const int w = A.slice_w[s];
+        for (int m = 0; m < w; ++m) {
+            const int32_t b = __ldg(A.nbr + base + (int64_t)m * 32);
+            const double4 xvb = ldg4(A.XV + b);
+            double xb[3], Tb[D * D], rel[D], g[D];
+            xget<D>(xvb, xb);
+            tload<D>(A.T, b, Tb);
+#pragma unroll
+            for (int k = 0; k < D; ++k) rel[k] = xb[k] - xa[k];
+            grad_w<D>(rel, A.ks, g);
+            const double volb = volof<D>(xvb);
+#pragma unroll
+            for (int r = 0; r < D; ++r) {
+                double sum = 0.0;
+#pragma unroll
+                for (int cc = 0; cc < D; ++cc) sum += (Ta[r * D + cc] + Tb[r * D + cc]) * g[cc];
+                acc[r] += volb * sum;
+            }
+        }
+        const double rinv = A.rho0[i];
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+            acc[k] /= rinv;
+            A.a[(int64_t)k * A.n + i] = acc[k];
+        }
+        if (A.flags[i] & FL_MOVABLE) {
+            V_t *V = reinterpret_cast<V_t *>(A.V);
+            double v[3];
+            vget(V[i], v);
+            double v2 = 0.0, aa = 0.0;
+#pragma unroll
+            for (int k = 0; k < D; ++k) {
+                v[k] += 0.5 * dt * acc[k];
+                v2 += v[k] * v[k];
+                aa += acc[k] * acc[k];
+            }
+            V_t w2;
+            vset(w2, v);
+            V[i] = w2;
+            ek = A.mass[i] * v2;
+            a2m = aa;
+        }
+    }
+    const double se = block_sum<256>(ek, sh);
+    const double sa = block_max<256>(a2m, sh);
+    if (threadIdx.x == 0) {
+        A.part[blockIdx.x] = se;
+        A.part[A.nblk + blockIdx.x] = sa;
+    }
+}
+
+// |v|^2 max over all particles (mode 0) or also |a|^2 over the free ones
+// (mode 1, used before the first step)
+template <int D>
+__global__ void __launch_bounds__(256) k_solid_vmax(SolidArgs A, int with_accel) {
+    using V_t = typename VT<D>::T;
+    __shared__ double sh[32];
+    if (!with_accel && A.ctrl->done) return;
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    double v2 = 0.0, a2 = 0.0;
+    if (i < A.n) {
+        const V_t *V = reinterpret_cast<const V_t *>(A.V);
+        double v[3];
+        vget(V[i], v);
+#pragma unroll
+        for (int k = 0; k < D; ++k) v2 += v[k] * v[k];
+        if (with_accel && (A.flags[i] & FL_MOVABLE)) {
+#pragma unroll
+            for (int k = 0; k < D; ++k) {
+                const double q = A.a[(int64_t)k * A.n + i];
+                a2 += q * q;
+            }
+        }
+    }
+    const double mv = block_max<256>(v2, sh);
+    const double ma = block_max<256>(a2, sh);
+    if (threadIdx.x == 0) {
+        A.part[2 * A.nblk + blockIdx.x] = mv;
+        if (with_accel) A.part[A.nblk + blockIdx.x] = ma;
+    }
+}
+
+enum { CTRL_INIT = 0, CTRL_STEP = 1, CTRL_SINGLE = 2 };
+
+__device__ __forceinline__ double stable_dt(const Ctrl *c, double vmax2, double amax2) {
+    double dt = c->h / (c->sound + sqrt(vmax2));
+    const double amax = sqrt(amax2);
+    if (amax > 0.0) dt = fmin(dt, sqrt(c->h / amax));
+    return c->cfl * dt;
+}
+
+// one block of 256; fixed-order reduction of the per-block partials
+__global__ void __launch_bounds__(256) k_ctrl(Ctrl *c, const double *part, int nblk, int mode) {
+    __shared__ double sh[32];
+    if (mode == CTRL_STEP && c->done) return;
+    double e = 0.0, am = 0.0, vm = 0.0;
+    for (int b = threadIdx.x; b < nblk; b += 256) {
+        if (mode != CTRL_INIT) e += part[b];
+        am = fmax(am, part[nblk + b]);
+        vm = fmax(vm, part[2 * nblk + b]);
+    }
+    const double E = block_sum<256>(e, sh);
+    const double AM = block_max<256>(am, sh);
+    const double VM = block_max<256>(vm, sh);
+    if (threadIdx.x != 0) return;
+    c->amax2 = AM;
+    c->vmax2 = VM;
+    if (mode == CTRL_INIT) {
+        c->dt = stable_dt(c, VM, AM);
+        return;
+    }
+    const double ek = 0.5 * E * (c->vol_movable > 0.0 ? 1.0 / c->vol_movable : 1.0);
+    c->ek = ek;
+    if (c->ramp_left > 0) c->ramp_left -= 1;
+    if (c->err_inv != ~0ull || c->err_rm != ~0ull) { c->done = 1; return; }
+    if (mode == CTRL_SINGLE) return;
+    const double dt_used = c->dt;
+    c->n_inner += 1;
+    c->last_dt = dt_used;
+    c->min_dt = fmin(c->min_dt, dt_used);
+    const bool conv = ek <= c->criterion;
+    long long cap = c->max_inner;
+    if (cap <= 0) cap = 10 * (long long)ceil(c->dt_outer / dt_used);
+    if (conv && c->n_inner >= c->min_inner && c->ramp_left <= 0) { c->done = 1; return; }
+    if (c->n_inner >= cap) { c->done = 1; c->cap_hit = 1; return; }
+    c->dt = stable_dt(c, VM, AM);
+}
+
+// observables (NeckingProblem.measure) as per-block partials
+template <int D>
+__global__ void __launch_bounds__(256) k_solid_measure(SolidArgs A, double *out /* [5][nblk] */) {
+    using V_t = typename VT<D>::T;
+    __shared__ double sh[32];
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    double fx = 0.0, rad = 0.0, amax = 0.0, amin = 1e308, bad = 0.0;
+    if (i < A.n) {
+        const uint8_t f = A.flags[i];
+        if (f & FL_RIGHT) fx = A.mass[i] * A.a[i];
+        if (f & FL_MID) {
+            double r2 = 0.0;
+#pragma unroll
+            for (int k = 1; k < D; ++k) {
+                const double q = A.x[(int64_t)k * A.n + i];
+                r2 += q * q;
+            }
+            rad = sqrt(r2);
+            if (A.mat.plastic) amin = A.alpha[i];
+        }
+        if (A.mat.plastic) amax = A.alpha[i];
+        double v[3];
+        vget(reinterpret_cast<const V_t *>(A.V)[i], v);
+#pragma unroll
+        for (int k = 0; k < D; ++k) if (!isfinite(v[k])) bad = 1.0;
+    }
+    const double s0 = block_sum<256>(fx, sh);
+    const double s1 = block_max<256>(rad, sh);
+    const double s2 = block_max<256>(amax, sh);
+    const double s3 = -block_max<256>(-amin, sh);
+    const double s4 = block_max<256>(bad, sh);
+    if (threadIdx.x == 0) {
+        const int nb = gridDim.x;
+        out[blockIdx.x] = s0;
+        out[nb + blockIdx.x] = s1;
+        out[2 * nb + blockIdx.x] = s2;
+        out[3 * nb + blockIdx.x] = s3;
+        out[4 * nb + blockIdx.x] = s4;
+    }
+}
+
+}  // namespace mtsph

@@ -1,0 +1,261 @@
+"""Thin Python handles over the device-resident problems of the C ABI.
+
+`DeviceSolid`  <-> mtsph_solid_*  (NeckingProblem state in HBM)
+`DevicePorous` <-> mtsph_porous_* (PorousProblem state in HBM)
+`DeviceNeighborhood` <-> mtsph_nbh_* (neighbors.py:59 on the GPU)
+
+All arrays crossing this boundary are host numpy arrays in the caller's
+(original) particle numbering; the library keeps its own Morton order.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, ptr
+
+
+def _f64(a, shape=None):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    if shape is not None:
+        a = a.reshape(shape)
+    return a
+
+
+def _u8(a, n):
+    if a is None:
+        return None
+    return np.ascontiguousarray(np.broadcast_to(np.asarray(a), (n,)), dtype=np.uint8)
+
+
+def _h3(h_axes):
+    h = list(map(float, h_axes)) + [1.0] * (3 - len(h_axes))
+    return (ctypes.c_double * 3)(*h[:3])
+
+
+class DeviceNeighborhood:
+    """Fixed reference neighbourhood built on the GPU."""
+
+    def __init__(self, pos, vol, h_axes, sweep="serial"):
+        lib = _lib.load_library()
+        pos = _f64(pos)
+        n, d = pos.shape
+        self.n, self.d = n, d
+        h = np.ascontiguousarray(h_axes, dtype=np.float64)
+        handle = ctypes.c_void_p()
+        check(lib.mtsph_nbh_create(n, d, ptr(pos), ptr(_f64(vol)), ptr(h),
+                                   _lib.SWEEPS[sweep], ctypes.byref(handle)))
+        self._h = handle
+        self._lib = lib
+
+    def sizes(self):
+        vals = [ctypes.c_int64() for _ in range(4)]
+        check(self._lib.mtsph_nbh_sizes(self._h, *[ctypes.byref(v) for v in vals]))
+        return tuple(v.value for v in vals)
+
+    def export(self):
+        nnz, npairs, ngroups, _ = self.sizes()
+        n, d = self.n, self.d
+        out = {
+            "indptr": np.zeros(n + 1, np.int64), "idx": np.zeros(nnz, np.int64),
+            "grad0": np.zeros((nnz, d)), "pair_i": np.zeros(npairs, np.int64),
+            "pair_j": np.zeros(npairs, np.int64), "pair_damp": np.zeros(npairs),
+            "pair_grad": np.zeros((npairs, d)), "pair_group": np.zeros(ngroups + 1, np.int64),
+            "corr": np.zeros((n, d, d)),
+        }
+        check(self._lib.mtsph_nbh_export(
+            self._h, ptr(out["indptr"]), ptr(out["idx"]), ptr(out["grad0"]),
+            ptr(out["pair_i"]), ptr(out["pair_j"]), ptr(out["pair_damp"]),
+            ptr(out["pair_grad"]), ptr(out["pair_group"]), ptr(out["corr"])))
+        return out
+
+    def permutation(self):
+        p = np.zeros(self.n, np.int64)
+        check(self._lib.mtsph_nbh_permutation(self._h, ptr(p)))
+        return p
+
+    def __del__(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            self._lib.mtsph_nbh_destroy(self._h)
+            self._h = None
+
+
+class DeviceSolid:
+    """Device-resident total-Lagrangian solid (NeckingProblem state)."""
+
+    FIELDS_D = {"pos", "vel", "accel", "ref_pos"}
+    FIELDS_DD = {"F", "cp_inv"}
+
+    def __init__(self, pos, vol, rho0, constrained, side, mid_mask, h_axes,
+                 shear_modulus, bulk_modulus, plastic=True, hardening_law=0,
+                 hard=(1.0, 1.0, 1.0, 0.0), rm_tol=0.0, rm_max_iter=50, sweep="serial"):
+        lib = _lib.load_library()
+        pos = _f64(pos)
+        n, d = pos.shape
+        self.n, self.d = n, d
+        self._keep = {
+            "pos": pos, "vol": _f64(vol, (n,)),
+            "rho0": _f64(np.broadcast_to(np.asarray(rho0, float), (n,))),
+            "constrained": _u8(constrained, n),
+            "side": np.ascontiguousarray(np.broadcast_to(np.asarray(side), (n,)), dtype=np.int8),
+            "mid": _u8(mid_mask if mid_mask is not None else np.zeros(n, bool), n),
+        }
+        k = self._keep
+        desc = _lib.SolidDesc(
+            n, d, ptr(k["pos"]).value, ptr(k["vol"]).value, ptr(k["rho0"]).value,
+            ptr(k["constrained"]).value, ptr(k["side"]).value, ptr(k["mid"]).value,
+            _h3(h_axes), float(shear_modulus), float(bulk_modulus), int(bool(plastic)),
+            int(hardening_law), (ctypes.c_double * 4)(*[float(v) for v in hard]),
+            float(rm_tol), int(rm_max_iter), _lib.SWEEPS[sweep])
+        handle = ctypes.c_void_p()
+        check(lib.mtsph_solid_create(ctypes.byref(desc), ctypes.byref(handle)))
+        self._h = handle
+        self._lib = lib
+
+    # -- control -------------------------------------------------------
+    def set_ramp(self, end_disp, ramp_steps, ramp_left):
+        check(self._lib.mtsph_solid_set_ramp(self._h, float(end_disp), int(ramp_steps),
+                                             int(ramp_left)))
+
+    def ramp_left(self):
+        v = ctypes.c_int64()
+        check(self._lib.mtsph_solid_ramp_left(self._h, ctypes.byref(v)))
+        return v.value
+
+    def stable_dt(self, cfl):
+        v = ctypes.c_double()
+        check(self._lib.mtsph_solid_stable_dt(self._h, float(cfl), ctypes.byref(v)))
+        return v.value
+
+    def relax_step(self, dt, eta):
+        v = ctypes.c_double()
+        check(self._lib.mtsph_solid_relax_step(self._h, float(dt), float(eta), ctypes.byref(v)))
+        return v.value
+
+    def relax(self, eta, cfl, criterion, dt_outer, max_inner=0, min_inner=1):
+        p = _lib.InnerParams(float(eta), float(cfl), float(criterion), float(dt_outer),
+                             int(max_inner), int(min_inner))
+        r = _lib.InnerResult()
+        check(self._lib.mtsph_solid_relax(self._h, ctypes.byref(p), ctypes.byref(r)))
+        return r
+
+    def measure(self):
+        out = np.zeros(5)
+        check(self._lib.mtsph_solid_measure(self._h, ptr(out)))
+        return {"reaction_force": out[0], "mid_radius": out[1], "max_alpha": out[2],
+                "mid_alpha_min": out[3], "finite": bool(out[4])}
+
+    def launches(self):
+        v = ctypes.c_int64()
+        check(self._lib.mtsph_solid_launches(self._h, ctypes.byref(v)))
+        return v.value
+
+    # -- fields ----------------------------------------------------------
+    def _shape(self, field):
+        if field in self.FIELDS_D:
+            return (self.n, self.d)
+        if field in self.FIELDS_DD:
+            return (self.n, self.d, self.d)
+        if field == "alpha":
+            return (self.n,)
+        raise KeyError(field)
+
+    def get(self, field):
+        out = np.zeros(self._shape(field))
+        check(self._lib.mtsph_solid_get(self._h, field.encode(), ptr(out)))
+        return out
+
+    def set(self, field, value):
+        arr = _f64(np.broadcast_to(np.asarray(value, float), self._shape(field)))
+        check(self._lib.mtsph_solid_set(self._h, field.encode(), ptr(arr)))
+
+    def __del__(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            self._lib.mtsph_solid_destroy(self._h)
+            self._h = None
+
+
+class DevicePorous:
+    """Device-resident porous membrane (PorousProblem state)."""
+
+    FIELDS_D = {"pos", "ref_pos", "momentum", "vel_solid", "vel_fluid", "flux"}
+    FIELDS_DD = {"F"}
+    FIELDS_1 = {"fluid_mass", "saturation", "pressure"}
+
+    def __init__(self, pos, vol, constrained, contact, h_axes, model, contact_time,
+                 evaporation_rate, sweep="serial"):
+        lib = _lib.load_library()
+        pos = _f64(pos)
+        n, d = pos.shape
+        self.n, self.d = n, d
+        self._keep = {"pos": pos, "vol": _f64(vol, (n,)), "constrained": _u8(constrained, n),
+                      "contact": _u8(contact, n)}
+        k = self._keep
+        m = model
+        desc = _lib.PorousDesc(
+            n, d, ptr(k["pos"]).value, ptr(k["vol"]).value, ptr(k["constrained"]).value,
+            ptr(k["contact"]).value, _h3(h_axes), m.density0, m.diffusivity, m.pressure_coeff,
+            m.shear_modulus, m.lame_lambda, m.bulk_modulus, m.porosity, m.fluid_density0,
+            m.initial_saturation, float(contact_time), float(evaporation_rate),
+            _lib.SWEEPS[sweep])
+        handle = ctypes.c_void_p()
+        check(lib.mtsph_porous_create(ctypes.byref(desc), ctypes.byref(handle)))
+        self._h = handle
+        self._lib = lib
+
+    def advance_slow(self, dt_outer, t):
+        v = ctypes.c_int64()
+        check(self._lib.mtsph_porous_advance_slow(self._h, float(dt_outer), float(t),
+                                                  ctypes.byref(v)))
+        return v.value
+
+    def stable_dt(self, cfl):
+        v = ctypes.c_double()
+        check(self._lib.mtsph_porous_stable_dt(self._h, float(cfl), ctypes.byref(v)))
+        return v.value
+
+    def relax_step(self, dt, eta):
+        v = ctypes.c_double()
+        check(self._lib.mtsph_porous_relax_step(self._h, float(dt), float(eta), ctypes.byref(v)))
+        return v.value
+
+    def relax(self, eta, cfl, criterion, dt_outer, max_inner=0, min_inner=1):
+        p = _lib.InnerParams(float(eta), float(cfl), float(criterion), float(dt_outer),
+                             int(max_inner), int(min_inner))
+        r = _lib.InnerResult()
+        check(self._lib.mtsph_porous_relax(self._h, ctypes.byref(p), ctypes.byref(r)))
+        return r
+
+    def refresh_velocities(self):
+        check(self._lib.mtsph_porous_refresh_velocities(self._h))
+
+    def launches(self):
+        v = ctypes.c_int64()
+        check(self._lib.mtsph_porous_launches(self._h, ctypes.byref(v)))
+        return v.value
+
+    def _shape(self, field):
+        if field in self.FIELDS_D:
+            return (self.n, self.d)
+        if field in self.FIELDS_DD:
+            return (self.n, self.d, self.d)
+        if field in self.FIELDS_1:
+            return (self.n,)
+        raise KeyError(field)
+
+    def get(self, field):
+        out = np.zeros(self._shape(field))
+        check(self._lib.mtsph_porous_get(self._h, field.encode(), ptr(out)))
+        return out
+
+    def set(self, field, value):
+        arr = _f64(np.broadcast_to(np.asarray(value, float), self._shape(field)))
+        check(self._lib.mtsph_porous_set(self._h, field.encode(), ptr(arr)))
+
+    def __del__(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            self._lib.mtsph_porous_destroy(self._h)
+            self._h = None
