@@ -1,0 +1,283 @@
+"""Run configuration: the reference's config grammar and scenario defaults.
+
+Mirrors /root/reference/pkg/src/mtsph/config.py (file format, strictness,
+defaults of the four paper scenarios) and adds the BASELINE.json
+workloads used by the benchmarks:
+
+  bar_2d       configs[0]  2D plane-strain power-law-hardening bar 20 x 2, dp 0.1
+  membrane_2d  configs[1]  2D Nafion strip 10 x 0.5, dp 0.025, top-face wetting
+  bar_3d       configs[2]  3D power-law-hardening bar 20 x 2 x 2, dp 0.02
+  block_3d     configs[4]  3D jittered elastic-plastic block (scaling sweep)
+
+Format: one ``key = value`` per line, ``#`` comments, optional
+``[geometry] [material] [stepping] [output]`` headers (organisational
+only).  Unknown keys, keys foreign to the chosen scenario, type errors and
+out-of-range values raise ConfigError naming the line.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+from .errors import ConfigError
+
+SECTIONS = ("geometry", "material", "stepping", "output")
+
+
+def _positive(v):
+    return v > 0
+
+
+def _non_negative(v):
+    return v >= 0
+
+
+def _unit_interval(v):
+    return 0.0 <= v <= 1.0
+
+
+@dataclass(frozen=True)
+class Key:
+    kind: type
+    check: object = None      # predicate or None
+    rule: str = "any"         # human description of the range
+
+
+_P = ("positive", _positive)
+_NN = ("non-negative", _non_negative)
+_U = ("in [0, 1]", _unit_interval)
+
+
+def _k(kind, rng=None):
+    if rng is None:
+        return Key(kind)
+    return Key(kind, rng[1], rng[0])
+
+
+KEYS = {
+    # run / output
+    "scenario": _k(str), "out_dir": _k(str), "snapshot_every": _k(int, _NN),
+    "seed": _k(int, _NN), "quiet": _k(bool),
+    "vm_strain_source": Key(str, lambda v: v in ("log_strain", "plastic"),
+                            "log_strain or plastic"),
+    # geometry
+    "length": _k(float, _P), "width": _k(float, _P), "breadth": _k(float, _P),
+    "thickness": _k(float, _P), "radius": _k(float, _P), "dp": _k(float, _P),
+    "layers": _k(int, _P), "imperfection": _k(float, _U),
+    "imperfection_extent": _k(float, _U),
+    "anisotropy": Key(float, lambda v: v >= 1.0, ">= 1"), "h_factor": _k(float, _P),
+    "jitter": _k(float, _U),
+    # material
+    "density": _k(float, _P), "shear_modulus": _k(float, _P), "bulk_modulus": _k(float, _P),
+    "youngs_modulus": _k(float, _P),
+    "poisson_ratio": Key(float, lambda v: 0.0 < v < 0.5, "in (0, 0.5)"),
+    "initial_flow_stress": _k(float, _P), "saturation_flow_stress": _k(float, _P),
+    "saturation_exponent": _k(float, _P), "hardening_coefficient": _k(float, _NN),
+    "hardening_law": Key(str, lambda v: v in ("saturation", "power"), "saturation or power"),
+    "reference_strain": _k(float, _P), "hardening_exponent": _k(float, _NN),
+    "plasticity": _k(bool), "diffusivity": _k(float, _P), "pressure_coeff": _k(float, _P),
+    "porosity": Key(float, lambda v: 0.0 < v < 1.0, "in (0, 1)"),
+    "fluid_density": _k(float, _P), "initial_saturation": _k(float, _U),
+    "evaporation_rate": _k(float, _NN),
+    # loading / stepping
+    "stretch_per_end": _k(float, _P), "pull": Key(str, lambda v: v in ("both", "right"),
+                                                  "both or right"),
+    "contact_time": _k(float, _P), "contact_frac": _k(float, _U),
+    "contact_face": Key(str, lambda v: v in ("centre", "top"), "centre or top"),
+    "t_total": _k(float, _P), "n_outer": _k(int, _NN), "eta": _k(float, _NN),
+    "energy_pct": _k(float, _P), "energy_ref": _k(float, _NN), "max_inner": _k(int, _NN),
+    "min_inner": _k(int, _P), "ramp_steps": _k(int, _P), "cfl": _k(float, _P),
+    "damping_sweep": Key(str, lambda v: v in ("serial", "coloured"), "serial or coloured"),
+    "ref_force": _k(float, _P), "ref_displacement": _k(float, _P),
+}
+
+_BASE = {"out_dir": "out", "snapshot_every": 0, "seed": 0, "quiet": False,
+         "vm_strain_source": "log_strain", "h_factor": 1.35, "cfl": 0.6, "max_inner": 0,
+         "min_inner": 1, "energy_ref": 0.0, "layers": 3, "damping_sweep": "serial"}
+
+# Table 1 steel (reference config.py defaults)
+_STEEL = {"shear_modulus": 80.1938e9, "bulk_modulus": 164.21e9, "density": 7850.0,
+          "initial_flow_stress": 450.0e6, "saturation_flow_stress": 715.0e6,
+          "saturation_exponent": 16.93, "hardening_coefficient": 129.24e6,
+          "hardening_law": "saturation", "plasticity": True, "imperfection": 0.018,
+          "imperfection_extent": 0.25, "ramp_steps": 50, "pull": "both"}
+
+# Table 3 Nafion
+_NAFION = {"density": 2000.0, "diffusivity": 1.0e-10, "pressure_coeff": 3.0e6,
+           "youngs_modulus": 8.242e6, "poisson_ratio": 0.2631, "porosity": 0.4,
+           "fluid_density": 1000.0, "initial_saturation": 0.0, "contact_frac": 0.3,
+           "contact_face": "centre"}
+
+# BASELINE configs[0]/[2]: rho 1, E 200, nu 0.3, power law s0 (1 + a/e0)^n
+_E200 = 200.0
+_NU = 0.3
+_K200 = _E200 / (3.0 * (1.0 - 2.0 * _NU))
+_MU200 = _E200 / (2.0 * (1.0 + _NU))
+_POWER = {"shear_modulus": _MU200, "bulk_modulus": _K200, "density": 1.0,
+          "hardening_law": "power", "initial_flow_stress": 0.25, "reference_strain": 0.01,
+          "hardening_exponent": 0.2, "plasticity": True, "imperfection": 0.0,
+          "imperfection_extent": 0.25, "ramp_steps": 50, "pull": "right",
+          "h_factor": 1.3, "cfl": 0.2, "energy_pct": 1.0e-8, "energy_ref": 1.0,
+          # eta = 0.1 rho c h with c = sqrt(K / rho), h = 1.3 dp (filled in _derive)
+          "eta": 0.0}
+
+SCENARIO_DEFAULTS = {
+    "necking_2d": {**_BASE, **_STEEL, "length": 53.334e-3, "width": 12.826e-3,
+                   "dp": 12.826e-3 / 50.0, "stretch_per_end": 5.0e-3, "t_total": 100.0,
+                   "n_outer": 10000, "eta": 1.0e4, "energy_pct": 0.005,
+                   "ref_force": 8000.0, "ref_displacement": 10.0e-3},
+    "necking_3d": {**_BASE, **_STEEL, "length": 53.334e-3, "radius": 6.413e-3, "dp": 0.3e-3,
+                   "stretch_per_end": 7.0e-3, "t_total": 100.0, "n_outer": 10000,
+                   "eta": 1.0e4, "energy_pct": 0.005, "ref_force": 80000.0,
+                   "ref_displacement": 14.0e-3},
+    "fsi_2d": {**_BASE, **_NAFION, "length": 10.0e-3, "width": 0.125e-3,
+               "dp": 0.125e-3 / 8.0, "anisotropy": 4.0, "contact_time": 10.0,
+               "t_total": 100.0, "n_outer": 125, "eta": 1.0e3, "energy_pct": 1.0e-6,
+               "evaporation_rate": 0.0},
+    "fsi_3d": {**_BASE, **_NAFION, "length": 10.0e-3, "breadth": 10.0e-3,
+               "thickness": 0.125e-3, "dp": 0.125e-3 / 8.0, "anisotropy": 8.0,
+               "contact_time": 450.0, "t_total": 2500.0, "n_outer": 0, "eta": 1.0e4,
+               "energy_pct": 3.0e-7, "evaporation_rate": 2.0e-3},
+    # BASELINE configs[0]: left clamp, right end pulled at 1e-3 per unit
+    # time to 20 % strain (4 length units), outer dt 0.01
+    "bar_2d": {**_BASE, **_POWER, "length": 20.0, "width": 2.0, "dp": 0.1,
+               "stretch_per_end": 4.0, "t_total": 4000.0, "n_outer": 400000,
+               "ref_force": 1.0, "ref_displacement": 1.0},
+    # BASELINE configs[2]: same material/loading, 3D
+    "bar_3d": {**_BASE, **_POWER, "length": 20.0, "width": 2.0, "breadth": 2.0,
+               "dp": 0.02, "stretch_per_end": 4.0, "t_total": 4000.0, "n_outer": 400000,
+               "ref_force": 1.0, "ref_displacement": 1.0},
+    # BASELINE configs[4]: +-5 % jittered block, config-0 material, uniaxial
+    "block_3d": {**_BASE, **_POWER, "length": 4.0, "width": 2.0, "breadth": 2.0,
+                 "dp": 0.02, "jitter": 0.05, "stretch_per_end": 0.8, "t_total": 800.0,
+                 "n_outer": 80000, "ref_force": 1.0, "ref_displacement": 1.0},
+    # BASELINE configs[1]: Nafion-like strip, rho 1, E 1, nu 0.35, D 1e-3,
+    # cantilever (left clamp), saturation held on the top face; swelling
+    # through the reference's pore-pressure law with C chosen so that full
+    # saturation gives 5 % free isotropic swelling strain
+    "membrane_2d": {**_BASE, "density": 1.0, "diffusivity": 1.0e-3, "pressure_coeff": 0.0,
+                    "youngs_modulus": 1.0, "poisson_ratio": 0.35, "porosity": 0.4,
+                    "fluid_density": 1.0, "initial_saturation": 0.0, "contact_frac": 1.0,
+                    "contact_face": "top", "length": 10.0, "width": 0.5, "dp": 0.025,
+                    "anisotropy": 1.0, "contact_time": 1.0e30, "t_total": 62.5,
+                    "n_outer": 400, "eta": 0.0, "energy_pct": 1.0e-8,
+                    "evaporation_rate": 0.0, "h_factor": 1.3},
+}
+
+FSI_SCENARIOS = ("fsi_2d", "fsi_3d", "membrane_2d")
+
+
+@dataclass
+class RunConfig:
+    path: str
+    raw: dict
+    params: dict
+    lines: dict = field(default_factory=dict)
+
+    @property
+    def scenario(self) -> str:
+        return self.params["scenario"]
+
+
+def _convert(key: str, text: str, line_no: int):
+    spec = KEYS[key]
+    try:
+        if spec.kind is bool:
+            t = text.lower()
+            if t in ("true", "yes", "on", "1"):
+                value = True
+            elif t in ("false", "no", "off", "0"):
+                value = False
+            else:
+                raise ValueError(text)
+        elif spec.kind is int:
+            f = float(text)          # counts may be written as 1e4
+            if f != int(f):
+                raise ValueError(text)
+            value = int(f)
+        elif spec.kind is float:
+            value = float(text)
+        else:
+            value = text
+    except ValueError:
+        raise ConfigError(f"line {line_no}: value {text!r} for key {key!r} is not "
+                          f"a valid {spec.kind.__name__}") from None
+    if spec.check is not None and not spec.check(value):
+        what = "out of range" if spec.kind in (int, float) else "invalid"
+        raise ConfigError(f"line {line_no}: value {value!r} for key {key!r} {what} "
+                          f"({spec.rule})")
+    return value
+
+
+def parse_file(path: str):
+    """(raw key/value dict, key -> line number) of a config file."""
+    raw, where = {}, {}
+    with open(path, "r", encoding="utf-8") as fh:
+        for no, line in enumerate(fh, start=1):
+            text = line.split("#", 1)[0].strip()
+            if not text:
+                continue
+            if text[0] == "[" and text[-1] == "]":
+                if text[1:-1].strip() not in SECTIONS:
+                    raise ConfigError(f"line {no}: unknown section {text}")
+                continue
+            if "=" not in text:
+                raise ConfigError(f"line {no}: expected 'key = value', got {text!r}")
+            key, _, val = (p.strip() for p in text.partition("="))
+            if key not in KEYS:
+                raise ConfigError(f"line {no}: unknown key {key!r}")
+            if key in raw:
+                raise ConfigError(f"line {no}: duplicate key {key!r}")
+            raw[key] = _convert(key, val, no)
+            where[key] = no
+    return raw, where
+
+
+def resolve(raw: dict, path: str = "<memory>", lines: dict | None = None,
+            overrides: dict | None = None) -> RunConfig:
+    """Scenario defaults + explicit keys (+ CLI overrides), validated."""
+    merged = dict(raw)
+    merged.update({k: v for k, v in (overrides or {}).items() if v is not None})
+    name = merged.get("scenario")
+    if name is None:
+        raise ConfigError("config must set 'scenario'")
+    if name not in SCENARIO_DEFAULTS:
+        raise ConfigError(f"unknown scenario {name!r} (known: "
+                          f"{', '.join(sorted(SCENARIO_DEFAULTS))})")
+    defaults = SCENARIO_DEFAULTS[name]
+    for key in merged:
+        if key != "scenario" and key not in defaults:
+            at = f"line {lines[key]}: " if lines and key in lines else ""
+            raise ConfigError(f"{at}key {key!r} does not apply to scenario {name!r}")
+    params = {**defaults, **merged, "scenario": name}
+    _derive(params)
+    return RunConfig(path=path, raw=merged, params=params, lines=dict(lines or {}))
+
+
+def _derive(p: dict) -> None:
+    name = p["scenario"]
+    if p["n_outer"] == 0:
+        if name not in FSI_SCENARIOS:
+            raise ConfigError("n_outer must be positive for necking scenarios")
+        h = p["h_factor"] * p["dp"]
+        p["n_outer"] = int(math.ceil(p["t_total"] / (0.5 * h * h / p["diffusivity"])))
+    if name in ("bar_2d", "bar_3d", "block_3d") and p["eta"] == 0.0:
+        c = math.sqrt(p["bulk_modulus"] / p["density"])
+        p["eta"] = 0.1 * p["density"] * c * p["h_factor"] * p["dp"]
+    if name == "membrane_2d":
+        e, nu = p["youngs_modulus"], p["poisson_ratio"]
+        mu = e / (2.0 * (1.0 + nu))
+        lam = e / (3.0 * (1.0 - 2.0 * nu)) - 2.0 * mu / 3.0
+        if p["pressure_coeff"] == 0.0:
+            # plane-strain free swelling: sigma = 2 mu e + lam tr(e) I - p I = 0
+            # with e = eps I  ->  p = 2 (mu + lam) eps;  eps = 0.05 at sat = a
+            p["pressure_coeff"] = 2.0 * (mu + lam) * 0.05 / p["porosity"]
+        if p["eta"] == 0.0:
+            c = math.sqrt((e / (3.0 * (1.0 - 2.0 * nu))) / p["density"])
+            p["eta"] = 0.1 * p["density"] * c * p["h_factor"] * p["dp"]
+
+
+def load_config(path: str, overrides: dict | None = None) -> RunConfig:
+    raw, where = parse_file(path)
+    return resolve(raw, path=path, lines=where, overrides=overrides)

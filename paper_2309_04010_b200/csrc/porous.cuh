@@ -1,1 +1,521 @@
+// porous.cuh -- partially saturated porous membrane on the GPU.
+//
+// Outer (slow) step = PorousProblem.advance_slow (scenarios.py:226):
+//   k_por_prep      J, current volume, rho_l, saturation, D rho_l, and the
+//                   gradient map A = F^-1 B^T              (porous.py:456-473)
+//   k_por_flux      q_a = D rho_l,a sum_b V_b (s_a - s_b) (A_a gradW)    (:503)
+//   k_por_mass      conservative pair-form mass rate, gathered per
+//                   particle (no atomics, fixed order), clamp + counting,
+//                   contact constraint / evaporation                      (:476)
+//   k_por_post      pressure, mixture masses, momentum rebuild, solid /
+//                   fluid velocity split with the dry guard               (:601)
+//   k_por_fluxrate  advected-momentum rate -sum V_b (vq_a+vq_b).(A_a gradW) (:574)
+// Inner step = PorousProblem.relax_step (scenarios.py:278):
+//   k_por_kick1     M += dt/2 rate, clamps, v_s, x += dt v_s
+//   k_por_stress    SELL gather dF/dt, F += dt dF/dt, Almansi mixture
+//                   stress, nominal stress, T = Pm B                   (_accel.py:240)
+//   k_por_accel     SELL gather of (T_a + T_b).gradW + flux rate, kick,
+//                   energy-density / |a| partials
+//   sweep           damping with mixture masses
+//   k_por_post_step momentum rebuild, |v|max partial
 #pragma once
+
+#include "damping.cuh"
+#include "solid.cuh"
+
+namespace mtsph {
+
+enum { PF_MOVABLE = 1, PF_CONTACT = 2 };
+
+struct PorMat {
+    double rho_s0, D, C, mu, lam, porosity, rho_l0, sat0;
+};
+
+struct PorousArgs {
+    int64_t n;
+    const double4 *XV;
+    void *V;                        // solid velocity (VT<D>)
+    double *x, *F, *M, *q, *vl, *rate, *frate;
+    double *mass_l, *sat, *pres, *J, *rho_lf, *mix, *inv_mix;
+    double *volc, *coeff, *amap, *mrate;
+    double *T;
+    const double *B;
+    const uint8_t *flags;
+    const int64_t *slice_ptr;
+    const int32_t *slice_w, *nbr;
+    const int64_t *perm;
+    double *part;
+    int nblk;
+    Ctrl *ctrl;
+    KSpec ks;
+    PorMat m;
+};
+
+template <int D>
+__global__ void __launch_bounds__(256) k_por_prep(PorousArgs A, int with_amap) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= A.n) return;
+    const int64_t n = A.n;
+    double F[D * D];
+#pragma unroll
+    for (int k = 0; k < D * D; ++k) F[k] = A.F[(int64_t)k * n + i];
+    const double j = det_d<D>(F);
+    if (!(j > 0.0)) atomicMin(&A.ctrl->err_inv, (unsigned long long)A.perm[i]);
+    const double vol = volof<D>(A.XV[i]) * j;
+    const double rho_l = A.mass_l[i] / vol;
+    A.volc[i] = vol;
+    A.sat[i] = rho_l / A.m.rho_l0;
+    A.coeff[i] = A.m.D * rho_l;
+    A.J[i] = j;
+    if (with_amap) {
+        double fi[D * D], Bm[D * D], am[D * D];
+        inv_d<D>(F, j, fi);
+#pragma unroll
+        for (int k = 0; k < D * D; ++k) Bm[k] = A.B[(int64_t)k * n + i];
+        mmt<D>(fi, Bm, am);  // F^-1 B^T
+#pragma unroll
+        for (int k = 0; k < D * D; ++k) A.amap[(int64_t)k * n + i] = am[k];
+    }
+}
+
+template <int D>
+__global__ void __launch_bounds__(256) k_por_flux(PorousArgs A) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= A.n) return;
+    const int64_t n = A.n;
+    double xa[3], am[D * D], acc[D];
+    xget<D>(A.XV[i], xa);
+#pragma unroll
+    for (int k = 0; k < D * D; ++k) am[k] = A.amap[(int64_t)k * n + i];
+#pragma unroll
+    for (int k = 0; k < D; ++k) acc[k] = 0.0;
+    const double sa = A.sat[i];
+    const int64_t base = A.slice_ptr[i >> 5] + (i & 31);
+    const int w = A.slice_w[i >> 5];
+    for (int m = 0; m < w; ++m) {
+        const int32_t b = __ldg(A.nbr + base + (int64_t)m * 32);
+        const double4 xvb = ldg4(A.XV + b);
+        double xb[3], rel[D], g[D];
+        xget<D>(xvb, xb);
+#pragma unroll
+        for (int k = 0; k < D; ++k) rel[k] = xb[k] - xa[k];
+        grad_w<D>(rel, A.ks, g);
+        const double wgt = A.volc[b] * (sa - A.sat[b]);
+#pragma unroll
+        for (int r = 0; r < D; ++r) {
+            double s = 0.0;
+#pragma unroll
+            for (int c = 0; c < D; ++c) s += am[r * D + c] * g[c];
+            acc[r] += wgt * s;
+        }
+    }
+    const double cf = A.coeff[i];
+#pragma unroll
+    for (int r = 0; r < D; ++r) A.q[(int64_t)r * n + i] = acc[r] * cf;
+}
+
+// mass update + clamp + contact/evaporation; partial[0][blk] = clamp count
+template <int D>
+__global__ void __launch_bounds__(256) k_por_mass(PorousArgs A, double dt, int contact_on, double evap_factor) {
+    __shared__ double sh[32];
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t n = A.n;
+    double clamped = 0.0;
+    if (i < n) {
+        double xa[3], ama[D * D], qa[D];
+        xget<D>(A.XV[i], xa);
+#pragma unroll
+        for (int k = 0; k < D * D; ++k) ama[k] = A.amap[(int64_t)k * n + i];
+#pragma unroll
+        for (int k = 0; k < D; ++k) qa[k] = A.q[(int64_t)k * n + i];
+        const double va = A.volc[i];
+        double rate = 0.0;
+        const int64_t base = A.slice_ptr[i >> 5] + (i & 31);
+        const int w = A.slice_w[i >> 5];
+        for (int m = 0; m < w; ++m) {
+            const int32_t b = __ldg(A.nbr + base + (int64_t)m * 32);
+            if (b == i) continue;
+            const double4 xvb = ldg4(A.XV + b);
+            double xb[3], rel[D], g[D];
+            xget<D>(xvb, xb);
+#pragma unroll
+            for (int k = 0; k < D; ++k) rel[k] = xb[k] - xa[k];
+            grad_w<D>(rel, A.ks, g);
+            double acc = 0.0;
+#pragma unroll
+            for (int r = 0; r < D; ++r) {
+                double s = 0.0;
+#pragma unroll
+                for (int c = 0; c < D; ++c) s += 0.5 * (ama[r * D + c] + A.amap[(int64_t)(r * D + c) * n + b]) * g[c];
+                acc += (qa[r] + A.q[(int64_t)r * n + b]) * s;
+            }
+            rate -= va * A.volc[b] * acc;
+        }
+        double mass = A.mass_l[i] + dt * rate;
+        const double cap = A.m.porosity * A.m.rho_l0 * va;
+        if (mass < 0.0 || mass > cap) clamped = 1.0;
+        mass = fmin(fmax(mass, 0.0), cap);
+        if (contact_on) {
+            if (A.flags[i] & PF_CONTACT) mass = A.m.porosity * A.m.rho_l0 * va;
+        } else if (evap_factor != 1.0) {
+            mass = mass * evap_factor;
+        }
+        A.mass_l[i] = mass;
+    }
+    const double s = block_sum<256>(clamped, sh);
+    if (threadIdx.x == 0) A.part[blockIdx.x] = s;
+}
+
+// split_velocities (porous.py:601) for particle i; returns v_s, v_l
+template <int D>
+__device__ __forceinline__ void split_vel(const PorousArgs &A, int64_t i, double j, const double *M,
+                                          const double *q, double *vs, double *vl) {
+    const double rho_s = A.m.rho_s0 / j;
+    const double rho_l = A.mass_l[i] / (volof<D>(A.XV[i]) * j);
+    const double rho = rho_s + rho_l;
+    const bool dry = rho_l < 1e-12 * A.m.rho_l0;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+        const double f = dry ? 0.0 : q[k];
+        vs[k] = (M[k] - f) / rho;
+        vl[k] = dry ? vs[k] : vs[k] + f / (dry ? 1.0 : rho_l);
+    }
+    if (!(A.flags[i] & PF_MOVABLE)) {
+#pragma unroll
+        for (int k = 0; k < D; ++k) { vs[k] = 0.0; vl[k] = 0.0; }
+    }
+}
+
+template <int D>
+__global__ void __launch_bounds__(256) k_por_post(PorousArgs A) {
+    using V_t = typename VT<D>::T;
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= A.n) return;
+    const int64_t n = A.n;
+    const double sat = A.sat[i];
+    A.pres[i] = A.m.C * (sat - A.m.sat0);
+    const double mix = A.m.rho_s0 * volof<D>(A.XV[i]) + A.mass_l[i];
+    A.mix[i] = mix;
+    const bool movable = A.flags[i] & PF_MOVABLE;
+    A.inv_mix[i] = movable ? 1.0 / mix : 0.0;
+    const double rho_lf = sat * A.m.rho_l0;
+    A.rho_lf[i] = rho_lf;
+    const double j = A.J[i];
+    const double rho = A.m.rho_s0 / j + rho_lf;
+    V_t *V = reinterpret_cast<V_t *>(A.V);
+    double v0[3], M[D], q[D], vs[D], vl[D];
+    vget(V[i], v0);
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+        q[k] = A.q[(int64_t)k * n + i];
+        M[k] = movable ? rho * v0[k] + q[k] : q[k];
+        A.M[(int64_t)k * n + i] = M[k];
+    }
+    split_vel<D>(A, i, j, M, q, vs, vl);
+    double v3[3] = {0, 0, 0};
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+        v3[k] = vs[k];
+        A.vl[(int64_t)k * n + i] = vl[k];
+    }
+    V_t w;
+    vset(w, v3);
+    V[i] = w;
+}
+
+template <int D>
+__global__ void __launch_bounds__(256) k_por_fluxrate(PorousArgs A) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= A.n) return;
+    const int64_t n = A.n;
+    double xa[3], am[D * D], vqa[D * D], acc[D];
+    xget<D>(A.XV[i], xa);
+#pragma unroll
+    for (int k = 0; k < D * D; ++k) am[k] = -A.amap[(int64_t)k * n + i];
+#pragma unroll
+    for (int r = 0; r < D; ++r)
+#pragma unroll
+        for (int c = 0; c < D; ++c) vqa[r * D + c] = A.vl[(int64_t)r * n + i] * A.q[(int64_t)c * n + i];
+#pragma unroll
+    for (int k = 0; k < D; ++k) acc[k] = 0.0;
+    const int64_t base = A.slice_ptr[i >> 5] + (i & 31);
+    const int w = A.slice_w[i >> 5];
+    for (int m = 0; m < w; ++m) {
+        const int32_t b = __ldg(A.nbr + base + (int64_t)m * 32);
+        const double4 xvb = ldg4(A.XV + b);
+        double xb[3], rel[D], g0[D], g[D];
+        xget<D>(xvb, xb);
+#pragma unroll
+        for (int k = 0; k < D; ++k) rel[k] = xb[k] - xa[k];
+        grad_w<D>(rel, A.ks, g0);
+#pragma unroll
+        for (int r = 0; r < D; ++r) {
+            double s = 0.0;
+#pragma unroll
+            for (int c = 0; c < D; ++c) s += am[r * D + c] * g0[c];
+            g[r] = s;
+        }
+        const double vb = A.volc[b];
+#pragma unroll
+        for (int r = 0; r < D; ++r) {
+            double s = 0.0;
+#pragma unroll
+            for (int c = 0; c < D; ++c)
+                s += (vqa[r * D + c] + A.vl[(int64_t)r * n + b] * A.q[(int64_t)c * n + b]) * g[c];
+            acc[r] += vb * s;
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < D; ++r) A.frate[(int64_t)r * n + i] = acc[r];
+}
+
+// ---------------------------------------------------------- inner step
+
+template <int D>
+__global__ void __launch_bounds__(256) k_por_kick1(PorousArgs A) {
+    using V_t = typename VT<D>::T;
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= A.n) return;
+    const Ctrl *c = A.ctrl;
+    if (c->done) return;
+    const double dt = c->dt;
+    const int64_t n = A.n;
+    const bool movable = A.flags[i] & PF_MOVABLE;
+    const double rho = A.m.rho_s0 / A.J[i] + A.rho_lf[i];
+    double v[3] = {0, 0, 0};
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+        const double q = A.q[(int64_t)k * n + i];
+        double M = A.M[(int64_t)k * n + i] + 0.5 * dt * A.rate[(int64_t)k * n + i];
+        if (!movable) M = q;
+        A.M[(int64_t)k * n + i] = M;
+        v[k] = movable ? (M - q) / rho : 0.0;
+        A.x[(int64_t)k * n + i] += dt * v[k];
+    }
+    V_t w;
+    vset(w, v);
+    reinterpret_cast<V_t *>(A.V)[i] = w;
+}
+
+template <int D>
+__global__ void __launch_bounds__(256) k_por_stress(PorousArgs A) {
+    using V_t = typename VT<D>::T;
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= A.n) return;
+    Ctrl *c = A.ctrl;
+    if (c->done) return;
+    const double dt = c->dt;
+    const int64_t n = A.n;
+    const V_t *V = reinterpret_cast<const V_t *>(A.V);
+    double xa[3], va[3], acc[D * D];
+    xget<D>(A.XV[i], xa);
+    vget(V[i], va);
+#pragma unroll
+    for (int k = 0; k < D * D; ++k) acc[k] = 0.0;
+    const int64_t base = A.slice_ptr[i >> 5] + (i & 31);
+    const int w = A.slice_w[i >> 5];
+    for (int m = 0; m < w; ++m) {
+        const int32_t b = __ldg(A.nbr + base + (int64_t)m * 32);
+        const double4 xvb = ldg4(A.XV + b);
+        double xb[3], vb[3], rel[D], g[D];
+        xget<D>(xvb, xb);
+        vget(V[b], vb);
+#pragma unroll
+        for (int k = 0; k < D; ++k) rel[k] = xb[k] - xa[k];
+        grad_w<D>(rel, A.ks, g);
+        const double volb = volof<D>(xvb);
+#pragma unroll
+        for (int r = 0; r < D; ++r) {
+            const double dv = volb * (vb[r] - va[r]);
+#pragma unroll
+            for (int cc = 0; cc < D; ++cc) acc[r * D + cc] += dv * g[cc];
+        }
+    }
+    double Bm[D * D], F[D * D], L[D * D];
+#pragma unroll
+    for (int k = 0; k < D * D; ++k) {
+        Bm[k] = A.B[(int64_t)k * n + i];
+        F[k] = A.F[(int64_t)k * n + i];
+    }
+    mm<D>(acc, Bm, L);
+#pragma unroll
+    for (int k = 0; k < D * D; ++k) {
+        F[k] += dt * L[k];
+        A.F[(int64_t)k * n + i] = F[k];
+    }
+    const double j = det_d<D>(F);
+    A.J[i] = j;
+    double Tm[D * D];
+    if (!(j > 0.0)) {
+        atomicMin(&c->err_inv, (unsigned long long)A.perm[i]);
+#pragma unroll
+        for (int k = 0; k < D * D; ++k) Tm[k] = 0.0;
+    } else {
+        double fi[D * D], e[D * D], sg[D * D], pm[D * D];
+        inv_d<D>(F, j, fi);
+        double tre = 0.0;
+#pragma unroll
+        for (int r = 0; r < D; ++r) {
+#pragma unroll
+            for (int cc = 0; cc < D; ++cc) {
+                double s = 0.0;
+#pragma unroll
+                for (int k = 0; k < D; ++k) s += fi[k * D + r] * fi[k * D + cc];
+                e[r * D + cc] = -0.5 * s;
+            }
+            e[r * D + r] += 0.5;
+            tre += e[r * D + r];
+        }
+        const double dia = A.m.lam * tre - A.pres[i];
+#pragma unroll
+        for (int k = 0; k < D * D; ++k) sg[k] = 2.0 * A.m.mu * e[k];
+#pragma unroll
+        for (int r = 0; r < D; ++r) sg[r * D + r] += dia;
+        double tmp[D * D];
+        mmt<D>(sg, fi, tmp);  // sigma F^-T
+#pragma unroll
+        for (int k = 0; k < D * D; ++k) pm[k] = j * tmp[k];
+        mm<D>(pm, Bm, Tm);
+    }
+    tstore<D>(A.T, i, Tm);
+}
+
+template <int D>
+__global__ void __launch_bounds__(256) k_por_accel(PorousArgs A) {
+    using V_t = typename VT<D>::T;
+    __shared__ double sh[32];
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const Ctrl *c = A.ctrl;
+    if (c->done) return;
+    const int64_t n = A.n;
+    double ek = 0.0, a2m = 0.0;
+    if (i < n) {
+        const double dt = c->dt;
+        double xa[3], Ta[D * D], acc[D];
+        xget<D>(A.XV[i], xa);
+        tload<D>(A.T, i, Ta);
+#pragma unroll
+        for (int k = 0; k < D; ++k) acc[k] = 0.0;
+        const int64_t base = A.slice_ptr[i >> 5] + (i & 31);
+        const int w = A.slice_w[i >> 5];
+        for (int m = 0; m < w; ++m) {
+            const int32_t b = __ldg(A.nbr + base + (int64_t)m * 32);
+            const double4 xvb = ldg4(A.XV + b);
+            double xb[3], Tb[D * D], rel[D], g[D];
+            xget<D>(xvb, xb);
+            tload<D>(A.T, b, Tb);
+#pragma unroll
+            for (int k = 0; k < D; ++k) rel[k] = xb[k] - xa[k];
+            grad_w<D>(rel, A.ks, g);
+            const double volb = volof<D>(xvb);
+#pragma unroll
+            for (int r = 0; r < D; ++r) {
+                double s = 0.0;
+#pragma unroll
+                for (int cc = 0; cc < D; ++cc) s += (Ta[r * D + cc] + Tb[r * D + cc]) * g[cc];
+                acc[r] += volb * s;
+            }
+        }
+        const bool movable = A.flags[i] & PF_MOVABLE;
+        const double rho = A.m.rho_s0 / A.J[i] + A.rho_lf[i];
+        const double rmix = A.mix[i] / volof<D>(A.XV[i]);
+        double v[3] = {0, 0, 0}, v2 = 0.0, aa = 0.0;
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+            const double rt = acc[k] + A.frate[(int64_t)k * n + i];
+            A.rate[(int64_t)k * n + i] = rt;
+            const double q = A.q[(int64_t)k * n + i];
+            double M = A.M[(int64_t)k * n + i] + 0.5 * dt * rt;
+            if (!movable) M = q;
+            A.M[(int64_t)k * n + i] = M;
+            v[k] = movable ? (M - q) / rho : 0.0;
+            v2 += v[k] * v[k];
+            aa += rt * rt;
+        }
+        V_t w2;
+        vset(w2, v);
+        reinterpret_cast<V_t *>(A.V)[i] = w2;
+        if (movable) {
+            ek = A.mix[i] * v2;
+            a2m = aa / (rmix * rmix);
+        }
+    }
+    const double se = block_sum<256>(ek, sh);
+    const double sa = block_max<256>(a2m, sh);
+    if (threadIdx.x == 0) {
+        A.part[blockIdx.x] = se;
+        A.part[A.nblk + blockIdx.x] = sa;
+    }
+}
+
+// momentum rebuild after damping + |v|^2 max; with_accel = 1 is the
+// pre-loop reduction (no rebuild; |a|^2 of the free particles)
+template <int D>
+__global__ void __launch_bounds__(256) k_por_post_step(PorousArgs A, int pre_loop) {
+    using V_t = typename VT<D>::T;
+    __shared__ double sh[32];
+    if (!pre_loop && A.ctrl->done) return;
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t n = A.n;
+    double v2 = 0.0, a2 = 0.0;
+    if (i < n) {
+        double v[3];
+        vget(reinterpret_cast<const V_t *>(A.V)[i], v);
+        const bool movable = A.flags[i] & PF_MOVABLE;
+        if (!pre_loop) {
+            const double rho = A.m.rho_s0 / A.J[i] + A.rho_lf[i];
+#pragma unroll
+            for (int k = 0; k < D; ++k) {
+                const double q = A.q[(int64_t)k * n + i];
+                A.M[(int64_t)k * n + i] = movable ? rho * v[k] + q : q;
+            }
+        } else if (movable) {
+            const double rmix = A.mix[i] / volof<D>(A.XV[i]);
+            double aa = 0.0;
+#pragma unroll
+            for (int k = 0; k < D; ++k) {
+                const double r = A.rate[(int64_t)k * n + i];
+                aa += r * r;
+            }
+            a2 = aa / (rmix * rmix);
+        }
+#pragma unroll
+        for (int k = 0; k < D; ++k) v2 += v[k] * v[k];
+    }
+    const double mv = block_max<256>(v2, sh);
+    const double ma = block_max<256>(a2, sh);
+    if (threadIdx.x == 0) {
+        A.part[2 * A.nblk + blockIdx.x] = mv;
+        if (pre_loop) A.part[A.nblk + blockIdx.x] = ma;
+    }
+}
+
+// measure(): split_velocities refresh (vel_solid, vel_fluid) from M and q
+template <int D>
+__global__ void __launch_bounds__(256) k_por_refresh(PorousArgs A) {
+    using V_t = typename VT<D>::T;
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= A.n) return;
+    const int64_t n = A.n;
+    double F[D * D], M[D], q[D], vs[D], vl[D];
+#pragma unroll
+    for (int k = 0; k < D * D; ++k) F[k] = A.F[(int64_t)k * n + i];
+    const double j = det_d<D>(F);
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+        M[k] = A.M[(int64_t)k * n + i];
+        q[k] = A.q[(int64_t)k * n + i];
+    }
+    split_vel<D>(A, i, j, M, q, vs, vl);
+    double v3[3] = {0, 0, 0};
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+        v3[k] = vs[k];
+        A.vl[(int64_t)k * n + i] = vl[k];
+    }
+    V_t w;
+    vset(w, v3);
+    reinterpret_cast<V_t *>(A.V)[i] = w;
+}
+
+}  // namespace mtsph
