@@ -1,0 +1,344 @@
+#!/usr/bin/env python
+"""Benchmark: inner solid-relaxation particle-steps/s on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload bar_3d] [--dp 0.02] [--sweep coloured|serial]
+
+One "step" = one inner relaxation step (NeckingProblem.relax_step +
+stable_time_step + energy bookkeeping) over every particle of the
+workload: kick/drift, deformation-rate gather, F update, J2 return map
+(power-law hardening), stress divergence gather, kick, pairwise implicit
+damping sweep, reductions and device-side control.
+
+Workload (BASELINE.json configs[2], the 1-GPU case): 3D bar 20 x 2 x 2,
+dp 0.02 (1000 x 100 x 100 = 10,000,000 particles), Wendland C2 with
+h = 1.3 dp, rho 1, E 200, nu 0.3, power-law hardening s0 = 0.25,
+e0 = 0.01, n = 0.2, left end clamped, fp64.  The bar is pre-stretched
+uniformly by 0.5 % (4x the yield strain) so the return map runs its
+plastic branch, then relaxed by the timed steps.  The state (~10 GB) is
+far larger than L2, so no L2 flush is needed between steps.
+
+`value`: device time (CUDA events captured into the step graph) of K
+steps with the state resident in HBM.  `e2e`: the same steps driven
+through the reference's per-step protocol over the C ABI
+(mtsph_solid_stable_dt + mtsph_solid_relax_step: pinned H2D of the step's
+control block, D2H of its energy/time-step result each step), wall clock.
+
+--impl reference: the CPU oracle (a C/OpenMP restatement of the
+reference's numba loops, oracle/) on a bounded slice of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM_GBS = 6650.0
+PRESTRAIN = 0.005
+
+
+def load_peaks():
+    try:
+        with open(PEAKS_PATH) as fh:
+            pk = json.load(fh)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback"
+
+
+def workload_params(args):
+    from paper_2309_04010_b200.config import resolve
+    raw = {"scenario": args.workload, "damping_sweep": args.sweep}
+    if args.dp:
+        raw["dp"] = args.dp
+    return resolve(raw).params
+
+
+def sample_params(params, target_cols):
+    """A slice of the workload (same cross-section, shorter length) for the
+    CPU baseline: per-particle work is identical."""
+    p = dict(params)
+    cols = max(int(target_cols), 8)
+    p["length"] = cols * p["dp"]
+    return p
+
+
+# ------------------------------------------------------------------ clocks
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.path = os.path.join("/tmp", f"bench_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        self.proc.wait()
+        sm, smax, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[4:8]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ model
+
+def algorithmic_bytes(d, nnz_pp, pairs_pp, groups_pp):
+    """Compulsory HBM bytes per particle per step for each kernel class
+    (every array element the kernel needs is moved once; the neighbour
+    index table counts its true entries).  See DESIGN.md §4."""
+    dd = d * d
+    vec, ten = 8 * d, 8 * dd
+    xv = 8 * (d + 1)                      # reference position + volume
+    return {
+        "kick_drift": 2 * vec + vec + 2 * vec + 1,
+        "stress": xv + vec + 4 * nnz_pp + ten + 2 * ten + 2 * ten + 16 + ten,
+        "accel": xv + ten + 4 * nnz_pp + 8 + 1 + 8 + 2 * vec + vec,
+        "sweep": 2 * vec + xv + 8 + 2 * (8 * pairs_pp + 8 * groups_pp),
+        "reduce": vec,
+    }
+
+
+def build_solid(params, sweep):
+    from paper_2309_04010_b200 import lattices
+    from paper_2309_04010_b200.device import DeviceSolid
+    from paper_2309_04010_b200.scenarios import _necking_materials
+    lat = lattices.build_lattice(params)
+    elastic, hard = _necking_materials(params)
+    law, hp = hard.device_params()
+    t0 = time.perf_counter()
+    dev = DeviceSolid(lat.pos, lat.vol, elastic.density0, lat.constrained, lat.side, lat.mid_mask,
+                      lat.h_axes, elastic.shear_modulus, elastic.bulk_modulus, plastic=True,
+                      hardening_law=law, hard=hp, sweep=sweep)
+    setup_s = time.perf_counter() - t0
+    d = lat.pos.shape[1]
+    nu = elastic.poisson_ratio
+    Fm = np.eye(d)
+    Fm[0, 0] = 1.0 + PRESTRAIN
+    for k in range(1, d):
+        Fm[k, k] = 1.0 - nu * PRESTRAIN
+    dev.set("F", np.broadcast_to(Fm, (lat.n, d, d)))
+    dev.set("pos", lat.pos @ Fm.T)
+    return dev, lat, elastic, setup_s
+
+
+def run_ours(args):
+    import torch  # noqa: F401  (plumbing only: torch.distributed for N > 1)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    os.environ.setdefault("CUDA_VISIBLE_DEVICES_LOCAL", str(local))
+    params = workload_params(args)
+    dev, lat, elastic, setup_s = build_solid(params, args.sweep)
+    eta, cfl = params["eta"], params["cfl"]
+    n, d = lat.pos.shape
+    sz = dev.sizes()
+    # warm-up (captures the step graph; at least W steps)
+    done = 0
+    while done < args.warmup:
+        dev.run_steps(args.steps, eta, cfl)
+        done += args.steps
+    launches0 = dev.launches()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    timing = dev.run_steps(args.steps, eta, cfl)
+    clk = clocks.stop()
+    launches = dev.launches() - launches0
+    ms = timing["total_ms"]
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * n * args.steps / (ms / 1e3)
+    # end to end through the per-step protocol (host round trip per step)
+    e2e_steps = max(3, min(args.steps, 20))
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        dt = dev.stable_dt(cfl)
+        dev.relax_step(dt, eta)
+    e2e_s = time.perf_counter() - t0
+    e2e = world * n * e2e_steps / e2e_s
+    ctrl_bytes = 160
+    # roofline of the dominant kernel class
+    peak, peak_kind = load_peaks()
+    model = algorithmic_bytes(d, sz["nnz"] / n, sz["npairs"] / n, sz["ngroups"] / n)
+    classes = {"kick_drift": timing["kick_drift_ms"], "stress": timing["stress_ms"],
+               "accel": timing["accel_ms"], "sweep": timing["sweep_ms"],
+               "reduce": timing["reduce_ms"]}
+    kernels = {}
+    for name, tms in classes.items():
+        per_step_s = tms / 1e3 / args.steps
+        gbs = model[name] * n / per_step_s / 1e9 if per_step_s > 0 else 0.0
+        kernels[name] = {"ms_per_step": tms / args.steps, "share": tms / ms if ms else 0.0,
+                         "bytes_per_particle": model[name], "achieved_gbs": gbs}
+    top = max(classes, key=classes.get)
+    k_top = kernels[top]
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic_r01.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(top)
+        except Exception:
+            traffic = None
+    line = {
+        "metric": "inner solid-relaxation particle-steps/sec",
+        "value": value, "unit": "particle-steps/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.workload} (BASELINE configs[2])",
+                   "particles_per_gpu": n, "dp": params["dp"], "h_over_dp": params["h_factor"],
+                   "material": "rho 1, E 200, nu 0.3, J2 power-law s0 0.25 e0 0.01 n 0.2",
+                   "prestrain": PRESTRAIN, "damping_sweep": args.sweep,
+                   "sweep_phases": sz["phases"], "neighbours_per_particle": sz["nnz"] / n,
+                   "pairs": sz["npairs"], "groups": sz["ngroups"],
+                   "l2": "state >> 126 MB L2 (no flush needed)",
+                   "parallelism": "replicas" if world > 1 else "1 GPU",
+                   "setup_s": setup_s},
+        "e2e": {"value": e2e, "unit": "particle-steps/s", "h2d_bytes_per_step": 2 * ctrl_bytes,
+                "d2h_bytes_per_step": 4 * ctrl_bytes,
+                "path": "C ABI per-step protocol mtsph_solid_stable_dt + mtsph_solid_relax_step"},
+        "roofline": {"kernel": top, "bound": "hbm", "achieved": k_top["achieved_gbs"],
+                     "peak": peak, "unit": "GB/s",
+                     "frac": k_top["achieved_gbs"] / peak, "traffic": traffic,
+                     "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"},
+        "kernels": kernels,
+        "gpu_launches": launches,
+        "clocks": clk,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(params, args, budget_s=args.cpu_budget)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def cpu_baseline(params, args, budget_s=20.0, steps=None):
+    """Oracle (C/OpenMP restatement of the reference loops) on a slice."""
+    from oracle import oracle as O
+    from oracle.problems import NeckingOracle
+    from paper_2309_04010_b200 import lattices
+    from paper_2309_04010_b200.scenarios import _necking_materials
+    sp = sample_params(params, args.cpu_cols)
+    lat = lattices.build_lattice(sp)
+    elastic, hard = _necking_materials(sp)
+    law, hd = hard.device_params()
+    t0 = time.perf_counter()
+    prob = NeckingOracle(lat.pos, lat.vol, elastic.density0, lat.constrained,
+                         lat.side < 0, lat.side > 0, lat.mid_mask, elastic.shear_modulus,
+                         elastic.bulk_modulus, hd, float(lat.h_axes[0]), hardening_law=law)
+    build_s = time.perf_counter() - t0
+    d = lat.pos.shape[1]
+    Fm = np.eye(d)
+    Fm[0, 0] = 1.0 + PRESTRAIN
+    for k in range(1, d):
+        Fm[k, k] = 1.0 - elastic.poisson_ratio * PRESTRAIN
+    prob.F[:] = Fm
+    prob.pos[:] = lat.pos @ Fm.T
+    n = lat.n
+    done, t0 = 0, time.perf_counter()
+    while True:
+        dt = prob.stable_time_step(params["cfl"])
+        prob.relax_step(dt, params["eta"])
+        done += 1
+        el = time.perf_counter() - t0
+        if (steps is not None and done >= steps) or (steps is None and el > budget_s):
+            break
+    return {"value": n * done / el, "unit": "particle-steps/s", "cores": O.lib().or_num_threads(),
+            "kind": "port",
+            "sample": f"{args.workload} slice {sp['length']:g} x {sp['width']:g} x "
+                      f"{sp['breadth']:g} ({n} particles), {done} inner steps in {el:.1f} s "
+                      f"(oracle build {build_s:.1f} s excluded); serial damping sweep"}
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    params = workload_params(args)
+    steps = max(args.steps, 1)
+    base = cpu_baseline(params, args, steps=steps + args.warmup)
+    line = {
+        "impl": "reference", "metric": "inner solid-relaxation particle-steps/sec",
+        "value": base["value"], "unit": "particle-steps/s", "n_gpus": world, "steps": steps,
+        "warmup": args.warmup, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.workload} (BASELINE configs[2])", "dp": params["dp"]},
+        "cpu_baseline": base,
+        "e2e": {"value": base["value"], "unit": "particle-steps/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--workload", default="bar_3d")
+    ap.add_argument("--dp", type=float, default=0.0)
+    ap.add_argument("--sweep", default="coloured", choices=("coloured", "serial"))
+    ap.add_argument("--cpu-cols", type=int, default=10)
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -189,6 +189,13 @@ mtsph_status mtsph_solid_relax_step(mtsph_solid *s, double dt, double eta, doubl
 /* the whole inner loop on the device (graph-captured chunks)            */
 mtsph_status mtsph_solid_relax(mtsph_solid *s, const mtsph_inner_params *p,
                                mtsph_inner_result *r);
+/* exactly nsteps inner steps as one CUDA graph with CUDA events captured
+ * around every kernel class (benchmark path; the stopping rule is
+ * disabled).  timing[0] = device ms of the whole region, timing[1..5] =
+ * summed ms of kick/drift, stress, divergence, damping sweep, reductions
+ * + control; timing[6] = kernel launches in the region.                 */
+mtsph_status mtsph_solid_run_steps(mtsph_solid *s, const mtsph_inner_params *p,
+                                   int64_t nsteps, double timing[7]);
 /* observables: reaction_force, neck radius, max alpha, min mid alpha,
  * all-finite flag (1/0)                                                 */
 mtsph_status mtsph_solid_measure(mtsph_solid *s, double out[5]);
@@ -196,6 +203,8 @@ mtsph_status mtsph_solid_measure(mtsph_solid *s, double out[5]);
  * "accel","cp_inv","alpha","ref_pos"                                    */
 mtsph_status mtsph_solid_get(mtsph_solid *s, const char *field, double *host);
 mtsph_status mtsph_solid_set(mtsph_solid *s, const char *field, const double *host);
+/* neighbour entries, pairs, groups, sweep phases of the problem         */
+mtsph_status mtsph_solid_sizes(const mtsph_solid *s, int64_t out[4]);
 /* launches of this library's kernels since creation (bench evidence)    */
 mtsph_status mtsph_solid_launches(const mtsph_solid *s, int64_t *count);
 

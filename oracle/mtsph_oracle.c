@@ -181,6 +181,55 @@ done:
     return np;
 }
 
+/* Split runs of equal-key pairs into particle-sharing components, in order
+ * of first appearance (neighbors.py:165).  starts has nruns+1 entries.
+ * Writes the permutation `order` (npairs) and group starts (<= npairs+1);
+ * returns the number of groups, -1 for a run longer than 64 pairs. */
+int64_t or_split_runs(int64_t nruns, const int64_t *starts, const int64_t *pi,
+                      const int64_t *pj, int64_t *order, int64_t *gstart) {
+    int64_t ng = 0;
+    int64_t node[128];
+    int par[128], ea[64], comp[64], roots[64];
+    for (int64_t r = 0; r < nruns; ++r) {
+        int64_t lo = starts[r], hi = starts[r + 1];
+        int m = (int)(hi - lo);
+        if (m == 1) { order[lo] = lo; gstart[ng++] = lo; continue; }
+        if (m > 64) return -1;
+        int nn = 0;
+        for (int k = 0; k < m; ++k) {
+            int64_t e[2] = {pi[lo + k], pj[lo + k]};
+            int idx[2];
+            for (int s = 0; s < 2; ++s) {
+                int f = -1;
+                for (int t = 0; t < nn; ++t) if (node[t] == e[s]) { f = t; break; }
+                if (f < 0) { node[nn] = e[s]; par[nn] = nn; f = nn++; }
+                idx[s] = f;
+            }
+            ea[k] = idx[0];
+            int ra = idx[0], rb = idx[1];
+            while (par[ra] != ra) ra = par[ra];
+            while (par[rb] != rb) rb = par[rb];
+            if (ra != rb) { if (ra < rb) par[rb] = ra; else par[ra] = rb; }
+        }
+        int nc = 0;
+        for (int k = 0; k < m; ++k) {
+            int x = ea[k];
+            while (par[x] != x) x = par[x];
+            int f = -1;
+            for (int t = 0; t < nc; ++t) if (roots[t] == x) { f = t; break; }
+            if (f < 0) { roots[nc] = x; f = nc++; }
+            comp[k] = f;
+        }
+        int64_t w = lo;
+        for (int c = 0; c < nc; ++c) {
+            gstart[ng++] = w;
+            for (int k = 0; k < m; ++k) if (comp[k] == c) order[w++] = lo + k;
+        }
+    }
+    gstart[ng] = starts[nruns];
+    return ng;
+}
+
 /* --------------------------------------------------------- CSR operators */
 
 void or_velocity_gradient_gather(int64_t n, int d, const double *src,
@@ -431,15 +480,19 @@ void or_damping_sweep(int d, double *vel, const int64_t *pi, const int64_t *pj,
 
 typedef struct {
     double mu, K;              /* shear, bulk */
-    double s0, sinf, delta, H; /* hardening k(a) = s0 + (sinf-s0)(1-e^{-delta a}) + H a */
+    double s0, sinf, delta, H; /* law 0: k(a) = s0 + (sinf-s0)(1-e^{-delta a}) + H a
+                                  law 1: k(a) = s0 (1 + a/e0)^m with e0 = sinf, m = delta */
     double tol;
     int max_iter;
+    int law;
 } or_material;
 
 static double hard_k(const or_material *m, double a) {
+    if (m->law == 1) return m->s0 * pow(1.0 + a / m->sinf, m->delta);
     return m->s0 + (m->sinf - m->s0) * (1.0 - exp(-m->delta * a)) + m->H * a;
 }
 static double hard_kp(const or_material *m, double a) {
+    if (m->law == 1) return m->s0 * m->delta / m->sinf * pow(1.0 + a / m->sinf, m->delta - 1.0);
     return (m->sinf - m->s0) * m->delta * exp(-m->delta * a) + m->H;
 }
 
@@ -532,7 +585,7 @@ int64_t or_return_map(int64_t n, int d, const double *F, double *cp,
                       double *pk1, int32_t *plastic, double *dgamma,
                       int elastic_only, int32_t *status) {
     or_material m = {matp[0], matp[1], matp[2], matp[3], matp[4], matp[5],
-                     matp[6], (int)matp[7]};
+                     matp[6], (int)matp[7], (int)matp[8]};
     int64_t first = -1;
     int kind = 0;
 #pragma omp parallel for schedule(dynamic, 256)

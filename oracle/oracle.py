@@ -45,6 +45,7 @@ def lib():
         _LIB.or_build_pairs.restype = ctypes.c_int64
         _LIB.or_return_map.restype = ctypes.c_int64
         _LIB.or_porous_stress_rhs.restype = ctypes.c_int64
+        _LIB.or_split_runs.restype = ctypes.c_int64
     return _LIB
 
 
@@ -145,43 +146,20 @@ def order_pairs(pos, pi, pj, extra_major=()):
         ks = key[order]
         brk |= ks[1:] != ks[:-1]
     starts = np.concatenate([[0], np.flatnonzero(brk) + 1, [len(pi)]])
+    sizes = np.diff(starts)
+    if np.all(sizes == 1):
+        return pi, pj, np.arange(len(pi) + 1, dtype=np.int64)
+    # union-find per run in C (mtsph_oracle.c or_split_runs)
+    starts = np.ascontiguousarray(starts, dtype=np.int64)
+    pi = np.ascontiguousarray(pi, dtype=np.int64)
+    pj = np.ascontiguousarray(pj, dtype=np.int64)
     out = np.empty(len(pi), dtype=np.int64)
-    gstarts = [0]
-    w = 0
-    for r in range(len(starts) - 1):
-        lo, hi = int(starts[r]), int(starts[r + 1])
-        if hi - lo == 1:
-            out[w] = lo
-            w += 1
-            gstarts.append(w)
-            continue
-        parent = {}
-
-        def root(x):
-            while parent[x] != x:
-                parent[x] = parent[parent[x]]
-                x = parent[x]
-            return x
-        for k in range(lo, hi):
-            for e in (pi[k], pj[k]):
-                parent.setdefault(int(e), int(e))
-            ra, rb = root(int(pi[k])), root(int(pj[k]))
-            if ra != rb:
-                parent[max(ra, rb)] = min(ra, rb)
-        comps = {}
-        seq = []
-        for k in range(lo, hi):
-            c = root(int(pi[k]))
-            if c not in comps:
-                comps[c] = []
-                seq.append(c)
-            comps[c].append(k)
-        for c in seq:
-            for k in comps[c]:
-                out[w] = k
-                w += 1
-            gstarts.append(w)
-    return pi[out], pj[out], np.asarray(gstarts, dtype=np.int64)
+    gs = np.empty(len(pi) + 1, dtype=np.int64)
+    ng = lib().or_split_runs(ctypes.c_int64(len(starts) - 1), _p(starts), _p(pi), _p(pj),
+                             _p(out), _p(gs))
+    if ng < 0:
+        raise OracleError("more than 64 pairs share a damping group key")
+    return pi[out], pj[out], gs[:ng + 1].copy()
 
 
 def build_nbh(pos, vol, h, aniso=None, check_singular=True) -> Nbh:
@@ -255,10 +233,12 @@ def stress_divergence(pk1, rho0, nbh: Nbh):
     return out / np.broadcast_to(rho0, (n,))[:, None]
 
 
-def material_vector(mu, K, s0=1.0, sinf=1.0, delta=1.0, H=0.0, tol=None, max_iter=50):
+def material_vector(mu, K, s0=1.0, sinf=1.0, delta=1.0, H=0.0, tol=None, max_iter=50, law=0):
+    """law 0: reference saturation+linear hardening (plasticity.py:64);
+    law 1: power law s0 (1 + a/e0)^m passed as (s0, e0, m, 0)."""
     if tol is None:
         tol = 1e-8 * s0
-    return np.array([mu, K, s0, sinf, delta, H, tol, float(max_iter)])
+    return np.array([mu, K, s0, sinf, delta, H, tol, float(max_iter), float(law)])
 
 
 def return_map(F, cp, alpha, matp, elastic_only=False):

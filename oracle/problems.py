@@ -24,7 +24,7 @@ class NeckingOracle:
 
     def __init__(self, pos, vol, rho0, constrained, left, right, mid_mask,
                  mu, bulk, hardening, h, aniso=None, end_disp_per_outer=0.0,
-                 ramp_steps=1, damping_order=None):
+                 ramp_steps=1, damping_order=None, hardening_law=0):
         pos = np.ascontiguousarray(pos, dtype=float)
         n, d = pos.shape
         self.n, self.d = n, d
@@ -53,7 +53,7 @@ class NeckingOracle:
         self.sound = math.sqrt(self.bulk / float(self.rho0[0]))
         self.elastic_only = hardening is None
         hd = hardening if hardening is not None else (1.0, 1.0, 1.0, 0.0)
-        self.matp = O.material_vector(self.mu, self.bulk, *hd)
+        self.matp = O.material_vector(self.mu, self.bulk, *hd, law=hardening_law)
         self.end_disp = float(end_disp_per_outer)
         self.ramp_steps = max(int(ramp_steps), 1)
         self._ramp_left = 0

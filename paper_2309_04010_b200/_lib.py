@@ -81,10 +81,12 @@ SIGNATURES = {
     "mtsph_solid_stable_dt": (c_int, [c_vp, c_dbl, c_vp]),
     "mtsph_solid_relax_step": (c_int, [c_vp, c_dbl, c_dbl, c_vp]),
     "mtsph_solid_relax": (c_int, [c_vp, c_vp, c_vp]),
+    "mtsph_solid_run_steps": (c_int, [c_vp, c_vp, c_i64, c_vp]),
     "mtsph_solid_measure": (c_int, [c_vp, c_vp]),
     "mtsph_solid_get": (c_int, [c_vp, ctypes.c_char_p, c_vp]),
     "mtsph_solid_set": (c_int, [c_vp, ctypes.c_char_p, c_vp]),
     "mtsph_solid_launches": (c_int, [c_vp, c_vp]),
+    "mtsph_solid_sizes": (c_int, [c_vp, c_vp]),
     "mtsph_porous_create": (c_int, [c_vp, c_vp]),
     "mtsph_porous_destroy": (c_int, [c_vp]),
     "mtsph_porous_advance_slow": (c_int, [c_vp, c_dbl, c_dbl, c_vp]),

@@ -252,22 +252,32 @@ struct mtsph_solid {
     }
 };
 
-template <int D> static int solid_step(mtsph_solid *S, int ctrl_mode) {
+// one inner step; ev (optional, 6 events) brackets the kernel classes
+template <int D> static int solid_step(mtsph_solid *S, int ctrl_mode, cudaEvent_t *ev = nullptr) {
     SolidArgs A = S->args();
     const unsigned nb = blocks_for(S->n);
+    // external record: under stream capture this becomes an event-record
+    // node of the graph (a plain record would only order the capture)
+    auto mark = [&](int k) { if (ev) MT_CUDA(cudaEventRecordWithFlags(ev[k], S->s, cudaEventRecordExternal)); };
+    mark(0);
     k_solid_kick_drift<D><<<nb, 256, 0, S->s>>>(A);
+    mark(1);
     k_solid_stress<D><<<nb, 256, 0, S->s>>>(A);
+    mark(2);
     k_solid_accel<D><<<nb, 256, 0, S->s>>>(A);
     MT_LAUNCH_CHECK();
+    mark(3);
     int l = 3 + launch_sweep<D>(S->nb, S->sweep_args(), S->level_ptr.p, S->ctrl.p, S->s);
+    mark(4);
     k_solid_vmax<D><<<nb, 256, 0, S->s>>>(A, 0);
     k_ctrl<<<1, 256, 0, S->s>>>(S->ctrl.p, S->part.p, S->nblk, ctrl_mode);
     MT_LAUNCH_CHECK();
+    mark(5);
     return l + 2;
 }
 
-static int solid_step_any(mtsph_solid *S, int mode) {
-    return S->d == 2 ? solid_step<2>(S, mode) : solid_step<3>(S, mode);
+static int solid_step_any(mtsph_solid *S, int mode, cudaEvent_t *ev = nullptr) {
+    return S->d == 2 ? solid_step<2>(S, mode, ev) : solid_step<3>(S, mode, ev);
 }
 
 template <int D> static void solid_init_dt(mtsph_solid *S) {
@@ -458,6 +468,68 @@ extern "C" mtsph_status mtsph_solid_relax(mtsph_solid *S, const mtsph_inner_para
     API_END
 }
 
+// benchmark path: exactly nsteps steps in one graph, events per kernel class
+struct TimedGraph {
+    int64_t steps = 0;
+    cudaGraphExec_t exec = nullptr;
+    std::vector<cudaEvent_t> ev;
+    int per_step = 0;
+    ~TimedGraph() {
+        if (exec) cudaGraphExecDestroy(exec);
+        for (auto e : ev) cudaEventDestroy(e);
+    }
+};
+static std::unique_ptr<TimedGraph> g_timed;  // one benchmark graph at a time
+
+extern "C" mtsph_status mtsph_solid_run_steps(mtsph_solid *S, const mtsph_inner_params *p, int64_t nsteps,
+                                              double timing[7]) {
+    API_BEGIN
+    if (nsteps <= 0) throw Error(MTSPH_ERR_ARG, "nsteps must be positive");
+    S->pull_ctrl();
+    Ctrl *c = S->hc;
+    c->eta = p->eta;
+    c->cfl = p->cfl;
+    c->criterion = -1.0;          // never converged: run exactly nsteps
+    c->dt_outer = p->dt_outer;
+    c->max_inner = nsteps;
+    c->min_inner = nsteps;
+    c->n_inner = 0;
+    c->done = 0;
+    c->cap_hit = 0;
+    c->min_dt = INFINITY;
+    c->err_inv = c->err_rm = ~0ull;
+    S->push_ctrl();
+    if (!g_timed || g_timed->steps != nsteps) {
+        g_timed = std::make_unique<TimedGraph>();
+        g_timed->steps = nsteps;
+        g_timed->ev.resize((size_t)nsteps * 6);
+        for (auto &e : g_timed->ev) MT_CUDA(cudaEventCreate(&e));
+        cudaGraph_t g;
+        MT_CUDA(cudaStreamBeginCapture(S->s, cudaStreamCaptureModeThreadLocal));
+        for (int64_t k = 0; k < nsteps; ++k)
+            g_timed->per_step = solid_step_any(S, CTRL_STEP, &g_timed->ev[(size_t)k * 6]);
+        MT_CUDA(cudaStreamEndCapture(S->s, &g));
+        MT_CUDA(cudaGraphInstantiate(&g_timed->exec, g, 0));
+        cudaGraphDestroy(g);
+    }
+    if (S->d == 2) solid_init_dt<2>(S); else solid_init_dt<3>(S);
+    MT_CUDA(cudaGraphLaunch(g_timed->exec, S->s));
+    S->launches += nsteps * g_timed->per_step;
+    S->pull_ctrl();
+    check_solid_errors(S);
+    for (int k = 0; k < 7; ++k) timing[k] = 0.0;
+    float ms = 0.f;
+    MT_CUDA(cudaEventElapsedTime(&ms, g_timed->ev[0], g_timed->ev[(size_t)nsteps * 6 - 1]));
+    timing[0] = ms;
+    for (int64_t k = 0; k < nsteps; ++k)
+        for (int q = 0; q < 5; ++q) {
+            MT_CUDA(cudaEventElapsedTime(&ms, g_timed->ev[(size_t)k * 6 + q], g_timed->ev[(size_t)k * 6 + q + 1]));
+            timing[1 + q] += ms;
+        }
+    timing[6] = (double)(nsteps * g_timed->per_step);
+    API_END
+}
+
 extern "C" mtsph_status mtsph_solid_measure(mtsph_solid *S, double out[5]) {
     API_BEGIN
     SolidArgs A = S->args();
@@ -548,6 +620,19 @@ extern "C" mtsph_status mtsph_solid_set(mtsph_solid *S, const char *field, const
     } else throw Error(MTSPH_ERR_ARG, "unknown or read-only solid field " + f);
     MT_CUDA(cudaStreamSynchronize(S->s));
     API_END
+}
+
+extern "C" mtsph_status mtsph_solid_sizes(const mtsph_solid *S, int64_t out[4]) {
+    const NbhDev &nb = S->nb;
+    out[0] = nb.nnz;
+    out[1] = nb.npairs;
+    out[2] = nb.ngroups;
+    int64_t ph = 0;
+    if (nb.sweep == 1) ph = nb.nlevels;
+    else if (nb.sweep == 2)
+        for (size_t k = 0; k + 1 < nb.colour_task_ptr.size(); ++k) ph += nb.colour_task_ptr[k + 1] > nb.colour_task_ptr[k];
+    out[3] = ph;
+    return MTSPH_OK;
 }
 
 extern "C" mtsph_status mtsph_solid_launches(const mtsph_solid *S, int64_t *count) {

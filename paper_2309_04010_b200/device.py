@@ -142,6 +142,21 @@ class DeviceSolid:
         check(self._lib.mtsph_solid_relax(self._h, ctypes.byref(p), ctypes.byref(r)))
         return r
 
+    def run_steps(self, nsteps, eta, cfl, dt_outer=1.0):
+        """Exactly nsteps inner steps (benchmark path); returns the device
+        timing dict (CUDA events captured in the graph)."""
+        p = _lib.InnerParams(float(eta), float(cfl), 0.0, float(dt_outer), int(nsteps), int(nsteps))
+        t = np.zeros(7)
+        check(self._lib.mtsph_solid_run_steps(self._h, ctypes.byref(p), int(nsteps), ptr(t)))
+        return {"total_ms": t[0], "kick_drift_ms": t[1], "stress_ms": t[2], "accel_ms": t[3],
+                "sweep_ms": t[4], "reduce_ms": t[5], "launches": int(t[6])}
+
+    def sizes(self):
+        out = np.zeros(4, np.int64)
+        check(self._lib.mtsph_solid_sizes(self._h, ptr(out)))
+        return {"nnz": int(out[0]), "npairs": int(out[1]), "ngroups": int(out[2]),
+                "phases": int(out[3])}
+
     def measure(self):
         out = np.zeros(5)
         check(self._lib.mtsph_solid_measure(self._h, ptr(out)))
