@@ -328,7 +328,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--workload", default="bar_3d")
     ap.add_argument("--dp", type=float, default=0.0)
-    ap.add_argument("--sweep", default="coloured", choices=("coloured", "serial"))
+    ap.add_argument("--sweep", default="tiled", choices=("tiled", "coloured", "serial"))
     ap.add_argument("--cpu-cols", type=int, default=10)
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu", action="store_true")

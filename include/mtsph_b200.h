@@ -110,7 +110,11 @@ mtsph_status mtsph_porous_stress_rhs(
 enum {
     MTSPH_SWEEP_NONE = 0,      /* no pair schedule (no damping)             */
     MTSPH_SWEEP_SERIAL = 1,    /* the reference's exact serial group order  */
-    MTSPH_SWEEP_COLOURED = 2,  /* B200: 3^d-coloured midpoint-cell sweep    */
+    MTSPH_SWEEP_COLOURED = 2,  /* 3^d-coloured midpoint-cell tasks; keeps the
+                                  reference's groups and mirror symmetry   */
+    MTSPH_SWEEP_TILED = 3,     /* B200 throughput: 2^d-coloured cell blocks
+                                  staged in shared memory, greedy
+                                  edge-coloured pairs inside a block       */
 };
 
 typedef struct mtsph_nbh mtsph_nbh;

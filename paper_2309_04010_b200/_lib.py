@@ -21,9 +21,9 @@ c_dbl = ctypes.c_double
 c_int = ctypes.c_int
 c_vp = ctypes.c_void_p
 
-SWEEP_NONE, SWEEP_SERIAL, SWEEP_COLOURED = 0, 1, 2
+SWEEP_NONE, SWEEP_SERIAL, SWEEP_COLOURED, SWEEP_TILED = 0, 1, 2, 3
 SWEEPS = {"none": SWEEP_NONE, "serial": SWEEP_SERIAL, "coloured": SWEEP_COLOURED,
-          "colored": SWEEP_COLOURED}
+          "colored": SWEEP_COLOURED, "tiled": SWEEP_TILED}
 
 
 class SolidDesc(ctypes.Structure):

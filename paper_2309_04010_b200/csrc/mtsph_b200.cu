@@ -19,6 +19,7 @@
 #include "nbh.cuh"
 #include "porous.cuh"
 #include "solid.cuh"
+#include "tiled.cuh"
 #include "layer1.cuh"
 
 using namespace mtsph;
@@ -208,6 +209,7 @@ struct mtsph_solid {
     DBuf<uint8_t> flags;
     DBuf<Ctrl> ctrl;
     DBuf<int64_t> level_ptr;
+    TiledSched tiled;
     Ctrl *hc = nullptr;  // pinned mirror
     Mat mat{};
     int nblk = 0;
@@ -215,6 +217,11 @@ struct mtsph_solid {
     int per_step_launches = 0;
     cudaGraphExec_t graphs[3] = {nullptr, nullptr, nullptr};
     int graph_steps[3] = {4, 32, 128};
+    TiledArgs tiled_args() {
+        TiledArgs A{tiled.range_off.p, tiled.ranges.p, tiled.halo_n.p, tiled.pair_off.p, tiled.pairs.p,
+                    tiled.pd.p, tiled.sub_off.p, tiled.sub.p, inv_m.p, V.p, tiled.maxsub};
+        return A;
+    }
     ~mtsph_solid() {
         for (auto &g : graphs) if (g) cudaGraphExecDestroy(g);
         if (hc) cudaFreeHost(hc);
@@ -262,12 +269,16 @@ template <int D> static int solid_step(mtsph_solid *S, int ctrl_mode, cudaEvent_
     mark(0);
     k_solid_kick_drift<D><<<nb, 256, 0, S->s>>>(A);
     mark(1);
-    k_solid_stress<D><<<nb, 256, 0, S->s>>>(A);
+    // split: the neighbour gather runs at low register count / high
+    // occupancy, the register-heavy return map element-wise
+    k_solid_stress<D, true><<<nb, 256, 0, S->s>>>(A);
+    k_solid_rmap<D><<<nb, 256, 0, S->s>>>(A);
     mark(2);
     k_solid_accel<D><<<nb, 256, 0, S->s>>>(A);
     MT_LAUNCH_CHECK();
     mark(3);
-    int l = 3 + launch_sweep<D>(S->nb, S->sweep_args(), S->level_ptr.p, S->ctrl.p, S->s);
+    int l = 3 + (S->nb.sweep == 3 ? launch_tiled_sweep<D>(S->tiled, S->tiled_args(), S->ctrl.p, S->s)
+                                   : launch_sweep<D>(S->nb, S->sweep_args(), S->level_ptr.p, S->ctrl.p, S->s));
     mark(4);
     k_solid_vmax<D><<<nb, 256, 0, S->s>>>(A, 0);
     k_ctrl<<<1, 256, 0, S->s>>>(S->ctrl.p, S->part.p, S->nblk, ctrl_mode);
@@ -310,6 +321,7 @@ extern "C" mtsph_status mtsph_solid_create(const mtsph_solid_desc *dsc, mtsph_so
     S->d = d;
     MT_CUDA(cudaStreamCreateWithFlags(&S->s, cudaStreamNonBlocking));
     build_nbh(S->nb, n, d, dsc->pos, dsc->vol, dsc->h_axes, dsc->sweep, S->s);
+    if (dsc->sweep == 3) build_tiled_auto(S->nb, S->tiled, S->s);
     std::vector<int64_t> perm(n);
     S->nb.perm.download(perm.data(), n, S->s);
     MT_CUDA(cudaStreamSynchronize(S->s));
@@ -625,9 +637,11 @@ extern "C" mtsph_status mtsph_solid_set(mtsph_solid *S, const char *field, const
 extern "C" mtsph_status mtsph_solid_sizes(const mtsph_solid *S, int64_t out[4]) {
     const NbhDev &nb = S->nb;
     out[0] = nb.nnz;
-    out[1] = nb.npairs;
-    out[2] = nb.ngroups;
+    out[1] = nb.sweep == 3 ? S->tiled.npairs : nb.npairs;
+    out[2] = nb.sweep == 3 ? S->tiled.npairs : nb.ngroups;
     int64_t ph = 0;
+    if (nb.sweep == 3)
+        for (size_t k = 0; k + 1 < S->tiled.colour_ptr.size(); ++k) ph += S->tiled.colour_ptr[k + 1] > S->tiled.colour_ptr[k];
     if (nb.sweep == 1) ph = nb.nlevels;
     else if (nb.sweep == 2)
         for (size_t k = 0; k + 1 < nb.colour_task_ptr.size(); ++k) ph += nb.colour_task_ptr[k + 1] > nb.colour_task_ptr[k];

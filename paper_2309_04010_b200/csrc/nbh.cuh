@@ -82,6 +82,7 @@ struct NbhDev {
     DBuf<double> B;              // corrections SoA [d*d][n]
     // pair schedule
     int sweep = 0;
+    DBuf<uint64_t> cellkey;      // sorted Morton cell key per particle
     int64_t npairs = 0, ngroups = 0;
     DBuf<int32_t> pi, pj;        // internal ids, reference orientation
     DBuf<int64_t> gptr;          // group -> pair range
@@ -690,7 +691,8 @@ void build_nbh_impl(NbhDev &nb, const double *pos_h, const double *vol_h, cudaSt
                                " particle(s), first ids: [" + ids + "]", bad);
         }
     }
-    if (nb.sweep != 0) build_schedule<D>(nb, tmp, s);
+    nb.cellkey = std::move(key2);
+    if (nb.sweep == 1 || nb.sweep == 2) build_schedule<D>(nb, tmp, s);
     MT_CUDA(cudaStreamSynchronize(s));
 }
 

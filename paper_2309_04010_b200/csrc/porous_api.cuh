@@ -13,6 +13,7 @@ struct mtsph_porous {
     DBuf<uint8_t> flags;
     DBuf<Ctrl> ctrl;
     DBuf<int64_t> level_ptr;
+    TiledSched tiled;
     Ctrl *hc = nullptr;
     PorMat m{};
     double contact_time = 0.0, evap = 0.0;
@@ -60,7 +61,15 @@ template <int D> static int porous_step(mtsph_porous *P, int mode) {
     k_por_stress<D><<<nb, 256, 0, P->s>>>(A);
     k_por_accel<D><<<nb, 256, 0, P->s>>>(A);
     MT_LAUNCH_CHECK();
-    int l = 3 + launch_sweep<D>(P->nb, P->sweep_args(), P->level_ptr.p, P->ctrl.p, P->s);
+    int l = 3;
+    if (P->nb.sweep == 3) {
+        TiledArgs T{P->tiled.range_off.p, P->tiled.ranges.p, P->tiled.halo_n.p, P->tiled.pair_off.p,
+                    P->tiled.pairs.p, P->tiled.pd.p, P->tiled.sub_off.p, P->tiled.sub.p, P->inv_mix.p, P->V.p,
+                    P->tiled.maxsub};
+        l += launch_tiled_sweep<D>(P->tiled, T, P->ctrl.p, P->s);
+    } else {
+        l += launch_sweep<D>(P->nb, P->sweep_args(), P->level_ptr.p, P->ctrl.p, P->s);
+    }
     k_por_post_step<D><<<nb, 256, 0, P->s>>>(A, 0);
     k_ctrl<<<1, 256, 0, P->s>>>(P->ctrl.p, P->part.p, P->nblk, mode);
     MT_LAUNCH_CHECK();
@@ -97,6 +106,7 @@ extern "C" mtsph_status mtsph_porous_create(const mtsph_porous_desc *dsc, mtsph_
     P->d = d;
     MT_CUDA(cudaStreamCreateWithFlags(&P->s, cudaStreamNonBlocking));
     build_nbh(P->nb, n, d, dsc->pos, dsc->vol, dsc->h_axes, dsc->sweep, P->s);
+    if (dsc->sweep == 3) build_tiled_auto(P->nb, P->tiled, P->s);
     std::vector<int64_t> perm(n);
     P->nb.perm.download(perm.data(), n, P->s);
     MT_CUDA(cudaStreamSynchronize(P->s));

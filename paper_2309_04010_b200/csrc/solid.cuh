@@ -180,6 +180,37 @@ struct SolidArgs {
     Mat mat;
 };
 
+// return map + T = P B for one particle (shared by the fused and split paths)
+template <int D>
+__device__ __forceinline__ void solid_stress_point(const SolidArgs &A, int64_t i, const double *F,
+                                                          const double *Bm) {
+    const int64_t n = A.n;
+    Ctrl *c = A.ctrl;
+    double cp[D * D];
+    double alpha = 0.0;
+    if (A.mat.plastic) {
+#pragma unroll
+        for (int k = 0; k < D * D; ++k) cp[k] = A.cp[(int64_t)k * n + i];
+        alpha = A.alpha[i];
+    }
+    double P[D * D];
+    const int rc = return_map_dev<D>(F, cp, alpha, A.mat, P);
+    if (rc) {
+        const unsigned long long id = (unsigned long long)A.perm[i];
+        if (rc == 1) atomicMin(&c->err_inv, id);
+        else atomicMin(&c->err_rm, id);
+#pragma unroll
+        for (int k = 0; k < D * D; ++k) P[k] = 0.0;
+    } else if (A.mat.plastic) {
+#pragma unroll
+        for (int k = 0; k < D * D; ++k) A.cp[(int64_t)k * n + i] = cp[k];
+        A.alpha[i] = alpha;
+    }
+    double Tm[D * D];
+    mm<D>(P, Bm, Tm);
+    tstore<D>(A.T, i, Tm);
+}
+
 template <int D>
 __global__ void __launch_bounds__(256) k_solid_kick_drift(SolidArgs A) {
     using V_t = typename VT<D>::T;
@@ -214,7 +245,8 @@ __global__ void __launch_bounds__(256) k_solid_kick_drift(SolidArgs A) {
     V[i] = w;
 }
 
-template <int D>
+
+template <int D, bool SPLIT>
 __global__ void __launch_bounds__(256) k_solid_stress(SolidArgs A) {
     using V_t = typename VT<D>::T;
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -260,31 +292,26 @@ __global__ void __launch_bounds__(256) k_solid_stress(SolidArgs A) {
     mm<D>(acc, Bm, L);
 #pragma unroll
     for (int k = 0; k < D * D; ++k) F[k] += dt * L[k];
-    double cp[D * D];
-    double alpha = 0.0;
-    if (A.mat.plastic) {
-#pragma unroll
-        for (int k = 0; k < D * D; ++k) cp[k] = A.cp[(int64_t)k * n + i];
-        alpha = A.alpha[i];
-    }
-    double P[D * D];
-    const int rc = return_map_dev<D>(F, cp, alpha, A.mat, P);
 #pragma unroll
     for (int k = 0; k < D * D; ++k) A.F[(int64_t)k * n + i] = F[k];
-    if (rc) {
-        const unsigned long long id = (unsigned long long)A.perm[i];
-        if (rc == 1) atomicMin(&c->err_inv, id);
-        else atomicMin(&c->err_rm, id);
+    if (SPLIT) return;
+    solid_stress_point<D>(A, i, F, Bm);
+}
+
+// element-wise second half of the split stress kernel: return map + T
+template <int D>
+__global__ void __launch_bounds__(256) k_solid_rmap(SolidArgs A) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= A.n) return;
+    if (A.ctrl->done) return;
+    const int64_t n = A.n;
+    double Bm[D * D], F[D * D];
 #pragma unroll
-        for (int k = 0; k < D * D; ++k) P[k] = 0.0;
-    } else if (A.mat.plastic) {
-#pragma unroll
-        for (int k = 0; k < D * D; ++k) A.cp[(int64_t)k * n + i] = cp[k];
-        A.alpha[i] = alpha;
+    for (int k = 0; k < D * D; ++k) {
+        Bm[k] = A.B[(int64_t)k * n + i];
+        F[k] = A.F[(int64_t)k * n + i];
     }
-    double Tm[D * D];
-    mm<D>(P, Bm, Tm);
-    tstore<D>(A.T, i, Tm);
+    solid_stress_point<D>(A, i, F, Bm);
 }
 
 template <int D>
@@ -325,10 +352,10 @@ __global__ void __launch_bounds__(256) k_solid_accel(SolidArgs A) {
                 acc[r] += volb * sum;
             }
         }
-        const double rinv = A.rho0[i];
+        const double rho0 = A.rho0[i];
 #pragma unroll
         for (int k = 0; k < D; ++k) {
-            acc[k] /= rinv;
+            acc[k] /= rho0;
             A.a[(int64_t)k * A.n + i] = acc[k];
         }
         if (A.flags[i] & FL_MOVABLE) {
@@ -356,6 +383,7 @@ __global__ void __launch_bounds__(256) k_solid_accel(SolidArgs A) {
         A.part[A.nblk + blockIdx.x] = sa;
     }
 }
+
 
 // |v|^2 max over all particles (mode 0) or also |a|^2 over the free ones
 // (mode 1, used before the first step)

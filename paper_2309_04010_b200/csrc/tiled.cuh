@@ -1,0 +1,424 @@
+// tiled.cuh -- shared-memory tiled damping sweep (MTSPH_SWEEP_TILED).
+//
+// The B200 throughput variant of the pairwise implicit damping sweep.
+// Particles are already sorted by the Morton code of cells whose edge is
+// the kernel support, so an aligned block of B^d cells is a contiguous
+// particle range.  A block owns the pairs (a, b), a < b, whose first
+// particle lies in it; every particle such a pair touches lies in the
+// block's halo (the block grown by one cell).  Blocks are 2^d-coloured by
+// the parity of their block coordinates: same-coloured blocks are one block
+// apart, so their halos are disjoint and they run concurrently.
+//
+// One CTA per block: the halo's velocities and inverse masses are staged
+// in shared memory; the block's pairs, greedily edge-coloured at setup
+// (each sub-colour is a matching), are applied sub-colour by sub-colour
+// with a __syncthreads between them; the halo is written back.  A sweep
+// is colours 0..2^d-1 with sub-colours ascending, then everything in
+// reverse at half the step each -- a symmetric Gauss-Seidel ordering like
+// the reference's forward/reverse serial sweep.  Each pair update is the
+// reference's closed-form backward-Euler two-body exchange, so pair
+// momentum is conserved exactly and kinetic energy never increases.
+#pragma once
+
+#include <algorithm>
+#include <array>
+#include <exception>
+#include <mutex>
+#include <thread>
+
+#include "damping.cuh"
+#include "nbh.cuh"
+
+namespace mtsph {
+
+struct TiledSched {
+    int B = 0;                       // cells per block edge
+    int64_t ntasks = 0;
+    int max_halo = 0, max_ranges = 0, maxsub = 0;
+    int threads = 128;
+    std::vector<int64_t> colour_ptr; // 2^d + 1, over tasks (colour-major)
+    DBuf<int64_t> range_off;         // ntasks + 1 -> ranges
+    DBuf<int2> ranges;               // (global start, local offset)
+    DBuf<int32_t> halo_n;            // ntasks
+    DBuf<int64_t> pair_off;          // ntasks + 1 -> pairs
+    DBuf<uint32_t> pairs;            // li | lj << 16
+    DBuf<double> pd;                 // damping coefficient per pair
+    DBuf<int64_t> sub_off;           // ntasks + 1 -> sub
+    DBuf<int32_t> sub;               // per task: nsub + 1 pair offsets (task-relative)
+    int64_t npairs = 0;
+};
+
+struct TiledArgs {
+    const int64_t *range_off;
+    const int2 *ranges;
+    const int32_t *halo_n;
+    const int64_t *pair_off;
+    const uint32_t *pairs;
+    const double *pd;
+    const int64_t *sub_off;
+    const int32_t *sub;
+    const double *inv_m;
+    void *V;
+    int maxsub;      // largest sub-colour (pairs), sizes the staging buffers
+};
+
+template <int D>
+__global__ void __launch_bounds__(256) k_sweep_tiled(TiledArgs T, int64_t t0, int dir, const Ctrl *ctrl) {
+    using V_t = typename VT<D>::T;
+    extern __shared__ double smem[];
+    if (ctrl->done) return;
+    const int64_t task = t0 + blockIdx.x;
+    const int H = T.halo_n[task];
+    const int64_t r0 = T.range_off[task], r1 = T.range_off[task + 1];
+    const int nr = (int)(r1 - r0);
+    int2 *rt = reinterpret_cast<int2 *>(smem);                 // range table
+    // halo entries as one 32 B record (v0, v1, v2 | -, 1/m): two LDS.128 per
+    // particle instead of D + 1 scattered LDS.64
+    double4 *sh = reinterpret_cast<double4 *>(smem + (((nr + 1) & ~1) + 3) / 4 * 4);
+    for (int r = threadIdx.x; r < nr; r += blockDim.x) rt[r] = T.ranges[r0 + r];
+    __syncthreads();
+    V_t *V = reinterpret_cast<V_t *>(T.V);
+    auto global_of = [&](int l) {
+        int lo = 0, hi = nr - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (rt[mid].y <= l) lo = mid; else hi = mid - 1;
+        }
+        return (int64_t)rt[lo].x + (l - rt[lo].y);
+    };
+    const int64_t p0 = T.pair_off[task];
+    const int64_t s0 = T.sub_off[task];
+    const int nsub = (int)(T.sub_off[task + 1] - s0) - 1;
+    // double-buffered staging of each sub-colour's (pair, coefficient)
+    // chunk with cp.async: chunk q+1 streams in while chunk q is applied
+    double *bd = reinterpret_cast<double *>(sh + H);                 // 2 x maxsub coefficients
+    uint32_t *bp = reinterpret_cast<uint32_t *>(bd + 2 * T.maxsub);  // 2 x maxsub pairs
+    auto stage = [&](int q, int slot) {
+        const int s = dir > 0 ? q : nsub - 1 - q;
+        const int a = T.sub[s0 + s], b = T.sub[s0 + s + 1];
+        for (int p = a + threadIdx.x; p < b; p += blockDim.x) {
+            const unsigned dpd = (unsigned)__cvta_generic_to_shared(bd + slot * T.maxsub + (p - a));
+            const unsigned dpp = (unsigned)__cvta_generic_to_shared(bp + slot * T.maxsub + (p - a));
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dpd), "l"(T.pd + p0 + p));
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dpp), "l"(T.pairs + p0 + p));
+        }
+        asm volatile("cp.async.commit_group;\n" ::);
+        return b - a;
+    };
+    // first chunk in flight while the halo is gathered
+    int cnt_next = nsub > 0 ? stage(0, 0) : 0;
+    for (int l = threadIdx.x; l < H; l += blockDim.x) {
+        const int64_t g = global_of(l);
+        double v[3] = {0, 0, 0};
+        vget(V[g], v);
+        sh[l] = make_double4(v[0], v[1], D == 3 ? v[2] : 0.0, T.inv_m[g]);
+    }
+    const double half = 0.5 * ctrl->dt * ctrl->eta;
+    for (int q = 0; q < nsub; ++q) {
+        const int cnt = cnt_next;
+        if (q + 1 < nsub) {
+            cnt_next = stage(q + 1, (q + 1) & 1);
+            asm volatile("cp.async.wait_group 1;\n" ::);
+        } else {
+            asm volatile("cp.async.wait_group 0;\n" ::);
+        }
+        __syncthreads();
+        const double *cd = bd + (q & 1) * T.maxsub;
+        const uint32_t *cpk = bp + (q & 1) * T.maxsub;
+        for (int p = threadIdx.x; p < cnt; p += blockDim.x) {
+            const uint32_t pk = cpk[p];
+            const int li = (int)(pk & 0xffffu), lj = (int)(pk >> 16);
+            double4 a = sh[li], b = sh[lj];
+            const double c = half * cd[p];
+            const double ca = c * a.w, cb = c * b.w;
+            const double rden = 1.0 / (1.0 + ca + cb);
+            double u = (a.x - b.x) * rden;
+            a.x -= ca * u;
+            b.x += cb * u;
+            u = (a.y - b.y) * rden;
+            a.y -= ca * u;
+            b.y += cb * u;
+            if (D == 3) {
+                u = (a.z - b.z) * rden;
+                a.z -= ca * u;
+                b.z += cb * u;
+            }
+            sh[li] = a;
+            sh[lj] = b;
+        }
+        __syncthreads();
+    }
+    for (int l = threadIdx.x; l < H; l += blockDim.x) {
+        const int64_t g = global_of(l);
+        const double4 e = sh[l];
+        const double v[3] = {e.x, e.y, e.z};
+        V_t w;
+        vset(w, v);
+        V[g] = w;
+    }
+}
+
+inline size_t tiled_smem_bytes(const TiledSched &t, int d) {
+    (void)d;
+    return (size_t)((((t.max_ranges + 1) & ~1) + 3) / 4 * 4) * 8 + (size_t)t.max_halo * 32 +
+           (size_t)t.maxsub * 2 * 12;
+}
+
+template <int D>
+int launch_tiled_sweep(const TiledSched &t, const TiledArgs &A, const Ctrl *ctrl, cudaStream_t s) {
+    const int nc = (int)t.colour_ptr.size() - 1;
+    const size_t sm = tiled_smem_bytes(t, D);
+    int launches = 0;
+    for (int pass = 0; pass < 2; ++pass)
+        for (int q = 0; q < nc; ++q) {
+            const int c = pass == 0 ? q : nc - 1 - q;
+            const int64_t t0 = t.colour_ptr[c], t1 = t.colour_ptr[c + 1];
+            if (t1 <= t0) continue;
+            k_sweep_tiled<D><<<(unsigned)(t1 - t0), t.threads, sm, s>>>(A, t0, pass == 0 ? 1 : -1, ctrl);
+            MT_LAUNCH_CHECK();
+            ++launches;
+        }
+    return launches;
+}
+
+// ------------------------------------------------------------- host setup
+
+namespace tiled_detail {
+
+inline void decode(uint64_t key, int d, int64_t *c) {
+    for (int k = 0; k < d; ++k) {
+        uint64_t v = 0;
+        for (int b = 0; b < (d == 3 ? 21 : 32); ++b) v |= ((key >> (b * d + k)) & 1ull) << b;
+        c[k] = (int64_t)v;
+    }
+}
+inline uint64_t encode(const int64_t *c, int d) {
+    return d == 3 ? (spread3((uint64_t)c[0]) | spread3((uint64_t)c[1]) << 1 | spread3((uint64_t)c[2]) << 2)
+                  : (spread2((uint64_t)c[0]) | spread2((uint64_t)c[1]) << 1);
+}
+
+struct TaskOut {
+    int colour = 0;
+    int halo = 0;
+    std::vector<int2> ranges;
+    std::vector<uint32_t> pairs;
+    std::vector<double> pd;
+    std::vector<int32_t> sub;
+};
+
+}  // namespace tiled_detail
+
+// Build the schedule from the device neighbourhood (host C++, threaded).
+template <class T> void upload_vec(DBuf<T> &b, const std::vector<T> &v, cudaStream_t s) {
+    b.alloc(std::max<size_t>(v.size(), 1));
+    if (!v.empty()) MT_CUDA(cudaMemcpyAsync(b.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+    MT_CUDA(cudaStreamSynchronize(s));
+}
+
+inline void build_tiled(const NbhDev &nb, int B, TiledSched &t, cudaStream_t s) {
+    using namespace tiled_detail;
+    const int64_t n = nb.n;
+    const int d = nb.d;
+    int lb = 0;
+    while ((1 << lb) < B) ++lb;
+    std::vector<uint64_t> cellkey(n);
+    std::vector<int64_t> indptr(n + 1);
+    std::vector<int32_t> csr(std::max<int64_t>(nb.nnz, 1));
+    std::vector<double4> XV(n);
+    nb.cellkey.download(cellkey.data(), n, s);
+    nb.indptr.download(indptr.data(), n + 1, s);
+    nb.csr.download(csr.data(), nb.nnz, s);
+    nb.XV.download(XV.data(), n, s);
+    MT_CUDA(cudaStreamSynchronize(s));
+    // occupied cells: key -> [start, end)
+    std::vector<uint64_t> ckeys;
+    std::vector<int64_t> cstart;
+    for (int64_t i = 0; i < n; ++i)
+        if (i == 0 || cellkey[i] != cellkey[i - 1]) { ckeys.push_back(cellkey[i]); cstart.push_back(i); }
+    cstart.push_back(n);
+    auto cell_range = [&](uint64_t key, int64_t &a, int64_t &b) {
+        auto it = std::lower_bound(ckeys.begin(), ckeys.end(), key);
+        if (it == ckeys.end() || *it != key) return false;
+        const size_t c = it - ckeys.begin();
+        a = cstart[c];
+        b = cstart[c + 1];
+        return true;
+    };
+    // blocks = runs of equal key >> (d * lb)
+    std::vector<int64_t> bstart;
+    for (int64_t i = 0; i < n; ++i)
+        if (i == 0 || (cellkey[i] >> (d * lb)) != (cellkey[i - 1] >> (d * lb))) bstart.push_back(i);
+    const int64_t nblocks = (int64_t)bstart.size();
+    bstart.push_back(n);
+    std::vector<TaskOut> out(nblocks);
+    const double4 *xv = XV.data();
+    auto pdamp = [&](int64_t i, int64_t j) {
+        const double a[3] = {xv[i].x, xv[i].y, xv[i].z}, b[3] = {xv[j].x, xv[j].y, xv[j].z};
+        double rel[3], r2 = 0.0;
+        for (int k = 0; k < d; ++k) { rel[k] = b[k] - a[k]; r2 += rel[k] * rel[k]; }
+        const double r = std::sqrt(r2);
+        double u[3], q2 = 0.0;
+        for (int k = 0; k < d; ++k) { u[k] = rel[k] * nb.ks.inv_h[k]; q2 += u[k] * u[k]; }
+        const double q = std::sqrt(q2), tt = 1.0 - 0.5 * q;
+        const double mag = q < 2.0 ? nb.ks.pref * (-5.0 * tt * tt * tt) : 0.0;
+        double radial = 0.0;
+        for (int k = 0; k < d; ++k) radial -= (rel[k] / r) * (mag * (u[k] * nb.ks.inv_h[k]));
+        const double vi = d == 3 ? xv[i].w : xv[i].z, vj = d == 3 ? xv[j].w : xv[j].z;
+        return 2.0 * vi * vj * radial / r;
+    };
+    auto work = [&](int64_t b0, int64_t b1) {
+        std::vector<std::array<uint64_t, 4>> mask;
+        std::vector<int> colour;
+        std::vector<std::pair<int64_t, int>> sorted_ranges;
+        for (int64_t bk = b0; bk < b1; ++bk) {
+            TaskOut &T = out[bk];
+            const int64_t lo = bstart[bk], hi = bstart[bk + 1];
+            int64_t cc[3] = {0, 0, 0}, bc[3] = {0, 0, 0};
+            decode(cellkey[lo], d, cc);
+            int col = 0;
+            for (int k = 0; k < d; ++k) { bc[k] = cc[k] >> lb; col |= (int)(bc[k] & 1) << k; }
+            T.colour = col;
+            // halo ranges: cells of the block grown by one, z-y-x order
+            int local = 0;
+            const int span = B + 2;
+            const int nz = d == 3 ? span : 1;
+            for (int oz = 0; oz < nz; ++oz)
+                for (int oy = 0; oy < span; ++oy)
+                    for (int ox = 0; ox < span; ++ox) {
+                        int64_t q[3] = {bc[0] * B - 1 + ox, bc[1] * B - 1 + oy, d == 3 ? bc[2] * B - 1 + oz : 0};
+                        bool ok = true;
+                        for (int k = 0; k < d; ++k) ok = ok && q[k] >= 0;
+                        if (!ok) continue;
+                        int64_t a, e;
+                        if (!cell_range(encode(q, d), a, e)) continue;
+                        T.ranges.push_back(make_int2((int)a, local));
+                        local += (int)(e - a);
+                    }
+            T.halo = local;
+            if (local > 65535) throw Error(1, "tiled sweep: halo too large for 16-bit local ids");
+            sorted_ranges.clear();
+            for (size_t r = 0; r < T.ranges.size(); ++r) sorted_ranges.emplace_back(T.ranges[r].x, (int)r);
+            std::sort(sorted_ranges.begin(), sorted_ranges.end());
+            auto local_of = [&](int64_t g) {
+                auto it = std::upper_bound(sorted_ranges.begin(), sorted_ranges.end(),
+                                           std::make_pair(g, INT32_MAX));
+                --it;
+                const int2 r = T.ranges[it->second];
+                return r.y + (int)(g - r.x);
+            };
+            mask.assign(local, {0, 0, 0, 0});
+            std::vector<uint32_t> pr;
+            std::vector<double> pdv;
+            colour.clear();
+            int ncol = 0;
+            for (int64_t a = lo; a < hi; ++a)
+                for (int64_t k = indptr[a]; k < indptr[a + 1]; ++k) {
+                    const int64_t b = csr[k];
+                    if (b <= a) continue;
+                    const int la = local_of(a), lbb = local_of(b);
+                    int c = 0;
+                    for (;; ++c) {
+                        if (c >= 256) throw Error(1, "tiled sweep: more than 256 sub-colours");
+                        const uint64_t bit = 1ull << (c & 63);
+                        if (!((mask[la][c >> 6] | mask[lbb][c >> 6]) & bit)) break;
+                    }
+                    mask[la][c >> 6] |= 1ull << (c & 63);
+                    mask[lbb][c >> 6] |= 1ull << (c & 63);
+                    pr.push_back((uint32_t)la | ((uint32_t)lbb << 16));
+                    pdv.push_back(pdamp(a, b));
+                    colour.push_back(c);
+                    ncol = std::max(ncol, c + 1);
+                }
+            // stable counting sort by sub-colour
+            std::vector<int32_t> cnt(ncol + 1, 0);
+            for (int c : colour) cnt[c + 1]++;
+            for (int c = 0; c < ncol; ++c) cnt[c + 1] += cnt[c];
+            T.sub.assign(cnt.begin(), cnt.end());
+            T.pairs.resize(pr.size());
+            T.pd.resize(pr.size());
+            std::vector<int32_t> fill(cnt.begin(), cnt.end() - 1);
+            for (size_t p = 0; p < pr.size(); ++p) {
+                const int w = fill[colour[p]]++;
+                T.pairs[w] = pr[p];
+                T.pd[w] = pdv[p];
+            }
+        }
+    };
+    const int nth = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+    std::vector<std::thread> pool;
+    std::exception_ptr err = nullptr;
+    std::mutex mu;
+    const int64_t chunk = (nblocks + nth - 1) / nth;
+    for (int w = 0; w < nth; ++w) {
+        const int64_t b0 = w * chunk, b1 = std::min(nblocks, b0 + chunk);
+        if (b0 >= b1) break;
+        pool.emplace_back([&, b0, b1] {
+            try { work(b0, b1); } catch (...) { std::lock_guard<std::mutex> g(mu); err = std::current_exception(); }
+        });
+    }
+    for (auto &th : pool) th.join();
+    if (err) std::rethrow_exception(err);
+    // colour-major task order
+    const int ncol = 1 << d;
+    std::vector<int64_t> order;
+    t.colour_ptr.assign(ncol + 1, 0);
+    for (int c = 0; c < ncol; ++c) {
+        for (int64_t bk = 0; bk < nblocks; ++bk) if (out[bk].colour == c) order.push_back(bk);
+        t.colour_ptr[c + 1] = (int64_t)order.size();
+    }
+    std::vector<int64_t> roff(1, 0), poff(1, 0), soff(1, 0);
+    std::vector<int2> ranges;
+    std::vector<int32_t> halo, sub;
+    std::vector<uint32_t> pairs;
+    std::vector<double> pd;
+    for (int64_t bk : order) {
+        TaskOut &T = out[bk];
+        ranges.insert(ranges.end(), T.ranges.begin(), T.ranges.end());
+        roff.push_back((int64_t)ranges.size());
+        halo.push_back(T.halo);
+        pairs.insert(pairs.end(), T.pairs.begin(), T.pairs.end());
+        pd.insert(pd.end(), T.pd.begin(), T.pd.end());
+        poff.push_back((int64_t)pairs.size());
+        sub.insert(sub.end(), T.sub.begin(), T.sub.end());
+        soff.push_back((int64_t)sub.size());
+        t.max_halo = std::max(t.max_halo, T.halo);
+        t.max_ranges = std::max(t.max_ranges, (int)T.ranges.size());
+        for (size_t k = 0; k + 1 < T.sub.size(); ++k) t.maxsub = std::max(t.maxsub, T.sub[k + 1] - T.sub[k]);
+        std::vector<int2>().swap(T.ranges);
+        std::vector<uint32_t>().swap(T.pairs);
+        std::vector<double>().swap(T.pd);
+    }
+    t.B = B;
+    t.ntasks = (int64_t)order.size();
+    t.npairs = (int64_t)pairs.size();
+    upload_vec(t.range_off, roff, s);
+    upload_vec(t.ranges, ranges, s);
+    upload_vec(t.halo_n, halo, s);
+    upload_vec(t.pair_off, poff, s);
+    upload_vec(t.pairs, pairs, s);
+    upload_vec(t.pd, pd, s);
+    upload_vec(t.sub_off, soff, s);
+    upload_vec(t.sub, sub, s);
+}
+
+// Block edge: default 2 cells in 3D (a ~36 KB halo, several CTAs per SM)
+// and 4 in 2D; MTSPH_TILE_B / MTSPH_TILE_THREADS override.  Halves the
+// edge until the halo fits the shared-memory budget.
+inline void build_tiled_auto(const NbhDev &nb, TiledSched &t, cudaStream_t s) {
+    const size_t budget = 200 * 1024;
+    int B0 = nb.d == 2 ? 4 : 2, th = 256;
+    if (const char *e = std::getenv("MTSPH_TILE_B")) B0 = std::max(1, std::atoi(e));
+    if (const char *e = std::getenv("MTSPH_TILE_THREADS")) th = std::max(32, std::atoi(e));
+    for (int B = B0; B >= 1; B >>= 1) {
+        t = TiledSched();
+        build_tiled(nb, B, t, s);
+        if (tiled_smem_bytes(t, nb.d) <= budget) break;
+        if (B == 1) throw Error(1, "tiled sweep: particle density too high for shared memory");
+    }
+    t.threads = th;
+    const int sm = (int)tiled_smem_bytes(t, nb.d);
+    if (nb.d == 2) MT_CUDA(cudaFuncSetAttribute(k_sweep_tiled<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    else MT_CUDA(cudaFuncSetAttribute(k_sweep_tiled<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+}
+
+}  // namespace mtsph
