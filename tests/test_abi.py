@@ -1,0 +1,72 @@
+"""CPU: the C-ABI library loads and exports exactly what include/mtsph_b200.h
+declares; without a GPU the product path refuses to run (no fallback)."""
+
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+HEADER = os.path.join(ROOT, "include", "mtsph_b200.h")
+
+
+def declared_functions():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(mtsph_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2309_04010_b200 import _lib
+    lib = _lib.load_library(require_device=False)
+    names = declared_functions()
+    assert len(names) >= 35
+    missing = [n for n in names if not hasattr(lib, n)]
+    assert not missing, missing
+    # the Python binding covers the whole header, and nothing else
+    assert sorted(_lib.SIGNATURES) == names
+    assert lib.mtsph_abi_version() == 1
+
+
+def test_library_is_sm100a():
+    so = os.path.join(ROOT, "paper_2309_04010_b200", "libmtsph_b200.so")
+    data = open(so, "rb").read()
+    assert b"sm_100a" in data
+
+
+def test_no_device_fails_loudly():
+    from paper_2309_04010_b200 import _lib, errors
+    lib = _lib.load_library(require_device=False)
+    if lib.mtsph_device_count() > 0:
+        pytest.skip("a GPU is visible")
+    with pytest.raises(errors.BackendError, match="no CUDA device"):
+        _lib.load_library(require_device=True)
+    # a C-level call also refuses (status 2, message), never computes on CPU
+    out = np.zeros((2, 2, 2))
+    st = lib.mtsph_velocity_gradient_gather(
+        2, 2, _lib.ptr(np.zeros((2, 2))), _lib.ptr(np.array([0, 0, 0], np.int64)),
+        _lib.ptr(np.zeros(0, np.int64)), _lib.ptr(np.zeros((0, 2))), _lib.ptr(np.ones(2)),
+        _lib.ptr(out))
+    assert st == 2 and b"no CUDA device" in lib.mtsph_last_error()
+
+
+def test_problem_construction_requires_gpu():
+    from paper_2309_04010_b200 import _lib, errors, scenarios
+    from paper_2309_04010_b200.config import resolve
+    if _lib.load_library(require_device=False).mtsph_device_count() > 0:
+        pytest.skip("a GPU is visible")
+    p = resolve({"scenario": "necking_2d", "length": 8e-3, "width": 2e-3, "dp": 0.5e-3,
+                 "n_outer": 4}).params
+    with pytest.raises(errors.BackendError):
+        scenarios.build(p)
+
+
+def test_product_never_imports_oracle():
+    pkg = os.path.join(ROOT, "paper_2309_04010_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh")):
+                src = open(os.path.join(dirpath, f)).read()
+                assert "from oracle" not in src and "import oracle" not in src, f
