@@ -20,6 +20,7 @@
 #include "porous.cuh"
 #include "solid.cuh"
 #include "tiled.cuh"
+#include "tgather.cuh"
 #include "layer1.cuh"
 
 using namespace mtsph;
@@ -210,6 +211,8 @@ struct mtsph_solid {
     DBuf<Ctrl> ctrl;
     DBuf<int64_t> level_ptr;
     TiledSched tiled;
+    bool tiled_gathers = false;
+    size_t smem_stress = 0, smem_accel = 0;
     Ctrl *hc = nullptr;  // pinned mirror
     Mat mat{};
     int nblk = 0;
@@ -271,10 +274,14 @@ template <int D> static int solid_step(mtsph_solid *S, int ctrl_mode, cudaEvent_
     mark(1);
     // split: the neighbour gather runs at low register count / high
     // occupancy, the register-heavy return map element-wise
-    k_solid_stress<D, true><<<nb, 256, 0, S->s>>>(A);
+    const bool tiled = S->nb.sweep == 3 && S->tiled_gathers;
+    const unsigned nt = (unsigned)S->tiled.ntasks;
+    if (tiled) k_stress_tiled<D><<<nt, 256, S->smem_stress, S->s>>>(A, gather_args(S->tiled));
+    else k_solid_stress<D, true><<<nb, 256, 0, S->s>>>(A);
     k_solid_rmap<D><<<nb, 256, 0, S->s>>>(A);
     mark(2);
-    k_solid_accel<D><<<nb, 256, 0, S->s>>>(A);
+    if (tiled) k_accel_tiled<D><<<nt, 256, S->smem_accel, S->s>>>(A, gather_args(S->tiled));
+    else k_solid_accel<D><<<nb, 256, 0, S->s>>>(A);
     MT_LAUNCH_CHECK();
     mark(3);
     int l = 3 + (S->nb.sweep == 3 ? launch_tiled_sweep<D>(S->tiled, S->tiled_args(), S->ctrl.p, S->s)
@@ -359,6 +366,30 @@ extern "C" mtsph_status mtsph_solid_create(const mtsph_solid_desc *dsc, mtsph_so
     S->inv_m.upload(inv_m.data(), n, S->s);
     S->flags.upload(flags.data(), n, S->s);
     S->nblk = (int)blocks_for(n);
+    if (dsc->sweep == 3) {
+        // shared-memory gathers over the sweep's blocks: opt-in
+        // (MTSPH_TILED_GATHERS=1).  Measured slower than the SELL gathers
+        // through L1 on the 10M bar (1 CTA/SM at ~170 KB halo): DESIGN.md §4
+        const char *e = std::getenv("MTSPH_TILED_GATHERS");
+        S->tiled_gathers = e && e[0] == '1';
+        S->smem_stress = gather_smem_bytes(S->tiled, 8);
+        S->smem_accel = gather_smem_bytes(S->tiled, 4 + d * d);
+        if (S->smem_accel > 220 * 1024) S->tiled_gathers = false;
+        if (S->tiled_gathers) {
+            auto setsm = [](const void *fn, size_t b) {
+                MT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b));
+            };
+            if (d == 2) {
+                setsm((const void *)k_stress_tiled<2>, S->smem_stress);
+                setsm((const void *)k_accel_tiled<2>, S->smem_accel);
+            } else {
+                setsm((const void *)k_stress_tiled<3>, S->smem_stress);
+                setsm((const void *)k_accel_tiled<3>, S->smem_accel);
+            }
+            // per-block partials of the tiled divergence share the layout
+            S->nblk = (int)std::max<int64_t>(S->nblk, S->tiled.ntasks);
+        }
+    }
     S->part.alloc((size_t)3 * S->nblk);
     S->part.zero(S->s);
     S->meas.alloc((size_t)5 * S->nblk);

@@ -31,10 +31,14 @@
 
 namespace mtsph {
 
+// depth of the cp.async ring that stages sub-colour chunks (prefetch
+// distance kSweepStages - 1 sub-colours)
+constexpr int kSweepStages = 4;
+
 struct TiledSched {
     int B = 0;                       // cells per block edge
     int64_t ntasks = 0;
-    int max_halo = 0, max_ranges = 0, maxsub = 0;
+    int max_halo = 0, max_ranges = 0, maxsub = 0, max_nsub = 0;
     int threads = 128;
     std::vector<int64_t> colour_ptr; // 2^d + 1, over tasks (colour-major)
     DBuf<int64_t> range_off;         // ntasks + 1 -> ranges
@@ -46,6 +50,11 @@ struct TiledSched {
     DBuf<int64_t> sub_off;           // ntasks + 1 -> sub
     DBuf<int32_t> sub;               // per task: nsub + 1 pair offsets (task-relative)
     int64_t npairs = 0;
+    // block-local neighbour tables for the shared-memory gathers
+    int max_own = 0;
+    DBuf<int64_t> nl_off, self_off;  // ntasks + 1
+    DBuf<uint16_t> nl, self;         // ELL (width x owned, column-major), owned local ids
+    DBuf<int32_t> width, own0, own_n;
 };
 
 struct TiledArgs {
@@ -91,22 +100,34 @@ __global__ void __launch_bounds__(256) k_sweep_tiled(TiledArgs T, int64_t t0, in
     const int nsub = (int)(T.sub_off[task + 1] - s0) - 1;
     // double-buffered staging of each sub-colour's (pair, coefficient)
     // chunk with cp.async: chunk q+1 streams in while chunk q is applied
-    double *bd = reinterpret_cast<double *>(sh + H);                 // 2 x maxsub coefficients
-    uint32_t *bp = reinterpret_cast<uint32_t *>(bd + 2 * T.maxsub);  // 2 x maxsub pairs
-    auto stage = [&](int q, int slot) {
+    double *bd = reinterpret_cast<double *>(sh + H);                 // ring of coefficients
+    uint32_t *bp = reinterpret_cast<uint32_t *>(bd + kSweepStages * T.maxsub);  // ring of pairs
+    int *ssub = reinterpret_cast<int *>(bp + kSweepStages * T.maxsub);         // sub-colour bounds
+    for (int k = threadIdx.x; k <= nsub; k += blockDim.x) ssub[k] = T.sub[s0 + k];
+    __syncthreads();
+    auto sub_range = [&](int q, int &a, int &b) {
         const int s = dir > 0 ? q : nsub - 1 - q;
-        const int a = T.sub[s0 + s], b = T.sub[s0 + s + 1];
-        for (int p = a + threadIdx.x; p < b; p += blockDim.x) {
-            const unsigned dpd = (unsigned)__cvta_generic_to_shared(bd + slot * T.maxsub + (p - a));
-            const unsigned dpp = (unsigned)__cvta_generic_to_shared(bp + slot * T.maxsub + (p - a));
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dpd), "l"(T.pd + p0 + p));
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dpp), "l"(T.pairs + p0 + p));
+        a = ssub[s];
+        b = ssub[s + 1];
+    };
+    // every call commits exactly one (possibly empty) cp.async group
+    auto stage = [&](int q) {
+        if (q < nsub) {
+            const int slot = q % kSweepStages;
+            int a, b;
+            sub_range(q, a, b);
+            for (int p = a + threadIdx.x; p < b; p += blockDim.x) {
+                const unsigned dpd = (unsigned)__cvta_generic_to_shared(bd + slot * T.maxsub + (p - a));
+                const unsigned dpp = (unsigned)__cvta_generic_to_shared(bp + slot * T.maxsub + (p - a));
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dpd), "l"(T.pd + p0 + p));
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dpp), "l"(T.pairs + p0 + p));
+            }
         }
         asm volatile("cp.async.commit_group;\n" ::);
-        return b - a;
     };
-    // first chunk in flight while the halo is gathered
-    int cnt_next = nsub > 0 ? stage(0, 0) : 0;
+    // prefetch distance kSweepStages-1 sub-colours; the first ones stream
+    // in while the halo is gathered
+    for (int q = 0; q < kSweepStages - 1; ++q) stage(q);
     for (int l = threadIdx.x; l < H; l += blockDim.x) {
         const int64_t g = global_of(l);
         double v[3] = {0, 0, 0};
@@ -115,16 +136,14 @@ __global__ void __launch_bounds__(256) k_sweep_tiled(TiledArgs T, int64_t t0, in
     }
     const double half = 0.5 * ctrl->dt * ctrl->eta;
     for (int q = 0; q < nsub; ++q) {
-        const int cnt = cnt_next;
-        if (q + 1 < nsub) {
-            cnt_next = stage(q + 1, (q + 1) & 1);
-            asm volatile("cp.async.wait_group 1;\n" ::);
-        } else {
-            asm volatile("cp.async.wait_group 0;\n" ::);
-        }
+        stage(q + kSweepStages - 1);
+        asm volatile("cp.async.wait_group %0;\n" ::"n"(kSweepStages - 1));
         __syncthreads();
-        const double *cd = bd + (q & 1) * T.maxsub;
-        const uint32_t *cpk = bp + (q & 1) * T.maxsub;
+        int a0, b0;
+        sub_range(q, a0, b0);
+        const int cnt = b0 - a0;
+        const double *cd = bd + (q % kSweepStages) * T.maxsub;
+        const uint32_t *cpk = bp + (q % kSweepStages) * T.maxsub;
         for (int p = threadIdx.x; p < cnt; p += blockDim.x) {
             const uint32_t pk = cpk[p];
             const int li = (int)(pk & 0xffffu), lj = (int)(pk >> 16);
@@ -161,7 +180,7 @@ __global__ void __launch_bounds__(256) k_sweep_tiled(TiledArgs T, int64_t t0, in
 inline size_t tiled_smem_bytes(const TiledSched &t, int d) {
     (void)d;
     return (size_t)((((t.max_ranges + 1) & ~1) + 3) / 4 * 4) * 8 + (size_t)t.max_halo * 32 +
-           (size_t)t.maxsub * 2 * 12;
+           (size_t)t.maxsub * kSweepStages * 12 + (size_t)(t.max_nsub + 1) * 4;
 }
 
 template <int D>
@@ -204,6 +223,10 @@ struct TaskOut {
     std::vector<uint32_t> pairs;
     std::vector<double> pd;
     std::vector<int32_t> sub;
+    int64_t own0 = 0;            // first owned particle (global)
+    int width = 0;               // ELL width of the block-local table
+    std::vector<uint16_t> self;  // local id of each owned particle
+    std::vector<uint16_t> nl;    // width x owned, column-major local ids
 };
 
 }  // namespace tiled_detail
@@ -306,6 +329,26 @@ inline void build_tiled(const NbhDev &nb, int B, TiledSched &t, cudaStream_t s) 
                 const int2 r = T.ranges[it->second];
                 return r.y + (int)(g - r.x);
             };
+            // block-local neighbour table for the shared-memory gathers:
+            // ELL, column-major over the owned particles, padded with self
+            {
+                const int cnt = (int)(hi - lo);
+                int W = 0;
+                for (int64_t a = lo; a < hi; ++a) W = std::max<int>(W, (int)(indptr[a + 1] - indptr[a]));
+                T.own0 = lo;
+                T.width = W;
+                T.self.resize(cnt);
+                T.nl.assign((size_t)W * cnt, 0);
+                for (int k = 0; k < cnt; ++k) {
+                    const int64_t a = lo + k;
+                    const uint16_t sl = (uint16_t)local_of(a);
+                    T.self[k] = sl;
+                    int m = 0;
+                    for (int64_t kk = indptr[a]; kk < indptr[a + 1]; ++kk, ++m)
+                        T.nl[(size_t)m * cnt + k] = (uint16_t)local_of(csr[kk]);
+                    for (; m < W; ++m) T.nl[(size_t)m * cnt + k] = sl;
+                }
+            }
             mask.assign(local, {0, 0, 0, 0});
             std::vector<uint32_t> pr;
             std::vector<double> pdv;
@@ -371,8 +414,21 @@ inline void build_tiled(const NbhDev &nb, int B, TiledSched &t, cudaStream_t s) 
     std::vector<int32_t> halo, sub;
     std::vector<uint32_t> pairs;
     std::vector<double> pd;
+    std::vector<int64_t> nloff(1, 0), selfoff(1, 0);
+    std::vector<int32_t> width, own0, ownn;
+    std::vector<uint16_t> nl, self;
     for (int64_t bk : order) {
         TaskOut &T = out[bk];
+        nl.insert(nl.end(), T.nl.begin(), T.nl.end());
+        nloff.push_back((int64_t)nl.size());
+        self.insert(self.end(), T.self.begin(), T.self.end());
+        selfoff.push_back((int64_t)self.size());
+        width.push_back(T.width);
+        own0.push_back((int32_t)T.own0);
+        ownn.push_back((int32_t)T.self.size());
+        t.max_own = std::max(t.max_own, (int)T.self.size());
+        std::vector<uint16_t>().swap(T.nl);
+        std::vector<uint16_t>().swap(T.self);
         ranges.insert(ranges.end(), T.ranges.begin(), T.ranges.end());
         roff.push_back((int64_t)ranges.size());
         halo.push_back(T.halo);
@@ -384,6 +440,7 @@ inline void build_tiled(const NbhDev &nb, int B, TiledSched &t, cudaStream_t s) 
         t.max_halo = std::max(t.max_halo, T.halo);
         t.max_ranges = std::max(t.max_ranges, (int)T.ranges.size());
         for (size_t k = 0; k + 1 < T.sub.size(); ++k) t.maxsub = std::max(t.maxsub, T.sub[k + 1] - T.sub[k]);
+        t.max_nsub = std::max(t.max_nsub, (int)T.sub.size() - 1);
         std::vector<int2>().swap(T.ranges);
         std::vector<uint32_t>().swap(T.pairs);
         std::vector<double>().swap(T.pd);
@@ -399,6 +456,13 @@ inline void build_tiled(const NbhDev &nb, int B, TiledSched &t, cudaStream_t s) 
     upload_vec(t.pd, pd, s);
     upload_vec(t.sub_off, soff, s);
     upload_vec(t.sub, sub, s);
+    upload_vec(t.nl_off, nloff, s);
+    upload_vec(t.nl, nl, s);
+    upload_vec(t.self_off, selfoff, s);
+    upload_vec(t.self, self, s);
+    upload_vec(t.width, width, s);
+    upload_vec(t.own0, own0, s);
+    upload_vec(t.own_n, ownn, s);
 }
 
 // Block edge: default 2 cells in 3D (a ~36 KB halo, several CTAs per SM)
@@ -406,7 +470,7 @@ inline void build_tiled(const NbhDev &nb, int B, TiledSched &t, cudaStream_t s) 
 // edge until the halo fits the shared-memory budget.
 inline void build_tiled_auto(const NbhDev &nb, TiledSched &t, cudaStream_t s) {
     const size_t budget = 200 * 1024;
-    int B0 = nb.d == 2 ? 4 : 2, th = 256;
+    int B0 = nb.d == 2 ? 4 : 2, th = 128;
     if (const char *e = std::getenv("MTSPH_TILE_B")) B0 = std::max(1, std::atoi(e));
     if (const char *e = std::getenv("MTSPH_TILE_THREADS")) th = std::max(32, std::atoi(e));
     for (int B = B0; B >= 1; B >>= 1) {

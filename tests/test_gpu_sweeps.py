@@ -46,6 +46,40 @@ def test_damping_conserves_momentum_and_dissipates(sweep, dim):
     assert e0 < 0.5 * 0.5 * np.sum(mass[:, None] * vel * vel)   # it did damp
 
 
+@pytest.mark.parametrize("dim", [2, 3])
+def test_tiled_gathers_match_sell_gathers_per_step(dim):
+    """With eta = 0 the sweep is the identity, so the tiled pipeline
+    (shared-memory gathers) must track the SELL/L1 pipeline step by step."""
+    from paper_2309_04010_b200 import lattices
+    from paper_2309_04010_b200.config import resolve
+    from paper_2309_04010_b200.device import DeviceSolid
+    from paper_2309_04010_b200.scenarios import _necking_materials
+    raw = {"scenario": "block_3d", "length": 0.3, "width": 0.16, "breadth": 0.16, "dp": 0.02} \
+        if dim == 3 else {"scenario": "bar_2d", "length": 2.0, "width": 0.6, "dp": 0.05}
+    p = resolve(raw).params
+    lat = lattices.build_lattice(p)
+    el, hard = _necking_materials(p)
+    law, hp = hard.device_params()
+    runs = {}
+    for sweep in ("serial", "tiled"):
+        s = DeviceSolid(lat.pos, lat.vol, el.density0, lat.constrained, lat.side, lat.mid_mask,
+                        lat.h_axes, el.shear_modulus, el.bulk_modulus, plastic=True,
+                        hardening_law=law, hard=hp, sweep=sweep)
+        s.set_ramp(0.01 * p["length"], 20, 20)
+        hist = []
+        for _ in range(40):
+            dt = s.stable_dt(0.2)
+            s.relax_step(dt, 0.0)
+            hist.append(dt)
+        runs[sweep] = (hist, s.get("pos") - lat.pos, s.get("vel"), s.get("F"), s.get("alpha"))
+    a, b = runs["serial"], runs["tiled"]
+    np.testing.assert_allclose(a[0], b[0], rtol=1e-10)
+    for x, y in zip(a[1:], b[1:]):
+        scale = max(np.max(np.abs(x)), 1e-300)
+        assert np.max(np.abs(x - y)) <= 1e-10 * scale
+    assert np.max(a[4]) > 0, "case must yield"
+
+
 def _relaxed(raw, sweep):
     from paper_2309_04010_b200 import scenarios
     from paper_2309_04010_b200.config import resolve
