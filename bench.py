@@ -121,18 +121,24 @@ class ClockSampler:
 
 # ------------------------------------------------------------------ model
 
-def algorithmic_bytes(d, nnz_pp, pairs_pp, groups_pp):
+def algorithmic_bytes(d, nnz_pp, pairs_pp, groups_pp, sweep="tiled"):
     """Compulsory HBM bytes per particle per step for each kernel class
     (every array element the kernel needs is moved once; the neighbour
     index table counts its true entries).  See DESIGN.md §4."""
     dd = d * d
     vec, ten = 8 * d, 8 * dd
     xv = 8 * (d + 1)                      # reference position + volume
+    if sweep == "tiled":
+        # v r/w + 1/m, per pair and pass: two 16-bit local ids + f64 coefficient
+        sweep_b = 2 * vec + 8 + 2 * 12 * pairs_pp
+    else:
+        # v r/w + X|vol + 1/m, per pair and pass: two int32 ids + group pointer
+        sweep_b = 2 * vec + xv + 8 + 2 * (8 * pairs_pp + 8 * groups_pp)
     return {
         "kick_drift": 2 * vec + vec + 2 * vec + 1,
         "stress": xv + vec + 4 * nnz_pp + ten + 2 * ten + 2 * ten + 16 + ten,
         "accel": xv + ten + 4 * nnz_pp + 8 + 1 + 8 + 2 * vec + vec,
-        "sweep": 2 * vec + xv + 8 + 2 * (8 * pairs_pp + 8 * groups_pp),
+        "sweep": sweep_b,
         "reduce": vec,
     }
 
@@ -208,7 +214,7 @@ def run_ours(args):
     ctrl_bytes = 160
     # roofline of the dominant kernel class
     peak, peak_kind = load_peaks()
-    model = algorithmic_bytes(d, sz["nnz"] / n, sz["npairs"] / n, sz["ngroups"] / n)
+    model = algorithmic_bytes(d, sz["nnz"] / n, sz["npairs"] / n, sz["ngroups"] / n, args.sweep)
     classes = {"kick_drift": timing["kick_drift_ms"], "stress": timing["stress_ms"],
                "accel": timing["accel_ms"], "sweep": timing["sweep_ms"],
                "reduce": timing["reduce_ms"]}
