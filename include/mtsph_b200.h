@@ -159,6 +159,10 @@ typedef struct {
     double rm_tol;              /* return-map tolerance (<=0: 1e-8 s0)     */
     int rm_max_iter;            /* 50 in the reference                      */
     int sweep;                  /* MTSPH_SWEEP_*                            */
+    /* multi-rank (NULL for a single domain): */
+    const uint8_t *ghost;       /* (n,) 1 = halo copy of another rank's particle */
+    const double *grid;         /* 6 doubles: global scaled-space bounds lo[3], hi[3]
+                                   of the cell grid (X/h), shared by all ranks */
 } mtsph_solid_desc;
 
 typedef struct mtsph_solid mtsph_solid;
@@ -200,6 +204,29 @@ mtsph_status mtsph_solid_relax(mtsph_solid *s, const mtsph_inner_params *p,
  * + control; timing[6] = kernel launches in the region.                 */
 mtsph_status mtsph_solid_run_steps(mtsph_solid *s, const mtsph_inner_params *p,
                                    int64_t nsteps, double timing[7]);
+/* --- multi-rank phases (slab decomposition, tiled sweep; the host driver
+ * paper_2309_04010_b200/distributed.py exchanges halos between them) --- */
+enum {
+    MTSPH_PHASE_KICK_DRIFT = 1,  /* v += dt/2 a, boundary, x += dt v (owned)        */
+    MTSPH_PHASE_STRESS = 2,      /* dF/dt gather, F update, return map, T (owned)    */
+    MTSPH_PHASE_ACCEL = 3,       /* divergence + kick; out[0] = sum m v^2, out[1] = max |a|^2 */
+    MTSPH_PHASE_SWEEP = 4,       /* damping, tasks of colour `arg` (forward, or
+                                    reverse when arg >= 64: colour arg - 64)       */
+    MTSPH_PHASE_VMAX = 5,        /* out[0] = max |v|^2 (owned)                       */
+    MTSPH_PHASE_AMAX = 6,        /* out[0] = max |v|^2, out[1] = max |a|^2 (free)    */
+};
+/* set the step size and viscosity used by the next phases                */
+mtsph_status mtsph_solid_set_step(mtsph_solid *s, double dt, double eta);
+mtsph_status mtsph_solid_phase(mtsph_solid *s, int phase, int arg, double out[2]);
+/* number of damping colours of the tiled schedule                        */
+mtsph_status mtsph_solid_colours(const mtsph_solid *s, int *ncolours);
+/* copy a field of the listed particles (ORIGINAL local ids) to / from a
+ * packed host buffer: "vel" (d doubles each) or "T" (d*d doubles each)   */
+mtsph_status mtsph_solid_pack(mtsph_solid *s, const char *field, int64_t m,
+                              const int64_t *ids, double *host);
+mtsph_status mtsph_solid_unpack(mtsph_solid *s, const char *field, int64_t m,
+                                const int64_t *ids, const double *host);
+
 /* observables: reaction_force, neck radius, max alpha, min mid alpha,
  * all-finite flag (1/0)                                                 */
 mtsph_status mtsph_solid_measure(mtsph_solid *s, double out[5]);

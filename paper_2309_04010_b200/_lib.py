@@ -31,7 +31,8 @@ class SolidDesc(ctypes.Structure):
                 ("constrained", c_vp), ("side", c_vp), ("mid_mask", c_vp),
                 ("h_axes", c_dbl * 3), ("shear_modulus", c_dbl), ("bulk_modulus", c_dbl),
                 ("plastic", c_int), ("hardening_law", c_int), ("hard", c_dbl * 4),
-                ("rm_tol", c_dbl), ("rm_max_iter", c_int), ("sweep", c_int)]
+                ("rm_tol", c_dbl), ("rm_max_iter", c_int), ("sweep", c_int),
+                ("ghost", c_vp), ("grid", c_vp)]
 
 
 class PorousDesc(ctypes.Structure):
@@ -82,6 +83,11 @@ SIGNATURES = {
     "mtsph_solid_relax_step": (c_int, [c_vp, c_dbl, c_dbl, c_vp]),
     "mtsph_solid_relax": (c_int, [c_vp, c_vp, c_vp]),
     "mtsph_solid_run_steps": (c_int, [c_vp, c_vp, c_i64, c_vp]),
+    "mtsph_solid_set_step": (c_int, [c_vp, c_dbl, c_dbl]),
+    "mtsph_solid_phase": (c_int, [c_vp, c_int, c_int, c_vp]),
+    "mtsph_solid_colours": (c_int, [c_vp, c_vp]),
+    "mtsph_solid_pack": (c_int, [c_vp, ctypes.c_char_p, c_i64, c_vp, c_vp]),
+    "mtsph_solid_unpack": (c_int, [c_vp, ctypes.c_char_p, c_i64, c_vp, c_vp]),
     "mtsph_solid_measure": (c_int, [c_vp, c_vp]),
     "mtsph_solid_get": (c_int, [c_vp, ctypes.c_char_p, c_vp]),
     "mtsph_solid_set": (c_int, [c_vp, ctypes.c_char_p, c_vp]),

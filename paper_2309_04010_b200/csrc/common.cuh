@@ -40,6 +40,14 @@ inline unsigned blocks_for(int64_t n, int t = kThreads) {
     return (unsigned)(b < 1 ? 1 : b);
 }
 
+// opt a kernel into the largest dynamic shared memory the device offers
+inline void allow_max_dynamic_smem(const void *fn) {
+    int dev = 0, optin = 0;
+    MT_CUDA(cudaGetDevice(&dev));
+    MT_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    MT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+}
+
 // device buffer with RAII
 template <class T> struct DBuf {
     T *p = nullptr;

@@ -211,6 +211,7 @@ struct mtsph_solid {
     DBuf<Ctrl> ctrl;
     DBuf<int64_t> level_ptr;
     TiledSched tiled;
+    std::vector<int64_t> iperm_h;  // original -> internal (lazy, for pack/unpack)
     bool tiled_gathers = false;
     size_t smem_stress = 0, smem_accel = 0;
     Ctrl *hc = nullptr;  // pinned mirror
@@ -327,7 +328,31 @@ extern "C" mtsph_status mtsph_solid_create(const mtsph_solid_desc *dsc, mtsph_so
     S->n = n;
     S->d = d;
     MT_CUDA(cudaStreamCreateWithFlags(&S->s, cudaStreamNonBlocking));
-    build_nbh(S->nb, n, d, dsc->pos, dsc->vol, dsc->h_axes, dsc->sweep, S->s);
+    if (dsc->grid) {
+        S->nb.has_grid = true;
+        for (int k = 0; k < 3; ++k) {
+            S->nb.grid_lo[k] = dsc->grid[k];
+            S->nb.grid_hi[k] = dsc->grid[3 + k];
+        }
+    }
+    if (dsc->ghost && dsc->sweep != 3 && dsc->sweep != 0)
+        throw Error(MTSPH_ERR_ARG, "ghost particles (multi-rank) need the tiled sweep");
+    if (dsc->ghost) {
+        // ghost flags in the internal order are needed by the tiled
+        // schedule; the neighbour build fixes that order, so build it first
+        // with the schedule deferred
+        S->nb.ghost_orig = dsc->ghost;
+        build_nbh(S->nb, n, d, dsc->pos, dsc->vol, dsc->h_axes, 0, S->s);
+        S->nb.ghost_orig = nullptr;
+        S->nb.sweep = dsc->sweep;
+        std::vector<int64_t> pm(n);
+        S->nb.perm.download(pm.data(), n, S->s);
+        MT_CUDA(cudaStreamSynchronize(S->s));
+        S->nb.ghost_internal.resize(n);
+        for (int64_t k = 0; k < n; ++k) S->nb.ghost_internal[k] = dsc->ghost[pm[k]] ? 1 : 0;
+    } else {
+        build_nbh(S->nb, n, d, dsc->pos, dsc->vol, dsc->h_axes, dsc->sweep, S->s);
+    }
     if (dsc->sweep == 3) build_tiled_auto(S->nb, S->tiled, S->s);
     std::vector<int64_t> perm(n);
     S->nb.perm.download(perm.data(), n, S->s);
@@ -347,6 +372,7 @@ extern "C" mtsph_status mtsph_solid_create(const mtsph_solid_desc *dsc, mtsph_so
         if (dsc->side && dsc->side[o] < 0) f |= FL_LEFT;
         if (dsc->side && dsc->side[o] > 0) f |= FL_RIGHT;
         if (dsc->mid_mask && dsc->mid_mask[o]) f |= FL_MID;
+        if (dsc->ghost && dsc->ghost[o]) f |= FL_GHOST;
         flags[k] = f;
     }
     const size_t vbytes = (size_t)n * (d == 3 ? sizeof(double4) : sizeof(double2));
@@ -376,16 +402,10 @@ extern "C" mtsph_status mtsph_solid_create(const mtsph_solid_desc *dsc, mtsph_so
         S->smem_accel = gather_smem_bytes(S->tiled, 4 + d * d);
         if (S->smem_accel > 220 * 1024) S->tiled_gathers = false;
         if (S->tiled_gathers) {
-            auto setsm = [](const void *fn, size_t b) {
-                MT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b));
-            };
-            if (d == 2) {
-                setsm((const void *)k_stress_tiled<2>, S->smem_stress);
-                setsm((const void *)k_accel_tiled<2>, S->smem_accel);
-            } else {
-                setsm((const void *)k_stress_tiled<3>, S->smem_stress);
-                setsm((const void *)k_accel_tiled<3>, S->smem_accel);
-            }
+            allow_max_dynamic_smem((const void *)k_stress_tiled<2>);
+            allow_max_dynamic_smem((const void *)k_accel_tiled<2>);
+            allow_max_dynamic_smem((const void *)k_stress_tiled<3>);
+            allow_max_dynamic_smem((const void *)k_accel_tiled<3>);
             // per-block partials of the tiled divergence share the layout
             S->nblk = (int)std::max<int64_t>(S->nblk, S->tiled.ntasks);
         }
@@ -570,6 +590,202 @@ extern "C" mtsph_status mtsph_solid_run_steps(mtsph_solid *S, const mtsph_inner_
             timing[1 + q] += ms;
         }
     timing[6] = (double)(nsteps * g_timed->per_step);
+    API_END
+}
+
+// ------------------------------------------------------------- multi-rank phases
+
+template <int D> __global__ void k_pack(int64_t m, const int64_t *__restrict__ ids, const void *V,
+                                        const double *__restrict__ T, int field, double *out) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= m) return;
+    const int64_t i = ids[k];
+    if (field == 0) {
+        double v[3];
+        vget(reinterpret_cast<const typename VT<D>::T *>(V)[i], v);
+#pragma unroll
+        for (int c = 0; c < D; ++c) out[k * D + c] = v[c];
+    } else {
+        double t[D * D];
+        tload<D>(T, i, t);
+#pragma unroll
+        for (int c = 0; c < D * D; ++c) out[k * D * D + c] = t[c];
+    }
+}
+
+template <int D> __global__ void k_unpack(int64_t m, const int64_t *__restrict__ ids, void *V, double *T,
+                                          int field, const double *__restrict__ in) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= m) return;
+    const int64_t i = ids[k];
+    if (field == 0) {
+        double v[3] = {0, 0, 0};
+#pragma unroll
+        for (int c = 0; c < D; ++c) v[c] = in[k * D + c];
+        typename VT<D>::T w;
+        vset(w, v);
+        reinterpret_cast<typename VT<D>::T *>(V)[i] = w;
+    } else {
+        double t[D * D];
+#pragma unroll
+        for (int c = 0; c < D * D; ++c) t[c] = in[k * D * D + c];
+        tstore<D>(T, i, t);
+    }
+}
+
+extern "C" mtsph_status mtsph_solid_set_step(mtsph_solid *S, double dt, double eta) {
+    API_BEGIN
+    S->pull_ctrl();
+    S->hc->dt = dt;
+    S->hc->eta = eta;
+    S->hc->done = 0;
+    S->hc->err_inv = S->hc->err_rm = ~0ull;
+    S->push_ctrl();
+    API_END
+}
+
+extern "C" mtsph_status mtsph_solid_colours(const mtsph_solid *S, int *nc) {
+    *nc = S->nb.sweep == 3 ? (int)S->tiled.colour_ptr.size() - 1 : 0;
+    return MTSPH_OK;
+}
+
+template <int D> static void solid_phase(mtsph_solid *S, int phase, int arg, double out[2]) {
+    SolidArgs A = S->args();
+    const unsigned nb = blocks_for(S->n);
+    cudaStream_t s = S->s;
+    out[0] = out[1] = 0.0;
+    auto reduce_parts = [&](int seg, bool is_sum) {
+        std::vector<double> h(S->nblk);
+        S->part.download(h.data(), S->nblk, s);
+        MT_CUDA(cudaStreamSynchronize(s));
+        double r = 0.0;
+        for (double v : h) r = is_sum ? r + v : std::max(r, v);
+        (void)seg;
+        return r;
+    };
+    switch (phase) {
+    case MTSPH_PHASE_KICK_DRIFT:
+        k_solid_kick_drift<D><<<nb, 256, 0, s>>>(A);
+        S->launches += 1;
+        break;
+    case MTSPH_PHASE_STRESS:
+        if (S->nb.sweep == 3 && S->tiled_gathers)
+            k_stress_tiled<D><<<(unsigned)S->tiled.ntasks, 256, S->smem_stress, s>>>(A, gather_args(S->tiled));
+        else
+            k_solid_stress<D, true><<<nb, 256, 0, s>>>(A);
+        k_solid_rmap<D><<<nb, 256, 0, s>>>(A);
+        S->launches += 2;
+        break;
+    case MTSPH_PHASE_ACCEL: {
+        S->part.zero(s);
+        if (S->nb.sweep == 3 && S->tiled_gathers)
+            k_accel_tiled<D><<<(unsigned)S->tiled.ntasks, 256, S->smem_accel, s>>>(A, gather_args(S->tiled));
+        else
+            k_solid_accel<D><<<nb, 256, 0, s>>>(A);
+        MT_LAUNCH_CHECK();
+        S->launches += 1;
+        std::vector<double> h((size_t)2 * S->nblk);
+        S->part.download(h.data(), h.size(), s);
+        MT_CUDA(cudaStreamSynchronize(s));
+        for (int b = 0; b < S->nblk; ++b) {
+            out[0] += h[b];
+            out[1] = std::max(out[1], h[S->nblk + b]);
+        }
+        break;
+    }
+    case MTSPH_PHASE_SWEEP: {
+        if (S->nb.sweep != 3) throw Error(MTSPH_ERR_ARG, "sweep phases need the tiled schedule");
+        const int c = arg & 63, dir = arg >= 64 ? -1 : 1;
+        const TiledSched &t = S->tiled;
+        if (c + 1 >= (int)t.colour_ptr.size()) throw Error(MTSPH_ERR_ARG, "colour out of range");
+        const int64_t t0 = t.colour_ptr[c], t1 = t.colour_ptr[c + 1];
+        if (t1 > t0) {
+            k_sweep_tiled<D><<<(unsigned)(t1 - t0), t.threads, tiled_smem_bytes(t, D), s>>>(S->tiled_args(), t0, dir,
+                                                                                           S->ctrl.p);
+            S->launches += 1;
+        }
+        break;
+    }
+    case MTSPH_PHASE_VMAX:
+    case MTSPH_PHASE_AMAX: {
+        const int with_a = phase == MTSPH_PHASE_AMAX ? 1 : 0;
+        S->part.zero(s);
+        k_solid_vmax<D><<<nb, 256, 0, s>>>(A, with_a);
+        MT_LAUNCH_CHECK();
+        S->launches += 1;
+        std::vector<double> h((size_t)3 * S->nblk);
+        S->part.download(h.data(), h.size(), s);
+        MT_CUDA(cudaStreamSynchronize(s));
+        for (int b = 0; b < S->nblk; ++b) {
+            out[0] = std::max(out[0], h[2 * S->nblk + b]);
+            out[1] = std::max(out[1], h[S->nblk + b]);
+        }
+        break;
+    }
+    default:
+        throw Error(MTSPH_ERR_ARG, "unknown phase");
+    }
+    (void)reduce_parts;
+    MT_LAUNCH_CHECK();
+    MT_CUDA(cudaStreamSynchronize(s));
+}
+
+extern "C" mtsph_status mtsph_solid_phase(mtsph_solid *S, int phase, int arg, double out[2]) {
+    API_BEGIN
+    if (S->d == 2) solid_phase<2>(S, phase, arg, out); else solid_phase<3>(S, phase, arg, out);
+    if (phase == MTSPH_PHASE_STRESS) {
+        S->pull_ctrl();
+        check_solid_errors(S);
+    }
+    API_END
+}
+
+static void pack_common(mtsph_solid *S, const char *field, int64_t m, const int64_t *ids, double *host,
+                        const double *in, bool pack) {
+    const std::string f(field);
+    const int which = f == "vel" ? 0 : (f == "T" ? 1 : -1);
+    if (which < 0) throw Error(MTSPH_ERR_ARG, "pack fields are 'vel' and 'T'");
+    if (m <= 0) return;
+    if (S->iperm_h.empty()) {
+        S->iperm_h.resize(S->n);
+        S->nb.iperm.download(S->iperm_h.data(), S->n, S->s);
+        MT_CUDA(cudaStreamSynchronize(S->s));
+    }
+    std::vector<int64_t> internal(m);
+    for (int64_t k = 0; k < m; ++k) {
+        if (ids[k] < 0 || ids[k] >= S->n) throw Error(MTSPH_ERR_ARG, "particle id out of range");
+        internal[k] = S->iperm_h[ids[k]];
+    }
+    const int w = which == 0 ? S->d : S->d * S->d;
+    DBuf<int64_t> dids(m);
+    DBuf<double> buf((size_t)m * w);
+    dids.upload(internal.data(), m, S->s);
+    if (pack) {
+        if (S->d == 2) k_pack<2><<<blocks_for(m), 256, 0, S->s>>>(m, dids.p, S->V.p, S->T.p, which, buf.p);
+        else k_pack<3><<<blocks_for(m), 256, 0, S->s>>>(m, dids.p, S->V.p, S->T.p, which, buf.p);
+        MT_LAUNCH_CHECK();
+        buf.download(host, (size_t)m * w, S->s);
+    } else {
+        buf.upload(in, (size_t)m * w, S->s);
+        if (S->d == 2) k_unpack<2><<<blocks_for(m), 256, 0, S->s>>>(m, dids.p, S->V.p, S->T.p, which, buf.p);
+        else k_unpack<3><<<blocks_for(m), 256, 0, S->s>>>(m, dids.p, S->V.p, S->T.p, which, buf.p);
+        MT_LAUNCH_CHECK();
+    }
+    S->launches += 1;
+    MT_CUDA(cudaStreamSynchronize(S->s));
+}
+
+extern "C" mtsph_status mtsph_solid_pack(mtsph_solid *S, const char *field, int64_t m, const int64_t *ids,
+                                         double *host) {
+    API_BEGIN
+    pack_common(S, field, m, ids, host, nullptr, true);
+    API_END
+}
+
+extern "C" mtsph_status mtsph_solid_unpack(mtsph_solid *S, const char *field, int64_t m, const int64_t *ids,
+                                           const double *host) {
+    API_BEGIN
+    pack_common(S, field, m, ids, nullptr, host, false);
     API_END
 }
 

@@ -83,6 +83,11 @@ struct NbhDev {
     // pair schedule
     int sweep = 0;
     DBuf<uint64_t> cellkey;      // sorted Morton cell key per particle
+    bool has_grid = false;       // global cell grid (multi-rank), scaled space
+    double grid_lo[3] = {0, 0, 0}, grid_hi[3] = {0, 0, 0};
+    std::vector<uint8_t> ghost_internal;  // 1 = ghost (internal order), empty = none
+    const uint8_t *ghost_orig = nullptr;  // during the build: ghost flags, caller order
+                                          // (ghosts may have one-sided, singular moments)
     int64_t npairs = 0, ngroups = 0;
     DBuf<int32_t> pi, pj;        // internal ids, reference orientation
     DBuf<int64_t> gptr;          // group -> pair range
@@ -587,6 +592,11 @@ void build_nbh_impl(NbhDev &nb, const double *pos_h, const double *vol_h, cudaSt
             if (i == 0 || x > xhi[k]) xhi[k] = x;
         }
     for (int k = 0; k < 3; ++k) nb.center[k] = 0.5 * (xlo[k] + xhi[k]);
+    if (nb.has_grid) {
+        // multi-rank: every rank bins on the GLOBAL cell grid, so a rank's
+        // Morton order, blocks and pair lists are the global ones restricted
+        for (int k = 0; k < D; ++k) { lo[k] = nb.grid_lo[k]; hi[k] = nb.grid_hi[k]; }
+    }
     int dims[3] = {1, 1, 1};
     for (int k = 0; k < D; ++k) {
         double span = std::floor((hi[k] - lo[k]) * 0.5) + 1.0;
@@ -682,7 +692,8 @@ void build_nbh_impl(NbhDev &nb, const double *pos_h, const double *vol_h, cudaSt
         nb.perm.download(perm_h.data(), n, s);
         MT_CUDA(cudaStreamSynchronize(s));
         std::vector<int64_t> bad;
-        for (int64_t k = 0; k < n; ++k) if (sh[k]) bad.push_back(perm_h[k]);
+        for (int64_t k = 0; k < n; ++k)
+            if (sh[k] && !(nb.ghost_orig && nb.ghost_orig[perm_h[k]])) bad.push_back(perm_h[k]);
         if (!bad.empty()) {
             std::sort(bad.begin(), bad.end());
             std::string ids;

@@ -25,7 +25,9 @@
 
 namespace mtsph {
 
-enum { FL_MOVABLE = 1, FL_LEFT = 2, FL_RIGHT = 4, FL_MID = 8 };
+// FL_GHOST: a halo copy of another rank's particle (multi-GPU); its state
+// is written by exchanges only and it is excluded from every reduction
+enum { FL_MOVABLE = 1, FL_LEFT = 2, FL_RIGHT = 4, FL_MID = 8, FL_GHOST = 16 };
 
 struct Mat {
     double mu, K;
@@ -219,10 +221,11 @@ __global__ void __launch_bounds__(256) k_solid_kick_drift(SolidArgs A) {
     const Ctrl *c = A.ctrl;
     if (c->done) return;
     const double dt = c->dt;
+    const uint8_t f = A.flags[i];
+    if (f & FL_GHOST) return;  // another rank integrates it
     V_t *V = reinterpret_cast<V_t *>(A.V);
     double v[3];
     vget(V[i], v);
-    const uint8_t f = A.flags[i];
     if (f & FL_MOVABLE) {
 #pragma unroll
         for (int k = 0; k < D; ++k) v[k] += 0.5 * dt * A.a[(int64_t)k * A.n + i];
@@ -253,6 +256,7 @@ __global__ void __launch_bounds__(256) k_solid_stress(SolidArgs A) {
     if (i >= A.n) return;
     Ctrl *c = A.ctrl;
     if (c->done) return;
+    if (A.flags[i] & FL_GHOST) return;
     const double dt = c->dt;
     const int64_t n = A.n;
     const V_t *V = reinterpret_cast<const V_t *>(A.V);
@@ -304,6 +308,7 @@ __global__ void __launch_bounds__(256) k_solid_rmap(SolidArgs A) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= A.n) return;
     if (A.ctrl->done) return;
+    if (A.flags[i] & FL_GHOST) return;
     const int64_t n = A.n;
     double Bm[D * D], F[D * D];
 #pragma unroll
@@ -322,7 +327,7 @@ __global__ void __launch_bounds__(256) k_solid_accel(SolidArgs A) {
     const Ctrl *c = A.ctrl;
     if (c->done) return;  // uniform across the grid
     double ek = 0.0, a2m = 0.0;
-    if (i < A.n) {
+    if (i < A.n && !(A.flags[i] & FL_GHOST)) {
         const double dt = c->dt;
         double xa[3], Ta[D * D];
         xget<D>(A.XV[i], xa);
@@ -394,7 +399,7 @@ __global__ void __launch_bounds__(256) k_solid_vmax(SolidArgs A, int with_accel)
     if (!with_accel && A.ctrl->done) return;
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     double v2 = 0.0, a2 = 0.0;
-    if (i < A.n) {
+    if (i < A.n && !(A.flags[i] & FL_GHOST)) {
         const V_t *V = reinterpret_cast<const V_t *>(A.V);
         double v[3];
         vget(V[i], v);
@@ -469,7 +474,7 @@ __global__ void __launch_bounds__(256) k_solid_measure(SolidArgs A, double *out 
     __shared__ double sh[32];
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     double fx = 0.0, rad = 0.0, amax = 0.0, amin = 1e308, bad = 0.0;
-    if (i < A.n) {
+    if (i < A.n && !(A.flags[i] & FL_GHOST)) {
         const uint8_t f = A.flags[i];
         if (f & FL_RIGHT) fx = A.mass[i] * A.a[i];
         if (f & FL_MID) {

@@ -273,6 +273,10 @@ inline void build_tiled(const NbhDev &nb, int B, TiledSched &t, cudaStream_t s) 
         if (i == 0 || (cellkey[i] >> (d * lb)) != (cellkey[i - 1] >> (d * lb))) bstart.push_back(i);
     const int64_t nblocks = (int64_t)bstart.size();
     bstart.push_back(n);
+    // multi-rank: blocks of ghost particles belong to another rank
+    std::vector<char> skip(nblocks, 0);
+    if (!nb.ghost_internal.empty())
+        for (int64_t bk = 0; bk < nblocks; ++bk) skip[bk] = nb.ghost_internal[bstart[bk]] != 0;
     std::vector<TaskOut> out(nblocks);
     const double4 *xv = XV.data();
     auto pdamp = [&](int64_t i, int64_t j) {
@@ -294,6 +298,7 @@ inline void build_tiled(const NbhDev &nb, int B, TiledSched &t, cudaStream_t s) 
         std::vector<int> colour;
         std::vector<std::pair<int64_t, int>> sorted_ranges;
         for (int64_t bk = b0; bk < b1; ++bk) {
+            if (skip[bk]) continue;
             TaskOut &T = out[bk];
             const int64_t lo = bstart[bk], hi = bstart[bk + 1];
             int64_t cc[3] = {0, 0, 0}, bc[3] = {0, 0, 0};
@@ -406,7 +411,7 @@ inline void build_tiled(const NbhDev &nb, int B, TiledSched &t, cudaStream_t s) 
     std::vector<int64_t> order;
     t.colour_ptr.assign(ncol + 1, 0);
     for (int c = 0; c < ncol; ++c) {
-        for (int64_t bk = 0; bk < nblocks; ++bk) if (out[bk].colour == c) order.push_back(bk);
+        for (int64_t bk = 0; bk < nblocks; ++bk) if (!skip[bk] && out[bk].colour == c) order.push_back(bk);
         t.colour_ptr[c + 1] = (int64_t)order.size();
     }
     std::vector<int64_t> roff(1, 0), poff(1, 0), soff(1, 0);
@@ -480,9 +485,10 @@ inline void build_tiled_auto(const NbhDev &nb, TiledSched &t, cudaStream_t s) {
         if (B == 1) throw Error(1, "tiled sweep: particle density too high for shared memory");
     }
     t.threads = th;
-    const int sm = (int)tiled_smem_bytes(t, nb.d);
-    if (nb.d == 2) MT_CUDA(cudaFuncSetAttribute(k_sweep_tiled<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-    else MT_CUDA(cudaFuncSetAttribute(k_sweep_tiled<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    // the attribute is per function, shared by every problem instance: allow
+    // the opt-in maximum once (the launch's own size sets the occupancy)
+    allow_max_dynamic_smem((const void *)k_sweep_tiled<2>);
+    allow_max_dynamic_smem((const void *)k_sweep_tiled<3>);
 }
 
 }  // namespace mtsph

@@ -89,9 +89,12 @@ class DeviceSolid:
     FIELDS_D = {"pos", "vel", "accel", "ref_pos"}
     FIELDS_DD = {"F", "cp_inv"}
 
+    PHASES = {"kick_drift": 1, "stress": 2, "accel": 3, "sweep": 4, "vmax": 5, "amax": 6}
+
     def __init__(self, pos, vol, rho0, constrained, side, mid_mask, h_axes,
                  shear_modulus, bulk_modulus, plastic=True, hardening_law=0,
-                 hard=(1.0, 1.0, 1.0, 0.0), rm_tol=0.0, rm_max_iter=50, sweep="serial"):
+                 hard=(1.0, 1.0, 1.0, 0.0), rm_tol=0.0, rm_max_iter=50, sweep="serial",
+                 ghost=None, grid=None):
         lib = _lib.load_library()
         pos = _f64(pos)
         n, d = pos.shape
@@ -102,6 +105,8 @@ class DeviceSolid:
             "constrained": _u8(constrained, n),
             "side": np.ascontiguousarray(np.broadcast_to(np.asarray(side), (n,)), dtype=np.int8),
             "mid": _u8(mid_mask if mid_mask is not None else np.zeros(n, bool), n),
+            "ghost": _u8(ghost, n) if ghost is not None else None,
+            "grid": _f64(grid, (6,)) if grid is not None else None,
         }
         k = self._keep
         desc = _lib.SolidDesc(
@@ -109,7 +114,9 @@ class DeviceSolid:
             ptr(k["constrained"]).value, ptr(k["side"]).value, ptr(k["mid"]).value,
             _h3(h_axes), float(shear_modulus), float(bulk_modulus), int(bool(plastic)),
             int(hardening_law), (ctypes.c_double * 4)(*[float(v) for v in hard]),
-            float(rm_tol), int(rm_max_iter), _lib.SWEEPS[sweep])
+            float(rm_tol), int(rm_max_iter), _lib.SWEEPS[sweep],
+            ptr(k["ghost"]).value if k["ghost"] is not None else None,
+            ptr(k["grid"]).value if k["grid"] is not None else None)
         handle = ctypes.c_void_p()
         check(lib.mtsph_solid_create(ctypes.byref(desc), ctypes.byref(handle)))
         self._h = handle
@@ -150,6 +157,32 @@ class DeviceSolid:
         check(self._lib.mtsph_solid_run_steps(self._h, ctypes.byref(p), int(nsteps), ptr(t)))
         return {"total_ms": t[0], "kick_drift_ms": t[1], "stress_ms": t[2], "accel_ms": t[3],
                 "sweep_ms": t[4], "reduce_ms": t[5], "launches": int(t[6])}
+
+    # -- multi-rank phases ------------------------------------------------
+    def set_step(self, dt, eta):
+        check(self._lib.mtsph_solid_set_step(self._h, float(dt), float(eta)))
+
+    def phase(self, name, arg=0):
+        out = np.zeros(2)
+        check(self._lib.mtsph_solid_phase(self._h, self.PHASES[name], int(arg), ptr(out)))
+        return out
+
+    def colours(self):
+        v = ctypes.c_int()
+        check(self._lib.mtsph_solid_colours(self._h, ctypes.byref(v)))
+        return v.value
+
+    def pack(self, field, ids):
+        ids = np.ascontiguousarray(ids, dtype=np.int64)
+        w = self.d if field == "vel" else self.d * self.d
+        out = np.zeros((len(ids), w))
+        check(self._lib.mtsph_solid_pack(self._h, field.encode(), len(ids), ptr(ids), ptr(out)))
+        return out
+
+    def unpack(self, field, ids, values):
+        ids = np.ascontiguousarray(ids, dtype=np.int64)
+        vals = _f64(values)
+        check(self._lib.mtsph_solid_unpack(self._h, field.encode(), len(ids), ptr(ids), ptr(vals)))
 
     def sizes(self):
         out = np.zeros(4, np.int64)

@@ -1,0 +1,149 @@
+"""Slab decomposition for multi-GPU runs (host logic, numpy only).
+
+Particles are binned on the GLOBAL cell grid the device uses (cells of edge
+2 in the scaled space X/h = the kernel support; global lower corner), and
+ranks own slabs of whole cell columns along x whose boundaries are
+multiples of 4 cells, so every Morton block of the tiled sweep (edge 1, 2 or
+4 cells) lies inside one rank.  A rank's local problem is its owned
+particles plus GHOSTS: the other ranks' particles within one cell (one
+support radius) of its slab.  Because every rank bins on the same grid and
+keeps the global relative order, its Morton order, blocks, neighbour lists,
+sweep pairs and greedy colouring are the global ones restricted to the
+slab, so a decomposed run performs exactly the single-domain operations.
+
+Exchange plan (per rank r, for every other rank q):
+  refresh[q]  = global ids of r's ghosts owned by q (sorted); q sends the
+                current values of those ids in that order
+  modified[c] = ghosts of r that lie in the halo (block grown by one cell)
+                of one of r's sweep blocks of colour c; after phase c they
+                are sent back to their owners (no other rank -- not even
+                the owner -- touches them in that phase: same-coloured
+                block halos are disjoint)
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+CELL = 2.0        # cell edge in the scaled space (kernel support radius)
+SLAB_ALIGN = 4    # slab boundaries at multiples of 4 cells (largest tile edge)
+
+
+def scaled_grid(pos, h_axes):
+    """(u = X/h per axis, global lo, global hi) exactly as the device bins."""
+    u = np.asarray(pos, float) / np.asarray(h_axes, float)
+    return u, u.min(axis=0), u.max(axis=0)
+
+
+def cell_coords(u, lo):
+    return np.floor((u - lo) * 0.5).astype(np.int64)
+
+
+@dataclass
+class RankPlan:
+    rank: int
+    local_ids: np.ndarray          # global ids of the local particles (owned then ghosts? no: sorted)
+    ghost: np.ndarray              # bool per local particle
+    owner: np.ndarray              # owning rank per local particle
+    cell_x_range: tuple            # owned cell columns [x0, x1)
+    refresh_recv: dict = field(default_factory=dict)   # q -> local indices (ghosts owned by q)
+    refresh_send: dict = field(default_factory=dict)   # q -> local indices (owned, ghosts on q)
+    pushback_send: dict = field(default_factory=dict)  # (colour, q) -> local indices
+    pushback_recv: dict = field(default_factory=dict)  # (colour, q) -> local indices
+
+
+def _cuts(ncell_x, counts_per_column, nranks):
+    """Slab boundaries in cell columns: multiples of SLAB_ALIGN, balanced
+    particle counts, at least one column group per rank."""
+    ngroups = -(-ncell_x // SLAB_ALIGN)
+    if ngroups < nranks:
+        raise ValueError(f"cannot split {ncell_x} cell columns into {nranks} slabs of whole "
+                         f"{SLAB_ALIGN}-column groups")
+    padded = np.zeros(ngroups * SLAB_ALIGN)
+    padded[:ncell_x] = counts_per_column
+    acc = np.cumsum(padded.reshape(ngroups, SLAB_ALIGN).sum(axis=1))
+    cut_groups = [0]
+    for r in range(1, nranks):
+        g = int(np.searchsorted(acc, acc[-1] * r / nranks)) + 1
+        g = max(g, cut_groups[-1] + 1)                 # non-empty slab
+        g = min(g, ngroups - (nranks - r))             # leave one group per remaining rank
+        cut_groups.append(g)
+    cut_groups.append(ngroups)
+    return np.asarray(cut_groups, np.int64) * SLAB_ALIGN
+
+
+def block_colour_and_halo(cells, B, d):
+    """Per particle: colour of its Morton block of edge B (parity of the block
+    coordinates) and the block coordinates."""
+    bc = cells >> int(np.log2(B))
+    col = np.zeros(len(cells), np.int64)
+    for k in range(d):
+        col |= (bc[:, k] & 1) << k
+    return col, bc
+
+
+def make_plans(pos, h_axes, nranks, tile_B=None):
+    """Partition into `nranks` x-slabs; returns (plans, grid(6), owner)."""
+    pos = np.asarray(pos, float)
+    n, d = pos.shape
+    if tile_B is None:
+        tile_B = 4 if d == 2 else 2
+    u, lo, hi = scaled_grid(pos, h_axes)
+    cells = cell_coords(u, lo)
+    ncx = int(cells[:, 0].max()) + 1
+    counts = np.bincount(cells[:, 0], minlength=ncx)
+    cuts = _cuts(ncx, counts, nranks)
+    owner = np.searchsorted(cuts, cells[:, 0], side="right") - 1
+    grid = np.concatenate([np.pad(lo, (0, 3 - d)), np.pad(hi, (0, 3 - d))])
+    col, bc = block_colour_and_halo(cells, tile_B, d)
+    plans = []
+    gid = np.arange(n)
+    for r in range(nranks):
+        x0, x1 = int(cuts[r]), int(cuts[r + 1])
+        near = (cells[:, 0] >= x0 - 1) & (cells[:, 0] <= x1)
+        local = gid[near]                                   # ascending global ids
+        ghost = owner[local] != r
+        plans.append(RankPlan(r, local, ghost, owner[local], (x0, x1)))
+    # refresh lists: ghosts of r owned by q <-> owned of q that are ghosts on r
+    pos_in = [{int(g): i for i, g in enumerate(p.local_ids)} for p in plans]
+    for p in plans:
+        for q in range(nranks):
+            if q == p.rank:
+                continue
+            gh = p.local_ids[p.ghost & (p.owner == q)]
+            if len(gh) == 0:
+                continue
+            p.refresh_recv[q] = np.array([pos_in[p.rank][int(g)] for g in gh], np.int64)
+            plans[q].refresh_send[p.rank] = np.array([pos_in[q][int(g)] for g in gh], np.int64)
+    # sweep push-back lists: ghosts of r inside the halo of r's blocks of colour c
+    span_lo = np.zeros(d, np.int64)
+    for p in plans:
+        owned = ~p.ghost
+        loc_cells = cells[p.local_ids]
+        blk = bc[p.local_ids]
+        for c in range(1 << d):
+            sel = owned & (col[p.local_ids] == c)
+            if not np.any(sel):
+                continue
+            blocks = np.unique(blk[sel], axis=0)
+            # a ghost cell is in the halo of block b iff each coordinate lies
+            # within [b*B - 1, b*B + B]
+            gmask = p.ghost.copy()
+            hit = np.zeros(len(p.local_ids), bool)
+            gc = loc_cells[gmask]
+            if len(gc):
+                inside = np.zeros(len(gc), bool)
+                for b in blocks:
+                    lo_c = b * tile_B - 1 + span_lo
+                    hi_c = b * tile_B + tile_B
+                    inside |= np.all((gc >= lo_c) & (gc <= hi_c), axis=1)
+                hit[np.flatnonzero(gmask)[inside]] = True
+            for q in np.unique(p.owner[hit]):
+                q = int(q)
+                idx = np.flatnonzero(hit & (p.owner == q))
+                p.pushback_send[(c, q)] = idx.astype(np.int64)
+                plans[q].pushback_recv[(c, p.rank)] = np.array(
+                    [pos_in[q][int(g)] for g in p.local_ids[idx]], np.int64)
+    return plans, grid, owner

@@ -1,0 +1,119 @@
+"""CPU: slab decomposition plans and the torch.distributed exchange layer
+(world_size 2, gloo) of the multi-GPU inner step."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from paper_2309_04010_b200 import lattices
+from paper_2309_04010_b200.config import resolve
+from paper_2309_04010_b200.partition import cell_coords, make_plans, scaled_grid
+
+
+def _lattice(length=0.8):
+    return lattices.build_lattice(resolve({"scenario": "block_3d", "length": length,
+                                           "width": 0.12, "breadth": 0.12}).params)
+
+
+@pytest.mark.parametrize("nranks", [1, 2, 3])
+def test_plans_partition_and_halos(nranks):
+    lat = _lattice()
+    plans, grid, owner = make_plans(lat.pos, lat.h_axes, nranks)
+    n = len(lat.vol)
+    owned = np.concatenate([p.local_ids[~p.ghost] for p in plans])
+    assert np.array_equal(np.sort(owned), np.arange(n))          # a partition
+    u, lo, _ = scaled_grid(lat.pos, lat.h_axes)
+    cells = cell_coords(u, lo)
+    for p in plans:
+        assert np.all(np.diff(p.local_ids) > 0)                  # global order kept
+        x0, x1 = p.cell_x_range
+        assert x0 % 4 == 0 and (x1 % 4 == 0 or p.rank == nranks - 1)
+        gx = cells[p.local_ids[p.ghost], 0]
+        assert np.all((gx == x0 - 1) | (gx == x1))               # one cell of ghosts
+        for q, idx in p.refresh_recv.items():                    # lists pair up
+            send = plans[q].refresh_send[p.rank]
+            assert np.array_equal(p.local_ids[idx], plans[q].local_ids[send])
+    # same-colour push-back sets of different ranks never share a particle
+    for c in range(8):
+        touched = [p.local_ids[idx] for p in plans for (cc, q), idx in p.pushback_send.items()
+                   if cc == c]
+        allt = np.concatenate(touched) if touched else np.zeros(0, int)
+        assert len(allt) == len(np.unique(allt))
+
+
+class FakeDevice:
+    """Test double of DeviceSolid's pack/unpack (host arrays)."""
+
+    def __init__(self, values, d):
+        self.v = values.copy()
+        self.d = d
+
+    def pack(self, field, ids):
+        return self.v[np.asarray(ids)].copy()
+
+    def unpack(self, field, ids, vals):
+        self.v[np.asarray(ids)] = vals
+
+
+def _worker(rank, world, port, result_q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2309_04010_b200.distributed import TorchGroup
+        lat = _lattice()
+        plans, _, owner = make_plans(lat.pos, lat.h_axes, world)
+        p = plans[rank]
+        # global "velocity" field: particle id encoded; ghosts start stale (-1)
+        glob = np.stack([np.arange(len(lat.vol), dtype=float)] * 3, axis=1)
+        vals = glob[p.local_ids].copy()
+        vals[p.ghost] = -1.0
+        dev = FakeDevice(vals, 3)
+        g = TorchGroup(p, dev, dist)
+        g.refresh("vel")
+        ok_refresh = bool(np.array_equal(dev.v, glob[p.local_ids]))
+        # colour-0 sweep touched: ghosts in our colour-0 halos get +1000
+        for (c, q), idx in p.pushback_send.items():
+            if c == 0:
+                dev.v[idx] += 1000.0
+        g.pushback(0)
+        g.refresh("vel")
+        # every particle pushed back by someone in colour 0 must now read +1000
+        mine = ~p.ghost
+        expect = glob[p.local_ids].copy()
+        pushed = set()
+        for pl in plans:
+            for (c, q), idx in pl.pushback_send.items():
+                if c == 0:
+                    pushed.update(pl.local_ids[idx].tolist())
+        bump = np.array([gid in pushed for gid in p.local_ids])
+        expect[bump] += 1000.0
+        ok_push = bool(np.array_equal(dev.v[mine], expect[mine]))
+        s = g.allsum([rank + 1.0])
+        m = g.allmax([float(rank)])
+        result_q.put((rank, ok_refresh, ok_push, s, m, int(bump.sum())))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_two_ranks_exchange():
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = sorted(q.get(timeout=240) for _ in procs)
+    for pr in procs:
+        pr.join(timeout=60)
+    assert [r[0] for r in res] == [0, 1]
+    for rank, ok_refresh, ok_push, s, m, nbump in res:
+        assert ok_refresh, rank
+        assert ok_push, rank
+        assert s == 3.0 and m == 1.0
+    assert sum(r[5] for r in res) > 0
