@@ -385,7 +385,7 @@ extern "C" mtsph_status mtsph_solid_create(const mtsph_solid_desc *dsc, mtsph_so
     S->cp.upload(F.data(), F.size(), S->s);
     S->alpha.alloc(n);
     S->alpha.zero(S->s);
-    S->T.alloc((size_t)n * (d == 3 ? 12 : 4));
+    S->T.alloc((size_t)n * (d == 3 ? 9 : 4));
     S->T.zero(S->s);
     S->mass.upload(mass.data(), n, S->s);
     S->rho0.upload(rho0.data(), n, S->s);
@@ -595,7 +595,7 @@ extern "C" mtsph_status mtsph_solid_run_steps(mtsph_solid *S, const mtsph_inner_
 
 // ------------------------------------------------------------- multi-rank phases
 
-template <int D> __global__ void k_pack(int64_t m, const int64_t *__restrict__ ids, const void *V,
+template <int D> __global__ void k_pack(int64_t n, int64_t m, const int64_t *__restrict__ ids, const void *V,
                                         const double *__restrict__ T, int field, double *out) {
     const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (k >= m) return;
@@ -607,13 +607,13 @@ template <int D> __global__ void k_pack(int64_t m, const int64_t *__restrict__ i
         for (int c = 0; c < D; ++c) out[k * D + c] = v[c];
     } else {
         double t[D * D];
-        tload<D>(T, i, t);
+        tload<D>(T, n, i, t);
 #pragma unroll
         for (int c = 0; c < D * D; ++c) out[k * D * D + c] = t[c];
     }
 }
 
-template <int D> __global__ void k_unpack(int64_t m, const int64_t *__restrict__ ids, void *V, double *T,
+template <int D> __global__ void k_unpack(int64_t n, int64_t m, const int64_t *__restrict__ ids, void *V, double *T,
                                           int field, const double *__restrict__ in) {
     const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (k >= m) return;
@@ -629,7 +629,7 @@ template <int D> __global__ void k_unpack(int64_t m, const int64_t *__restrict__
         double t[D * D];
 #pragma unroll
         for (int c = 0; c < D * D; ++c) t[c] = in[k * D * D + c];
-        tstore<D>(T, i, t);
+        tstore<D>(T, n, i, t);
     }
 }
 
@@ -761,14 +761,14 @@ static void pack_common(mtsph_solid *S, const char *field, int64_t m, const int6
     DBuf<double> buf((size_t)m * w);
     dids.upload(internal.data(), m, S->s);
     if (pack) {
-        if (S->d == 2) k_pack<2><<<blocks_for(m), 256, 0, S->s>>>(m, dids.p, S->V.p, S->T.p, which, buf.p);
-        else k_pack<3><<<blocks_for(m), 256, 0, S->s>>>(m, dids.p, S->V.p, S->T.p, which, buf.p);
+        if (S->d == 2) k_pack<2><<<blocks_for(m), 256, 0, S->s>>>(S->n, m, dids.p, S->V.p, S->T.p, which, buf.p);
+        else k_pack<3><<<blocks_for(m), 256, 0, S->s>>>(S->n, m, dids.p, S->V.p, S->T.p, which, buf.p);
         MT_LAUNCH_CHECK();
         buf.download(host, (size_t)m * w, S->s);
     } else {
         buf.upload(in, (size_t)m * w, S->s);
-        if (S->d == 2) k_unpack<2><<<blocks_for(m), 256, 0, S->s>>>(m, dids.p, S->V.p, S->T.p, which, buf.p);
-        else k_unpack<3><<<blocks_for(m), 256, 0, S->s>>>(m, dids.p, S->V.p, S->T.p, which, buf.p);
+        if (S->d == 2) k_unpack<2><<<blocks_for(m), 256, 0, S->s>>>(S->n, m, dids.p, S->V.p, S->T.p, which, buf.p);
+        else k_unpack<3><<<blocks_for(m), 256, 0, S->s>>>(S->n, m, dids.p, S->V.p, S->T.p, which, buf.p);
         MT_LAUNCH_CHECK();
     }
     S->launches += 1;

@@ -377,7 +377,7 @@ __global__ void __launch_bounds__(256) k_por_stress(PorousArgs A) {
         for (int k = 0; k < D * D; ++k) pm[k] = j * tmp[k];
         mm<D>(pm, Bm, Tm);
     }
-    tstore<D>(A.T, i, Tm);
+    tstore<D>(A.T, A.n, i, Tm);
 }
 
 template <int D>
@@ -393,7 +393,7 @@ __global__ void __launch_bounds__(256) k_por_accel(PorousArgs A) {
         const double dt = c->dt;
         double xa[3], Ta[D * D], acc[D];
         xget<D>(A.XV[i], xa);
-        tload<D>(A.T, i, Ta);
+        tload<D>(A.T, A.n, i, Ta);
 #pragma unroll
         for (int k = 0; k < D; ++k) acc[k] = 0.0;
         const int64_t base = A.slice_ptr[i >> 5] + (i & 31);
@@ -403,7 +403,7 @@ __global__ void __launch_bounds__(256) k_por_accel(PorousArgs A) {
             const double4 xvb = ldg4(A.XV + b);
             double xb[3], Tb[D * D], rel[D], g[D];
             xget<D>(xvb, xb);
-            tload<D>(A.T, b, Tb);
+            tload<D>(A.T, A.n, b, Tb);
 #pragma unroll
             for (int k = 0; k < D; ++k) rel[k] = xb[k] - xa[k];
             grad_w<D>(rel, A.ks, g);

@@ -143,7 +143,7 @@ extern "C" mtsph_status mtsph_porous_create(const mtsph_porous_desc *dsc, mtsph_
     P->inv_mix.upload(inv.data(), n, P->s);
     P->amap.alloc((size_t)dd * n);
     P->amap.zero(P->s);
-    P->T.alloc((size_t)n * (d == 3 ? 12 : 4));
+    P->T.alloc((size_t)n * (d == 3 ? 9 : 4));
     P->T.zero(P->s);
     P->flags.upload(flags.data(), n, P->s);
     P->nblk = (int)blocks_for(n);

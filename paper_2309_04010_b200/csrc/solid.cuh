@@ -17,7 +17,7 @@
 //
 // State lives in HBM in the Morton order of the neighbourhood: own-access
 // fields SoA (coalesced), gathered fields AoS (X|vol and v as one 32 B
-// sector, T as 3 x 32 B rows), so a neighbour costs whole sectors.
+// sector, T planar 72 B -- see TS below), so a neighbour costs whole sectors.
 #pragma once
 
 #include "damping.cuh"
@@ -140,28 +140,34 @@ __device__ __forceinline__ int return_map_dev(const double *F, double *cp, doubl
     return 0;
 }
 
-template <int D> struct TS { static constexpr int n = D == 3 ? 12 : 4; };
+// Divergence tensor T = P B^T, gathered once per neighbour by the
+// acceleration kernel.  2D: one double4 per particle.  3D: planar, 72 B per
+// particle with no padding -- plane 0 = double4 (T00 T01 T02 T10), plane 1 =
+// double4 (T11 T12 T20 T21), plane 2 = double (T22) -- so the gather fetches
+// 9 doubles instead of three padded 32 B rows, and consecutive particles
+// share the sectors of the scalar plane.
+template <int D> struct TS { static constexpr int n = D == 3 ? 9 : 4; };
 
-template <int D> __device__ __forceinline__ void tload(const double *Tp, int64_t a, double *t) {
-    const double4 *r = reinterpret_cast<const double4 *>(Tp + a * TS<D>::n);
+template <int D> __device__ __forceinline__ void tload(const double *Tp, int64_t n, int64_t a, double *t) {
+    const double4 *r = reinterpret_cast<const double4 *>(Tp);
     if (D == 2) {
-        double4 q = r[0];
+        const double4 q = r[a];
         t[0] = q.x; t[1] = q.y; t[2] = q.z; t[3] = q.w;
     } else {
-#pragma unroll
-        for (int row = 0; row < 3; ++row) {
-            double4 q = r[row];
-            t[row * 3] = q.x; t[row * 3 + 1] = q.y; t[row * 3 + 2] = q.z;
-        }
+        const double4 q0 = r[a], q1 = r[n + a];
+        t[0] = q0.x; t[1] = q0.y; t[2] = q0.z; t[3] = q0.w;
+        t[4] = q1.x; t[5] = q1.y; t[6] = q1.z; t[7] = q1.w;
+        t[8] = Tp[8 * n + a];
     }
 }
-template <int D> __device__ __forceinline__ void tstore(double *Tp, int64_t a, const double *t) {
-    double4 *r = reinterpret_cast<double4 *>(Tp + a * TS<D>::n);
+template <int D> __device__ __forceinline__ void tstore(double *Tp, int64_t n, int64_t a, const double *t) {
+    double4 *r = reinterpret_cast<double4 *>(Tp);
     if (D == 2) {
-        r[0] = make_double4(t[0], t[1], t[2], t[3]);
+        r[a] = make_double4(t[0], t[1], t[2], t[3]);
     } else {
-#pragma unroll
-        for (int row = 0; row < 3; ++row) r[row] = make_double4(t[row * 3], t[row * 3 + 1], t[row * 3 + 2], 0.0);
+        r[a] = make_double4(t[0], t[1], t[2], t[3]);
+        r[n + a] = make_double4(t[4], t[5], t[6], t[7]);
+        Tp[8 * n + a] = t[8];
     }
 }
 
@@ -210,7 +216,7 @@ __device__ __forceinline__ void solid_stress_point(const SolidArgs &A, int64_t i
     }
     double Tm[D * D];
     mm<D>(P, Bm, Tm);
-    tstore<D>(A.T, i, Tm);
+    tstore<D>(A.T, A.n, i, Tm);
 }
 
 template <int D>
@@ -331,7 +337,7 @@ __global__ void __launch_bounds__(256) k_solid_accel(SolidArgs A) {
         const double dt = c->dt;
         double xa[3], Ta[D * D];
         xget<D>(A.XV[i], xa);
-        tload<D>(A.T, i, Ta);
+        tload<D>(A.T, A.n, i, Ta);
         double acc[D];
 #pragma unroll
         for (int k = 0; k < D; ++k) acc[k] = 0.0;
@@ -344,7 +350,7 @@ __global__ void __launch_bounds__(256) k_solid_accel(SolidArgs A) {
             const double4 xvb = ldg4(A.XV + b);
             double xb[3], Tb[D * D], rel[D], g[D];
             xget<D>(xvb, xb);
-            tload<D>(A.T, b, Tb);
+            tload<D>(A.T, A.n, b, Tb);
 #pragma unroll
             for (int k = 0; k < D; ++k) rel[k] = xb[k] - xa[k];
             grad_w<D>(rel, A.ks, g);

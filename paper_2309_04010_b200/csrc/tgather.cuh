@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(256) k_accel_tiled(SolidArgs A, GatherArgs G) 
         const int64_t g = hm.global(l);
         sx[l] = ldg4(A.XV + g);
         double t[D * D];
-        tload<D>(A.T, g, t);
+        tload<D>(A.T, A.n, g, t);
 #pragma unroll
         for (int q = 0; q < D * D; ++q) sT[(size_t)l * D * D + q] = t[q];
     }

@@ -244,6 +244,10 @@ inline void build_tiled(const NbhDev &nb, int B, TiledSched &t, cudaStream_t s) 
     const int d = nb.d;
     int lb = 0;
     while ((1 << lb) < B) ++lb;
+    // block colour period: same-colour blocks must be two cells apart so
+    // their one-cell halos are disjoint -- parity works from B = 2, single
+    // cells need period 3 (3^d colours)
+    const int P = B >= 2 ? 2 : 3;
     std::vector<uint64_t> cellkey(n);
     std::vector<int64_t> indptr(n + 1);
     std::vector<int32_t> csr(std::max<int64_t>(nb.nnz, 1));
@@ -304,7 +308,7 @@ inline void build_tiled(const NbhDev &nb, int B, TiledSched &t, cudaStream_t s) 
             int64_t cc[3] = {0, 0, 0}, bc[3] = {0, 0, 0};
             decode(cellkey[lo], d, cc);
             int col = 0;
-            for (int k = 0; k < d; ++k) { bc[k] = cc[k] >> lb; col |= (int)(bc[k] & 1) << k; }
+            for (int k = d - 1; k >= 0; --k) { bc[k] = cc[k] >> lb; col = col * P + (int)(bc[k] % P); }
             T.colour = col;
             // halo ranges: cells of the block grown by one, z-y-x order
             int local = 0;
@@ -407,7 +411,8 @@ inline void build_tiled(const NbhDev &nb, int B, TiledSched &t, cudaStream_t s) 
     for (auto &th : pool) th.join();
     if (err) std::rethrow_exception(err);
     // colour-major task order
-    const int ncol = 1 << d;
+    int ncol = 1;
+    for (int k = 0; k < d; ++k) ncol *= P;
     std::vector<int64_t> order;
     t.colour_ptr.assign(ncol + 1, 0);
     for (int c = 0; c < ncol; ++c) {

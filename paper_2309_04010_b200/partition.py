@@ -75,12 +75,15 @@ def _cuts(ncell_x, counts_per_column, nranks):
 
 
 def block_colour_and_halo(cells, B, d):
-    """Per particle: colour of its Morton block of edge B (parity of the block
-    coordinates) and the block coordinates."""
+    """Per particle: colour of its Morton block of edge B and the block
+    coordinates.  Colour = block coordinates mod P, mixed-radix with the
+    highest axis most significant (P = 2 for B >= 2, 3 for single cells),
+    matching tiled.cuh build_tiled."""
     bc = cells >> int(np.log2(B))
+    P = 2 if B >= 2 else 3
     col = np.zeros(len(cells), np.int64)
-    for k in range(d):
-        col |= (bc[:, k] & 1) << k
+    for k in reversed(range(d)):
+        col = col * P + bc[:, k] % P
     return col, bc
 
 
