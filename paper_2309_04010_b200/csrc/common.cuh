@@ -111,11 +111,27 @@ __device__ __forceinline__ void grad_w(const double *rel, const KSpec &ks, doubl
     for (int k = 0; k < D; ++k) g[k] = mag * (u[k] * ks.inv_h[k]);
 }
 
-// read-only 32 B load through the non-coherent path (two LDG.128)
+// 32 B accesses.  sm_100 has 256-bit global loads/stores (SASS
+// LDG.E.ENL2.256 / STG.E.ENL2.256) but nvcc splits a plain double4 access
+// into two 128-bit ones, each of which costs the L1 a tag lookup on the same
+// sector.  In the neighbour gathers that doubled the sectors per request, so
+// the gathered records go through these explicit v4.f64 forms.
+//   ldg4: read-only for the whole kernel (non-coherent path)
+//   ld4 / st4: coherent, for records the kernel also writes
 __device__ __forceinline__ double4 ldg4(const double4 *p) {
-    const double2 *q = reinterpret_cast<const double2 *>(p);
-    const double2 a = __ldg(q), b = __ldg(q + 1);
-    return make_double4(a.x, a.y, b.x, b.y);
+    double4 r;
+    asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ double4 ld4(const double4 *p) {
+    double4 r;
+    asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w) : "l"(p) : "memory");
+    return r;
+}
+__device__ __forceinline__ void st4(double4 *p, const double4 &v) {
+    asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" :: "l"(p), "d"(v.x), "d"(v.y), "d"(v.z), "d"(v.w)
+                 : "memory");
 }
 
 // ------------------------------------------------------ small tensors

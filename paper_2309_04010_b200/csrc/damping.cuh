@@ -40,6 +40,11 @@ template <> struct VT<3> { using T = double4; };
 
 __device__ __forceinline__ void vget(const double2 &v, double *o) { o[0] = v.x; o[1] = v.y; }
 __device__ __forceinline__ void vget(const double4 &v, double *o) { o[0] = v.x; o[1] = v.y; o[2] = v.z; }
+// read-only velocity record (kernels that do not write V)
+__device__ __forceinline__ double2 vldg(const double2 *p) { return __ldg(p); }
+__device__ __forceinline__ double4 vldg(const double4 *p) { return ldg4(p); }
+__device__ __forceinline__ void vst(double2 *p, const double2 &v) { *p = v; }
+__device__ __forceinline__ void vst(double4 *p, const double4 &v) { st4(p, v); }
 __device__ __forceinline__ void vset(double2 &v, const double *o) { v.x = o[0]; v.y = o[1]; }
 __device__ __forceinline__ void vset(double4 &v, const double *o) { v.x = o[0]; v.y = o[1]; v.z = o[2]; v.w = 0.0; }
 

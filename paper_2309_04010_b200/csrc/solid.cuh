@@ -148,25 +148,26 @@ __device__ __forceinline__ int return_map_dev(const double *F, double *cp, doubl
 // share the sectors of the scalar plane.
 template <int D> struct TS { static constexpr int n = D == 3 ? 9 : 4; };
 
+// (tload: only from kernels that do not write T -- non-coherent loads)
 template <int D> __device__ __forceinline__ void tload(const double *Tp, int64_t n, int64_t a, double *t) {
     const double4 *r = reinterpret_cast<const double4 *>(Tp);
     if (D == 2) {
-        const double4 q = r[a];
+        const double4 q = ldg4(r + a);
         t[0] = q.x; t[1] = q.y; t[2] = q.z; t[3] = q.w;
     } else {
-        const double4 q0 = r[a], q1 = r[n + a];
+        const double4 q0 = ldg4(r + a), q1 = ldg4(r + n + a);
         t[0] = q0.x; t[1] = q0.y; t[2] = q0.z; t[3] = q0.w;
         t[4] = q1.x; t[5] = q1.y; t[6] = q1.z; t[7] = q1.w;
-        t[8] = Tp[8 * n + a];
+        t[8] = __ldg(Tp + 8 * n + a);
     }
 }
 template <int D> __device__ __forceinline__ void tstore(double *Tp, int64_t n, int64_t a, const double *t) {
     double4 *r = reinterpret_cast<double4 *>(Tp);
     if (D == 2) {
-        r[a] = make_double4(t[0], t[1], t[2], t[3]);
+        st4(r + a, make_double4(t[0], t[1], t[2], t[3]));
     } else {
-        r[a] = make_double4(t[0], t[1], t[2], t[3]);
-        r[n + a] = make_double4(t[4], t[5], t[6], t[7]);
+        st4(r + a, make_double4(t[0], t[1], t[2], t[3]));
+        st4(r + n + a, make_double4(t[4], t[5], t[6], t[7]));
         Tp[8 * n + a] = t[8];
     }
 }
@@ -267,8 +268,8 @@ __global__ void __launch_bounds__(256) k_solid_stress(SolidArgs A) {
     const int64_t n = A.n;
     const V_t *V = reinterpret_cast<const V_t *>(A.V);
     double xa[3], va[3];
-    xget<D>(A.XV[i], xa);
-    vget(V[i], va);
+    xget<D>(ldg4(A.XV + i), xa);
+    vget(vldg(V + i), va);
     double acc[D * D];
 #pragma unroll
     for (int k = 0; k < D * D; ++k) acc[k] = 0.0;
@@ -281,7 +282,7 @@ __global__ void __launch_bounds__(256) k_solid_stress(SolidArgs A) {
         const double4 xvb = ldg4(A.XV + b);
         double xb[3], vb[3], rel[D], g[D];
         xget<D>(xvb, xb);
-        vget(V[b], vb);
+        vget(vldg(V + b), vb);
 #pragma unroll
         for (int k = 0; k < D; ++k) rel[k] = xb[k] - xa[k];
         grad_w<D>(rel, A.ks, g);
@@ -336,7 +337,7 @@ __global__ void __launch_bounds__(256) k_solid_accel(SolidArgs A) {
     if (i < A.n && !(A.flags[i] & FL_GHOST)) {
         const double dt = c->dt;
         double xa[3], Ta[D * D];
-        xget<D>(A.XV[i], xa);
+        xget<D>(ldg4(A.XV + i), xa);
         tload<D>(A.T, A.n, i, Ta);
         double acc[D];
 #pragma unroll

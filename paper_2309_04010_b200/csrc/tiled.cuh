@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(256) k_sweep_tiled(TiledArgs T, int64_t t0, in
     for (int l = threadIdx.x; l < H; l += blockDim.x) {
         const int64_t g = global_of(l);
         double v[3] = {0, 0, 0};
-        vget(V[g], v);
+        vget(vldg(V + g), v);  // halos of one launch are disjoint: read-only here
         sh[l] = make_double4(v[0], v[1], D == 3 ? v[2] : 0.0, T.inv_m[g]);
     }
     const double half = 0.5 * ctrl->dt * ctrl->eta;
@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(256) k_sweep_tiled(TiledArgs T, int64_t t0, in
         const double v[3] = {e.x, e.y, e.z};
         V_t w;
         vset(w, v);
-        V[g] = w;
+        vst(V + g, w);
     }
 }
 
