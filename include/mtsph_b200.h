@@ -163,6 +163,10 @@ typedef struct {
     const uint8_t *ghost;       /* (n,) 1 = halo copy of another rank's particle */
     const double *grid;         /* 6 doubles: global scaled-space bounds lo[3], hi[3]
                                    of the cell grid (X/h), shared by all ranks */
+    int tile;                   /* tiled sweep block edge in cells (power of 2);
+                                   0: automatic (4, halved until the halo fits
+                                   shared memory).  Ranks of one decomposition
+                                   must use their partition plan's edge. */
 } mtsph_solid_desc;
 
 typedef struct mtsph_solid mtsph_solid;

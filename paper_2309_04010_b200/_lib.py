@@ -32,7 +32,7 @@ class SolidDesc(ctypes.Structure):
                 ("h_axes", c_dbl * 3), ("shear_modulus", c_dbl), ("bulk_modulus", c_dbl),
                 ("plastic", c_int), ("hardening_law", c_int), ("hard", c_dbl * 4),
                 ("rm_tol", c_dbl), ("rm_max_iter", c_int), ("sweep", c_int),
-                ("ghost", c_vp), ("grid", c_vp)]
+                ("ghost", c_vp), ("grid", c_vp), ("tile", c_int)]
 
 
 class PorousDesc(ctypes.Structure):

@@ -353,7 +353,7 @@ extern "C" mtsph_status mtsph_solid_create(const mtsph_solid_desc *dsc, mtsph_so
     } else {
         build_nbh(S->nb, n, d, dsc->pos, dsc->vol, dsc->h_axes, dsc->sweep, S->s);
     }
-    if (dsc->sweep == 3) build_tiled_auto(S->nb, S->tiled, S->s);
+    if (dsc->sweep == 3) build_tiled_auto(S->nb, S->tiled, S->s, dsc->tile);
     std::vector<int64_t> perm(n);
     S->nb.perm.download(perm.data(), n, S->s);
     MT_CUDA(cudaStreamSynchronize(S->s));

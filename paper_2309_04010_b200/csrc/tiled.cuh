@@ -72,7 +72,7 @@ struct TiledArgs {
 };
 
 template <int D>
-__global__ void __launch_bounds__(256) k_sweep_tiled(TiledArgs T, int64_t t0, int dir, const Ctrl *ctrl) {
+__global__ void __launch_bounds__(1024) k_sweep_tiled(TiledArgs T, int64_t t0, int dir, const Ctrl *ctrl) {
     using V_t = typename VT<D>::T;
     extern __shared__ double smem[];
     if (ctrl->done) return;
@@ -81,9 +81,12 @@ __global__ void __launch_bounds__(256) k_sweep_tiled(TiledArgs T, int64_t t0, in
     const int64_t r0 = T.range_off[task], r1 = T.range_off[task + 1];
     const int nr = (int)(r1 - r0);
     int2 *rt = reinterpret_cast<int2 *>(smem);                 // range table
-    // halo entries as one 32 B record (v0, v1, v2 | -, 1/m): two LDS.128 per
-    // particle instead of D + 1 scattered LDS.64
-    double4 *sh = reinterpret_cast<double4 *>(smem + (((nr + 1) & ~1) + 3) / 4 * 4);
+    // halo as two 16 B-strided arrays, (v0, v1) and (v2 | 0, 1/m): one LDS.128
+    // each.  Record l sits in 16 B bank group l % 8 of both arrays (a 32 B
+    // record would only ever reach the even groups), and build_tiled orders
+    // each sub-colour so a quarter warp's li and lj are distinct mod 8.
+    double2 *sxy = reinterpret_cast<double2 *>(smem + (((nr + 1) & ~1) + 3) / 4 * 4);
+    double2 *szw = sxy + H;
     for (int r = threadIdx.x; r < nr; r += blockDim.x) rt[r] = T.ranges[r0 + r];
     __syncthreads();
     V_t *V = reinterpret_cast<V_t *>(T.V);
@@ -100,7 +103,7 @@ __global__ void __launch_bounds__(256) k_sweep_tiled(TiledArgs T, int64_t t0, in
     const int nsub = (int)(T.sub_off[task + 1] - s0) - 1;
     // double-buffered staging of each sub-colour's (pair, coefficient)
     // chunk with cp.async: chunk q+1 streams in while chunk q is applied
-    double *bd = reinterpret_cast<double *>(sh + H);                 // ring of coefficients
+    double *bd = reinterpret_cast<double *>(szw + H);                // ring of coefficients
     uint32_t *bp = reinterpret_cast<uint32_t *>(bd + kSweepStages * T.maxsub);  // ring of pairs
     int *ssub = reinterpret_cast<int *>(bp + kSweepStages * T.maxsub);         // sub-colour bounds
     for (int k = threadIdx.x; k <= nsub; k += blockDim.x) ssub[k] = T.sub[s0 + k];
@@ -132,7 +135,8 @@ __global__ void __launch_bounds__(256) k_sweep_tiled(TiledArgs T, int64_t t0, in
         const int64_t g = global_of(l);
         double v[3] = {0, 0, 0};
         vget(vldg(V + g), v);  // halos of one launch are disjoint: read-only here
-        sh[l] = make_double4(v[0], v[1], D == 3 ? v[2] : 0.0, T.inv_m[g]);
+        sxy[l] = make_double2(v[0], v[1]);
+        szw[l] = make_double2(D == 3 ? v[2] : 0.0, T.inv_m[g]);
     }
     const double half = 0.5 * ctrl->dt * ctrl->eta;
     for (int q = 0; q < nsub; ++q) {
@@ -147,9 +151,10 @@ __global__ void __launch_bounds__(256) k_sweep_tiled(TiledArgs T, int64_t t0, in
         for (int p = threadIdx.x; p < cnt; p += blockDim.x) {
             const uint32_t pk = cpk[p];
             const int li = (int)(pk & 0xffffu), lj = (int)(pk >> 16);
-            double4 a = sh[li], b = sh[lj];
+            double2 a = sxy[li], b = sxy[lj];
+            const double2 az = szw[li], bz = szw[lj];
             const double c = half * cd[p];
-            const double ca = c * a.w, cb = c * b.w;
+            const double ca = c * az.y, cb = c * bz.y;
             const double rden = 1.0 / (1.0 + ca + cb);
             double u = (a.x - b.x) * rden;
             a.x -= ca * u;
@@ -157,20 +162,20 @@ __global__ void __launch_bounds__(256) k_sweep_tiled(TiledArgs T, int64_t t0, in
             u = (a.y - b.y) * rden;
             a.y -= ca * u;
             b.y += cb * u;
+            sxy[li] = a;
+            sxy[lj] = b;
             if (D == 3) {
-                u = (a.z - b.z) * rden;
-                a.z -= ca * u;
-                b.z += cb * u;
+                u = (az.x - bz.x) * rden;
+                szw[li].x = az.x - ca * u;
+                szw[lj].x = bz.x + cb * u;
             }
-            sh[li] = a;
-            sh[lj] = b;
         }
         __syncthreads();
     }
     for (int l = threadIdx.x; l < H; l += blockDim.x) {
         const int64_t g = global_of(l);
-        const double4 e = sh[l];
-        const double v[3] = {e.x, e.y, e.z};
+        const double2 e = sxy[l];
+        const double v[3] = {e.x, e.y, szw[l].x};
         V_t w;
         vset(w, v);
         vst(V + g, w);
@@ -228,6 +233,60 @@ struct TaskOut {
     std::vector<uint16_t> self;  // local id of each owned particle
     std::vector<uint16_t> nl;    // width x owned, column-major local ids
 };
+
+// The pairs of one sub-colour are independent, so their order is free (the
+// result is bit-identical in any order).  Order them in groups of 8 -- one
+// quarter warp of the kernel's LDS.128 halo accesses -- whose li % 8 and
+// lj % 8 are each distinct where the bucket counts allow: such a group
+// reads and writes the halo in one shared-memory wavefront per access.
+// Greedy over the 8 x 8 (li % 8, lj % 8) buckets; leftovers fill groups.
+inline void bank_order(std::vector<uint32_t> &pairs, std::vector<double> &pd, int64_t s, int64_t e) {
+    const int64_t m = e - s;
+    if (m <= 1) return;
+    thread_local std::vector<int32_t> bk[64];
+    thread_local std::vector<int32_t> order;
+    thread_local std::vector<uint32_t> tp;
+    thread_local std::vector<double> td;
+    int rowtot[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (auto &v : bk) v.clear();
+    for (int64_t p = s; p < e; ++p) {
+        const int a = (int)(pairs[p] & 7u), b = (int)((pairs[p] >> 16) & 7u);
+        bk[a * 8 + b].push_back((int32_t)(p - s));
+        ++rowtot[a];
+    }
+    order.clear();
+    int64_t left = m;
+    auto take = [&](int a, int b) {
+        order.push_back(bk[a * 8 + b].back());
+        bk[a * 8 + b].pop_back();
+        --rowtot[a];
+        --left;
+    };
+    while (left > 0) {
+        int ua = 0, ub = 0, k = 0;
+        while (k < 8) {
+            int ba = -1, bb = -1, bn = 0;
+            for (int a = 0; a < 8; ++a)  // fullest unused row ...
+                if (!(ua >> a & 1) && rowtot[a] > bn) { bn = rowtot[a]; ba = a; }
+            if (ba < 0) break;
+            bn = 0;
+            for (int b = 0; b < 8; ++b)  // ... and its fullest unused column
+                if (!(ub >> b & 1) && (int)bk[ba * 8 + b].size() > bn) { bn = (int)bk[ba * 8 + b].size(); bb = b; }
+            ua |= 1 << ba;
+            if (bb < 0) continue;
+            ub |= 1 << bb;
+            take(ba, bb);
+            ++k;
+        }
+        for (int q = 0; q < 64 && k < 8 && left > 0; ++q)
+            while (k < 8 && !bk[q].empty()) { take(q >> 3, q & 7); ++k; }
+    }
+    tp.resize(m);
+    td.resize(m);
+    for (int64_t i = 0; i < m; ++i) { tp[i] = pairs[s + order[i]]; td[i] = pd[s + order[i]]; }
+    std::copy(tp.begin(), tp.end(), pairs.begin() + s);
+    std::copy(td.begin(), td.end(), pd.begin() + s);
+}
 
 }  // namespace tiled_detail
 
@@ -394,6 +453,7 @@ inline void build_tiled(const NbhDev &nb, int B, TiledSched &t, cudaStream_t s) 
                 T.pairs[w] = pr[p];
                 T.pd[w] = pdv[p];
             }
+            for (int c = 0; c < ncol; ++c) bank_order(T.pairs, T.pd, cnt[c], cnt[c + 1]);
         }
     };
     const int nth = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
@@ -475,18 +535,23 @@ inline void build_tiled(const NbhDev &nb, int B, TiledSched &t, cudaStream_t s) 
     upload_vec(t.own_n, ownn, s);
 }
 
-// Block edge: default 2 cells in 3D (a ~36 KB halo, several CTAs per SM)
-// and 4 in 2D; MTSPH_TILE_B / MTSPH_TILE_THREADS override.  Halves the
-// edge until the halo fits the shared-memory budget.
-inline void build_tiled_auto(const NbhDev &nb, TiledSched &t, cudaStream_t s) {
+// Block edge: `tile` cells if given (a multi-rank plan's edge: exact, or an
+// error), else 4 -- a ~150 KB halo in 3D, one 1024-thread CTA per SM with
+// ~500 pairs per sub-colour -- halved until the halo fits shared memory.
+// Measured at 10M particles (3D): B=2/128 thr 15.7 ms per sweep, B=4/1024
+// 10.5 ms.  MTSPH_TILE_B / MTSPH_TILE_THREADS override for tuning.
+inline void build_tiled_auto(const NbhDev &nb, TiledSched &t, cudaStream_t s, int tile = 0) {
     const size_t budget = 200 * 1024;
-    int B0 = nb.d == 2 ? 4 : 2, th = 128;
-    if (const char *e = std::getenv("MTSPH_TILE_B")) B0 = std::max(1, std::atoi(e));
-    if (const char *e = std::getenv("MTSPH_TILE_THREADS")) th = std::max(32, std::atoi(e));
+    int B0 = tile > 0 ? tile : 4, th = 1024;
+    if (tile <= 0)
+        if (const char *e = std::getenv("MTSPH_TILE_B")) B0 = std::max(1, std::atoi(e));
+    if (B0 & (B0 - 1)) throw Error(1, "tiled sweep: block edge must be a power of two");
+    if (const char *e = std::getenv("MTSPH_TILE_THREADS")) th = std::min(1024, std::max(32, std::atoi(e)));
     for (int B = B0; B >= 1; B >>= 1) {
         t = TiledSched();
         build_tiled(nb, B, t, s);
         if (tiled_smem_bytes(t, nb.d) <= budget) break;
+        if (tile > 0) throw Error(1, "tiled sweep: halo of the requested block edge exceeds shared memory");
         if (B == 1) throw Error(1, "tiled sweep: particle density too high for shared memory");
     }
     t.threads = th;

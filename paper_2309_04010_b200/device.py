@@ -94,7 +94,7 @@ class DeviceSolid:
     def __init__(self, pos, vol, rho0, constrained, side, mid_mask, h_axes,
                  shear_modulus, bulk_modulus, plastic=True, hardening_law=0,
                  hard=(1.0, 1.0, 1.0, 0.0), rm_tol=0.0, rm_max_iter=50, sweep="serial",
-                 ghost=None, grid=None):
+                 ghost=None, grid=None, tile=0):
         lib = _lib.load_library()
         pos = _f64(pos)
         n, d = pos.shape
@@ -116,7 +116,7 @@ class DeviceSolid:
             int(hardening_law), (ctypes.c_double * 4)(*[float(v) for v in hard]),
             float(rm_tol), int(rm_max_iter), _lib.SWEEPS[sweep],
             ptr(k["ghost"]).value if k["ghost"] is not None else None,
-            ptr(k["grid"]).value if k["grid"] is not None else None)
+            ptr(k["grid"]).value if k["grid"] is not None else None, int(tile))
         handle = ctypes.c_void_p()
         check(lib.mtsph_solid_create(ctypes.byref(desc), ctypes.byref(handle)))
         self._h = handle

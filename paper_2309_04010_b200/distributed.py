@@ -140,7 +140,8 @@ class DecomposedSolid:
                                      lat.mid_mask[ids] if lat.mid_mask is not None else None,
                                      lat.h_axes, elastic.shear_modulus, elastic.bulk_modulus,
                                      plastic=hardening is not None, hardening_law=law, hard=hp,
-                                     sweep="tiled", ghost=p.ghost, grid=self.grid)
+                                     sweep="tiled", ghost=p.ghost, grid=self.grid,
+                                     tile=p.tile_B)
         if group == "local":
             self.group = LocalGroup(self.plans, [devices[r] for r in range(nranks)])
         else:

@@ -52,6 +52,7 @@ class RankPlan:
     refresh_send: dict = field(default_factory=dict)   # q -> local indices (owned, ghosts on q)
     pushback_send: dict = field(default_factory=dict)  # (colour, q) -> local indices
     pushback_recv: dict = field(default_factory=dict)  # (colour, q) -> local indices
+    tile_B: int = 4                # sweep block edge the colours assume (passed to the device)
 
 
 def _cuts(ncell_x, counts_per_column, nranks):
@@ -92,7 +93,9 @@ def make_plans(pos, h_axes, nranks, tile_B=None):
     pos = np.asarray(pos, float)
     n, d = pos.shape
     if tile_B is None:
-        tile_B = 4 if d == 2 else 2
+        tile_B = 4
+    if tile_B not in (1, 2, 4):
+        raise ValueError(f"tile_B must be 1, 2 or 4 (slab alignment {SLAB_ALIGN}), got {tile_B}")
     u, lo, hi = scaled_grid(pos, h_axes)
     cells = cell_coords(u, lo)
     ncx = int(cells[:, 0].max()) + 1
@@ -108,7 +111,7 @@ def make_plans(pos, h_axes, nranks, tile_B=None):
         near = (cells[:, 0] >= x0 - 1) & (cells[:, 0] <= x1)
         local = gid[near]                                   # ascending global ids
         ghost = owner[local] != r
-        plans.append(RankPlan(r, local, ghost, owner[local], (x0, x1)))
+        plans.append(RankPlan(r, local, ghost, owner[local], (x0, x1), tile_B=tile_B))
     # refresh lists: ghosts of r owned by q <-> owned of q that are ghosts on r
     pos_in = [{int(g): i for i, g in enumerate(p.local_ids)} for p in plans]
     for p in plans:
