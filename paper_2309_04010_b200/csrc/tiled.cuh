@@ -23,6 +23,7 @@
 #include <algorithm>
 #include <array>
 #include <exception>
+#include <functional>
 #include <mutex>
 #include <thread>
 
@@ -108,6 +109,9 @@ __global__ void __launch_bounds__(1024) k_sweep_tiled(TiledArgs T, int64_t t0, i
     int *ssub = reinterpret_cast<int *>(bp + kSweepStages * T.maxsub);         // sub-colour bounds
     for (int k = threadIdx.x; k <= nsub; k += blockDim.x) ssub[k] = T.sub[s0 + k];
     __syncthreads();
+    // dir 1: sub-colours ascending, -1: descending.  (Merging the last
+    // forward and first reverse colour into one launch was measured slower.)
+    const int nq = nsub;
     auto sub_range = [&](int q, int &a, int &b) {
         const int s = dir > 0 ? q : nsub - 1 - q;
         a = ssub[s];
@@ -115,7 +119,7 @@ __global__ void __launch_bounds__(1024) k_sweep_tiled(TiledArgs T, int64_t t0, i
     };
     // every call commits exactly one (possibly empty) cp.async group
     auto stage = [&](int q) {
-        if (q < nsub) {
+        if (q < nq) {
             const int slot = q % kSweepStages;
             int a, b;
             sub_range(q, a, b);
@@ -139,7 +143,7 @@ __global__ void __launch_bounds__(1024) k_sweep_tiled(TiledArgs T, int64_t t0, i
         szw[l] = make_double2(D == 3 ? v[2] : 0.0, T.inv_m[g]);
     }
     const double half = 0.5 * ctrl->dt * ctrl->eta;
-    for (int q = 0; q < nsub; ++q) {
+    for (int q = 0; q < nq; ++q) {
         stage(q + kSweepStages - 1);
         asm volatile("cp.async.wait_group %0;\n" ::"n"(kSweepStages - 1));
         __syncthreads();
@@ -150,6 +154,7 @@ __global__ void __launch_bounds__(1024) k_sweep_tiled(TiledArgs T, int64_t t0, i
         const uint32_t *cpk = bp + (q % kSweepStages) * T.maxsub;
         for (int p = threadIdx.x; p < cnt; p += blockDim.x) {
             const uint32_t pk = cpk[p];
+            if (pk == 0xffffffffu) continue;  // kPadPair
             const int li = (int)(pk & 0xffffu), lj = (int)(pk >> 16);
             double2 a = sxy[li], b = sxy[lj];
             const double2 az = szw[li], bz = szw[lj];
@@ -164,10 +169,10 @@ __global__ void __launch_bounds__(1024) k_sweep_tiled(TiledArgs T, int64_t t0, i
             b.y += cb * u;
             sxy[li] = a;
             sxy[lj] = b;
-            if (D == 3) {
+            if (D == 3) {  // 16 B stores: conflict-free like the loads
                 u = (az.x - bz.x) * rden;
-                szw[li].x = az.x - ca * u;
-                szw[lj].x = bz.x + cb * u;
+                szw[li] = make_double2(az.x - ca * u, az.y);
+                szw[lj] = make_double2(bz.x + cb * u, bz.y);
             }
         }
         __syncthreads();
@@ -234,58 +239,64 @@ struct TaskOut {
     std::vector<uint16_t> nl;    // width x owned, column-major local ids
 };
 
+// Padding entry of a sub-colour: the lane idles (local ids are < 65535).
+constexpr uint32_t kPadPair = 0xffffffffu;
+
 // The pairs of one sub-colour are independent, so their order is free (the
-// result is bit-identical in any order).  Order them in groups of 8 -- one
+// result is bit-identical in any order).  Emit them in groups of 8 -- one
 // quarter warp of the kernel's LDS.128 halo accesses -- whose li % 8 and
-// lj % 8 are each distinct where the bucket counts allow: such a group
-// reads and writes the halo in one shared-memory wavefront per access.
-// Greedy over the 8 x 8 (li % 8, lj % 8) buckets; leftovers fill groups.
-inline void bank_order(std::vector<uint32_t> &pairs, std::vector<double> &pd, int64_t s, int64_t e) {
-    const int64_t m = e - s;
-    if (m <= 1) return;
+// lj % 8 are all distinct, so each group reads and writes the halo in one
+// shared-memory wavefront per access.  Each group is a maximum matching
+// (Kuhn's augmenting paths) in the 8 x 8 bipartite graph of non-empty
+// (li % 8, lj % 8) buckets, fullest rows and columns first; a group the
+// buckets cannot complete is padded with kPadPair rather than given a
+// conflicting pair.  The group count meets the lower bound max(row, column
+// total) -- ~69 groups for a 470-pair sub-colour, where a random order
+// costs ~137 quarter-warp wavefronts and a greedy one ~89.
+inline void bank_order(const uint32_t *pairs, const double *pd, int64_t m, std::vector<uint32_t> &op,
+                       std::vector<double> &od) {
     thread_local std::vector<int32_t> bk[64];
-    thread_local std::vector<int32_t> order;
-    thread_local std::vector<uint32_t> tp;
-    thread_local std::vector<double> td;
-    int rowtot[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     for (auto &v : bk) v.clear();
-    for (int64_t p = s; p < e; ++p) {
+    int rowtot[8] = {0, 0, 0, 0, 0, 0, 0, 0}, coltot[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int64_t p = 0; p < m; ++p) {
         const int a = (int)(pairs[p] & 7u), b = (int)((pairs[p] >> 16) & 7u);
-        bk[a * 8 + b].push_back((int32_t)(p - s));
+        bk[a * 8 + b].push_back((int32_t)p);
         ++rowtot[a];
+        ++coltot[b];
     }
-    order.clear();
     int64_t left = m;
-    auto take = [&](int a, int b) {
-        order.push_back(bk[a * 8 + b].back());
-        bk[a * 8 + b].pop_back();
-        --rowtot[a];
-        --left;
-    };
     while (left > 0) {
-        int ua = 0, ub = 0, k = 0;
-        while (k < 8) {
-            int ba = -1, bb = -1, bn = 0;
-            for (int a = 0; a < 8; ++a)  // fullest unused row ...
-                if (!(ua >> a & 1) && rowtot[a] > bn) { bn = rowtot[a]; ba = a; }
-            if (ba < 0) break;
-            bn = 0;
-            for (int b = 0; b < 8; ++b)  // ... and its fullest unused column
-                if (!(ub >> b & 1) && (int)bk[ba * 8 + b].size() > bn) { bn = (int)bk[ba * 8 + b].size(); bb = b; }
-            ua |= 1 << ba;
-            if (bb < 0) continue;
-            ub |= 1 << bb;
-            take(ba, bb);
-            ++k;
+        int rows[8], cols[8], mc[8];
+        for (int k = 0; k < 8; ++k) { rows[k] = cols[k] = k; mc[k] = -1; }
+        std::sort(rows, rows + 8, [&](int x, int y) { return rowtot[x] > rowtot[y]; });
+        std::sort(cols, cols + 8, [&](int x, int y) { return coltot[x] > coltot[y]; });
+        unsigned vis = 0;
+        std::function<bool(int)> augment = [&](int a) -> bool {
+            for (int k = 0; k < 8; ++k) {
+                const int b = cols[k];
+                if (bk[a * 8 + b].empty() || (vis >> b & 1)) continue;
+                vis |= 1u << b;
+                if (mc[b] < 0 || augment(mc[b])) { mc[b] = a; return true; }
+            }
+            return false;
+        };
+        for (int k = 0; k < 8; ++k) { vis = 0; augment(rows[k]); }
+        int g = 0;
+        for (int b = 0; b < 8; ++b) {
+            if (mc[b] < 0) continue;
+            const int a = mc[b];
+            const int32_t p = bk[a * 8 + b].back();
+            bk[a * 8 + b].pop_back();
+            --rowtot[a];
+            --coltot[b];
+            --left;
+            op.push_back(pairs[p]);
+            od.push_back(pd[p]);
+            ++g;
         }
-        for (int q = 0; q < 64 && k < 8 && left > 0; ++q)
-            while (k < 8 && !bk[q].empty()) { take(q >> 3, q & 7); ++k; }
+        if (left > 0)
+            for (; g < 8; ++g) { op.push_back(kPadPair); od.push_back(0.0); }
     }
-    tp.resize(m);
-    td.resize(m);
-    for (int64_t i = 0; i < m; ++i) { tp[i] = pairs[s + order[i]]; td[i] = pd[s + order[i]]; }
-    std::copy(tp.begin(), tp.end(), pairs.begin() + s);
-    std::copy(td.begin(), td.end(), pd.begin() + s);
 }
 
 }  // namespace tiled_detail
@@ -440,20 +451,26 @@ inline void build_tiled(const NbhDev &nb, int B, TiledSched &t, cudaStream_t s) 
                     colour.push_back(c);
                     ncol = std::max(ncol, c + 1);
                 }
-            // stable counting sort by sub-colour
+            // stable counting sort by sub-colour, then each sub-colour in
+            // bank-conflict-free quarter-warp groups (padded)
             std::vector<int32_t> cnt(ncol + 1, 0);
             for (int c : colour) cnt[c + 1]++;
             for (int c = 0; c < ncol; ++c) cnt[c + 1] += cnt[c];
-            T.sub.assign(cnt.begin(), cnt.end());
-            T.pairs.resize(pr.size());
-            T.pd.resize(pr.size());
+            std::vector<uint32_t> sp(pr.size());
+            std::vector<double> sd(pr.size());
             std::vector<int32_t> fill(cnt.begin(), cnt.end() - 1);
             for (size_t p = 0; p < pr.size(); ++p) {
                 const int w = fill[colour[p]]++;
-                T.pairs[w] = pr[p];
-                T.pd[w] = pdv[p];
+                sp[w] = pr[p];
+                sd[w] = pdv[p];
             }
-            for (int c = 0; c < ncol; ++c) bank_order(T.pairs, T.pd, cnt[c], cnt[c + 1]);
+            T.pairs.clear();
+            T.pd.clear();
+            T.sub.assign(1, 0);
+            for (int c = 0; c < ncol; ++c) {
+                bank_order(sp.data() + cnt[c], sd.data() + cnt[c], cnt[c + 1] - cnt[c], T.pairs, T.pd);
+                T.sub.push_back((int32_t)T.pairs.size());
+            }
         }
     };
     const int nth = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
@@ -517,7 +534,7 @@ inline void build_tiled(const NbhDev &nb, int B, TiledSched &t, cudaStream_t s) 
     }
     t.B = B;
     t.ntasks = (int64_t)order.size();
-    t.npairs = (int64_t)pairs.size();
+    t.npairs = (int64_t)std::count_if(pairs.begin(), pairs.end(), [](uint32_t p) { return p != kPadPair; });
     upload_vec(t.range_off, roff, s);
     upload_vec(t.ranges, ranges, s);
     upload_vec(t.halo_n, halo, s);
