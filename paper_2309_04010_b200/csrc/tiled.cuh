@@ -34,10 +34,13 @@ namespace mtsph {
 
 // depth of the cp.async ring that stages sub-colour chunks (prefetch
 // distance kSweepStages - 1 sub-colours)
-constexpr int kSweepStages = 4;
+#ifndef MTSPH_SWEEP_STAGES
+#define MTSPH_SWEEP_STAGES 4  // measured: 6 and 8 are slower (10M, 3D)
+#endif
+constexpr int kSweepStages = MTSPH_SWEEP_STAGES;
 
 struct TiledSched {
-    int B = 0;                       // cells per block edge
+    int sh = 0;                      // low Morton bits per block (build_tiled)
     int64_t ntasks = 0;
     int max_halo = 0, max_ranges = 0, maxsub = 0, max_nsub = 0;
     int threads = 128;
@@ -143,10 +146,14 @@ __global__ void __launch_bounds__(1024) k_sweep_tiled(TiledArgs T, int64_t t0, i
         szw[l] = make_double2(D == 3 ? v[2] : 0.0, T.inv_m[g]);
     }
     const double half = 0.5 * ctrl->dt * ctrl->eta;
+    // One barrier per sub-colour: after it, chunk q (this thread's copies
+    // waited for, the others' by the barrier) is visible and every thread has
+    // finished sub-colour q-1, so the halo is consistent and ring slot
+    // (q-1) % S -- the one refilled by stage(q + S - 1) -- is free.
     for (int q = 0; q < nq; ++q) {
-        stage(q + kSweepStages - 1);
-        asm volatile("cp.async.wait_group %0;\n" ::"n"(kSweepStages - 1));
+        asm volatile("cp.async.wait_group %0;\n" ::"n"(kSweepStages - 2));
         __syncthreads();
+        stage(q + kSweepStages - 1);
         int a0, b0;
         sub_range(q, a0, b0);
         const int cnt = b0 - a0;
@@ -175,8 +182,8 @@ __global__ void __launch_bounds__(1024) k_sweep_tiled(TiledArgs T, int64_t t0, i
                 szw[lj] = make_double2(bz.x + cb * u, bz.y);
             }
         }
-        __syncthreads();
     }
+    __syncthreads();
     for (int l = threadIdx.x; l < H; l += blockDim.x) {
         const int64_t g = global_of(l);
         const double2 e = sxy[l];
@@ -308,16 +315,20 @@ template <class T> void upload_vec(DBuf<T> &b, const std::vector<T> &v, cudaStre
     MT_CUDA(cudaStreamSynchronize(s));
 }
 
-inline void build_tiled(const NbhDev &nb, int B, TiledSched &t, cudaStream_t s) {
+// A block is the run of particles whose cell keys agree above the low `sh`
+// Morton bits: an aligned box of ext[0] x ext[1] (x ext[2]) cells, the
+// interleave (x0 y0 z0 x1 ...) giving axis k the bits i < sh with i % d == k
+// (sh = d log2 B: cubic edge B; sh = 5 in 3D: 4 x 4 x 2).
+inline void build_tiled(const NbhDev &nb, int sh, TiledSched &t, cudaStream_t s) {
     using namespace tiled_detail;
     const int64_t n = nb.n;
     const int d = nb.d;
-    int lb = 0;
-    while ((1 << lb) < B) ++lb;
-    // block colour period: same-colour blocks must be two cells apart so
-    // their one-cell halos are disjoint -- parity works from B = 2, single
-    // cells need period 3 (3^d colours)
-    const int P = B >= 2 ? 2 : 3;
+    int lg[3] = {0, 0, 0}, ext[3] = {1, 1, 1}, P[3] = {1, 1, 1};
+    for (int i = 0; i < sh; ++i) ++lg[i % d];
+    // block colour period per axis: same-coloured blocks must be two cells
+    // apart so their one-cell halos are disjoint -- parity works from an
+    // extent of 2 cells, single-cell extents need period 3
+    for (int k = 0; k < d; ++k) { ext[k] = 1 << lg[k]; P[k] = ext[k] >= 2 ? 2 : 3; }
     std::vector<uint64_t> cellkey(n);
     std::vector<int64_t> indptr(n + 1);
     std::vector<int32_t> csr(std::max<int64_t>(nb.nnz, 1));
@@ -341,10 +352,10 @@ inline void build_tiled(const NbhDev &nb, int B, TiledSched &t, cudaStream_t s) 
         b = cstart[c + 1];
         return true;
     };
-    // blocks = runs of equal key >> (d * lb)
+    // blocks = runs of equal key >> sh
     std::vector<int64_t> bstart;
     for (int64_t i = 0; i < n; ++i)
-        if (i == 0 || (cellkey[i] >> (d * lb)) != (cellkey[i - 1] >> (d * lb))) bstart.push_back(i);
+        if (i == 0 || (cellkey[i] >> sh) != (cellkey[i - 1] >> sh)) bstart.push_back(i);
     const int64_t nblocks = (int64_t)bstart.size();
     bstart.push_back(n);
     // multi-rank: blocks of ghost particles belong to another rank
@@ -378,16 +389,16 @@ inline void build_tiled(const NbhDev &nb, int B, TiledSched &t, cudaStream_t s) 
             int64_t cc[3] = {0, 0, 0}, bc[3] = {0, 0, 0};
             decode(cellkey[lo], d, cc);
             int col = 0;
-            for (int k = d - 1; k >= 0; --k) { bc[k] = cc[k] >> lb; col = col * P + (int)(bc[k] % P); }
+            for (int k = d - 1; k >= 0; --k) { bc[k] = cc[k] >> lg[k]; col = col * P[k] + (int)(bc[k] % P[k]); }
             T.colour = col;
             // halo ranges: cells of the block grown by one, z-y-x order
             int local = 0;
-            const int span = B + 2;
-            const int nz = d == 3 ? span : 1;
+            const int nz = d == 3 ? ext[2] + 2 : 1;
             for (int oz = 0; oz < nz; ++oz)
-                for (int oy = 0; oy < span; ++oy)
-                    for (int ox = 0; ox < span; ++ox) {
-                        int64_t q[3] = {bc[0] * B - 1 + ox, bc[1] * B - 1 + oy, d == 3 ? bc[2] * B - 1 + oz : 0};
+                for (int oy = 0; oy < ext[1] + 2; ++oy)
+                    for (int ox = 0; ox < ext[0] + 2; ++ox) {
+                        int64_t q[3] = {bc[0] * ext[0] - 1 + ox, bc[1] * ext[1] - 1 + oy,
+                                        d == 3 ? bc[2] * ext[2] - 1 + oz : 0};
                         bool ok = true;
                         for (int k = 0; k < d; ++k) ok = ok && q[k] >= 0;
                         if (!ok) continue;
@@ -489,7 +500,7 @@ inline void build_tiled(const NbhDev &nb, int B, TiledSched &t, cudaStream_t s) 
     if (err) std::rethrow_exception(err);
     // colour-major task order
     int ncol = 1;
-    for (int k = 0; k < d; ++k) ncol *= P;
+    for (int k = 0; k < d; ++k) ncol *= P[k];
     std::vector<int64_t> order;
     t.colour_ptr.assign(ncol + 1, 0);
     for (int c = 0; c < ncol; ++c) {
@@ -532,7 +543,7 @@ inline void build_tiled(const NbhDev &nb, int B, TiledSched &t, cudaStream_t s) 
         std::vector<uint32_t>().swap(T.pairs);
         std::vector<double>().swap(T.pd);
     }
-    t.B = B;
+    t.sh = sh;
     t.ntasks = (int64_t)order.size();
     t.npairs = (int64_t)std::count_if(pairs.begin(), pairs.end(), [](uint32_t p) { return p != kPadPair; });
     upload_vec(t.range_off, roff, s);
@@ -552,24 +563,31 @@ inline void build_tiled(const NbhDev &nb, int B, TiledSched &t, cudaStream_t s) 
     upload_vec(t.own_n, ownn, s);
 }
 
-// Block edge: `tile` cells if given (a multi-rank plan's edge: exact, or an
-// error), else 4 -- a ~150 KB halo in 3D, one 1024-thread CTA per SM with
-// ~500 pairs per sub-colour -- halved until the halo fits shared memory.
-// Measured at 10M particles (3D): B=2/128 thr 15.7 ms per sweep, B=4/1024
-// 10.5 ms.  MTSPH_TILE_B / MTSPH_TILE_THREADS override for tuning.
+// Block shape: a cubic edge of `tile` cells if given (a multi-rank plan's
+// edge: exact, or an error), else 4 x 4 (x 4) cells -- a ~150 KB halo in
+// 3D, one 1024-thread CTA per SM with ~500 pairs per sub-colour -- losing
+// one Morton bit (halving one axis) until the halo fits shared memory.
+// Measured at 10M particles (3D, bar_3d): 2^3 cells / 128 threads 15.7 ms
+// per sweep, 4^3 / 1024 10.5 ms.  MTSPH_TILE_BITS (low Morton bits per
+// block) / MTSPH_TILE_THREADS override for tuning.
 inline void build_tiled_auto(const NbhDev &nb, TiledSched &t, cudaStream_t s, int tile = 0) {
-    const size_t budget = 200 * 1024;
-    int B0 = tile > 0 ? tile : 4, th = 1024;
-    if (tile <= 0)
-        if (const char *e = std::getenv("MTSPH_TILE_B")) B0 = std::max(1, std::atoi(e));
-    if (B0 & (B0 - 1)) throw Error(1, "tiled sweep: block edge must be a power of two");
+    const size_t budget = 224 * 1024;  // opt-in maximum per CTA is 227 KB
+    const int d = nb.d;
+    int sh0 = 2 * d, th = 1024;
+    if (tile > 0) {
+        if (tile & (tile - 1)) throw Error(1, "tiled sweep: block edge must be a power of two");
+        sh0 = 0;
+        while ((1 << (sh0 / d)) < tile) sh0 += d;
+    } else if (const char *e = std::getenv("MTSPH_TILE_BITS")) {
+        sh0 = std::max(0, std::atoi(e));
+    }
     if (const char *e = std::getenv("MTSPH_TILE_THREADS")) th = std::min(1024, std::max(32, std::atoi(e)));
-    for (int B = B0; B >= 1; B >>= 1) {
+    for (int sh = sh0; sh >= 0; --sh) {
         t = TiledSched();
-        build_tiled(nb, B, t, s);
-        if (tiled_smem_bytes(t, nb.d) <= budget) break;
+        build_tiled(nb, sh, t, s);
+        if (tiled_smem_bytes(t, d) <= budget) break;
         if (tile > 0) throw Error(1, "tiled sweep: halo of the requested block edge exceeds shared memory");
-        if (B == 1) throw Error(1, "tiled sweep: particle density too high for shared memory");
+        if (sh == 0) throw Error(1, "tiled sweep: particle density too high for shared memory");
     }
     t.threads = th;
     // the attribute is per function, shared by every problem instance: allow
