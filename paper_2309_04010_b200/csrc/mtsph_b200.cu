@@ -21,6 +21,7 @@
 #include "solid.cuh"
 #include "tiled.cuh"
 #include "tgather.cuh"
+#include "gather_csr.cuh"
 #include "layer1.cuh"
 
 using namespace mtsph;
@@ -213,6 +214,10 @@ struct mtsph_solid {
     TiledSched tiled;
     std::vector<int64_t> iperm_h;  // original -> internal (lazy, for pack/unpack)
     bool tiled_gathers = false;
+    // 0: SELL gathers; G: row-parallel CSR gathers, G lanes per particle.
+    // Measured (10M, 3D): SELL 7.4 + 10.0 ms, G=2 5.8 + 7.4, G=4 5.8 + 7.3,
+    // G=8 6.9 + 8.7 (stress + accel); MTSPH_GATHER_LANES overrides
+    int gather_g = 4;
     size_t smem_stress = 0, smem_accel = 0;
     Ctrl *hc = nullptr;  // pinned mirror
     Mat mat{};
@@ -239,6 +244,7 @@ struct mtsph_solid {
         A.x = x.p; A.a = a.p; A.F = F.p; A.cp = cp.p; A.alpha = alpha.p; A.T = T.p;
         A.B = nb.B.p; A.mass = mass.p; A.rho0 = rho0.p; A.flags = flags.p;
         A.slice_ptr = nb.slice_ptr.p; A.slice_w = nb.slice_w.p; A.nbr = nb.nbr.p;
+        A.indptr = nb.indptr.p; A.csr = nb.csr.p;
         A.perm = nb.perm.p;
         A.part = part.p;
         A.nblk = nblk;
@@ -263,6 +269,27 @@ struct mtsph_solid {
     }
 };
 
+// neighbour gathers: row-parallel CSR (default, gather_g lanes per particle),
+// SELL (gather_g = 0), or block-tiled shared memory (opt-in, slower)
+template <int D> static void launch_stress_gather(mtsph_solid *S, const SolidArgs &A, cudaStream_t s) {
+    const unsigned nb = blocks_for(S->n);
+    if (S->nb.sweep == 3 && S->tiled_gathers)
+        k_stress_tiled<D><<<(unsigned)S->tiled.ntasks, 256, S->smem_stress, s>>>(A, gather_args(S->tiled));
+    else if (S->gather_g == 4) k_solid_stress_csr<D, 4><<<nb, 256, 0, s>>>(A);
+    else if (S->gather_g == 8) k_solid_stress_csr<D, 8><<<nb, 256, 0, s>>>(A);
+    else if (S->gather_g == 2) k_solid_stress_csr<D, 2><<<nb, 256, 0, s>>>(A);
+    else k_solid_stress<D, true><<<nb, 256, 0, s>>>(A);
+}
+template <int D> static void launch_accel_gather(mtsph_solid *S, const SolidArgs &A, cudaStream_t s) {
+    const unsigned nb = blocks_for(S->n);
+    if (S->nb.sweep == 3 && S->tiled_gathers)
+        k_accel_tiled<D><<<(unsigned)S->tiled.ntasks, 256, S->smem_accel, s>>>(A, gather_args(S->tiled));
+    else if (S->gather_g == 4) k_solid_accel_csr<D, 4><<<nb, 256, 0, s>>>(A);
+    else if (S->gather_g == 8) k_solid_accel_csr<D, 8><<<nb, 256, 0, s>>>(A);
+    else if (S->gather_g == 2) k_solid_accel_csr<D, 2><<<nb, 256, 0, s>>>(A);
+    else k_solid_accel<D><<<nb, 256, 0, s>>>(A);
+}
+
 // one inner step; ev (optional, 6 events) brackets the kernel classes
 template <int D> static int solid_step(mtsph_solid *S, int ctrl_mode, cudaEvent_t *ev = nullptr) {
     SolidArgs A = S->args();
@@ -275,14 +302,10 @@ template <int D> static int solid_step(mtsph_solid *S, int ctrl_mode, cudaEvent_
     mark(1);
     // split: the neighbour gather runs at low register count / high
     // occupancy, the register-heavy return map element-wise
-    const bool tiled = S->nb.sweep == 3 && S->tiled_gathers;
-    const unsigned nt = (unsigned)S->tiled.ntasks;
-    if (tiled) k_stress_tiled<D><<<nt, 256, S->smem_stress, S->s>>>(A, gather_args(S->tiled));
-    else k_solid_stress<D, true><<<nb, 256, 0, S->s>>>(A);
+    launch_stress_gather<D>(S, A, S->s);
     k_solid_rmap<D><<<nb, 256, 0, S->s>>>(A);
     mark(2);
-    if (tiled) k_accel_tiled<D><<<nt, 256, S->smem_accel, S->s>>>(A, gather_args(S->tiled));
-    else k_solid_accel<D><<<nb, 256, 0, S->s>>>(A);
+    launch_accel_gather<D>(S, A, S->s);
     MT_LAUNCH_CHECK();
     mark(3);
     int l = 3 + (S->nb.sweep == 3 ? launch_tiled_sweep<D>(S->tiled, S->tiled_args(), S->ctrl.p, S->s)
@@ -392,6 +415,11 @@ extern "C" mtsph_status mtsph_solid_create(const mtsph_solid_desc *dsc, mtsph_so
     S->inv_m.upload(inv_m.data(), n, S->s);
     S->flags.upload(flags.data(), n, S->s);
     S->nblk = (int)blocks_for(n);
+    if (const char *e = std::getenv("MTSPH_GATHER_LANES")) {
+        const int g = std::atoi(e);
+        if (g != 0 && g != 2 && g != 4 && g != 8) throw Error(MTSPH_ERR_ARG, "MTSPH_GATHER_LANES: 0, 2, 4 or 8");
+        S->gather_g = g;
+    }
     if (dsc->sweep == 3) {
         // shared-memory gathers over the sweep's blocks: opt-in
         // (MTSPH_TILED_GATHERS=1).  Measured slower than the SELL gathers
@@ -669,19 +697,13 @@ template <int D> static void solid_phase(mtsph_solid *S, int phase, int arg, dou
         S->launches += 1;
         break;
     case MTSPH_PHASE_STRESS:
-        if (S->nb.sweep == 3 && S->tiled_gathers)
-            k_stress_tiled<D><<<(unsigned)S->tiled.ntasks, 256, S->smem_stress, s>>>(A, gather_args(S->tiled));
-        else
-            k_solid_stress<D, true><<<nb, 256, 0, s>>>(A);
+        launch_stress_gather<D>(S, A, s);
         k_solid_rmap<D><<<nb, 256, 0, s>>>(A);
         S->launches += 2;
         break;
     case MTSPH_PHASE_ACCEL: {
         S->part.zero(s);
-        if (S->nb.sweep == 3 && S->tiled_gathers)
-            k_accel_tiled<D><<<(unsigned)S->tiled.ntasks, 256, S->smem_accel, s>>>(A, gather_args(S->tiled));
-        else
-            k_solid_accel<D><<<nb, 256, 0, s>>>(A);
+        launch_accel_gather<D>(S, A, s);
         MT_LAUNCH_CHECK();
         S->launches += 1;
         std::vector<double> h((size_t)2 * S->nblk);

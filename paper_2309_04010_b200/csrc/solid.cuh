@@ -181,6 +181,8 @@ struct SolidArgs {
     const uint8_t *flags;
     const int64_t *slice_ptr;
     const int32_t *slice_w, *nbr;
+    const int64_t *indptr;   // CSR rows (sorted), for the row-parallel gathers
+    const int32_t *csr;
     const int64_t *perm;
     double *part;    // [3][nblk]: ek, amax2, vmax2
     int nblk;

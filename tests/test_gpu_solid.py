@@ -60,6 +60,20 @@ def _neck_inputs(gold_traj, prefix):
 @pytest.mark.parametrize("prefix", ["n2_", "n3_"])
 def test_necking_trajectory_100_steps(gold_traj, prefix):
     """Per-step state within 1e-10 of the reference over 100 inner steps."""
+    _check_trajectory(gold_traj, prefix)
+
+
+@pytest.mark.parametrize("lanes", ["0", "2", "8"])
+@pytest.mark.parametrize("prefix", ["n2_", "n3_"])
+def test_necking_trajectory_gather_modes(gold_traj, prefix, lanes, monkeypatch):
+    """The same 100-step bar for every neighbour-gather mode: SELL (0) and the
+    row-parallel CSR gathers with 2 / 8 lanes per particle (4 is the default,
+    covered above).  Only the summation order differs between them."""
+    monkeypatch.setenv("MTSPH_GATHER_LANES", lanes)
+    _check_trajectory(gold_traj, prefix)
+
+
+def _check_trajectory(gold_traj, prefix):
     dev = _device()
     pos, vol, con, side, mid, dp = _neck_inputs(gold_traj, prefix)
     d = pos.shape[1]
