@@ -120,13 +120,18 @@ __global__ void __launch_bounds__(1024) k_sweep_tiled(TiledArgs T, int64_t t0, i
         a = ssub[s];
         b = ssub[s + 1];
     };
-    // every call commits exactly one (possibly empty) cp.async group
+    // Warp-specialised: the top eighth of the threads only stage chunks, the
+    // rest only apply pairs, so a chunk's copy overlaps the pair updates.
+    const int nst = blockDim.x >> 3, npr = blockDim.x - nst;
+    const bool stager = (int)threadIdx.x >= npr;
+    const int st = (int)threadIdx.x - npr;
+    // (stagers) every call commits exactly one (possibly empty) cp.async group
     auto stage = [&](int q) {
         if (q < nq) {
             const int slot = q % kSweepStages;
             int a, b;
             sub_range(q, a, b);
-            for (int p = a + threadIdx.x; p < b; p += blockDim.x) {
+            for (int p = a + st; p < b; p += nst) {
                 const unsigned dpd = (unsigned)__cvta_generic_to_shared(bd + slot * T.maxsub + (p - a));
                 const unsigned dpp = (unsigned)__cvta_generic_to_shared(bp + slot * T.maxsub + (p - a));
                 asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dpd), "l"(T.pd + p0 + p));
@@ -137,7 +142,8 @@ __global__ void __launch_bounds__(1024) k_sweep_tiled(TiledArgs T, int64_t t0, i
     };
     // prefetch distance kSweepStages-1 sub-colours; the first ones stream
     // in while the halo is gathered
-    for (int q = 0; q < kSweepStages - 1; ++q) stage(q);
+    if (stager)
+        for (int q = 0; q < kSweepStages - 1; ++q) stage(q);
     for (int l = threadIdx.x; l < H; l += blockDim.x) {
         const int64_t g = global_of(l);
         double v[3] = {0, 0, 0};
@@ -146,20 +152,26 @@ __global__ void __launch_bounds__(1024) k_sweep_tiled(TiledArgs T, int64_t t0, i
         szw[l] = make_double2(D == 3 ? v[2] : 0.0, T.inv_m[g]);
     }
     const double half = 0.5 * ctrl->dt * ctrl->eta;
-    // One barrier per sub-colour: after it, chunk q (this thread's copies
-    // waited for, the others' by the barrier) is visible and every thread has
-    // finished sub-colour q-1, so the halo is consistent and ring slot
-    // (q-1) % S -- the one refilled by stage(q + S - 1) -- is free.
+    if (stager) asm volatile("cp.async.wait_group %0;\n" ::"n"(kSweepStages - 2));  // chunk 0
+    __syncthreads();
+    // One barrier per sub-colour, at the end of iteration q.  Before it the
+    // stagers have issued chunk q + S - 1 into slot (q - 1) % S (free: every
+    // thread passed the previous barrier, so sub-colour q - 1 is done) and
+    // waited for chunks <= q + 1; after it chunk q + 1 is visible to all and
+    // sub-colour q is complete in the halo.
     for (int q = 0; q < nq; ++q) {
-        asm volatile("cp.async.wait_group %0;\n" ::"n"(kSweepStages - 2));
-        __syncthreads();
-        stage(q + kSweepStages - 1);
+        if (stager) {
+            stage(q + kSweepStages - 1);
+            asm volatile("cp.async.wait_group %0;\n" ::"n"(kSweepStages - 2));
+            __syncthreads();
+            continue;
+        }
         int a0, b0;
         sub_range(q, a0, b0);
         const int cnt = b0 - a0;
         const double *cd = bd + (q % kSweepStages) * T.maxsub;
         const uint32_t *cpk = bp + (q % kSweepStages) * T.maxsub;
-        for (int p = threadIdx.x; p < cnt; p += blockDim.x) {
+        for (int p = threadIdx.x; p < cnt; p += npr) {  // npr % 8 == 0: groups stay quarter warps
             const uint32_t pk = cpk[p];
             if (pk == 0xffffffffu) continue;  // kPadPair
             const int li = (int)(pk & 0xffffu), lj = (int)(pk >> 16);
@@ -182,8 +194,8 @@ __global__ void __launch_bounds__(1024) k_sweep_tiled(TiledArgs T, int64_t t0, i
                 szw[lj] = make_double2(bz.x + cb * u, bz.y);
             }
         }
+        __syncthreads();
     }
-    __syncthreads();
     for (int l = threadIdx.x; l < H; l += blockDim.x) {
         const int64_t g = global_of(l);
         const double2 e = sxy[l];
@@ -581,7 +593,8 @@ inline void build_tiled_auto(const NbhDev &nb, TiledSched &t, cudaStream_t s, in
     } else if (const char *e = std::getenv("MTSPH_TILE_BITS")) {
         sh0 = std::max(0, std::atoi(e));
     }
-    if (const char *e = std::getenv("MTSPH_TILE_THREADS")) th = std::min(1024, std::max(32, std::atoi(e)));
+    // multiple of 64: blockDim/8 staging threads, and a multiple of 8 pair lanes
+    if (const char *e = std::getenv("MTSPH_TILE_THREADS")) th = std::min(1024, std::max(64, std::atoi(e) & ~63));
     for (int sh = sh0; sh >= 0; --sh) {
         t = TiledSched();
         build_tiled(nb, sh, t, s);
