@@ -16,6 +16,16 @@
 
 #include "solid.cuh"
 
+// minimum resident CTAs per SM (register caps 85): measured at 10M (3D) accel
+// 7.3 ms at 2 CTAs (92 regs), 6.3 ms at 3, 7.0 ms at 4 (spills); stress is
+// flat from 3 up, and slower when the cap is lifted (1: 7.2 vs 5.8 ms)
+#ifndef MTSPH_STRESS_CTAS
+#define MTSPH_STRESS_CTAS 3
+#endif
+#ifndef MTSPH_ACCEL_CTAS
+#define MTSPH_ACCEL_CTAS 3
+#endif
+
 namespace mtsph {
 
 template <int G, int K> __device__ __forceinline__ void group_sum(double (&v)[K]) {
@@ -27,7 +37,7 @@ template <int G, int K> __device__ __forceinline__ void group_sum(double (&v)[K]
 
 // dF/dt gather + F update (the split path: the return map runs in k_solid_rmap)
 template <int D, int G>
-__global__ void __launch_bounds__(256) k_solid_stress_csr(SolidArgs A) {
+__global__ void __launch_bounds__(256, MTSPH_STRESS_CTAS) k_solid_stress_csr(SolidArgs A) {
     using V_t = typename VT<D>::T;
     const Ctrl *c = A.ctrl;
     if (c->done) return;
@@ -81,7 +91,7 @@ __global__ void __launch_bounds__(256) k_solid_stress_csr(SolidArgs A) {
 
 // a = 1/rho0 sum_b V_b (T_a + T_b) gradW, v += dt/2 a, E_k and |a|max partials
 template <int D, int G>
-__global__ void __launch_bounds__(256) k_solid_accel_csr(SolidArgs A) {
+__global__ void __launch_bounds__(256, MTSPH_ACCEL_CTAS) k_solid_accel_csr(SolidArgs A) {
     using V_t = typename VT<D>::T;
     __shared__ double sh[32];
     const Ctrl *c = A.ctrl;
@@ -93,13 +103,14 @@ __global__ void __launch_bounds__(256) k_solid_accel_csr(SolidArgs A) {
     for (int it = 0; it < G; ++it) {
         const int64_t i = (int64_t)blockIdx.x * 256 + it * (256 / G) + threadIdx.x / G;
         const bool act = i < n && !(A.flags[i] & FL_GHOST);
-        double acc[D];
+        // sum_b V_b (T_a + T_b) gradW = T_a (sum_b V_b gradW) + sum_b V_b T_b gradW:
+        // T_a stays out of the loop (registers: 3 CTAs per SM without it)
+        double acc[2 * D];  // [0, D): sum V_b T_b gradW, [D, 2D): sum V_b gradW
 #pragma unroll
-        for (int k = 0; k < D; ++k) acc[k] = 0.0;
+        for (int k = 0; k < 2 * D; ++k) acc[k] = 0.0;
         if (act) {
-            double xa[3], Ta[D * D];
+            double xa[3];
             xget<D>(ldg4(A.XV + i), xa);
-            tload<D>(A.T, n, i, Ta);
             const int64_t k1 = A.indptr[i + 1];
             for (int64_t k = A.indptr[i] + sub; k < k1; k += G) {
                 const int32_t b = __ldg(A.csr + k);
@@ -115,17 +126,23 @@ __global__ void __launch_bounds__(256) k_solid_accel_csr(SolidArgs A) {
                 for (int r = 0; r < D; ++r) {
                     double sum = 0.0;
 #pragma unroll
-                    for (int cc = 0; cc < D; ++cc) sum += (Ta[r * D + cc] + Tb[r * D + cc]) * g[cc];
+                    for (int cc = 0; cc < D; ++cc) sum += Tb[r * D + cc] * g[cc];
                     acc[r] += volb * sum;
+                    acc[D + r] += volb * g[r];
                 }
             }
         }
         group_sum<G>(acc);
         if (act && sub == 0) {
+            double Ta[D * D];
+            tload<D>(A.T, n, i, Ta);
             const double rho0 = A.rho0[i];
 #pragma unroll
             for (int k = 0; k < D; ++k) {
-                acc[k] /= rho0;
+                double ta = 0.0;
+#pragma unroll
+                for (int cc = 0; cc < D; ++cc) ta += Ta[k * D + cc] * acc[D + cc];
+                acc[k] = (acc[k] + ta) / rho0;
                 A.a[(int64_t)k * n + i] = acc[k];
             }
             if (A.flags[i] & FL_MOVABLE) {
