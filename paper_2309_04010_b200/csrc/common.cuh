@@ -41,11 +41,15 @@ inline unsigned blocks_for(int64_t n, int t = kThreads) {
 }
 
 // opt a kernel into the largest dynamic shared memory the device offers
+// (the opt-in limit covers static + dynamic)
 inline void allow_max_dynamic_smem(const void *fn) {
     int dev = 0, optin = 0;
+    cudaFuncAttributes fa{};
     MT_CUDA(cudaGetDevice(&dev));
     MT_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-    MT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    MT_CUDA(cudaFuncGetAttributes(&fa, fn));
+    MT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 optin - (int)fa.sharedSizeBytes));
 }
 
 // device buffer with RAII
@@ -121,6 +125,13 @@ __device__ __forceinline__ void grad_w(const double *rel, const KSpec &ks, doubl
 __device__ __forceinline__ double4 ldg4(const double4 *p) {
     double4 r;
     asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w) : "l"(p));
+    return r;
+}
+// L2-coherent 32 B load (bypasses L1): data another SM wrote during this launch
+__device__ __forceinline__ double4 ldcg4(const double4 *p) {
+    double4 r;
+    asm volatile("ld.global.cg.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w) : "l"(p) : "memory");
     return r;
 }
 __device__ __forceinline__ double4 ld4(const double4 *p) {

@@ -43,6 +43,8 @@ __device__ __forceinline__ void vget(const double4 &v, double *o) { o[0] = v.x; 
 // read-only velocity record (kernels that do not write V)
 __device__ __forceinline__ double2 vldg(const double2 *p) { return __ldg(p); }
 __device__ __forceinline__ double4 vldg(const double4 *p) { return ldg4(p); }
+__device__ __forceinline__ double2 vldcg(const double2 *p) { return __ldcg(p); }
+__device__ __forceinline__ double4 vldcg(const double4 *p) { return ldcg4(p); }
 __device__ __forceinline__ void vst(double2 *p, const double2 &v) { *p = v; }
 __device__ __forceinline__ void vst(double4 *p, const double4 &v) { st4(p, v); }
 __device__ __forceinline__ void vset(double2 &v, const double *o) { v.x = o[0]; v.y = o[1]; }

@@ -25,6 +25,7 @@
 #include <exception>
 #include <functional>
 #include <mutex>
+#include <unordered_map>
 #include <thread>
 
 #include "damping.cuh"
@@ -59,6 +60,10 @@ struct TiledSched {
     DBuf<int64_t> nl_off, self_off;  // ntasks + 1
     DBuf<uint16_t> nl, self;         // ELL (width x owned, column-major), owned local ids
     DBuf<int32_t> width, own0, own_n;
+    // dataflow (persistent) sweep: overlapping-halo task lists, colours,
+    // reverse-pass order, per-task completion + work counter (ntasks + 1)
+    DBuf<int32_t> f_nboff, f_nbt, f_col, f_rev, f_done;
+    int flow_grid = 0;               // 0: per-colour launches
 };
 
 struct TiledArgs {
@@ -75,12 +80,13 @@ struct TiledArgs {
     int maxsub;      // largest sub-colour (pairs), sizes the staging buffers
 };
 
-template <int D>
-__global__ void __launch_bounds__(1024) k_sweep_tiled(TiledArgs T, int64_t t0, int dir, const Ctrl *ctrl) {
+// One block task (one CTA): stage the halo, apply the sub-colours in
+// direction dir, write the halo back.  FLOW: other SMs write V during the
+// launch (persistent dataflow sweep), so the halo is read through L2.
+template <int D, bool FLOW>
+__device__ __forceinline__ void sweep_task(const TiledArgs &T, int64_t task, int dir, double half,
+                                           double *smem) {
     using V_t = typename VT<D>::T;
-    extern __shared__ double smem[];
-    if (ctrl->done) return;
-    const int64_t task = t0 + blockIdx.x;
     const int H = T.halo_n[task];
     const int64_t r0 = T.range_off[task], r1 = T.range_off[task + 1];
     const int nr = (int)(r1 - r0);
@@ -147,11 +153,11 @@ __global__ void __launch_bounds__(1024) k_sweep_tiled(TiledArgs T, int64_t t0, i
     for (int l = threadIdx.x; l < H; l += blockDim.x) {
         const int64_t g = global_of(l);
         double v[3] = {0, 0, 0};
-        vget(vldg(V + g), v);  // halos of one launch are disjoint: read-only here
+        // per-colour launches: halos of one launch are disjoint, read-only here
+        vget(FLOW ? vldcg(V + g) : vldg(V + g), v);
         sxy[l] = make_double2(v[0], v[1]);
         szw[l] = make_double2(D == 3 ? v[2] : 0.0, T.inv_m[g]);
     }
-    const double half = 0.5 * ctrl->dt * ctrl->eta;
     if (stager) asm volatile("cp.async.wait_group %0;\n" ::"n"(kSweepStages - 2));  // chunk 0
     __syncthreads();
     // One barrier per sub-colour, at the end of iteration q.  Before it the
@@ -206,6 +212,74 @@ __global__ void __launch_bounds__(1024) k_sweep_tiled(TiledArgs T, int64_t t0, i
     }
 }
 
+// per-colour launch: one CTA per block task of the colour
+template <int D>
+__global__ void __launch_bounds__(1024) k_sweep_tiled(TiledArgs T, int64_t t0, int dir, const Ctrl *ctrl) {
+    extern __shared__ double smem[];
+    if (ctrl->done) return;
+    sweep_task<D, false>(T, t0 + blockIdx.x, dir, 0.5 * ctrl->dt * ctrl->eta, smem);
+}
+
+// Dataflow schedule of a whole sweep (both passes) in one persistent launch.
+struct TiledFlow {
+    const int32_t *nb_off, *nb_task;  // per task: the tasks whose halos overlap its halo
+    const int32_t *colour;            // per task
+    const int32_t *rev;               // reverse-pass task order (colours descending)
+    int32_t *done;                    // per task: passes completed in this sweep
+    int32_t *counter;                 // next work item
+    int32_t ntasks;
+};
+
+__device__ __forceinline__ int ld_acquire_gpu(const int32_t *p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_gpu(int32_t *p, int v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Persistent sweep: CTAs claim work items in phase order (forward pass in
+// colour-major task order, then the reverse pass with colours descending)
+// and start an item once every task that touches its halo in an earlier
+// phase is done -- so colour c+1 starts block by block as its neighbours of
+// colour c finish, with no launch boundary (and no tail) between colours.
+// Deadlock-free: an item only waits on items claimed earlier by running CTAs.
+// Result identical to the per-colour launches (same tasks, same order on
+// every particle).
+template <int D>
+__global__ void __launch_bounds__(1024) k_sweep_flow(TiledArgs T, TiledFlow F, const Ctrl *ctrl) {
+    extern __shared__ double smem[];
+    __shared__ int s_w;
+    if (ctrl->done) return;
+    const double half = 0.5 * ctrl->dt * ctrl->eta;
+    for (;;) {
+        if (threadIdx.x == 0) s_w = atomicAdd(F.counter, 1);
+        __syncthreads();
+        const int w = s_w;
+        if (w >= 2 * F.ntasks) return;
+        const int pass = w >= F.ntasks;
+        const int t = pass ? F.rev[w - F.ntasks] : w;
+        if (threadIdx.x < 32) {  // warp 0: one lane per dependency, so one L2 round trip
+            const int ct = F.colour[t];
+            if (pass && threadIdx.x == 0)
+                while (ld_acquire_gpu(F.done + t) < 1) __nanosleep(32);
+            for (int k = F.nb_off[t] + (int)threadIdx.x; k < F.nb_off[t + 1]; k += 32) {
+                const int u = F.nb_task[k], cu = F.colour[u];
+                const int need = pass == 0 ? (cu < ct ? 1 : 0) : (cu > ct ? 2 : 1);
+                while (ld_acquire_gpu(F.done + u) < need) __nanosleep(32);
+            }
+        }
+        __syncthreads();
+        sweep_task<D, true>(T, t, pass ? -1 : 1, half, smem);
+        __syncthreads();  // every write-back of the halo issued
+        if (threadIdx.x == 0) {
+            __threadfence();
+            st_release_gpu(F.done + t, pass + 1);
+        }
+    }
+}
+
 inline size_t tiled_smem_bytes(const TiledSched &t, int d) {
     (void)d;
     return (size_t)((((t.max_ranges + 1) & ~1) + 3) / 4 * 4) * 8 + (size_t)t.max_halo * 32 +
@@ -216,6 +290,14 @@ template <int D>
 int launch_tiled_sweep(const TiledSched &t, const TiledArgs &A, const Ctrl *ctrl, cudaStream_t s) {
     const int nc = (int)t.colour_ptr.size() - 1;
     const size_t sm = tiled_smem_bytes(t, D);
+    if (t.flow_grid > 0 && t.ntasks > 0) {
+        MT_CUDA(cudaMemsetAsync(t.f_done.p, 0, sizeof(int32_t) * (size_t)(t.ntasks + 1), s));
+        TiledFlow F{t.f_nboff.p, t.f_nbt.p, t.f_col.p, t.f_rev.p, t.f_done.p, t.f_done.p + t.ntasks,
+                    (int32_t)t.ntasks};
+        k_sweep_flow<D><<<(unsigned)t.flow_grid, t.threads, sm, s>>>(A, F, ctrl);
+        MT_LAUNCH_CHECK();
+        return 1;
+    }
     int launches = 0;
     for (int pass = 0; pass < 2; ++pass)
         for (int q = 0; q < nc; ++q) {
@@ -519,6 +601,42 @@ inline void build_tiled(const NbhDev &nb, int sh, TiledSched &t, cudaStream_t s)
         for (int64_t bk = 0; bk < nblocks; ++bk) if (!skip[bk] && out[bk].colour == c) order.push_back(bk);
         t.colour_ptr[c + 1] = (int64_t)order.size();
     }
+    // dataflow sweep: per task, the tasks whose halos overlap its halo (block
+    // coordinates within 1, or 2 along a one-cell axis), its colour, and the
+    // reverse-pass order
+    {
+        std::unordered_map<uint64_t, int32_t> at;
+        at.reserve(order.size() * 2);
+        for (size_t q = 0; q < order.size(); ++q) at[cellkey[bstart[order[q]]] >> sh] = (int32_t)q;
+        std::vector<int32_t> nboff(1, 0), nbt, col(order.size()), rev;
+        int r[3] = {0, 0, 0};
+        for (int k = 0; k < d; ++k) r[k] = ext[k] == 1 ? 2 : 1;
+        for (size_t q = 0; q < order.size(); ++q) {
+            const int64_t bk = order[q];
+            col[q] = out[bk].colour;
+            int64_t cc[3] = {0, 0, 0}, bc[3] = {0, 0, 0};
+            decode(cellkey[bstart[bk]], d, cc);
+            for (int k = 0; k < d; ++k) bc[k] = cc[k] >> lg[k];
+            for (int oz = -r[2]; oz <= r[2]; ++oz)
+                for (int oy = -r[1]; oy <= r[1]; ++oy)
+                    for (int ox = -r[0]; ox <= r[0]; ++ox) {
+                        if (ox == 0 && oy == 0 && oz == 0) continue;
+                        const int64_t nbc[3] = {bc[0] + ox, bc[1] + oy, bc[2] + oz};
+                        if (nbc[0] < 0 || nbc[1] < 0 || nbc[2] < 0) continue;
+                        const int64_t qc[3] = {nbc[0] << lg[0], nbc[1] << lg[1], nbc[2] << lg[2]};
+                        auto it = at.find(encode(qc, d) >> sh);
+                        if (it != at.end()) nbt.push_back(it->second);
+                    }
+            nboff.push_back((int32_t)nbt.size());
+        }
+        for (int c = ncol - 1; c >= 0; --c)
+            for (int64_t q = t.colour_ptr[c]; q < t.colour_ptr[c + 1]; ++q) rev.push_back((int32_t)q);
+        upload_vec(t.f_nboff, nboff, s);
+        upload_vec(t.f_nbt, nbt, s);
+        upload_vec(t.f_col, col, s);
+        upload_vec(t.f_rev, rev, s);
+        t.f_done.alloc(order.size() + 1);
+    }
     std::vector<int64_t> roff(1, 0), poff(1, 0), soff(1, 0);
     std::vector<int2> ranges;
     std::vector<int32_t> halo, sub;
@@ -607,6 +725,20 @@ inline void build_tiled_auto(const NbhDev &nb, TiledSched &t, cudaStream_t s, in
     // the opt-in maximum once (the launch's own size sets the occupancy)
     allow_max_dynamic_smem((const void *)k_sweep_tiled<2>);
     allow_max_dynamic_smem((const void *)k_sweep_tiled<3>);
+    allow_max_dynamic_smem((const void *)k_sweep_flow<2>);
+    allow_max_dynamic_smem((const void *)k_sweep_flow<3>);
+    // persistent dataflow launch (default; MTSPH_SWEEP_FLOW=0: per-colour
+    // launches): as many CTAs as fit at once
+    const char *fe = std::getenv("MTSPH_SWEEP_FLOW");
+    if (!(fe && fe[0] == '0')) {
+        int dev = 0, sms = 0, per = 0;
+        MT_CUDA(cudaGetDevice(&dev));
+        MT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        MT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &per, d == 3 ? (const void *)k_sweep_flow<3> : (const void *)k_sweep_flow<2>, th,
+            tiled_smem_bytes(t, d)));
+        t.flow_grid = sms * per;
+    }
 }
 
 }  // namespace mtsph
