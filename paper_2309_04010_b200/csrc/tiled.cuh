@@ -44,6 +44,7 @@ struct TiledSched {
     int sh = 0;                      // low Morton bits per block (build_tiled)
     int64_t ntasks = 0;
     int max_halo = 0, max_ranges = 0, maxsub = 0, max_nsub = 0;
+    int64_t nsub_total = 0;          // sub-colours over all tasks (one pass)
     int threads = 128;
     std::vector<int64_t> colour_ptr; // 2^d + 1, over tasks (colour-major)
     DBuf<int64_t> range_off;         // ntasks + 1 -> ranges
@@ -126,9 +127,12 @@ __device__ __forceinline__ void sweep_task(const TiledArgs &T, int64_t task, int
         a = ssub[s];
         b = ssub[s + 1];
     };
-    // Warp-specialised: the top eighth of the threads only stage chunks, the
-    // rest only apply pairs, so a chunk's copy overlaps the pair updates.
-    const int nst = blockDim.x >> 3, npr = blockDim.x - nst;
+    // Warp-specialised: the top eighth of the threads (whole warps, at least
+    // one) only stage chunks, the rest only apply pairs, so a chunk's copy
+    // overlaps the pair updates.  Whole warps: the two roles reach
+    // __syncthreads (bar.sync, .aligned) from different call sites, which a
+    // warp may only do if all its lanes take the same one.
+    const int nst = std::max(32, (int)(blockDim.x >> 3) & ~31), npr = (int)blockDim.x - nst;
     const bool stager = (int)threadIdx.x >= npr;
     const int st = (int)threadIdx.x - npr;
     // (stagers) every call commits exactly one (possibly empty) cp.async group
@@ -669,6 +673,7 @@ inline void build_tiled(const NbhDev &nb, int sh, TiledSched &t, cudaStream_t s)
         t.max_ranges = std::max(t.max_ranges, (int)T.ranges.size());
         for (size_t k = 0; k + 1 < T.sub.size(); ++k) t.maxsub = std::max(t.maxsub, T.sub[k + 1] - T.sub[k]);
         t.max_nsub = std::max(t.max_nsub, (int)T.sub.size() - 1);
+        t.nsub_total += (int64_t)T.sub.size() - 1;
         std::vector<int2>().swap(T.ranges);
         std::vector<uint32_t>().swap(T.pairs);
         std::vector<double>().swap(T.pd);
@@ -703,7 +708,9 @@ inline void build_tiled(const NbhDev &nb, int sh, TiledSched &t, cudaStream_t s)
 inline void build_tiled_auto(const NbhDev &nb, TiledSched &t, cudaStream_t s, int tile = 0) {
     const size_t budget = 224 * 1024;  // opt-in maximum per CTA is 227 KB
     const int d = nb.d;
-    int sh0 = 2 * d, th = 1024;
+    // 3D: 4^3 cells; 2D: 16^2 cells (measured, 10M 2D bar: 4^2 / 1024 thr
+    // 15.3 ms per sweep, 4^2 / 256 2.9, 8^2 4.3, 16^2 2.05; larger does not fit)
+    int sh0 = d == 3 ? 6 : 8, th = 0;
     if (tile > 0) {
         if (tile & (tile - 1)) throw Error(1, "tiled sweep: block edge must be a power of two");
         sh0 = 0;
@@ -711,7 +718,7 @@ inline void build_tiled_auto(const NbhDev &nb, TiledSched &t, cudaStream_t s, in
     } else if (const char *e = std::getenv("MTSPH_TILE_BITS")) {
         sh0 = std::max(0, std::atoi(e));
     }
-    // multiple of 64: blockDim/8 staging threads, and a multiple of 8 pair lanes
+    // multiple of 64 (>= 64): whole staging warps plus whole pair warps
     if (const char *e = std::getenv("MTSPH_TILE_THREADS")) th = std::min(1024, std::max(64, std::atoi(e) & ~63));
     for (int sh = sh0; sh >= 0; --sh) {
         t = TiledSched();
@@ -719,6 +726,13 @@ inline void build_tiled_auto(const NbhDev &nb, TiledSched &t, cudaStream_t s, in
         if (tiled_smem_bytes(t, d) <= budget) break;
         if (tile > 0) throw Error(1, "tiled sweep: halo of the requested block edge exceeds shared memory");
         if (sh == 0) throw Error(1, "tiled sweep: particle density too high for shared memory");
+    }
+    if (th == 0) {
+        // about two threads per (padded) pair of an average sub-colour: the
+        // measured optimum for 4^3 (3D, ~550 -> 1024), 16^2 (2D, ~700 ->
+        // 1024) and the small fallback blocks (4^2 in 2D: 256 beat 1024 5x)
+        const double avg = t.nsub_total ? (double)t.pairs.n / (double)t.nsub_total : 0.0;
+        th = std::min(1024, std::max(128, ((int)(2.0 * avg) + 63) & ~63));
     }
     t.threads = th;
     // the attribute is per function, shared by every problem instance: allow

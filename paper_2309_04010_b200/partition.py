@@ -28,7 +28,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 CELL = 2.0        # cell edge in the scaled space (kernel support radius)
-SLAB_ALIGN = 4    # slab boundaries at multiples of 4 cells (largest tile edge)
+SLAB_ALIGN = 4    # minimum slab alignment in cells (raised to the sweep tile edge)
 
 
 def scaled_grid(pos, h_axes):
@@ -55,16 +55,16 @@ class RankPlan:
     tile_B: int = 4                # sweep block edge the colours assume (passed to the device)
 
 
-def _cuts(ncell_x, counts_per_column, nranks):
-    """Slab boundaries in cell columns: multiples of SLAB_ALIGN, balanced
+def _cuts(ncell_x, counts_per_column, nranks, align=SLAB_ALIGN):
+    """Slab boundaries in cell columns: multiples of `align`, balanced
     particle counts, at least one column group per rank."""
-    ngroups = -(-ncell_x // SLAB_ALIGN)
+    ngroups = -(-ncell_x // align)
     if ngroups < nranks:
         raise ValueError(f"cannot split {ncell_x} cell columns into {nranks} slabs of whole "
-                         f"{SLAB_ALIGN}-column groups")
-    padded = np.zeros(ngroups * SLAB_ALIGN)
+                         f"{align}-column groups")
+    padded = np.zeros(ngroups * align)
     padded[:ncell_x] = counts_per_column
-    acc = np.cumsum(padded.reshape(ngroups, SLAB_ALIGN).sum(axis=1))
+    acc = np.cumsum(padded.reshape(ngroups, align).sum(axis=1))
     cut_groups = [0]
     for r in range(1, nranks):
         g = int(np.searchsorted(acc, acc[-1] * r / nranks)) + 1
@@ -72,7 +72,7 @@ def _cuts(ncell_x, counts_per_column, nranks):
         g = min(g, ngroups - (nranks - r))             # leave one group per remaining rank
         cut_groups.append(g)
     cut_groups.append(ngroups)
-    return np.asarray(cut_groups, np.int64) * SLAB_ALIGN
+    return np.asarray(cut_groups, np.int64) * align
 
 
 def block_colour_and_halo(cells, B, d):
@@ -93,14 +93,15 @@ def make_plans(pos, h_axes, nranks, tile_B=None):
     pos = np.asarray(pos, float)
     n, d = pos.shape
     if tile_B is None:
-        tile_B = 4
-    if tile_B not in (1, 2, 4):
-        raise ValueError(f"tile_B must be 1, 2 or 4 (slab alignment {SLAB_ALIGN}), got {tile_B}")
+        tile_B = 4 if d == 3 else 16    # the device defaults (tiled.cuh build_tiled_auto)
+    if tile_B not in (1, 2, 4, 8, 16):
+        raise ValueError(f"tile_B must be a power of two <= 16, got {tile_B}")
+    align = max(SLAB_ALIGN, tile_B)     # every sweep block inside one slab
     u, lo, hi = scaled_grid(pos, h_axes)
     cells = cell_coords(u, lo)
     ncx = int(cells[:, 0].max()) + 1
     counts = np.bincount(cells[:, 0], minlength=ncx)
-    cuts = _cuts(ncx, counts, nranks)
+    cuts = _cuts(ncx, counts, nranks, align)
     owner = np.searchsorted(cuts, cells[:, 0], side="right") - 1
     grid = np.concatenate([np.pad(lo, (0, 3 - d)), np.pad(hi, (0, 3 - d))])
     col, bc = block_colour_and_halo(cells, tile_B, d)
