@@ -19,9 +19,10 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 
-CLASS_OF = {"k_solid_stress": "stress", "k_solid_rmap": "stress", "k_solid_accel": "accel",
-            "k_sweep_tiled": "sweep", "k_solid_kick_drift": "kick_drift", "k_solid_vmax": "reduce",
-            "k_ctrl": "reduce"}
+CLASS_OF = {"k_solid_stress": "stress", "k_solid_stress_csr": "stress", "k_solid_rmap": "stress",
+            "k_solid_accel": "accel", "k_solid_accel_csr": "accel",
+            "k_sweep_tiled": "sweep", "k_sweep_flow": "sweep",
+            "k_solid_kick_drift": "kick_drift", "k_solid_vmax": "reduce", "k_ctrl": "reduce"}
 KEY = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
        "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
        "sm__warps_active.avg.pct_of_peak_sustained_active",
