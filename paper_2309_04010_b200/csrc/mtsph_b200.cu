@@ -20,7 +20,6 @@
 #include "porous.cuh"
 #include "solid.cuh"
 #include "tiled.cuh"
-#include "tgather.cuh"
 #include "gather_csr.cuh"
 #include "layer1.cuh"
 
@@ -213,12 +212,10 @@ struct mtsph_solid {
     DBuf<int64_t> level_ptr;
     TiledSched tiled;
     std::vector<int64_t> iperm_h;  // original -> internal (lazy, for pack/unpack)
-    bool tiled_gathers = false;
     // 0: SELL gathers; G: row-parallel CSR gathers, G lanes per particle.
     // Measured (10M, 3D): SELL 7.4 + 10.0 ms, G=2 5.8 + 7.4, G=4 5.8 + 7.3,
     // G=8 6.9 + 8.7 (stress + accel); MTSPH_GATHER_LANES overrides
     int gather_g = 4;
-    size_t smem_stress = 0, smem_accel = 0;
     Ctrl *hc = nullptr;  // pinned mirror
     Mat mat{};
     int nblk = 0;
@@ -273,18 +270,14 @@ struct mtsph_solid {
 // SELL (gather_g = 0), or block-tiled shared memory (opt-in, slower)
 template <int D> static void launch_stress_gather(mtsph_solid *S, const SolidArgs &A, cudaStream_t s) {
     const unsigned nb = blocks_for(S->n);
-    if (S->nb.sweep == 3 && S->tiled_gathers)
-        k_stress_tiled<D><<<(unsigned)S->tiled.ntasks, 256, S->smem_stress, s>>>(A, gather_args(S->tiled));
-    else if (S->gather_g == 4) k_solid_stress_csr<D, 4><<<nb, 256, 0, s>>>(A);
+    if (S->gather_g == 4) k_solid_stress_csr<D, 4><<<nb, 256, 0, s>>>(A);
     else if (S->gather_g == 8) k_solid_stress_csr<D, 8><<<nb, 256, 0, s>>>(A);
     else if (S->gather_g == 2) k_solid_stress_csr<D, 2><<<nb, 256, 0, s>>>(A);
     else k_solid_stress<D, true><<<nb, 256, 0, s>>>(A);
 }
 template <int D> static void launch_accel_gather(mtsph_solid *S, const SolidArgs &A, cudaStream_t s) {
     const unsigned nb = blocks_for(S->n);
-    if (S->nb.sweep == 3 && S->tiled_gathers)
-        k_accel_tiled<D><<<(unsigned)S->tiled.ntasks, 256, S->smem_accel, s>>>(A, gather_args(S->tiled));
-    else if (S->gather_g == 4) k_solid_accel_csr<D, 4><<<nb, 256, 0, s>>>(A);
+    if (S->gather_g == 4) k_solid_accel_csr<D, 4><<<nb, 256, 0, s>>>(A);
     else if (S->gather_g == 8) k_solid_accel_csr<D, 8><<<nb, 256, 0, s>>>(A);
     else if (S->gather_g == 2) k_solid_accel_csr<D, 2><<<nb, 256, 0, s>>>(A);
     else k_solid_accel<D><<<nb, 256, 0, s>>>(A);
@@ -419,24 +412,6 @@ extern "C" mtsph_status mtsph_solid_create(const mtsph_solid_desc *dsc, mtsph_so
         const int g = std::atoi(e);
         if (g != 0 && g != 2 && g != 4 && g != 8) throw Error(MTSPH_ERR_ARG, "MTSPH_GATHER_LANES: 0, 2, 4 or 8");
         S->gather_g = g;
-    }
-    if (dsc->sweep == 3) {
-        // shared-memory gathers over the sweep's blocks: opt-in
-        // (MTSPH_TILED_GATHERS=1).  Measured slower than the SELL gathers
-        // through L1 on the 10M bar (1 CTA/SM at ~170 KB halo): DESIGN.md §4
-        const char *e = std::getenv("MTSPH_TILED_GATHERS");
-        S->tiled_gathers = e && e[0] == '1';
-        S->smem_stress = gather_smem_bytes(S->tiled, 8);
-        S->smem_accel = gather_smem_bytes(S->tiled, 4 + d * d);
-        if (S->smem_accel > 220 * 1024) S->tiled_gathers = false;
-        if (S->tiled_gathers) {
-            allow_max_dynamic_smem((const void *)k_stress_tiled<2>);
-            allow_max_dynamic_smem((const void *)k_accel_tiled<2>);
-            allow_max_dynamic_smem((const void *)k_stress_tiled<3>);
-            allow_max_dynamic_smem((const void *)k_accel_tiled<3>);
-            // per-block partials of the tiled divergence share the layout
-            S->nblk = (int)std::max<int64_t>(S->nblk, S->tiled.ntasks);
-        }
     }
     S->part.alloc((size_t)3 * S->nblk);
     S->part.zero(S->s);

@@ -56,11 +56,6 @@ struct TiledSched {
     DBuf<int64_t> sub_off;           // ntasks + 1 -> sub
     DBuf<int32_t> sub;               // per task: nsub + 1 pair offsets (task-relative)
     int64_t npairs = 0;
-    // block-local neighbour tables for the shared-memory gathers
-    int max_own = 0;
-    DBuf<int64_t> nl_off, self_off;  // ntasks + 1
-    DBuf<uint16_t> nl, self;         // ELL (width x owned, column-major), owned local ids
-    DBuf<int32_t> width, own0, own_n;
     // dataflow (persistent) sweep: overlapping-halo task lists, colours,
     // reverse-pass order, per-task completion + work counter (ntasks + 1)
     DBuf<int32_t> f_nboff, f_nbt, f_col, f_rev, f_done;
@@ -338,10 +333,6 @@ struct TaskOut {
     std::vector<uint32_t> pairs;
     std::vector<double> pd;
     std::vector<int32_t> sub;
-    int64_t own0 = 0;            // first owned particle (global)
-    int width = 0;               // ELL width of the block-local table
-    std::vector<uint16_t> self;  // local id of each owned particle
-    std::vector<uint16_t> nl;    // width x owned, column-major local ids
 };
 
 // Padding entry of a sub-colour: the lane idles (local ids are < 65535).
@@ -517,26 +508,6 @@ inline void build_tiled(const NbhDev &nb, int sh, TiledSched &t, cudaStream_t s)
                 const int2 r = T.ranges[it->second];
                 return r.y + (int)(g - r.x);
             };
-            // block-local neighbour table for the shared-memory gathers:
-            // ELL, column-major over the owned particles, padded with self
-            {
-                const int cnt = (int)(hi - lo);
-                int W = 0;
-                for (int64_t a = lo; a < hi; ++a) W = std::max<int>(W, (int)(indptr[a + 1] - indptr[a]));
-                T.own0 = lo;
-                T.width = W;
-                T.self.resize(cnt);
-                T.nl.assign((size_t)W * cnt, 0);
-                for (int k = 0; k < cnt; ++k) {
-                    const int64_t a = lo + k;
-                    const uint16_t sl = (uint16_t)local_of(a);
-                    T.self[k] = sl;
-                    int m = 0;
-                    for (int64_t kk = indptr[a]; kk < indptr[a + 1]; ++kk, ++m)
-                        T.nl[(size_t)m * cnt + k] = (uint16_t)local_of(csr[kk]);
-                    for (; m < W; ++m) T.nl[(size_t)m * cnt + k] = sl;
-                }
-            }
             mask.assign(local, {0, 0, 0, 0});
             std::vector<uint32_t> pr;
             std::vector<double> pdv;
@@ -646,21 +617,8 @@ inline void build_tiled(const NbhDev &nb, int sh, TiledSched &t, cudaStream_t s)
     std::vector<int32_t> halo, sub;
     std::vector<uint32_t> pairs;
     std::vector<double> pd;
-    std::vector<int64_t> nloff(1, 0), selfoff(1, 0);
-    std::vector<int32_t> width, own0, ownn;
-    std::vector<uint16_t> nl, self;
     for (int64_t bk : order) {
         TaskOut &T = out[bk];
-        nl.insert(nl.end(), T.nl.begin(), T.nl.end());
-        nloff.push_back((int64_t)nl.size());
-        self.insert(self.end(), T.self.begin(), T.self.end());
-        selfoff.push_back((int64_t)self.size());
-        width.push_back(T.width);
-        own0.push_back((int32_t)T.own0);
-        ownn.push_back((int32_t)T.self.size());
-        t.max_own = std::max(t.max_own, (int)T.self.size());
-        std::vector<uint16_t>().swap(T.nl);
-        std::vector<uint16_t>().swap(T.self);
         ranges.insert(ranges.end(), T.ranges.begin(), T.ranges.end());
         roff.push_back((int64_t)ranges.size());
         halo.push_back(T.halo);
@@ -689,13 +647,6 @@ inline void build_tiled(const NbhDev &nb, int sh, TiledSched &t, cudaStream_t s)
     upload_vec(t.pd, pd, s);
     upload_vec(t.sub_off, soff, s);
     upload_vec(t.sub, sub, s);
-    upload_vec(t.nl_off, nloff, s);
-    upload_vec(t.nl, nl, s);
-    upload_vec(t.self_off, selfoff, s);
-    upload_vec(t.self, self, s);
-    upload_vec(t.width, width, s);
-    upload_vec(t.own0, own0, s);
-    upload_vec(t.own_n, ownn, s);
 }
 
 // Block shape: a cubic edge of `tile` cells if given (a multi-rank plan's

@@ -47,9 +47,10 @@ def test_damping_conserves_momentum_and_dissipates(sweep, dim):
 
 
 @pytest.mark.parametrize("dim", [2, 3])
-def test_tiled_gathers_match_sell_gathers_per_step(dim):
-    """With eta = 0 the sweep is the identity, so the tiled pipeline
-    (shared-memory gathers) must track the SELL/L1 pipeline step by step."""
+def test_tiled_pipeline_matches_serial_pipeline_without_damping(dim):
+    """With eta = 0 the sweep is the identity, so a solid built for the tiled
+    sweep (block schedule, dataflow launch) must track one built for the
+    serial sweep step by step."""
     from paper_2309_04010_b200 import lattices
     from paper_2309_04010_b200.config import resolve
     from paper_2309_04010_b200.device import DeviceSolid
