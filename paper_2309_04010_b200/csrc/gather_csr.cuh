@@ -103,46 +103,43 @@ __global__ void __launch_bounds__(256, MTSPH_ACCEL_CTAS) k_solid_accel_csr(Solid
     for (int it = 0; it < G; ++it) {
         const int64_t i = (int64_t)blockIdx.x * 256 + it * (256 / G) + threadIdx.x / G;
         const bool act = i < n && !(A.flags[i] & FL_GHOST);
-        // sum_b V_b (T_a + T_b) gradW = T_a (sum_b V_b gradW) + sum_b V_b T_b gradW:
-        // T_a stays out of the loop (registers: 3 CTAs per SM without it)
-        double acc[2 * D];  // [0, D): sum V_b T_b gradW, [D, 2D): sum V_b gradW
+        // sum_b V_b (T_a + T_b) gradW = sum_b T~_b gradW + T_a G_a, with
+        // T~_b = V_b T_b from the divergence record (three 256-bit loads per
+        // neighbour, X included) and G_a = sum_b V_b gradW static
+        double acc[D];
 #pragma unroll
-        for (int k = 0; k < 2 * D; ++k) acc[k] = 0.0;
+        for (int k = 0; k < D; ++k) acc[k] = 0.0;
         if (act) {
             double xa[3];
             xget<D>(ldg4(A.XV + i), xa);
             const int64_t k1 = A.indptr[i + 1];
             for (int64_t k = A.indptr[i] + sub; k < k1; k += G) {
                 const int32_t b = __ldg(A.csr + k);
-                const double4 xvb = ldg4(A.XV + b);
                 double xb[3], Tb[D * D], rel[D], g[D];
-                xget<D>(xvb, xb);
-                tload<D>(A.T, n, b, Tb);
+                dload<D>(A.T, n, A.XV, b, Tb, xb);
 #pragma unroll
                 for (int q = 0; q < D; ++q) rel[q] = xb[q] - xa[q];
                 grad_w<D>(rel, A.ks, g);
-                const double volb = volof<D>(xvb);
 #pragma unroll
                 for (int r = 0; r < D; ++r) {
                     double sum = 0.0;
 #pragma unroll
                     for (int cc = 0; cc < D; ++cc) sum += Tb[r * D + cc] * g[cc];
-                    acc[r] += volb * sum;
-                    acc[D + r] += volb * g[r];
+                    acc[r] += sum;
                 }
             }
         }
         group_sum<G>(acc);
         if (act && sub == 0) {
-            double Ta[D * D];
-            tload<D>(A.T, n, i, Ta);
-            const double rho0 = A.rho0[i];
+            double Ta[D * D], xd[3];
+            dload<D>(A.T, n, A.XV, i, Ta, xd);
+            const double rho0 = A.rho0[i], vola = volof<D>(ldg4(A.XV + i));
 #pragma unroll
             for (int k = 0; k < D; ++k) {
                 double ta = 0.0;
 #pragma unroll
-                for (int cc = 0; cc < D; ++cc) ta += Ta[k * D + cc] * acc[D + cc];
-                acc[k] = (acc[k] + ta) / rho0;
+                for (int cc = 0; cc < D; ++cc) ta += Ta[k * D + cc] * A.G[(int64_t)cc * n + i];
+                acc[k] = (acc[k] + ta / vola) / rho0;
                 A.a[(int64_t)k * n + i] = acc[k];
             }
             if (A.flags[i] & FL_MOVABLE) {

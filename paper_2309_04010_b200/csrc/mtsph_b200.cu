@@ -206,7 +206,7 @@ struct mtsph_solid {
     int64_t n = 0;
     cudaStream_t s = nullptr;
     DBuf<unsigned char> V;
-    DBuf<double> x, a, F, cp, alpha, T, mass, rho0, inv_m, part, meas;
+    DBuf<double> x, a, F, cp, alpha, T, G, mass, rho0, inv_m, part, meas;
     DBuf<uint8_t> flags;
     DBuf<Ctrl> ctrl;
     DBuf<int64_t> level_ptr;
@@ -239,7 +239,7 @@ struct mtsph_solid {
         A.XV = nb.XV.p;
         A.V = V.p;
         A.x = x.p; A.a = a.p; A.F = F.p; A.cp = cp.p; A.alpha = alpha.p; A.T = T.p;
-        A.B = nb.B.p; A.mass = mass.p; A.rho0 = rho0.p; A.flags = flags.p;
+        A.B = nb.B.p; A.G = G.p; A.mass = mass.p; A.rho0 = rho0.p; A.flags = flags.p;
         A.slice_ptr = nb.slice_ptr.p; A.slice_w = nb.slice_w.p; A.nbr = nb.nbr.p;
         A.indptr = nb.indptr.p; A.csr = nb.csr.p;
         A.perm = nb.perm.p;
@@ -401,13 +401,17 @@ extern "C" mtsph_status mtsph_solid_create(const mtsph_solid_desc *dsc, mtsph_so
     S->cp.upload(F.data(), F.size(), S->s);
     S->alpha.alloc(n);
     S->alpha.zero(S->s);
-    S->T.alloc((size_t)n * (d == 3 ? 9 : 4));
+    S->T.alloc((size_t)n * (d == 3 ? DS<3>::n : DS<2>::n));
     S->T.zero(S->s);
     S->mass.upload(mass.data(), n, S->s);
     S->rho0.upload(rho0.data(), n, S->s);
     S->inv_m.upload(inv_m.data(), n, S->s);
     S->flags.upload(flags.data(), n, S->s);
     S->nblk = (int)blocks_for(n);
+    S->G.alloc((size_t)d * n);  // static sum_b V_b gradW_ab
+    if (d == 2) k_solid_gsum<2><<<blocks_for(n), 256, 0, S->s>>>(S->args(), S->G.p);
+    else k_solid_gsum<3><<<blocks_for(n), 256, 0, S->s>>>(S->args(), S->G.p);
+    MT_LAUNCH_CHECK();
     if (const char *e = std::getenv("MTSPH_GATHER_LANES")) {
         const int g = std::atoi(e);
         if (g != 0 && g != 2 && g != 4 && g != 8) throw Error(MTSPH_ERR_ARG, "MTSPH_GATHER_LANES: 0, 2, 4 or 8");
@@ -598,8 +602,11 @@ extern "C" mtsph_status mtsph_solid_run_steps(mtsph_solid *S, const mtsph_inner_
 
 // ------------------------------------------------------------- multi-rank phases
 
+// field 0: velocity; field 1: T~ of the divergence record (the receiver
+// completes the record with its own copy of the reference position)
 template <int D> __global__ void k_pack(int64_t n, int64_t m, const int64_t *__restrict__ ids, const void *V,
-                                        const double *__restrict__ T, int field, double *out) {
+                                        const double *__restrict__ T, const double4 *__restrict__ XV, int field,
+                                        double *out) {
     const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (k >= m) return;
     const int64_t i = ids[k];
@@ -609,15 +616,16 @@ template <int D> __global__ void k_pack(int64_t n, int64_t m, const int64_t *__r
 #pragma unroll
         for (int c = 0; c < D; ++c) out[k * D + c] = v[c];
     } else {
-        double t[D * D];
-        tload<D>(T, n, i, t);
+        double t[D * D], x[3];
+        dload<D>(T, n, XV, i, t, x);
 #pragma unroll
         for (int c = 0; c < D * D; ++c) out[k * D * D + c] = t[c];
     }
 }
 
 template <int D> __global__ void k_unpack(int64_t n, int64_t m, const int64_t *__restrict__ ids, void *V, double *T,
-                                          int field, const double *__restrict__ in) {
+                                          const double4 *__restrict__ XV, int field,
+                                          const double *__restrict__ in) {
     const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (k >= m) return;
     const int64_t i = ids[k];
@@ -632,7 +640,7 @@ template <int D> __global__ void k_unpack(int64_t n, int64_t m, const int64_t *_
         double t[D * D];
 #pragma unroll
         for (int c = 0; c < D * D; ++c) t[c] = in[k * D * D + c];
-        tstore<D>(T, n, i, t);
+        dstore_raw<D>(T, n, i, t, XV[i]);
     }
 }
 
@@ -758,14 +766,18 @@ static void pack_common(mtsph_solid *S, const char *field, int64_t m, const int6
     DBuf<double> buf((size_t)m * w);
     dids.upload(internal.data(), m, S->s);
     if (pack) {
-        if (S->d == 2) k_pack<2><<<blocks_for(m), 256, 0, S->s>>>(S->n, m, dids.p, S->V.p, S->T.p, which, buf.p);
-        else k_pack<3><<<blocks_for(m), 256, 0, S->s>>>(S->n, m, dids.p, S->V.p, S->T.p, which, buf.p);
+        if (S->d == 2)
+            k_pack<2><<<blocks_for(m), 256, 0, S->s>>>(S->n, m, dids.p, S->V.p, S->T.p, S->nb.XV.p, which, buf.p);
+        else
+            k_pack<3><<<blocks_for(m), 256, 0, S->s>>>(S->n, m, dids.p, S->V.p, S->T.p, S->nb.XV.p, which, buf.p);
         MT_LAUNCH_CHECK();
         buf.download(host, (size_t)m * w, S->s);
     } else {
         buf.upload(in, (size_t)m * w, S->s);
-        if (S->d == 2) k_unpack<2><<<blocks_for(m), 256, 0, S->s>>>(S->n, m, dids.p, S->V.p, S->T.p, which, buf.p);
-        else k_unpack<3><<<blocks_for(m), 256, 0, S->s>>>(S->n, m, dids.p, S->V.p, S->T.p, which, buf.p);
+        if (S->d == 2)
+            k_unpack<2><<<blocks_for(m), 256, 0, S->s>>>(S->n, m, dids.p, S->V.p, S->T.p, S->nb.XV.p, which, buf.p);
+        else
+            k_unpack<3><<<blocks_for(m), 256, 0, S->s>>>(S->n, m, dids.p, S->V.p, S->T.p, S->nb.XV.p, which, buf.p);
         MT_LAUNCH_CHECK();
     }
     S->launches += 1;

@@ -172,12 +172,52 @@ template <int D> __device__ __forceinline__ void tstore(double *Tp, int64_t n, i
     }
 }
 
+// Solid divergence record: T~ = V0 T (the neighbour's volume folded in) and,
+// in 3D, the reference position in the same three 32 B planes, so the
+// acceleration gather reads three 256-bit records per neighbour and nothing
+// else (sum_b V_b gradW, the T_a part, is static: SolidArgs::G).
+//   3D: (T~00 T~01 T~02 T~10) (T~11 T~12 T~20 T~21) (X0 X1 X2 T~22)
+//   2D: (T~00 T~01 T~10 T~11), X from XV
+template <int D> struct DS { static constexpr int n = D == 3 ? 12 : 4; };
+
+// store T~ (already scaled) with the particle's reference position
+template <int D>
+__device__ __forceinline__ void dstore_raw(double *Tp, int64_t n, int64_t a, const double *tt, const double4 &xv) {
+    double4 *r = reinterpret_cast<double4 *>(Tp);
+    if (D == 2) {
+        st4(r + a, make_double4(tt[0], tt[1], tt[2], tt[3]));
+    } else {
+        st4(r + a, make_double4(tt[0], tt[1], tt[2], tt[3]));
+        st4(r + n + a, make_double4(tt[4], tt[5], tt[6], tt[7]));
+        st4(r + 2 * n + a, make_double4(xv.x, xv.y, xv.z, tt[8]));
+    }
+}
+// (read-only kernels) T~ and the reference position of particle b
+template <int D>
+__device__ __forceinline__ void dload(const double *Tp, int64_t n, const double4 *XV, int64_t b, double *tt,
+                                      double *x) {
+    const double4 *r = reinterpret_cast<const double4 *>(Tp);
+    const double4 q0 = ldg4(r + b);
+    if (D == 2) {
+        tt[0] = q0.x; tt[1] = q0.y; tt[2] = q0.z; tt[3] = q0.w;
+        const double4 xv = ldg4(XV + b);
+        x[0] = xv.x; x[1] = xv.y;
+    } else {
+        const double4 q1 = ldg4(r + n + b), q2 = ldg4(r + 2 * n + b);
+        tt[0] = q0.x; tt[1] = q0.y; tt[2] = q0.z; tt[3] = q0.w;
+        tt[4] = q1.x; tt[5] = q1.y; tt[6] = q1.z; tt[7] = q1.w;
+        tt[8] = q2.w;
+        x[0] = q2.x; x[1] = q2.y; x[2] = q2.z;
+    }
+}
+
 struct SolidArgs {
     int64_t n;
     const double4 *XV;
     void *V;
-    double *x, *a, *F, *cp, *alpha, *T;
+    double *x, *a, *F, *cp, *alpha, *T;   // T: divergence records (DS)
     const double *B, *mass, *rho0;
+    const double *G;         // [d][n] sum_b V_b gradW_ab (static, setup)
     const uint8_t *flags;
     const int64_t *slice_ptr;
     const int32_t *slice_w, *nbr;
@@ -219,7 +259,35 @@ __device__ __forceinline__ void solid_stress_point(const SolidArgs &A, int64_t i
     }
     double Tm[D * D];
     mm<D>(P, Bm, Tm);
-    tstore<D>(A.T, A.n, i, Tm);
+    const double4 xv = ldg4(A.XV + i);
+    const double vol = volof<D>(xv);
+#pragma unroll
+    for (int k = 0; k < D * D; ++k) Tm[k] *= vol;
+    dstore_raw<D>(A.T, A.n, i, Tm, xv);
+}
+
+// sum_b V_b gradW_ab per particle, CSR row order (static; once at setup)
+template <int D>
+__global__ void __launch_bounds__(256) k_solid_gsum(SolidArgs A, double *G) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= A.n) return;
+    double xa[3], s[D];
+    xget<D>(ldg4(A.XV + i), xa);
+#pragma unroll
+    for (int k = 0; k < D; ++k) s[k] = 0.0;
+    for (int64_t k = A.indptr[i]; k < A.indptr[i + 1]; ++k) {
+        const double4 xvb = ldg4(A.XV + A.csr[k]);
+        double xb[3], rel[D], g[D];
+        xget<D>(xvb, xb);
+#pragma unroll
+        for (int q = 0; q < D; ++q) rel[q] = xb[q] - xa[q];
+        grad_w<D>(rel, A.ks, g);
+        const double volb = volof<D>(xvb);
+#pragma unroll
+        for (int q = 0; q < D; ++q) s[q] += volb * g[q];
+    }
+#pragma unroll
+    for (int k = 0; k < D; ++k) G[(int64_t)k * A.n + i] = s[k];
 }
 
 template <int D>
@@ -338,9 +406,9 @@ __global__ void __launch_bounds__(256) k_solid_accel(SolidArgs A) {
     double ek = 0.0, a2m = 0.0;
     if (i < A.n && !(A.flags[i] & FL_GHOST)) {
         const double dt = c->dt;
-        double xa[3], Ta[D * D];
-        xget<D>(ldg4(A.XV + i), xa);
-        tload<D>(A.T, A.n, i, Ta);
+        const double4 xva = ldg4(A.XV + i);
+        double xa[3];
+        xget<D>(xva, xa);
         double acc[D];
 #pragma unroll
         for (int k = 0; k < D; ++k) acc[k] = 0.0;
@@ -350,26 +418,29 @@ __global__ void __launch_bounds__(256) k_solid_accel(SolidArgs A) {
         const int w = A.slice_w[s];
         for (int m = 0; m < w; ++m) {
             const int32_t b = __ldg(A.nbr + base + (int64_t)m * 32);
-            const double4 xvb = ldg4(A.XV + b);
             double xb[3], Tb[D * D], rel[D], g[D];
-            xget<D>(xvb, xb);
-            tload<D>(A.T, A.n, b, Tb);
+            dload<D>(A.T, A.n, A.XV, b, Tb, xb);
 #pragma unroll
             for (int k = 0; k < D; ++k) rel[k] = xb[k] - xa[k];
             grad_w<D>(rel, A.ks, g);
-            const double volb = volof<D>(xvb);
 #pragma unroll
             for (int r = 0; r < D; ++r) {
                 double sum = 0.0;
 #pragma unroll
-                for (int cc = 0; cc < D; ++cc) sum += (Ta[r * D + cc] + Tb[r * D + cc]) * g[cc];
-                acc[r] += volb * sum;
+                for (int cc = 0; cc < D; ++cc) sum += Tb[r * D + cc] * g[cc];
+                acc[r] += sum;
             }
         }
-        const double rho0 = A.rho0[i];
+        // + T_a sum_b V_b gradW = (T~_a / V_a) G_a
+        double Ta[D * D], xd[3];
+        dload<D>(A.T, A.n, A.XV, i, Ta, xd);
+        const double rho0 = A.rho0[i], vola = volof<D>(xva);
 #pragma unroll
         for (int k = 0; k < D; ++k) {
-            acc[k] /= rho0;
+            double ta = 0.0;
+#pragma unroll
+            for (int cc = 0; cc < D; ++cc) ta += Ta[k * D + cc] * A.G[(int64_t)cc * A.n + i];
+            acc[k] = (acc[k] + ta / vola) / rho0;
             A.a[(int64_t)k * A.n + i] = acc[k];
         }
         if (A.flags[i] & FL_MOVABLE) {
