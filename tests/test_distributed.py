@@ -43,6 +43,44 @@ def test_plans_partition_and_halos(nranks):
         assert len(allt) == len(np.unique(allt))
 
 
+@pytest.mark.parametrize("d", [2, 3])
+@pytest.mark.parametrize("B", [1, 2, 4])
+def test_block_colours_keep_same_colour_halos_disjoint(d, B):
+    """Sweep-block colouring (partition.block_colour_and_halo, the host twin
+    of tiled.cuh build_tiled): blocks of one colour run concurrently, so
+    their halos (block grown by one cell) must never overlap -- period 2
+    per axis from an edge of 2 cells, period 3 for single-cell blocks."""
+    from paper_2309_04010_b200.partition import block_colour_and_halo
+    ext = 4 * B + 2
+    grid = np.stack(np.meshgrid(*[np.arange(ext)] * d, indexing="ij"), -1).reshape(-1, d)
+    col, bc = block_colour_and_halo(grid, B, d)
+    ncol = (2 if B >= 2 else 3) ** d
+    assert col.min() >= 0 and col.max() < ncol
+    blocks = {}
+    for c, b in zip(col, map(tuple, bc)):
+        assert blocks.setdefault(b, c) == c                         # one colour per block
+    keys = list(blocks)
+    for i, a in enumerate(keys):
+        for b in keys[i + 1:]:
+            if blocks[a] != blocks[b]:
+                continue
+            # halos [a*B - 1, a*B + B] per axis overlap iff every axis overlaps
+            overlap = all(a[k] * B - 1 <= b[k] * B + B and b[k] * B - 1 <= a[k] * B + B
+                          for k in range(d))
+            assert not overlap, (a, b)
+
+
+def test_2d_plans_align_slabs_to_the_sweep_tile():
+    lat = lattices.build_lattice(resolve({"scenario": "bar_2d", "length": 8.0, "width": 1.0,
+                                          "dp": 0.05}).params)
+    plans, _, _ = make_plans(lat.pos, lat.h_axes, 3)
+    assert all(p.tile_B == 16 for p in plans)                    # the 2D device default
+    for p in plans[:-1]:
+        assert p.cell_x_range[1] % 16 == 0
+    with pytest.raises(ValueError, match="power of two"):
+        make_plans(lat.pos, lat.h_axes, 2, tile_B=3)
+
+
 class FakeDevice:
     """Test double of DeviceSolid's pack/unpack (host arrays)."""
 
