@@ -230,6 +230,18 @@ mtsph_status mtsph_solid_pack(mtsph_solid *s, const char *field, int64_t m,
                               const int64_t *ids, double *host);
 mtsph_status mtsph_solid_unpack(mtsph_solid *s, const char *field, int64_t m,
                                 const int64_t *ids, const double *host);
+/* device-resident exchange (NCCL send/recv of device buffers, no host
+ * staging).  Map ORIGINAL local ids to the solid's internal ids once, keep
+ * them on the device, and pack / unpack between device buffers; both are
+ * enqueued on the solid's stream (returned by mtsph_solid_stream, a
+ * cudaStream_t) without synchronising the host.                          */
+mtsph_status mtsph_solid_internal_ids(mtsph_solid *s, int64_t m, const int64_t *ids,
+                                      int64_t *internal);
+mtsph_status mtsph_solid_stream(const mtsph_solid *s, void **stream);
+mtsph_status mtsph_solid_pack_device(mtsph_solid *s, const char *field, int64_t m,
+                                     const int64_t *dev_internal_ids, double *dev_out);
+mtsph_status mtsph_solid_unpack_device(mtsph_solid *s, const char *field, int64_t m,
+                                       const int64_t *dev_internal_ids, const double *dev_in);
 
 /* observables: reaction_force, neck radius, max alpha, min mid alpha,
  * all-finite flag (1/0)                                                 */

@@ -88,6 +88,10 @@ SIGNATURES = {
     "mtsph_solid_colours": (c_int, [c_vp, c_vp]),
     "mtsph_solid_pack": (c_int, [c_vp, ctypes.c_char_p, c_i64, c_vp, c_vp]),
     "mtsph_solid_unpack": (c_int, [c_vp, ctypes.c_char_p, c_i64, c_vp, c_vp]),
+    "mtsph_solid_internal_ids": (c_int, [c_vp, c_i64, c_vp, c_vp]),
+    "mtsph_solid_stream": (c_int, [c_vp, ctypes.POINTER(c_vp)]),
+    "mtsph_solid_pack_device": (c_int, [c_vp, ctypes.c_char_p, c_i64, c_vp, c_vp]),
+    "mtsph_solid_unpack_device": (c_int, [c_vp, ctypes.c_char_p, c_i64, c_vp, c_vp]),
     "mtsph_solid_measure": (c_int, [c_vp, c_vp]),
     "mtsph_solid_get": (c_int, [c_vp, ctypes.c_char_p, c_vp]),
     "mtsph_solid_set": (c_int, [c_vp, ctypes.c_char_p, c_vp]),

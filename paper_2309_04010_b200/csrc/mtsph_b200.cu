@@ -798,6 +798,59 @@ extern "C" mtsph_status mtsph_solid_unpack(mtsph_solid *S, const char *field, in
     API_END
 }
 
+// ---- device-resident exchange
+
+static int pack_field(const char *field) {
+    const std::string f(field ? field : "");
+    const int which = f == "vel" ? 0 : (f == "T" ? 1 : -1);
+    if (which < 0) throw Error(MTSPH_ERR_ARG, "pack fields are 'vel' and 'T'");
+    return which;
+}
+
+extern "C" mtsph_status mtsph_solid_internal_ids(mtsph_solid *S, int64_t m, const int64_t *ids,
+                                                 int64_t *internal) {
+    API_BEGIN
+    if (S->iperm_h.empty()) {
+        S->iperm_h.resize(S->n);
+        S->nb.iperm.download(S->iperm_h.data(), S->n, S->s);
+        MT_CUDA(cudaStreamSynchronize(S->s));
+    }
+    for (int64_t k = 0; k < m; ++k) {
+        if (ids[k] < 0 || ids[k] >= S->n) throw Error(MTSPH_ERR_ARG, "particle id out of range");
+        internal[k] = S->iperm_h[ids[k]];
+    }
+    API_END
+}
+
+extern "C" mtsph_status mtsph_solid_stream(const mtsph_solid *S, void **stream) {
+    *stream = (void *)S->s;
+    return MTSPH_OK;
+}
+
+extern "C" mtsph_status mtsph_solid_pack_device(mtsph_solid *S, const char *field, int64_t m,
+                                                const int64_t *ids, double *out) {
+    API_BEGIN
+    const int which = pack_field(field);
+    if (m <= 0) return MTSPH_OK;
+    if (S->d == 2) k_pack<2><<<blocks_for(m), 256, 0, S->s>>>(S->n, m, ids, S->V.p, S->T.p, S->nb.XV.p, which, out);
+    else k_pack<3><<<blocks_for(m), 256, 0, S->s>>>(S->n, m, ids, S->V.p, S->T.p, S->nb.XV.p, which, out);
+    MT_LAUNCH_CHECK();
+    S->launches += 1;
+    API_END
+}
+
+extern "C" mtsph_status mtsph_solid_unpack_device(mtsph_solid *S, const char *field, int64_t m,
+                                                  const int64_t *ids, const double *in) {
+    API_BEGIN
+    const int which = pack_field(field);
+    if (m <= 0) return MTSPH_OK;
+    if (S->d == 2) k_unpack<2><<<blocks_for(m), 256, 0, S->s>>>(S->n, m, ids, S->V.p, S->T.p, S->nb.XV.p, which, in);
+    else k_unpack<3><<<blocks_for(m), 256, 0, S->s>>>(S->n, m, ids, S->V.p, S->T.p, S->nb.XV.p, which, in);
+    MT_LAUNCH_CHECK();
+    S->launches += 1;
+    API_END
+}
+
 extern "C" mtsph_status mtsph_solid_measure(mtsph_solid *S, double out[5]) {
     API_BEGIN
     SolidArgs A = S->args();

@@ -184,6 +184,28 @@ class DeviceSolid:
         vals = _f64(values)
         check(self._lib.mtsph_solid_unpack(self._h, field.encode(), len(ids), ptr(ids), ptr(vals)))
 
+    # -- device-resident exchange (no host staging) ----------------------
+    def internal_ids(self, ids):
+        """Original local ids -> the internal ids pack/unpack_device take."""
+        ids = np.ascontiguousarray(ids, dtype=np.int64)
+        out = np.zeros(len(ids), np.int64)
+        check(self._lib.mtsph_solid_internal_ids(self._h, len(ids), ptr(ids), ptr(out)))
+        return out
+
+    def stream_handle(self):
+        """The cudaStream_t every kernel of this solid is enqueued on."""
+        s = ctypes.c_void_p()
+        check(self._lib.mtsph_solid_stream(self._h, ctypes.byref(s)))
+        return s.value or 0
+
+    def pack_device(self, field, m, ids_ptr, out_ptr):
+        """Pack `field` of m particles (internal ids at device address
+        ids_ptr) into the device buffer at out_ptr, on stream_handle()."""
+        check(self._lib.mtsph_solid_pack_device(self._h, field.encode(), int(m), ids_ptr, out_ptr))
+
+    def unpack_device(self, field, m, ids_ptr, in_ptr):
+        check(self._lib.mtsph_solid_unpack_device(self._h, field.encode(), int(m), ids_ptr, in_ptr))
+
     def sizes(self):
         out = np.zeros(4, np.int64)
         check(self._lib.mtsph_solid_sizes(self._h, ptr(out)))

@@ -18,9 +18,10 @@ Because every rank bins on the global cell grid, the decomposed run
 performs the single-domain tiled operations; `LocalGroup` runs all ranks in
 one process (the single-GPU emulation used by the tests), `TorchGroup` is
 one process per GPU over torch.distributed (NCCL on GPUs, gloo on CPU).
-Exchanges are host-staged in this version (pack -> D2H -> send -> H2D ->
-unpack); moving them into NCCL calls captured in the step graph is the
-next step.
+TorchGroup exchanges are host-staged over gloo (pack -> D2H -> send -> H2D
+-> unpack) and device-resident over NCCL (pack kernel -> NCCL send/recv of
+device buffers -> unpack kernel, stream-ordered on the solid's stream);
+the per-phase reductions still return to the host.
 """
 
 from __future__ import annotations
@@ -34,25 +35,49 @@ from .partition import make_plans
 
 
 class LocalGroup:
-    """All ranks of the decomposition in this process (emulation)."""
+    """All ranks of the decomposition in this process (emulation).
 
-    def __init__(self, plans, devices):
+    device_buffers=False: host pack/unpack.  True: the device-resident path
+    of TorchGroup(tensor_device="cuda") -- internal-id lists on the device,
+    pack kernel -> CUDA buffer -> unpack kernel -- with a device copy between
+    the two solids' streams standing in for the NCCL send/recv."""
+
+    def __init__(self, plans, devices, device_buffers=False):
         self.plans = plans
         self.devices = devices
+        self.device_buffers = device_buffers
+        self._cache = {}
+
+    def _move(self, field, src, src_idx, dst, dst_idx):
+        if not self.device_buffers:
+            self.devices[dst].unpack(field, dst_idx, self.devices[src].pack(field, src_idx))
+            return
+        import torch
+        key = (field, src, dst, id(src_idx))
+        if key not in self._cache:
+            s, t = self.devices[src], self.devices[dst]
+            w = s.d if field == "vel" else s.d * s.d
+            self._cache[key] = (torch.from_numpy(s.internal_ids(src_idx)).cuda(),
+                                torch.from_numpy(t.internal_ids(dst_idx)).cuda(),
+                                torch.empty((len(src_idx), w), dtype=torch.float64, device="cuda"))
+        ids_s, ids_t, buf = self._cache[key]
+        s, t = self.devices[src], self.devices[dst]
+        s.pack_device(field, len(ids_s), ids_s.data_ptr(), buf.data_ptr())
+        torch.cuda.ExternalStream(s.stream_handle()).synchronize()
+        t.unpack_device(field, len(ids_t), ids_t.data_ptr(), buf.data_ptr())
+        torch.cuda.ExternalStream(t.stream_handle()).synchronize()
 
     def refresh(self, field):
         for p in self.plans:
             for q, recv_idx in p.refresh_recv.items():
-                vals = self.devices[q].pack(field, self.plans[q].refresh_send[p.rank])
-                self.devices[p.rank].unpack(field, recv_idx, vals)
+                self._move(field, q, self.plans[q].refresh_send[p.rank], p.rank, recv_idx)
 
     def pushback(self, colour):
         for p in self.plans:
             for (c, q), idx in p.pushback_send.items():
                 if c != colour:
                     continue
-                vals = self.devices[p.rank].pack("vel", idx)
-                self.devices[q].unpack("vel", self.plans[q].pushback_recv[(c, p.rank)], vals)
+                self._move("vel", p.rank, idx, q, self.plans[q].pushback_recv[(c, p.rank)])
 
     def allsum(self, values):
         return float(sum(values))
@@ -63,7 +88,14 @@ class LocalGroup:
 
 class TorchGroup:
     """One rank per process; point-to-point exchanges and reductions through
-    torch.distributed (host-staged buffers)."""
+    torch.distributed.
+
+    tensor_device "cpu" (gloo): host-staged buffers (pack -> D2H -> send ->
+    H2D -> unpack).  tensor_device "cuda" (NCCL): device-resident exchange --
+    the index lists are mapped to the solid's internal ids and uploaded once,
+    send/receive buffers are persistent CUDA tensors, and pack kernel ->
+    NCCL isend/irecv -> unpack kernel are all ordered on the solid's own
+    stream (torch.cuda.ExternalStream), with no host synchronisation."""
 
     def __init__(self, plan, device, dist, tensor_device="cpu"):
         import torch
@@ -72,7 +104,42 @@ class TorchGroup:
         self.plans = [plan]
         self.devices = [device]
         self.tdev = tensor_device
+        self.on_device = str(tensor_device).startswith("cuda")
+        if self.on_device:
+            self._setup_device_lists()
 
+    # -- device-resident exchange -------------------------------------
+    def _setup_device_lists(self):
+        torch = self.torch
+        p, dev = self.plans[0], self.devices[0]
+        d = dev.d
+
+        def entry(idx, width):
+            ids = torch.from_numpy(dev.internal_ids(idx)).to(self.tdev)
+            return ids, torch.empty((len(idx), width), dtype=torch.float64, device=self.tdev)
+
+        self.dl = {}
+        for field, width in (("vel", d), ("T", d * d)):
+            self.dl[("refresh_send", field)] = {q: entry(i, width) for q, i in p.refresh_send.items()}
+            self.dl[("refresh_recv", field)] = {q: entry(i, width) for q, i in p.refresh_recv.items()}
+        self.dl["push_send"] = {k: entry(i, d) for k, i in p.pushback_send.items()}
+        self.dl["push_recv"] = {k: entry(i, d) for k, i in p.pushback_recv.items()}
+        self.stream = torch.cuda.ExternalStream(dev.stream_handle())
+
+    def _exchange_device(self, field, sends, recvs):
+        """sends / recvs: {peer: (internal ids, buffer)} (CUDA tensors)."""
+        torch, dist, dev = self.torch, self.dist, self.devices[0]
+        with torch.cuda.stream(self.stream):
+            for q, (ids, buf) in sorted(sends.items()):
+                dev.pack_device(field, len(ids), ids.data_ptr(), buf.data_ptr())
+            reqs = [dist.irecv(buf, src=q) for q, (ids, buf) in sorted(recvs.items())]
+            reqs += [dist.isend(buf, dst=q) for q, (ids, buf) in sorted(sends.items())]
+            for r in reqs:
+                r.wait()          # NCCL: the stream waits, the host does not
+            for q, (ids, buf) in sorted(recvs.items()):
+                dev.unpack_device(field, len(ids), ids.data_ptr(), buf.data_ptr())
+
+    # -- host-staged exchange -----------------------------------------
     def _swap(self, sends, recvs, width):
         """sends: {q: np.ndarray}, recvs: {q: count} -> {q: np.ndarray}"""
         torch, dist = self.torch, self.dist
@@ -87,6 +154,10 @@ class TorchGroup:
         return {q: b.cpu().numpy() for q, b in bufs.items()}
 
     def refresh(self, field):
+        if self.on_device:
+            self._exchange_device(field, self.dl[("refresh_send", field)],
+                                  self.dl[("refresh_recv", field)])
+            return
         p, dev = self.plans[0], self.devices[0]
         width = dev.d if field == "vel" else dev.d * dev.d
         sends = {q: dev.pack(field, idx) for q, idx in p.refresh_send.items()}
@@ -95,6 +166,11 @@ class TorchGroup:
             dev.unpack(field, p.refresh_recv[q], vals)
 
     def pushback(self, colour):
+        if self.on_device:
+            self._exchange_device(
+                "vel", {q: e for (c, q), e in self.dl["push_send"].items() if c == colour},
+                {q: e for (c, q), e in self.dl["push_recv"].items() if c == colour})
+            return
         p, dev = self.plans[0], self.devices[0]
         sends = {q: dev.pack("vel", idx) for (c, q), idx in p.pushback_send.items() if c == colour}
         recvs = {q: len(idx) for (c, q), idx in p.pushback_recv.items() if c == colour}
@@ -142,8 +218,9 @@ class DecomposedSolid:
                                      plastic=hardening is not None, hardening_law=law, hard=hp,
                                      sweep="tiled", ghost=p.ghost, grid=self.grid,
                                      tile=p.tile_B)
-        if group == "local":
-            self.group = LocalGroup(self.plans, [devices[r] for r in range(nranks)])
+        if group in ("local", "local_device"):
+            self.group = LocalGroup(self.plans, [devices[r] for r in range(nranks)],
+                                    device_buffers=group == "local_device")
         else:
             (r,) = ranks
             self.group = TorchGroup(self.plans[r], devices[r], dist, tensor_device)

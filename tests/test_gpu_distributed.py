@@ -1,6 +1,9 @@
 """GPU: the slab-decomposed inner step reproduces the single-domain tiled
 pipeline.  All ranks run in one process on one GPU (LocalGroup) -- no
-kernel waits on another rank, exchanges are host-staged copies."""
+kernel waits on another rank.  Exchanges are host-staged copies, or the
+device-resident path of the NCCL group (internal-id lists and buffers on
+the device, pack / unpack kernels on each solid's stream) with a device copy
+in place of the NCCL send/recv."""
 
 import numpy as np
 import pytest
@@ -18,7 +21,8 @@ def _setup(length=0.8):
     return p, lat, el, hard
 
 
-def test_decomposed_matches_single_domain_tiled():
+@pytest.mark.parametrize("group", ["local", "local_device"])
+def test_decomposed_matches_single_domain_tiled(group):
     from paper_2309_04010_b200.device import DeviceSolid
     from paper_2309_04010_b200.distributed import DecomposedSolid
     p, lat, el, hard = _setup()
@@ -35,7 +39,8 @@ def test_decomposed_matches_single_domain_tiled():
     want = {f: ref.get(f) for f in ("pos", "vel", "F", "alpha")}
     assert np.max(want["alpha"]) > 0
     for nranks in (1, 2, 3):
-        dec = DecomposedSolid(lat, el, hard, nranks, end_disp_per_outer=end_disp, ramp_steps=10)
+        dec = DecomposedSolid(lat, el, hard, nranks, group=group, end_disp_per_outer=end_disp,
+                              ramp_steps=10)
         assert sum((~pl.ghost).sum() for pl in dec.plans) == len(lat.vol)
         dec.advance_slow()
         dec.relax(eta, cfl, 0.0, 1.0, fixed_steps=steps)
