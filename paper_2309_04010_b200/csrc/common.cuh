@@ -8,8 +8,14 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+#include <chrono>
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
 #include <stdexcept>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -40,6 +46,18 @@ inline unsigned blocks_for(int64_t n, int t = kThreads) {
     return (unsigned)(b < 1 ? 1 : b);
 }
 
+// MTSPH_VERBOSE=1: wall time since the previous mark, per setup phase, on
+// stderr (synchronises the stream; a no-op otherwise)
+inline void setup_mark(cudaStream_t s, const char *what) {
+    static const bool on = [] { const char *e = std::getenv("MTSPH_VERBOSE"); return e && e[0] == '1'; }();
+    if (!on) return;
+    static thread_local std::chrono::steady_clock::time_point last = std::chrono::steady_clock::now();
+    cudaStreamSynchronize(s);
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[mtsph] %-24s %8.3f s\n", what, std::chrono::duration<double>(now - last).count());
+    last = now;
+}
+
 // opt a kernel into the largest dynamic shared memory the device offers
 // (the opt-in limit covers static + dynamic)
 inline void allow_max_dynamic_smem(const void *fn) {
@@ -50,6 +68,72 @@ inline void allow_max_dynamic_smem(const void *fn) {
     MT_CUDA(cudaFuncGetAttributes(&fa, fn));
     MT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  optin - (int)fa.sharedSizeBytes));
+}
+
+// memcpy split over host threads (first-touch page faults of a fresh
+// multi-GB destination serialise a single-threaded copy at ~2 GB/s)
+inline void par_memcpy(void *dst, const void *src, size_t len) {
+    constexpr int kThreadsCopy = 8;
+    if (len < (size_t(4) << 20)) { std::memcpy(dst, src, len); return; }
+    std::thread th[kThreadsCopy];
+    const size_t per = (len + kThreadsCopy - 1) / kThreadsCopy;
+    for (int k = 0; k < kThreadsCopy; ++k) {
+        const size_t off = k * per, n = off < len ? std::min(per, len - off) : 0;
+        th[k] = std::thread([=] { if (n) std::memcpy(static_cast<char *>(dst) + off, static_cast<const char *>(src) + off, n); });
+    }
+    for (auto &t : th) t.join();
+}
+
+// Large host<->device copies of pageable host memory through a
+// double-buffered pinned staging ring (a plain pageable cudaMemcpy ran at
+// ~3 GB/s for the multi-GB setup arrays): the DMA of one chunk overlaps the
+// host memcpy of the other.  Synchronous on return.
+inline void copy_staged(void *dst, const void *src, size_t bytes, cudaMemcpyKind kind, cudaStream_t s) {
+    constexpr size_t kChunk = size_t(64) << 20;
+    if (bytes < (size_t(8) << 20)) {  // small: not worth the staging
+        MT_CUDA(cudaMemcpyAsync(dst, src, bytes, kind, s));
+        MT_CUDA(cudaStreamSynchronize(s));
+        return;
+    }
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lock(mu);
+    static char *stage[2] = {nullptr, nullptr};
+    static cudaEvent_t done[2];
+    if (!stage[0])
+        for (int k = 0; k < 2; ++k) {
+            MT_CUDA(cudaMallocHost(&stage[k], kChunk));
+            MT_CUDA(cudaEventCreateWithFlags(&done[k], cudaEventDisableTiming));
+        }
+    const size_t nchunk = (bytes + kChunk - 1) / kChunk;
+    char *d = static_cast<char *>(dst);
+    const char *h = static_cast<const char *>(src);
+    if (kind == cudaMemcpyHostToDevice) {
+        for (size_t c = 0; c < nchunk; ++c) {
+            const int k = (int)(c & 1);
+            const size_t off = c * kChunk, len = std::min(kChunk, bytes - off);
+            if (c >= 2) MT_CUDA(cudaEventSynchronize(done[k]));  // buffer k free again
+            par_memcpy(stage[k], h + off, len);
+            MT_CUDA(cudaMemcpyAsync(d + off, stage[k], len, kind, s));
+            MT_CUDA(cudaEventRecord(done[k], s));
+        }
+    } else {
+        // D2H: chunk c+1's DMA runs while chunk c is copied out
+        auto issue = [&](size_t c) {
+            const int k = (int)(c & 1);
+            const size_t off = c * kChunk, len = std::min(kChunk, bytes - off);
+            MT_CUDA(cudaMemcpyAsync(stage[k], h + off, len, kind, s));
+            MT_CUDA(cudaEventRecord(done[k], s));
+        };
+        issue(0);
+        for (size_t c = 0; c < nchunk; ++c) {
+            if (c + 1 < nchunk) issue(c + 1);
+            const int k = (int)(c & 1);
+            const size_t off = c * kChunk, len = std::min(kChunk, bytes - off);
+            MT_CUDA(cudaEventSynchronize(done[k]));
+            par_memcpy(d + off, stage[k], len);
+        }
+    }
+    MT_CUDA(cudaStreamSynchronize(s));
 }
 
 // device buffer with RAII
@@ -79,12 +163,16 @@ template <class T> struct DBuf {
         p = nullptr;
         n = 0;
     }
+    // small copies stay asynchronous; >= 8 MB go through the pinned staging
+    // ring (synchronous) -- setup-time arrays of pageable host memory
     void upload(const T *h, size_t cnt, cudaStream_t s = 0) {
         if (cnt > n) alloc(cnt);
-        if (cnt) MT_CUDA(cudaMemcpyAsync(p, h, cnt * sizeof(T), cudaMemcpyHostToDevice, s));
+        if (cnt * sizeof(T) >= (size_t(8) << 20)) copy_staged(p, h, cnt * sizeof(T), cudaMemcpyHostToDevice, s);
+        else if (cnt) MT_CUDA(cudaMemcpyAsync(p, h, cnt * sizeof(T), cudaMemcpyHostToDevice, s));
     }
     void download(T *h, size_t cnt, cudaStream_t s = 0) const {
-        if (cnt) MT_CUDA(cudaMemcpyAsync(h, p, cnt * sizeof(T), cudaMemcpyDeviceToHost, s));
+        if (cnt * sizeof(T) >= (size_t(8) << 20)) copy_staged(h, p, cnt * sizeof(T), cudaMemcpyDeviceToHost, s);
+        else if (cnt) MT_CUDA(cudaMemcpyAsync(h, p, cnt * sizeof(T), cudaMemcpyDeviceToHost, s));
     }
     T *get() const { return p; }
 };

@@ -6,6 +6,7 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -shared
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -344,6 +345,7 @@ extern "C" mtsph_status mtsph_solid_create(const mtsph_solid_desc *dsc, mtsph_so
     S->n = n;
     S->d = d;
     MT_CUDA(cudaStreamCreateWithFlags(&S->s, cudaStreamNonBlocking));
+    setup_mark(S->s, "solid: start");
     if (dsc->grid) {
         S->nb.has_grid = true;
         for (int k = 0; k < 3; ++k) {
@@ -369,7 +371,9 @@ extern "C" mtsph_status mtsph_solid_create(const mtsph_solid_desc *dsc, mtsph_so
     } else {
         build_nbh(S->nb, n, d, dsc->pos, dsc->vol, dsc->h_axes, dsc->sweep, S->s);
     }
+    setup_mark(S->s, "neighbourhood");
     if (dsc->sweep == 3) build_tiled_auto(S->nb, S->tiled, S->s, dsc->tile);
+    setup_mark(S->s, "tiled schedule");
     std::vector<int64_t> perm(n);
     S->nb.perm.download(perm.data(), n, S->s);
     MT_CUDA(cudaStreamSynchronize(S->s));
@@ -439,6 +443,7 @@ extern "C" mtsph_status mtsph_solid_create(const mtsph_solid_desc *dsc, mtsph_so
     S->hc->vol_movable = 0.0;
     S->ctrl.alloc(1);
     S->push_ctrl();
+    setup_mark(S->s, "state");
     *out = S.release();
     API_END
 }

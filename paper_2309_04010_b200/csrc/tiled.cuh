@@ -398,10 +398,26 @@ inline void bank_order(const uint32_t *pairs, const double *pd, int64_t m, std::
 }  // namespace tiled_detail
 
 // Build the schedule from the device neighbourhood (host C++, threaded).
-template <class T> void upload_vec(DBuf<T> &b, const std::vector<T> &v, cudaStream_t s) {
+// vector whose elements are default-initialised (no zero fill of the
+// multi-GB setup arrays that are overwritten anyway)
+template <class T> struct NoInit : std::allocator<T> {
+    using std::allocator<T>::allocator;
+    template <class U> struct rebind { using other = NoInit<U>; };
+    template <class U> void construct(U *p) noexcept { ::new (static_cast<void *>(p)) U; }
+    template <class U, class... A> void construct(U *p, A &&...a) {
+        ::new (static_cast<void *>(p)) U(std::forward<A>(a)...);
+    }
+};
+template <class T> using RawVec = std::vector<T, NoInit<T>>;
+
+template <class T, class Al> void upload_vec(DBuf<T> &b, const std::vector<T, Al> &v, cudaStream_t s) {
     b.alloc(std::max<size_t>(v.size(), 1));
-    if (!v.empty()) MT_CUDA(cudaMemcpyAsync(b.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+    if (!v.empty()) copy_staged(b.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s);
     MT_CUDA(cudaStreamSynchronize(s));
+}
+template <class T, class Al> void download_vec(std::vector<T, Al> &v, const DBuf<T> &b, size_t count, cudaStream_t s) {
+    v.resize(std::max<size_t>(count, 1));
+    if (count) copy_staged(v.data(), b.p, count * sizeof(T), cudaMemcpyDeviceToHost, s);
 }
 
 // A block is the run of particles whose cell keys agree above the low `sh`
@@ -418,15 +434,15 @@ inline void build_tiled(const NbhDev &nb, int sh, TiledSched &t, cudaStream_t s)
     // apart so their one-cell halos are disjoint -- parity works from an
     // extent of 2 cells, single-cell extents need period 3
     for (int k = 0; k < d; ++k) { ext[k] = 1 << lg[k]; P[k] = ext[k] >= 2 ? 2 : 3; }
-    std::vector<uint64_t> cellkey(n);
-    std::vector<int64_t> indptr(n + 1);
-    std::vector<int32_t> csr(std::max<int64_t>(nb.nnz, 1));
-    std::vector<double4> XV(n);
-    nb.cellkey.download(cellkey.data(), n, s);
-    nb.indptr.download(indptr.data(), n + 1, s);
-    nb.csr.download(csr.data(), nb.nnz, s);
-    nb.XV.download(XV.data(), n, s);
-    MT_CUDA(cudaStreamSynchronize(s));
+    RawVec<uint64_t> cellkey;
+    RawVec<int64_t> indptr;
+    RawVec<int32_t> csr;
+    RawVec<double4> XV;
+    download_vec(cellkey, nb.cellkey, n, s);
+    download_vec(indptr, nb.indptr, n + 1, s);
+    download_vec(csr, nb.csr, nb.nnz, s);
+    download_vec(XV, nb.XV, n, s);
+    setup_mark(s, "tiled: download");
     // occupied cells: key -> [start, end)
     std::vector<uint64_t> ckeys;
     std::vector<int64_t> cstart;
@@ -566,6 +582,7 @@ inline void build_tiled(const NbhDev &nb, int sh, TiledSched &t, cudaStream_t s)
         });
     }
     for (auto &th : pool) th.join();
+    setup_mark(s, "tiled: blocks + colouring");
     if (err) std::rethrow_exception(err);
     // colour-major task order
     int ncol = 1;
@@ -612,33 +629,57 @@ inline void build_tiled(const NbhDev &nb, int sh, TiledSched &t, cudaStream_t s)
         upload_vec(t.f_rev, rev, s);
         t.f_done.alloc(order.size() + 1);
     }
-    std::vector<int64_t> roff(1, 0), poff(1, 0), soff(1, 0);
-    std::vector<int2> ranges;
-    std::vector<int32_t> halo, sub;
-    std::vector<uint32_t> pairs;
-    std::vector<double> pd;
-    for (int64_t bk : order) {
-        TaskOut &T = out[bk];
-        ranges.insert(ranges.end(), T.ranges.begin(), T.ranges.end());
-        roff.push_back((int64_t)ranges.size());
-        halo.push_back(T.halo);
-        pairs.insert(pairs.end(), T.pairs.begin(), T.pairs.end());
-        pd.insert(pd.end(), T.pd.begin(), T.pd.end());
-        poff.push_back((int64_t)pairs.size());
-        sub.insert(sub.end(), T.sub.begin(), T.sub.end());
-        soff.push_back((int64_t)sub.size());
+    setup_mark(s, "tiled: dataflow lists");
+    // task-major concatenation: offsets first, then a parallel copy into
+    // arrays sized once (growing multi-GB vectors cost ~8 s at 10M)
+    const size_t ntk = order.size();
+    std::vector<int64_t> roff(ntk + 1, 0), poff(ntk + 1, 0), soff(ntk + 1, 0);
+    std::vector<int32_t> halo(ntk);
+    int64_t real_pairs = 0;
+    for (size_t q = 0; q < ntk; ++q) {
+        const TaskOut &T = out[order[q]];
+        roff[q + 1] = roff[q] + (int64_t)T.ranges.size();
+        poff[q + 1] = poff[q] + (int64_t)T.pairs.size();
+        soff[q + 1] = soff[q] + (int64_t)T.sub.size();
+        halo[q] = T.halo;
         t.max_halo = std::max(t.max_halo, T.halo);
         t.max_ranges = std::max(t.max_ranges, (int)T.ranges.size());
         for (size_t k = 0; k + 1 < T.sub.size(); ++k) t.maxsub = std::max(t.maxsub, T.sub[k + 1] - T.sub[k]);
         t.max_nsub = std::max(t.max_nsub, (int)T.sub.size() - 1);
         t.nsub_total += (int64_t)T.sub.size() - 1;
-        std::vector<int2>().swap(T.ranges);
-        std::vector<uint32_t>().swap(T.pairs);
-        std::vector<double>().swap(T.pd);
     }
+    std::vector<int64_t> real_part(nth, 0);
+    RawVec<int2> ranges(roff[ntk]);
+    RawVec<int32_t> sub(soff[ntk]);
+    RawVec<uint32_t> pairs(poff[ntk]);
+    RawVec<double> pd(poff[ntk]);
+    {
+        std::vector<std::thread> cp;
+        const size_t per = (ntk + nth - 1) / nth;
+        for (int w = 0; w < nth; ++w) {
+            const size_t q0 = w * per, q1 = std::min(ntk, q0 + per);
+            if (q0 >= q1) break;
+            cp.emplace_back([&, q0, q1, w] {
+                for (size_t q = q0; q < q1; ++q) {
+                    TaskOut &T = out[order[q]];
+                    for (uint32_t p : T.pairs) real_part[w] += p != kPadPair;
+                    std::copy(T.ranges.begin(), T.ranges.end(), ranges.begin() + roff[q]);
+                    std::copy(T.pairs.begin(), T.pairs.end(), pairs.begin() + poff[q]);
+                    std::copy(T.pd.begin(), T.pd.end(), pd.begin() + poff[q]);
+                    std::copy(T.sub.begin(), T.sub.end(), sub.begin() + soff[q]);
+                    std::vector<int2>().swap(T.ranges);
+                    std::vector<uint32_t>().swap(T.pairs);
+                    std::vector<double>().swap(T.pd);
+                }
+            });
+        }
+        for (auto &th : cp) th.join();
+        for (int64_t v : real_part) real_pairs += v;
+    }
+    setup_mark(s, "tiled: concatenate");
     t.sh = sh;
-    t.ntasks = (int64_t)order.size();
-    t.npairs = (int64_t)std::count_if(pairs.begin(), pairs.end(), [](uint32_t p) { return p != kPadPair; });
+    t.ntasks = (int64_t)ntk;
+    t.npairs = real_pairs;
     upload_vec(t.range_off, roff, s);
     upload_vec(t.ranges, ranges, s);
     upload_vec(t.halo_n, halo, s);
@@ -647,6 +688,7 @@ inline void build_tiled(const NbhDev &nb, int sh, TiledSched &t, cudaStream_t s)
     upload_vec(t.pd, pd, s);
     upload_vec(t.sub_off, soff, s);
     upload_vec(t.sub, sub, s);
+    setup_mark(s, "tiled: upload");
 }
 
 // Block shape: a cubic edge of `tile` cells if given (a multi-rank plan's
