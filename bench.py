@@ -121,23 +121,27 @@ class ClockSampler:
 
 # ------------------------------------------------------------------ model
 
-def algorithmic_bytes(d, nnz_pp, pairs_pp, groups_pp, sweep="tiled"):
+def algorithmic_bytes(d, nnz_pp, pairs_pp, groups_pp, sweep="tiled", w=8):
     """Compulsory HBM bytes per particle per step for each kernel class
     (every array element the kernel needs is moved once; the neighbour
-    index table counts its true entries).  See DESIGN.md §4."""
+    index table counts its true entries).  w: bytes per real (8: fp64,
+    4: the fp32 variant).  See DESIGN.md §4."""
     dd = d * d
-    vec, ten = 8 * d, 8 * dd
-    xv = 8 * (d + 1)                      # reference position + volume
+    vec, ten = w * d, w * dd
+    xv = w * (d + 1)                      # reference position + volume
     if sweep == "tiled":
-        # v r/w + 1/m, per pair and pass: two 16-bit local ids + f64 coefficient
-        sweep_b = 2 * vec + 8 + 2 * 12 * pairs_pp
+        # v r/w + 1/m, per pair and pass: two 16-bit local ids + coefficient
+        sweep_b = 2 * vec + w + 2 * (4 + w) * pairs_pp
     else:
         # v r/w + X|vol + 1/m, per pair and pass: two int32 ids + group pointer
-        sweep_b = 2 * vec + xv + 8 + 2 * (8 * pairs_pp + 8 * groups_pp)
+        sweep_b = 2 * vec + xv + w + 2 * (8 * pairs_pp + 8 * groups_pp)
     return {
+        # v r/w, a, x (displacement in fp32) r/w, flags
         "kick_drift": 2 * vec + vec + 2 * vec + 1,
-        "stress": xv + vec + 4 * nnz_pp + ten + 2 * ten + 2 * ten + 16 + ten,
-        "accel": xv + ten + 4 * nnz_pp + 8 + 1 + 8 + 2 * vec + vec,
+        # X|V0, v, csr, B, F r/w, C_p^-1 r/w, alpha r/w, T write
+        "stress": xv + vec + 4 * nnz_pp + ten + 2 * ten + 2 * ten + 2 * w + ten,
+        # X|V0, T, csr, rho0, flags, mass, v r/w, a write, static sum V gradW
+        "accel": xv + ten + 4 * nnz_pp + w + 1 + w + 2 * vec + vec + vec,
         "sweep": sweep_b,
         "reduce": vec,
     }
@@ -233,6 +237,9 @@ def run_ours(args):
             traffic = json.load(open(tpath)).get(top)
         except Exception:
             traffic = None
+    variants = {}
+    if not args.no_fp32 and args.sweep == "tiled":
+        variants["fp32"] = fp32_variant(dev, args, params, n, d, sz, world, peak)
     line = {
         "metric": "inner solid-relaxation particle-steps/sec",
         "value": value, "unit": "particle-steps/s", "n_gpus": world, "steps": args.steps,
@@ -255,6 +262,7 @@ def run_ours(args):
                      "frac": k_top["achieved_gbs"] / peak, "traffic": traffic,
                      "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"},
         "kernels": kernels,
+        "variants": variants,
         "gpu_launches": launches,
         "clocks": clk,
     }
@@ -265,6 +273,43 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+
+
+def fp32_variant(dev, args, params, n, d, sz, world, peak):
+    """The north star's separately reported fp32 variant: the same solid
+    switched to single-precision state (csrc/solid32.cuh), same steps."""
+    eta, cfl = params["eta"], params["cfl"]
+    dev.set_precision(32)
+    done = 0
+    while done < args.warmup:
+        dev.run_steps(args.steps, eta, cfl)
+        done += args.steps
+    timing = dev.run_steps(args.steps, eta, cfl)
+    ms = timing["total_ms"]
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    fin = dev.measure()["finite"]
+    dev.set_precision(64)
+    model = algorithmic_bytes(d, sz["nnz"] / n, sz["npairs"] / n, sz["ngroups"] / n, "tiled", w=4)
+    kernels = {}
+    for name in ("kick_drift", "stress", "accel", "sweep", "reduce"):
+        tms = timing[name + "_ms"]
+        per_step_s = tms / 1e3 / args.steps
+        gbs = model[name] * n / per_step_s / 1e9 if per_step_s > 0 else 0.0
+        kernels[name] = {"ms_per_step": tms / args.steps, "share": tms / ms if ms else 0.0,
+                         "bytes_per_particle": model[name], "achieved_gbs": gbs}
+    top = max(kernels, key=lambda k: kernels[k]["ms_per_step"])
+    return {"dtype": "f32 (state, gathers, sweep; return map evaluated in f64)",
+            "value": world * n * args.steps / (ms / 1e3), "unit": "particle-steps/s",
+            "ms_per_step": ms / args.steps, "finite": fin,
+            "roofline": {"kernel": top, "bound": "hbm", "achieved": kernels[top]["achieved_gbs"],
+                         "peak": peak, "unit": "GB/s",
+                         "frac": kernels[top]["achieved_gbs"] / peak},
+            "kernels": kernels}
 
 
 def cpu_baseline(params, args, budget_s=20.0, steps=None):
@@ -338,6 +383,7 @@ def main():
     ap.add_argument("--cpu-cols", type=int, default=10)
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-fp32", action="store_true", help="skip the fp32 variant")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

@@ -208,6 +208,16 @@ mtsph_status mtsph_solid_relax(mtsph_solid *s, const mtsph_inner_params *p,
  * + control; timing[6] = kernel launches in the region.                 */
 mtsph_status mtsph_solid_run_steps(mtsph_solid *s, const mtsph_inner_params *p,
                                    int64_t nsteps, double timing[7]);
+/* fp32 variant (the north star's "fp32 variant reported separately"):
+ * bits = 32 moves the state to single-precision arrays (displacement,
+ * F - I, C_p^-1 - I, velocities, divergence records, sweep coefficients)
+ * and runs relax_step / relax / run_steps with the fp32 kernels
+ * (csrc/solid32.cuh; the return map stays fp64).  get / set / measure
+ * read and write through the fp64 copy.  bits = 64 converts back.  Tiled
+ * sweep, single domain only.  No reference counterpart: the reference is
+ * fp64 throughout.                                                       */
+mtsph_status mtsph_solid_set_precision(mtsph_solid *s, int bits);
+mtsph_status mtsph_solid_precision(const mtsph_solid *s, int *bits);
 /* --- multi-rank phases (slab decomposition, tiled sweep; the host driver
  * paper_2309_04010_b200/distributed.py exchanges halos between them) --- */
 enum {

@@ -97,6 +97,8 @@ SIGNATURES = {
     "mtsph_solid_set": (c_int, [c_vp, ctypes.c_char_p, c_vp]),
     "mtsph_solid_launches": (c_int, [c_vp, c_vp]),
     "mtsph_solid_sizes": (c_int, [c_vp, c_vp]),
+    "mtsph_solid_set_precision": (c_int, [c_vp, c_int]),
+    "mtsph_solid_precision": (c_int, [c_vp, c_vp]),
     "mtsph_porous_create": (c_int, [c_vp, c_vp]),
     "mtsph_porous_destroy": (c_int, [c_vp]),
     "mtsph_porous_advance_slow": (c_int, [c_vp, c_dbl, c_dbl, c_vp]),

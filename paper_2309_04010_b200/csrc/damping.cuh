@@ -50,6 +50,21 @@ __device__ __forceinline__ void vst(double4 *p, const double4 &v) { st4(p, v); }
 __device__ __forceinline__ void vset(double2 &v, const double *o) { v.x = o[0]; v.y = o[1]; }
 __device__ __forceinline__ void vset(double4 &v, const double *o) { v.x = o[0]; v.y = o[1]; v.z = o[2]; v.w = 0.0; }
 
+// fp32 variant (solid32.cuh): the same records in single precision
+template <int D, class R> struct VTR { using T = typename VT<D>::T; };
+template <> struct VTR<2, float> { using T = float2; };
+template <> struct VTR<3, float> { using T = float4; };
+__device__ __forceinline__ void vget(const float2 &v, float *o) { o[0] = v.x; o[1] = v.y; }
+__device__ __forceinline__ void vget(const float4 &v, float *o) { o[0] = v.x; o[1] = v.y; o[2] = v.z; }
+__device__ __forceinline__ float2 vldg(const float2 *p) { return __ldg(p); }
+__device__ __forceinline__ float4 vldg(const float4 *p) { return __ldg(p); }
+__device__ __forceinline__ float2 vldcg(const float2 *p) { return __ldcg(p); }
+__device__ __forceinline__ float4 vldcg(const float4 *p) { return __ldcg(p); }
+__device__ __forceinline__ void vst(float2 *p, const float2 &v) { *p = v; }
+__device__ __forceinline__ void vst(float4 *p, const float4 &v) { *p = v; }
+__device__ __forceinline__ void vset(float2 &v, const float *o) { v.x = o[0]; v.y = o[1]; }
+__device__ __forceinline__ void vset(float4 &v, const float *o) { v.x = o[0]; v.y = o[1]; v.z = o[2]; v.w = 0.f; }
+
 template <int D> __device__ __forceinline__ void xget(const double4 &xv, double *x) {
     x[0] = xv.x; x[1] = xv.y;
     if (D == 3) x[2] = xv.z;

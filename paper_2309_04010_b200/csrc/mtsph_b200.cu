@@ -22,6 +22,7 @@
 #include "solid.cuh"
 #include "tiled.cuh"
 #include "gather_csr.cuh"
+#include "solid32.cuh"
 #include "layer1.cuh"
 
 using namespace mtsph;
@@ -224,6 +225,36 @@ struct mtsph_solid {
     int per_step_launches = 0;
     cudaGraphExec_t graphs[3] = {nullptr, nullptr, nullptr};
     int graph_steps[3] = {4, 32, 128};
+    // fp32 variant (solid32.cuh): prec 32 = the fp32 arrays below hold the
+    // state and the fp64 ones are a mirror, refreshed on demand (dirty32)
+    int prec = 64;
+    bool dirty32 = false;
+    DBuf<float> XV32, B32, G32, mass32, rho032, inv_m32, pd32, u32, a32, H32, Hc32, alpha32, T32;
+    DBuf<unsigned char> V32;
+    TiledArgsT<float> tiled_args32() {
+        TiledArgsT<float> A{tiled.range_off.p, tiled.ranges.p, tiled.halo_n.p, tiled.pair_off.p, tiled.pairs.p,
+                            pd32.p, tiled.sub_off.p, tiled.sub.p, inv_m32.p, V32.p, tiled.maxsub};
+        return A;
+    }
+    Solid32Args args32() {
+        Solid32Args A{};
+        A.n = n;
+        A.XV = reinterpret_cast<const float4 *>(XV32.p);
+        A.V = V32.p;
+        A.u = u32.p; A.a = a32.p; A.H = H32.p; A.Hc = Hc32.p; A.alpha = alpha32.p; A.T = T32.p;
+        A.B = B32.p; A.G = G32.p; A.mass = mass32.p; A.rho0 = rho032.p; A.flags = flags.p;
+        A.indptr = nb.indptr.p; A.csr = nb.csr.p;
+        A.perm = nb.perm.p;
+        A.part = part.p;
+        A.nblk = nblk;
+        A.ctrl = ctrl.p;
+        A.ks = kspec32(nb.ks);
+        A.mat = mat;
+        return A;
+    }
+    void drop_graphs() {
+        for (auto &g : graphs) if (g) { cudaGraphExecDestroy(g); g = nullptr; }
+    }
     TiledArgs tiled_args() {
         TiledArgs A{tiled.range_off.p, tiled.ranges.p, tiled.halo_n.p, tiled.pair_off.p, tiled.pairs.p,
                     tiled.pd.p, tiled.sub_off.p, tiled.sub.p, inv_m.p, V.p, tiled.maxsub};
@@ -312,16 +343,116 @@ template <int D> static int solid_step(mtsph_solid *S, int ctrl_mode, cudaEvent_
     return l + 2;
 }
 
+// the fp32 variant of solid_step (solid32.cuh): same kernel classes and
+// event marks, row-parallel gathers with 4 lanes per particle, tiled sweep
+template <int D> static int solid_step32(mtsph_solid *S, int ctrl_mode, cudaEvent_t *ev = nullptr) {
+    Solid32Args A = S->args32();
+    const unsigned nb = blocks_for(S->n);
+    auto mark = [&](int k) { if (ev) MT_CUDA(cudaEventRecordWithFlags(ev[k], S->s, cudaEventRecordExternal)); };
+    mark(0);
+    k32_kick_drift<D><<<nb, 256, 0, S->s>>>(A);
+    mark(1);
+    k32_stress_csr<D, 4><<<nb, 256, 0, S->s>>>(A);
+    k32_rmap<D><<<nb, 256, 0, S->s>>>(A);
+    mark(2);
+    k32_accel_csr<D, 4><<<nb, 256, 0, S->s>>>(A);
+    MT_LAUNCH_CHECK();
+    mark(3);
+    int l = 3 + launch_tiled_sweep<D, float>(S->tiled, S->tiled_args32(), S->ctrl.p, S->s);
+    mark(4);
+    k32_vmax<D><<<nb, 256, 0, S->s>>>(A, 0);
+    k_ctrl<<<1, 256, 0, S->s>>>(S->ctrl.p, S->part.p, S->nblk, ctrl_mode);
+    MT_LAUNCH_CHECK();
+    mark(5);
+    S->dirty32 = true;
+    return l + 2;
+}
+
 static int solid_step_any(mtsph_solid *S, int mode, cudaEvent_t *ev = nullptr) {
+    if (S->prec == 32) return S->d == 2 ? solid_step32<2>(S, mode, ev) : solid_step32<3>(S, mode, ev);
     return S->d == 2 ? solid_step<2>(S, mode, ev) : solid_step<3>(S, mode, ev);
 }
 
 template <int D> static void solid_init_dt(mtsph_solid *S) {
-    SolidArgs A = S->args();
-    k_solid_vmax<D><<<blocks_for(S->n), 256, 0, S->s>>>(A, 1);
+    if (S->prec == 32) k32_vmax<D><<<blocks_for(S->n), 256, 0, S->s>>>(S->args32(), 1);
+    else k_solid_vmax<D><<<blocks_for(S->n), 256, 0, S->s>>>(S->args(), 1);
     k_ctrl<<<1, 256, 0, S->s>>>(S->ctrl.p, S->part.p, S->nblk, CTRL_INIT);
     MT_LAUNCH_CHECK();
     S->launches += 2;
+}
+
+static void g_timed_reset();
+static void g_timed_drop(const mtsph_solid *owner);
+
+// fp32 state -> the fp64 mirror (before anything reads the fp64 arrays)
+static void sync64(mtsph_solid *S) {
+    if (S->prec != 32 || !S->dirty32) return;
+    const unsigned nb = blocks_for(S->n);
+    if (S->d == 2) k32_convert<2><<<nb, 256, 0, S->s>>>(S->args(), S->args32(), 0);
+    else k32_convert<3><<<nb, 256, 0, S->s>>>(S->args(), S->args32(), 0);
+    MT_LAUNCH_CHECK();
+    S->launches += 1;
+    S->dirty32 = false;
+}
+// the fp64 arrays -> the fp32 state (after the host wrote the fp64 ones)
+static void sync32(mtsph_solid *S) {
+    if (S->prec != 32) return;
+    const unsigned nb = blocks_for(S->n);
+    if (S->d == 2) k32_convert<2><<<nb, 256, 0, S->s>>>(S->args(), S->args32(), 1);
+    else k32_convert<3><<<nb, 256, 0, S->s>>>(S->args(), S->args32(), 1);
+    MT_LAUNCH_CHECK();
+    S->launches += 1;
+    S->dirty32 = false;
+}
+
+extern "C" mtsph_status mtsph_solid_set_precision(mtsph_solid *S, int bits) {
+    API_BEGIN
+    if (bits != 32 && bits != 64) throw Error(MTSPH_ERR_ARG, "precision must be 32 or 64 bits");
+    if (bits == S->prec) return MTSPH_OK;
+    if (bits == 32) {
+        if (S->nb.sweep != 3) throw Error(MTSPH_ERR_ARG, "the fp32 variant needs the tiled sweep");
+        if (!S->nb.ghost_internal.empty()) throw Error(MTSPH_ERR_ARG, "the fp32 variant is single-domain only");
+        const int64_t n = S->n;
+        const int d = S->d;
+        if (!S->u32.p) {
+            S->XV32.alloc((size_t)4 * n);
+            S->B32.alloc((size_t)d * d * n);
+            S->G32.alloc((size_t)d * n);
+            S->mass32.alloc(n);
+            S->rho032.alloc(n);
+            S->inv_m32.alloc(n);
+            S->pd32.alloc(std::max<size_t>(S->tiled.pd.n, 1));
+            S->u32.alloc((size_t)d * n);
+            S->a32.alloc((size_t)d * n);
+            S->H32.alloc((size_t)d * d * n);
+            S->Hc32.alloc((size_t)d * d * n);
+            S->alpha32.alloc(n);
+            S->T32.alloc((size_t)n * (d == 3 ? DS<3>::n : DS<2>::n));
+            S->T32.zero(S->s);
+            S->V32.alloc((size_t)n * (d == 3 ? sizeof(float4) : sizeof(float2)));
+            const unsigned nb = blocks_for(n);
+            if (d == 2) k32_static<2><<<nb, 256, 0, S->s>>>(S->args(), S->args32(), S->inv_m.p, S->inv_m32.p);
+            else k32_static<3><<<nb, 256, 0, S->s>>>(S->args(), S->args32(), S->inv_m.p, S->inv_m32.p);
+            const int64_t np = (int64_t)S->tiled.pd.n;
+            if (np > 0) k32_narrow<<<blocks_for(np), 256, 0, S->s>>>(S->tiled.pd.p, S->pd32.p, np);
+            MT_LAUNCH_CHECK();
+            S->launches += np > 0 ? 2 : 1;
+        }
+        S->prec = 32;
+        sync32(S);
+    } else {
+        sync64(S);
+        S->prec = 64;
+    }
+    S->drop_graphs();
+    g_timed_reset();
+    MT_CUDA(cudaStreamSynchronize(S->s));
+    API_END
+}
+
+extern "C" mtsph_status mtsph_solid_precision(const mtsph_solid *S, int *bits) {
+    *bits = S->prec;
+    return MTSPH_OK;
 }
 
 static void check_solid_errors(mtsph_solid *S) {
@@ -449,6 +580,7 @@ extern "C" mtsph_status mtsph_solid_create(const mtsph_solid_desc *dsc, mtsph_so
 }
 
 extern "C" mtsph_status mtsph_solid_destroy(mtsph_solid *s) {
+    g_timed_drop(s);
     delete s;
     return MTSPH_OK;
 }
@@ -546,6 +678,7 @@ extern "C" mtsph_status mtsph_solid_relax(mtsph_solid *S, const mtsph_inner_para
 // benchmark path: exactly nsteps steps in one graph, events per kernel class
 struct TimedGraph {
     int64_t steps = 0;
+    const mtsph_solid *owner = nullptr;
     cudaGraphExec_t exec = nullptr;
     std::vector<cudaEvent_t> ev;
     int per_step = 0;
@@ -555,6 +688,10 @@ struct TimedGraph {
     }
 };
 static std::unique_ptr<TimedGraph> g_timed;  // one benchmark graph at a time
+static void g_timed_reset() { g_timed.reset(); }
+static void g_timed_drop(const mtsph_solid *owner) {
+    if (g_timed && g_timed->owner == owner) g_timed.reset();
+}
 
 extern "C" mtsph_status mtsph_solid_run_steps(mtsph_solid *S, const mtsph_inner_params *p, int64_t nsteps,
                                               double timing[7]) {
@@ -574,9 +711,10 @@ extern "C" mtsph_status mtsph_solid_run_steps(mtsph_solid *S, const mtsph_inner_
     c->min_dt = INFINITY;
     c->err_inv = c->err_rm = ~0ull;
     S->push_ctrl();
-    if (!g_timed || g_timed->steps != nsteps) {
+    if (!g_timed || g_timed->steps != nsteps || g_timed->owner != S) {
         g_timed = std::make_unique<TimedGraph>();
         g_timed->steps = nsteps;
+        g_timed->owner = S;
         g_timed->ev.resize((size_t)nsteps * 6);
         for (auto &e : g_timed->ev) MT_CUDA(cudaEventCreate(&e));
         cudaGraph_t g;
@@ -742,6 +880,7 @@ template <int D> static void solid_phase(mtsph_solid *S, int phase, int arg, dou
 
 extern "C" mtsph_status mtsph_solid_phase(mtsph_solid *S, int phase, int arg, double out[2]) {
     API_BEGIN
+    if (S->prec != 64) throw Error(MTSPH_ERR_ARG, "multi-rank phases run in fp64");
     if (S->d == 2) solid_phase<2>(S, phase, arg, out); else solid_phase<3>(S, phase, arg, out);
     if (phase == MTSPH_PHASE_STRESS) {
         S->pull_ctrl();
@@ -752,6 +891,7 @@ extern "C" mtsph_status mtsph_solid_phase(mtsph_solid *S, int phase, int arg, do
 
 static void pack_common(mtsph_solid *S, const char *field, int64_t m, const int64_t *ids, double *host,
                         const double *in, bool pack) {
+    if (S->prec != 64) throw Error(MTSPH_ERR_ARG, "multi-rank exchanges run in fp64");
     const std::string f(field);
     const int which = f == "vel" ? 0 : (f == "T" ? 1 : -1);
     if (which < 0) throw Error(MTSPH_ERR_ARG, "pack fields are 'vel' and 'T'");
@@ -835,6 +975,7 @@ extern "C" mtsph_status mtsph_solid_stream(const mtsph_solid *S, void **stream) 
 extern "C" mtsph_status mtsph_solid_pack_device(mtsph_solid *S, const char *field, int64_t m,
                                                 const int64_t *ids, double *out) {
     API_BEGIN
+    if (S->prec != 64) throw Error(MTSPH_ERR_ARG, "multi-rank exchanges run in fp64");
     const int which = pack_field(field);
     if (m <= 0) return MTSPH_OK;
     if (S->d == 2) k_pack<2><<<blocks_for(m), 256, 0, S->s>>>(S->n, m, ids, S->V.p, S->T.p, S->nb.XV.p, which, out);
@@ -847,6 +988,7 @@ extern "C" mtsph_status mtsph_solid_pack_device(mtsph_solid *S, const char *fiel
 extern "C" mtsph_status mtsph_solid_unpack_device(mtsph_solid *S, const char *field, int64_t m,
                                                   const int64_t *ids, const double *in) {
     API_BEGIN
+    if (S->prec != 64) throw Error(MTSPH_ERR_ARG, "multi-rank exchanges run in fp64");
     const int which = pack_field(field);
     if (m <= 0) return MTSPH_OK;
     if (S->d == 2) k_unpack<2><<<blocks_for(m), 256, 0, S->s>>>(S->n, m, ids, S->V.p, S->T.p, S->nb.XV.p, which, in);
@@ -858,6 +1000,7 @@ extern "C" mtsph_status mtsph_solid_unpack_device(mtsph_solid *S, const char *fi
 
 extern "C" mtsph_status mtsph_solid_measure(mtsph_solid *S, double out[5]) {
     API_BEGIN
+    sync64(S);
     SolidArgs A = S->args();
     const int nb = S->nblk;
     if (S->d == 2) k_solid_measure<2><<<nb, 256, 0, S->s>>>(A, S->meas.p);
@@ -887,6 +1030,7 @@ enum FieldKind { FK_SOA_VEC, FK_SOA_TEN, FK_SCALAR, FK_VEL, FK_REF };
 
 extern "C" mtsph_status mtsph_solid_get(mtsph_solid *S, const char *field, double *host) {
     API_BEGIN
+    sync64(S);
     const int64_t n = S->n;
     const int d = S->d;
     std::vector<int64_t> perm(n);
@@ -919,6 +1063,7 @@ extern "C" mtsph_status mtsph_solid_get(mtsph_solid *S, const char *field, doubl
 
 extern "C" mtsph_status mtsph_solid_set(mtsph_solid *S, const char *field, const double *host) {
     API_BEGIN
+    sync64(S);
     const int64_t n = S->n;
     const int d = S->d;
     std::vector<int64_t> perm(n);
@@ -944,6 +1089,7 @@ extern "C" mtsph_status mtsph_solid_set(mtsph_solid *S, const char *field, const
             for (int c = 0; c < d; ++c) buf[(size_t)k * stride + c] = host[perm[k] * d + c];
         MT_CUDA(cudaMemcpyAsync(S->V.p, buf.data(), buf.size() * 8, cudaMemcpyHostToDevice, S->s));
     } else throw Error(MTSPH_ERR_ARG, "unknown or read-only solid field " + f);
+    sync32(S);
     MT_CUDA(cudaStreamSynchronize(S->s));
     API_END
 }

@@ -60,39 +60,78 @@ struct TiledSched {
     // reverse-pass order, per-task completion + work counter (ntasks + 1)
     DBuf<int32_t> f_nboff, f_nbt, f_col, f_rev, f_done;
     int flow_grid = 0;               // 0: per-colour launches
+    int flow_grid32 = 0;             // the same for the fp32 variant's kernel
 };
 
-struct TiledArgs {
+// R: the precision of the velocities, inverse masses and coefficients
+// (double: the reference path; float: the fp32 variant, solid32.cuh)
+template <class R> struct TiledArgsT {
     const int64_t *range_off;
     const int2 *ranges;
     const int32_t *halo_n;
     const int64_t *pair_off;
     const uint32_t *pairs;
-    const double *pd;
+    const R *pd;
     const int64_t *sub_off;
     const int32_t *sub;
-    const double *inv_m;
+    const R *inv_m;
     void *V;
     int maxsub;      // largest sub-colour (pairs), sizes the staging buffers
+};
+using TiledArgs = TiledArgsT<double>;
+
+// Shared-memory halo record (v0, v1, v2, 1/m), 16 B-strided so record l
+// sits in 16 B bank group l % 8 (see sweep_task).  fp64: two arrays,
+// (v0, v1) and (v2 | 0, 1/m), one LDS.128 each; fp32: one float4 array.
+template <class R> struct Halo;
+template <> struct Halo<double> {
+    double2 *xy, *zw;
+    __device__ __forceinline__ Halo(void *base, int H) : xy(reinterpret_cast<double2 *>(base)), zw(xy + H) {}
+    __device__ __forceinline__ void *end(int H) const { return zw + H; }
+    __device__ __forceinline__ void ld(int l, double &x, double &y, double &z, double &im) const {
+        const double2 a = xy[l], b = zw[l];
+        x = a.x; y = a.y; z = b.x; im = b.y;
+    }
+    template <int D> __device__ __forceinline__ void st(int l, double x, double y, double z, double im) {
+        xy[l] = make_double2(x, y);
+        if (D == 3) zw[l] = make_double2(z, im);  // 2D: the z|1/m half never changes
+    }
+    __device__ __forceinline__ void init(int l, double x, double y, double z, double im) {
+        xy[l] = make_double2(x, y);
+        zw[l] = make_double2(z, im);
+    }
+    static constexpr size_t bytes = 32;
+};
+template <> struct Halo<float> {
+    float4 *r;
+    __device__ __forceinline__ Halo(void *base, int) : r(reinterpret_cast<float4 *>(base)) {}
+    __device__ __forceinline__ void *end(int H) const { return r + H; }
+    __device__ __forceinline__ void ld(int l, float &x, float &y, float &z, float &im) const {
+        const float4 a = r[l];
+        x = a.x; y = a.y; z = a.z; im = a.w;
+    }
+    template <int D> __device__ __forceinline__ void st(int l, float x, float y, float z, float im) {
+        r[l] = make_float4(x, y, z, im);
+    }
+    __device__ __forceinline__ void init(int l, float x, float y, float z, float im) { r[l] = make_float4(x, y, z, im); }
+    static constexpr size_t bytes = 16;
 };
 
 // One block task (one CTA): stage the halo, apply the sub-colours in
 // direction dir, write the halo back.  FLOW: other SMs write V during the
 // launch (persistent dataflow sweep), so the halo is read through L2.
-template <int D, bool FLOW>
-__device__ __forceinline__ void sweep_task(const TiledArgs &T, int64_t task, int dir, double half,
+template <int D, bool FLOW, class R>
+__device__ __forceinline__ void sweep_task(const TiledArgsT<R> &T, int64_t task, int dir, R half,
                                            double *smem) {
-    using V_t = typename VT<D>::T;
+    using V_t = typename VTR<D, R>::T;
     const int H = T.halo_n[task];
     const int64_t r0 = T.range_off[task], r1 = T.range_off[task + 1];
     const int nr = (int)(r1 - r0);
     int2 *rt = reinterpret_cast<int2 *>(smem);                 // range table
-    // halo as two 16 B-strided arrays, (v0, v1) and (v2 | 0, 1/m): one LDS.128
-    // each.  Record l sits in 16 B bank group l % 8 of both arrays (a 32 B
-    // record would only ever reach the even groups), and build_tiled orders
-    // each sub-colour so a quarter warp's li and lj are distinct mod 8.
-    double2 *sxy = reinterpret_cast<double2 *>(smem + (((nr + 1) & ~1) + 3) / 4 * 4);
-    double2 *szw = sxy + H;
+    // halo (Halo<R>): record l sits in 16 B bank group l % 8, and
+    // build_tiled orders each sub-colour so a quarter warp's li and lj are
+    // distinct mod 8 -- one wavefront per halo access
+    Halo<R> hal(smem + (((nr + 1) & ~1) + 3) / 4 * 4, H);
     for (int r = threadIdx.x; r < nr; r += blockDim.x) rt[r] = T.ranges[r0 + r];
     __syncthreads();
     V_t *V = reinterpret_cast<V_t *>(T.V);
@@ -107,9 +146,8 @@ __device__ __forceinline__ void sweep_task(const TiledArgs &T, int64_t task, int
     const int64_t p0 = T.pair_off[task];
     const int64_t s0 = T.sub_off[task];
     const int nsub = (int)(T.sub_off[task + 1] - s0) - 1;
-    // double-buffered staging of each sub-colour's (pair, coefficient)
-    // chunk with cp.async: chunk q+1 streams in while chunk q is applied
-    double *bd = reinterpret_cast<double *>(szw + H);                // ring of coefficients
+    // ring of kSweepStages (pair, coefficient) chunks staged with cp.async
+    R *bd = reinterpret_cast<R *>(hal.end(H));                                 // ring of coefficients
     uint32_t *bp = reinterpret_cast<uint32_t *>(bd + kSweepStages * T.maxsub);  // ring of pairs
     int *ssub = reinterpret_cast<int *>(bp + kSweepStages * T.maxsub);         // sub-colour bounds
     for (int k = threadIdx.x; k <= nsub; k += blockDim.x) ssub[k] = T.sub[s0 + k];
@@ -139,7 +177,10 @@ __device__ __forceinline__ void sweep_task(const TiledArgs &T, int64_t task, int
             for (int p = a + st; p < b; p += nst) {
                 const unsigned dpd = (unsigned)__cvta_generic_to_shared(bd + slot * T.maxsub + (p - a));
                 const unsigned dpp = (unsigned)__cvta_generic_to_shared(bp + slot * T.maxsub + (p - a));
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dpd), "l"(T.pd + p0 + p));
+                if (sizeof(R) == 8)
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dpd), "l"(T.pd + p0 + p));
+                else
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dpd), "l"(T.pd + p0 + p));
                 asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dpp), "l"(T.pairs + p0 + p));
             }
         }
@@ -151,11 +192,10 @@ __device__ __forceinline__ void sweep_task(const TiledArgs &T, int64_t task, int
         for (int q = 0; q < kSweepStages - 1; ++q) stage(q);
     for (int l = threadIdx.x; l < H; l += blockDim.x) {
         const int64_t g = global_of(l);
-        double v[3] = {0, 0, 0};
+        R v[3] = {0, 0, 0};
         // per-colour launches: halos of one launch are disjoint, read-only here
         vget(FLOW ? vldcg(V + g) : vldg(V + g), v);
-        sxy[l] = make_double2(v[0], v[1]);
-        szw[l] = make_double2(D == 3 ? v[2] : 0.0, T.inv_m[g]);
+        hal.init(l, v[0], v[1], D == 3 ? v[2] : R(0), T.inv_m[g]);
     }
     if (stager) asm volatile("cp.async.wait_group %0;\n" ::"n"(kSweepStages - 2));  // chunk 0
     __syncthreads();
@@ -174,37 +214,38 @@ __device__ __forceinline__ void sweep_task(const TiledArgs &T, int64_t task, int
         int a0, b0;
         sub_range(q, a0, b0);
         const int cnt = b0 - a0;
-        const double *cd = bd + (q % kSweepStages) * T.maxsub;
+        const R *cd = bd + (q % kSweepStages) * T.maxsub;
         const uint32_t *cpk = bp + (q % kSweepStages) * T.maxsub;
         for (int p = threadIdx.x; p < cnt; p += npr) {  // npr % 8 == 0: groups stay quarter warps
             const uint32_t pk = cpk[p];
             if (pk == 0xffffffffu) continue;  // kPadPair
             const int li = (int)(pk & 0xffffu), lj = (int)(pk >> 16);
-            double2 a = sxy[li], b = sxy[lj];
-            const double2 az = szw[li], bz = szw[lj];
-            const double c = half * cd[p];
-            const double ca = c * az.y, cb = c * bz.y;
-            const double rden = 1.0 / (1.0 + ca + cb);
-            double u = (a.x - b.x) * rden;
-            a.x -= ca * u;
-            b.x += cb * u;
-            u = (a.y - b.y) * rden;
-            a.y -= ca * u;
-            b.y += cb * u;
-            sxy[li] = a;
-            sxy[lj] = b;
-            if (D == 3) {  // 16 B stores: conflict-free like the loads
-                u = (az.x - bz.x) * rden;
-                szw[li] = make_double2(az.x - ca * u, az.y);
-                szw[lj] = make_double2(bz.x + cb * u, bz.y);
+            R ax, ay, az, ai, bx, by, bz, bi;
+            hal.ld(li, ax, ay, az, ai);
+            hal.ld(lj, bx, by, bz, bi);
+            const R c = half * cd[p];
+            const R ca = c * ai, cb = c * bi;
+            const R rden = R(1) / (R(1) + ca + cb);
+            R u = (ax - bx) * rden;
+            ax -= ca * u;
+            bx += cb * u;
+            u = (ay - by) * rden;
+            ay -= ca * u;
+            by += cb * u;
+            if (D == 3) {
+                u = (az - bz) * rden;
+                az -= ca * u;
+                bz += cb * u;
             }
+            hal.template st<D>(li, ax, ay, az, ai);
+            hal.template st<D>(lj, bx, by, bz, bi);
         }
         __syncthreads();
     }
     for (int l = threadIdx.x; l < H; l += blockDim.x) {
         const int64_t g = global_of(l);
-        const double2 e = sxy[l];
-        const double v[3] = {e.x, e.y, szw[l].x};
+        R v[3], im;
+        hal.ld(l, v[0], v[1], v[2], im);
         V_t w;
         vset(w, v);
         vst(V + g, w);
@@ -212,11 +253,11 @@ __device__ __forceinline__ void sweep_task(const TiledArgs &T, int64_t task, int
 }
 
 // per-colour launch: one CTA per block task of the colour
-template <int D>
-__global__ void __launch_bounds__(1024) k_sweep_tiled(TiledArgs T, int64_t t0, int dir, const Ctrl *ctrl) {
+template <int D, class R = double>
+__global__ void __launch_bounds__(1024) k_sweep_tiled(TiledArgsT<R> T, int64_t t0, int dir, const Ctrl *ctrl) {
     extern __shared__ double smem[];
     if (ctrl->done) return;
-    sweep_task<D, false>(T, t0 + blockIdx.x, dir, 0.5 * ctrl->dt * ctrl->eta, smem);
+    sweep_task<D, false, R>(T, t0 + blockIdx.x, dir, R(0.5 * ctrl->dt * ctrl->eta), smem);
 }
 
 // Dataflow schedule of a whole sweep (both passes) in one persistent launch.
@@ -246,12 +287,12 @@ __device__ __forceinline__ void st_release_gpu(int32_t *p, int v) {
 // Deadlock-free: an item only waits on items claimed earlier by running CTAs.
 // Result identical to the per-colour launches (same tasks, same order on
 // every particle).
-template <int D>
-__global__ void __launch_bounds__(1024) k_sweep_flow(TiledArgs T, TiledFlow F, const Ctrl *ctrl) {
+template <int D, class R = double>
+__global__ void __launch_bounds__(1024) k_sweep_flow(TiledArgsT<R> T, TiledFlow F, const Ctrl *ctrl) {
     extern __shared__ double smem[];
     __shared__ int s_w;
     if (ctrl->done) return;
-    const double half = 0.5 * ctrl->dt * ctrl->eta;
+    const R half = R(0.5 * ctrl->dt * ctrl->eta);
     for (;;) {
         if (threadIdx.x == 0) s_w = atomicAdd(F.counter, 1);
         __syncthreads();
@@ -270,7 +311,7 @@ __global__ void __launch_bounds__(1024) k_sweep_flow(TiledArgs T, TiledFlow F, c
             }
         }
         __syncthreads();
-        sweep_task<D, true>(T, t, pass ? -1 : 1, half, smem);
+        sweep_task<D, true, R>(T, t, pass ? -1 : 1, half, smem);
         __syncthreads();  // every write-back of the halo issued
         if (threadIdx.x == 0) {
             __threadfence();
@@ -279,21 +320,23 @@ __global__ void __launch_bounds__(1024) k_sweep_flow(TiledArgs T, TiledFlow F, c
     }
 }
 
-inline size_t tiled_smem_bytes(const TiledSched &t, int d) {
+// rsize: bytes of the sweep's real type (8: fp64, 4: the fp32 variant)
+inline size_t tiled_smem_bytes(const TiledSched &t, int d, int rsize = 8) {
     (void)d;
-    return (size_t)((((t.max_ranges + 1) & ~1) + 3) / 4 * 4) * 8 + (size_t)t.max_halo * 32 +
-           (size_t)t.maxsub * kSweepStages * 12 + (size_t)(t.max_nsub + 1) * 4;
+    return (size_t)((((t.max_ranges + 1) & ~1) + 3) / 4 * 4) * 8 + (size_t)t.max_halo * 4 * rsize +
+           (size_t)t.maxsub * kSweepStages * (4 + rsize) + (size_t)(t.max_nsub + 1) * 4;
 }
 
-template <int D>
-int launch_tiled_sweep(const TiledSched &t, const TiledArgs &A, const Ctrl *ctrl, cudaStream_t s) {
+template <int D, class R = double>
+int launch_tiled_sweep(const TiledSched &t, const TiledArgsT<R> &A, const Ctrl *ctrl, cudaStream_t s) {
     const int nc = (int)t.colour_ptr.size() - 1;
-    const size_t sm = tiled_smem_bytes(t, D);
-    if (t.flow_grid > 0 && t.ntasks > 0) {
+    const size_t sm = tiled_smem_bytes(t, D, (int)sizeof(R));
+    const int flow_grid = sizeof(R) == 8 ? t.flow_grid : t.flow_grid32;
+    if (flow_grid > 0 && t.ntasks > 0) {
         MT_CUDA(cudaMemsetAsync(t.f_done.p, 0, sizeof(int32_t) * (size_t)(t.ntasks + 1), s));
         TiledFlow F{t.f_nboff.p, t.f_nbt.p, t.f_col.p, t.f_rev.p, t.f_done.p, t.f_done.p + t.ntasks,
                     (int32_t)t.ntasks};
-        k_sweep_flow<D><<<(unsigned)t.flow_grid, t.threads, sm, s>>>(A, F, ctrl);
+        k_sweep_flow<D, R><<<(unsigned)flow_grid, t.threads, sm, s>>>(A, F, ctrl);
         MT_LAUNCH_CHECK();
         return 1;
     }
@@ -303,7 +346,7 @@ int launch_tiled_sweep(const TiledSched &t, const TiledArgs &A, const Ctrl *ctrl
             const int c = pass == 0 ? q : nc - 1 - q;
             const int64_t t0 = t.colour_ptr[c], t1 = t.colour_ptr[c + 1];
             if (t1 <= t0) continue;
-            k_sweep_tiled<D><<<(unsigned)(t1 - t0), t.threads, sm, s>>>(A, t0, pass == 0 ? 1 : -1, ctrl);
+            k_sweep_tiled<D, R><<<(unsigned)(t1 - t0), t.threads, sm, s>>>(A, t0, pass == 0 ? 1 : -1, ctrl);
             MT_LAUNCH_CHECK();
             ++launches;
         }
@@ -734,6 +777,10 @@ inline void build_tiled_auto(const NbhDev &nb, TiledSched &t, cudaStream_t s, in
     allow_max_dynamic_smem((const void *)k_sweep_tiled<3>);
     allow_max_dynamic_smem((const void *)k_sweep_flow<2>);
     allow_max_dynamic_smem((const void *)k_sweep_flow<3>);
+    allow_max_dynamic_smem((const void *)k_sweep_tiled<2, float>);
+    allow_max_dynamic_smem((const void *)k_sweep_tiled<3, float>);
+    allow_max_dynamic_smem((const void *)k_sweep_flow<2, float>);
+    allow_max_dynamic_smem((const void *)k_sweep_flow<3, float>);
     // persistent dataflow launch (default; MTSPH_SWEEP_FLOW=0: per-colour
     // launches): as many CTAs as fit at once
     const char *fe = std::getenv("MTSPH_SWEEP_FLOW");
@@ -745,6 +792,10 @@ inline void build_tiled_auto(const NbhDev &nb, TiledSched &t, cudaStream_t s, in
             &per, d == 3 ? (const void *)k_sweep_flow<3> : (const void *)k_sweep_flow<2>, th,
             tiled_smem_bytes(t, d)));
         t.flow_grid = sms * per;
+        MT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &per, d == 3 ? (const void *)k_sweep_flow<3, float> : (const void *)k_sweep_flow<2, float>, th,
+            tiled_smem_bytes(t, d, 4)));
+        t.flow_grid32 = sms * per;
     }
 }
 

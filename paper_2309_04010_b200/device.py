@@ -158,6 +158,17 @@ class DeviceSolid:
         return {"total_ms": t[0], "kick_drift_ms": t[1], "stress_ms": t[2], "accel_ms": t[3],
                 "sweep_ms": t[4], "reduce_ms": t[5], "launches": int(t[6])}
 
+    def set_precision(self, bits):
+        """64: the reference's fp64 state (default).  32: the fp32 variant
+        (csrc/solid32.cuh) -- state converted in place, the same stepping
+        calls run the single-precision kernels; get/set/measure convert."""
+        check(self._lib.mtsph_solid_set_precision(self._h, int(bits)))
+
+    def precision(self):
+        v = ctypes.c_int()
+        check(self._lib.mtsph_solid_precision(self._h, ctypes.byref(v)))
+        return v.value
+
     # -- multi-rank phases ------------------------------------------------
     def set_step(self, dt, eta):
         check(self._lib.mtsph_solid_set_step(self._h, float(dt), float(eta)))

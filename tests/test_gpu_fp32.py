@@ -1,0 +1,142 @@
+"""GPU: the fp32 variant of the inner step (csrc/solid32.cuh) against the
+fp64 path.
+
+The reference is fp64 throughout; the north star asks for an fp32 variant
+reported separately.  It is checked against the parity-tested fp64 tiled
+pipeline on the same problem and the same step sizes:
+  * precision switches round-trip the state to fp32 rounding;
+  * per-step state over 100 plastic inner steps (bench material, boundary
+    ramp active): displacement, velocity, F - I and the plastic strain
+    within FP32_TRAJ_TOL of each field's scale;
+  * a whole device-loop relaxation reaches the fp64 equilibrium within
+    FP32_EQ_TOL relative L2 in displacement and F - I;
+  * the fp32 damping sweep conserves momentum and never raises E_k beyond
+    fp32 rounding;
+  * the benchmark entry (run_steps) runs in fp32.
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+FP32_TRAJ_TOL = 2e-5     # max |fp32 - fp64| / max |fp64| per field, 100 steps
+FP32_EQ_TOL = 1e-5       # relative L2 after 4000 relaxation steps (north-star bound)
+
+
+def _bar(dim, sweep="tiled"):
+    from paper_2309_04010_b200 import lattices
+    from paper_2309_04010_b200.config import resolve
+    from paper_2309_04010_b200.device import DeviceSolid
+    from paper_2309_04010_b200.scenarios import _necking_materials
+    raw = {"scenario": "block_3d", "length": 0.4, "width": 0.16, "breadth": 0.16, "dp": 0.02} \
+        if dim == 3 else {"scenario": "bar_2d", "length": 2.0, "width": 0.4, "dp": 0.025}
+    p = resolve(raw).params
+    lat = lattices.build_lattice(p)
+    el, hard = _necking_materials(p)
+    law, hp = hard.device_params()
+    s = DeviceSolid(lat.pos, lat.vol, el.density0, lat.constrained, lat.side, lat.mid_mask,
+                    lat.h_axes, el.shear_modulus, el.bulk_modulus, plastic=True,
+                    hardening_law=law, hard=hp, sweep=sweep)
+    return s, lat, p
+
+
+def _fields(s, lat):
+    d = lat.pos.shape[1]
+    return {"u": s.get("pos") - lat.pos, "vel": s.get("vel"),
+            "H": s.get("F") - np.eye(d), "alpha": s.get("alpha")}
+
+
+def _scaled_err(a, b):
+    scale = max(float(np.max(np.abs(b))), 1e-300)
+    return float(np.max(np.abs(a - b))) / scale
+
+
+def test_precision_switch_round_trips():
+    s, lat, _ = _bar(3)
+    rng = np.random.default_rng(3)
+    v = rng.normal(size=(lat.n, 3))
+    s.set("vel", v)
+    s.set_precision(32)
+    assert s.precision() == 32
+    np.testing.assert_allclose(s.get("vel"), v, rtol=1e-7, atol=0)
+    s.set_precision(64)
+    assert s.precision() == 64
+    np.testing.assert_allclose(s.get("vel"), v, rtol=1e-7, atol=0)
+    with pytest.raises(Exception):
+        s.set_precision(16)
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_fp32_trajectory_tracks_fp64(dim):
+    runs = {}
+    for bits in (64, 32):
+        s, lat, p = _bar(dim)
+        s.set_precision(bits)
+        s.set_ramp(0.02 * p["length"], 30, 30)
+        hist = []
+        for k in range(100):
+            dt = runs[64][0][k] if bits == 32 else s.stable_dt(p["cfl"])
+            s.relax_step(dt, p["eta"])
+            hist.append(dt)
+        runs[bits] = (hist, _fields(s, lat), s.measure())
+    f64, f32 = runs[64][1], runs[32][1]
+    assert np.max(f64["alpha"]) > 0, "the case must reach plastic flow"
+    errs = {k: _scaled_err(f32[k], f64[k]) for k in f64}
+    print(f"fp32 vs fp64, {dim}D, 100 steps:", errs)
+    for k, e in errs.items():
+        assert e < FP32_TRAJ_TOL, (k, e)
+    assert runs[32][2]["finite"]
+
+
+def test_fp32_relaxation_reaches_fp64_equilibrium():
+    out = {}
+    for bits in (64, 32):
+        s, lat, p = _bar(2)
+        s.set_precision(bits)
+        s.set_ramp(0.01 * p["length"], 20, 20)
+        r = s.relax(eta=p["eta"], cfl=p["cfl"], criterion=1e-9, dt_outer=1.0, max_inner=4000)
+        out[bits] = (_fields(s, lat), r.n_inner)
+    a, b = out[64][0], out[32][0]
+    for k in ("u", "H"):
+        e = float(np.linalg.norm(b[k] - a[k]) / np.linalg.norm(a[k]))
+        print(f"equilibrium {k}: rel L2 {e:.3e} (steps fp64 {out[64][1]}, fp32 {out[32][1]})")
+        assert e < FP32_EQ_TOL, (k, e)
+
+
+def test_fp32_damping_conserves_momentum_and_dissipates():
+    from conftest import jittered_lattice
+    from paper_2309_04010_b200.device import DeviceSolid
+    pos, vol = jittered_lattice(8, 3, dp=0.01, jitter=0.05, seed=5)
+    n = len(vol)
+    s = DeviceSolid(pos, vol, 2.0, np.zeros(n, bool), np.zeros(n, np.int8), None,
+                    [1.35 * 0.01] * 3, 1e-12, 1e-12, plastic=False, sweep="tiled")
+    s.set_precision(32)
+    mass = 2.0 * vol
+    vel = np.random.default_rng(7).normal(size=(n, 3))
+    s.set("vel", vel)
+    v0 = s.get("vel")
+    p0 = mass @ v0
+    e0 = 0.5 * np.sum(mass[:, None] * v0 * v0)
+    first = e0
+    for _ in range(20):
+        s.relax_step(1e-9, 1e7)
+        v = s.get("vel")
+        e = 0.5 * np.sum(mass[:, None] * v * v)
+        assert e <= e0 * (1 + 1e-6)
+        e0 = e
+    p1 = mass @ s.get("vel")
+    scale = np.sum(mass * np.linalg.norm(vel, axis=1))
+    assert np.max(np.abs(p1 - p0)) <= 1e-5 * scale
+    assert e0 < 0.25 * first
+
+
+def test_fp32_run_steps():
+    s, lat, p = _bar(3)
+    s.set_precision(32)
+    t = s.run_steps(8, p["eta"], p["cfl"])
+    assert t["total_ms"] > 0 and t["launches"] >= 8 * 6
+    assert s.measure()["finite"]
+    s.set_precision(64)
+    t = s.run_steps(8, p["eta"], p["cfl"])
+    assert t["total_ms"] > 0
