@@ -229,6 +229,7 @@ struct mtsph_solid {
     // state and the fp64 ones are a mirror, refreshed on demand (dirty32)
     int prec = 64;
     bool dirty32 = false;
+    int gather_g32 = 4;  // lanes per particle of the fp32 gathers (MTSPH_GATHER_LANES32)
     DBuf<float> XV32, B32, G32, mass32, rho032, inv_m32, pd32, u32, a32, H32, Hc32, alpha32, T32;
     DBuf<unsigned char> V32;
     TiledArgsT<float> tiled_args32() {
@@ -307,6 +308,12 @@ template <int D> static void launch_stress_gather(mtsph_solid *S, const SolidArg
     else if (S->gather_g == 2) k_solid_stress_csr<D, 2><<<nb, 256, 0, s>>>(A);
     else k_solid_stress<D, true><<<nb, 256, 0, s>>>(A);
 }
+// the split return map, instantiated per hardening law
+template <int D> static void launch_rmap(mtsph_solid *S, const SolidArgs &A, cudaStream_t s) {
+    const unsigned nb = blocks_for(S->n);
+    if (S->mat.law == 1) k_solid_rmap<D, 1><<<nb, 256, 0, s>>>(A);
+    else k_solid_rmap<D, 0><<<nb, 256, 0, s>>>(A);
+}
 template <int D> static void launch_accel_gather(mtsph_solid *S, const SolidArgs &A, cudaStream_t s) {
     const unsigned nb = blocks_for(S->n);
     if (S->gather_g == 4) k_solid_accel_csr<D, 4><<<nb, 256, 0, s>>>(A);
@@ -328,7 +335,7 @@ template <int D> static int solid_step(mtsph_solid *S, int ctrl_mode, cudaEvent_
     // split: the neighbour gather runs at low register count / high
     // occupancy, the register-heavy return map element-wise
     launch_stress_gather<D>(S, A, S->s);
-    k_solid_rmap<D><<<nb, 256, 0, S->s>>>(A);
+    launch_rmap<D>(S, A, S->s);
     mark(2);
     launch_accel_gather<D>(S, A, S->s);
     MT_LAUNCH_CHECK();
@@ -352,10 +359,21 @@ template <int D> static int solid_step32(mtsph_solid *S, int ctrl_mode, cudaEven
     mark(0);
     k32_kick_drift<D><<<nb, 256, 0, S->s>>>(A);
     mark(1);
-    k32_stress_csr<D, 4><<<nb, 256, 0, S->s>>>(A);
-    k32_rmap<D><<<nb, 256, 0, S->s>>>(A);
+    switch (S->gather_g32) {
+    case 2: k32_stress_csr<D, 2><<<nb, 256, 0, S->s>>>(A); break;
+    case 8: k32_stress_csr<D, 8><<<nb, 256, 0, S->s>>>(A); break;
+    case 16: k32_stress_csr<D, 16><<<nb, 256, 0, S->s>>>(A); break;
+    default: k32_stress_csr<D, 4><<<nb, 256, 0, S->s>>>(A);
+    }
+    if (S->mat.law == 1) k32_rmap<D, 1><<<nb, 256, 0, S->s>>>(A);
+    else k32_rmap<D, 0><<<nb, 256, 0, S->s>>>(A);
     mark(2);
-    k32_accel_csr<D, 4><<<nb, 256, 0, S->s>>>(A);
+    switch (S->gather_g32) {
+    case 2: k32_accel_csr<D, 2><<<nb, 256, 0, S->s>>>(A); break;
+    case 8: k32_accel_csr<D, 8><<<nb, 256, 0, S->s>>>(A); break;
+    case 16: k32_accel_csr<D, 16><<<nb, 256, 0, S->s>>>(A); break;
+    default: k32_accel_csr<D, 4><<<nb, 256, 0, S->s>>>(A);
+    }
     MT_LAUNCH_CHECK();
     mark(3);
     int l = 3 + launch_tiled_sweep<D, float>(S->tiled, S->tiled_args32(), S->ctrl.p, S->s);
@@ -437,6 +455,11 @@ extern "C" mtsph_status mtsph_solid_set_precision(mtsph_solid *S, int bits) {
             if (np > 0) k32_narrow<<<blocks_for(np), 256, 0, S->s>>>(S->tiled.pd.p, S->pd32.p, np);
             MT_LAUNCH_CHECK();
             S->launches += np > 0 ? 2 : 1;
+        }
+        if (const char *e = std::getenv("MTSPH_GATHER_LANES32")) {
+            const int g = std::atoi(e);
+            if (g != 2 && g != 4 && g != 8 && g != 16) throw Error(MTSPH_ERR_ARG, "MTSPH_GATHER_LANES32: 2, 4, 8 or 16");
+            S->gather_g32 = g;
         }
         S->prec = 32;
         sync32(S);
@@ -824,7 +847,7 @@ template <int D> static void solid_phase(mtsph_solid *S, int phase, int arg, dou
         break;
     case MTSPH_PHASE_STRESS:
         launch_stress_gather<D>(S, A, s);
-        k_solid_rmap<D><<<nb, 256, 0, s>>>(A);
+        launch_rmap<D>(S, A, s);
         S->launches += 2;
         break;
     case MTSPH_PHASE_ACCEL: {

@@ -38,20 +38,33 @@ struct Mat {
     int plastic;
 };
 
-__device__ __forceinline__ double hard_k(const Mat &m, double a) {
-    if (m.law == 1) return m.p[0] * pow(1.0 + a / m.p[1], m.p[2]);
+// LAW: the hardening law as a compile-time constant (0, 1), or -1 to
+// read m.law at run time.  The split return-map kernels are instantiated
+// per law, so each carries one law's code and registers.
+template <int LAW = -1> __device__ __forceinline__ double hard_k(const Mat &m, double a) {
+    if (LAW == 1 || (LAW < 0 && m.law == 1)) return m.p[0] * pow(1.0 + a / m.p[1], m.p[2]);
     return m.p[0] + (m.p[1] - m.p[0]) * (1.0 - exp(-m.p[2] * a)) + m.p[3] * a;
 }
-__device__ __forceinline__ double hard_kp(const Mat &m, double a) {
-    if (m.law == 1) return m.p[0] * m.p[2] / m.p[1] * pow(1.0 + a / m.p[1], m.p[2] - 1.0);
-    return (m.p[1] - m.p[0]) * m.p[2] * exp(-m.p[2] * a) + m.p[3];
+// K(a) and K'(a) from one pow / exp (the Newton iterate needs both):
+// law 1: K' = m K / (e0 (1 + a/e0)), equal to s0 m/e0 (1 + a/e0)^(m-1) up
+// to rounding; law 0: K' = (sinf - s0) delta e^(-delta a) + H
+template <int LAW = -1> __device__ __forceinline__ double hard_k_kp(const Mat &m, double a, double &kp) {
+    if (LAW == 1 || (LAW < 0 && m.law == 1)) {
+        const double t = 1.0 + a / m.p[1];
+        const double k = m.p[0] * pow(t, m.p[2]);
+        kp = k * m.p[2] / (m.p[1] * t);
+        return k;
+    }
+    const double e = exp(-m.p[2] * a);
+    kp = (m.p[1] - m.p[0]) * m.p[2] * e + m.p[3];
+    return m.p[0] + (m.p[1] - m.p[0]) * (1.0 - e) + m.p[3] * a;
 }
 
 #define SQ23_D 0.81649658092772603273
 
 // plasticity.py:118 for one particle.  Returns 0, 1 (det F <= 0),
 // 2 (no convergence), 3 (plastic tensor inverted).
-template <int D>
+template <int D, int LAW = -1>
 __device__ __forceinline__ int return_map_dev(const double *F, double *cp, double &alpha, const Mat &m,
                                               double *P) {
     const double j = det_d<D>(F);
@@ -87,21 +100,27 @@ __device__ __forceinline__ int return_map_dev(const double *F, double *cp, doubl
 #pragma unroll
         for (int k = 0; k < D * D; ++k) sn2 += s[k] * s[k];
         const double sn = sqrt(sn2);
-        const double fpre = sn - SQ23_D * hard_k(m, alpha);
+        const double fpre = sn - SQ23_D * hard_k<LAW>(m, alpha);
         if (fpre > 0.0) {
             const double mue = (tr / D) * m.mu;
-            double x = 0.0, lo = 0.0, hi = sn / (2.0 * mue);
+            // plasticity.py:118 Newton-bisection.  One hardening evaluation
+            // per iterate; when the loop stops on the tolerance the residual
+            // of the final x is the one just computed (same x), so only an
+            // exhausted loop re-evaluates it.
+            double x = 0.0, lo = 0.0, hi = sn / (2.0 * mue), gf = 0.0;
+            bool conv = false;
             for (int it = 0; it < m.max_iter; ++it) {
                 const double at = alpha + SQ23_D * x;
-                const double g = sn - 2.0 * mue * x - SQ23_D * hard_k(m, at);
-                if (!(fabs(g) > m.tol)) break;
+                double kp;
+                const double g = sn - 2.0 * mue * x - SQ23_D * hard_k_kp<LAW>(m, at, kp);
+                if (!(fabs(g) > m.tol)) { gf = g; conv = true; break; }
                 if (g > 0.0) lo = x;
                 if (g < 0.0) hi = x;
-                const double gp = -2.0 * mue - (2.0 / 3.0) * hard_kp(m, at);
+                const double gp = -2.0 * mue - (2.0 / 3.0) * kp;
                 const double nw = x - g / gp;
                 x = (nw > lo && nw < hi) ? nw : 0.5 * (lo + hi);
             }
-            const double gf = sn - 2.0 * mue * x - SQ23_D * hard_k(m, alpha + SQ23_D * x);
+            if (!conv) gf = sn - 2.0 * mue * x - SQ23_D * hard_k<LAW>(m, alpha + SQ23_D * x);
             if (fabs(gf) > m.tol) return 2;
             const double dg = x > 0.0 ? x : 0.0;
             const double scale = 1.0 - 2.0 * mue * dg / sn;
@@ -232,7 +251,7 @@ struct SolidArgs {
 };
 
 // return map + T = P B for one particle (shared by the fused and split paths)
-template <int D>
+template <int D, int LAW = -1>
 __device__ __forceinline__ void solid_stress_point(const SolidArgs &A, int64_t i, const double *F,
                                                           const double *Bm) {
     const int64_t n = A.n;
@@ -245,7 +264,7 @@ __device__ __forceinline__ void solid_stress_point(const SolidArgs &A, int64_t i
         alpha = A.alpha[i];
     }
     double P[D * D];
-    const int rc = return_map_dev<D>(F, cp, alpha, A.mat, P);
+    const int rc = return_map_dev<D, LAW>(F, cp, alpha, A.mat, P);
     if (rc) {
         const unsigned long long id = (unsigned long long)A.perm[i];
         if (rc == 1) atomicMin(&c->err_inv, id);
@@ -380,8 +399,8 @@ __global__ void __launch_bounds__(256) k_solid_stress(SolidArgs A) {
 }
 
 // element-wise second half of the split stress kernel: return map + T
-template <int D>
-__global__ void __launch_bounds__(256) k_solid_rmap(SolidArgs A) {
+template <int D, int LAW>
+__global__ void __launch_bounds__(256, 2) k_solid_rmap(SolidArgs A) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= A.n) return;
     if (A.ctrl->done) return;
@@ -393,7 +412,7 @@ __global__ void __launch_bounds__(256) k_solid_rmap(SolidArgs A) {
         Bm[k] = A.B[(int64_t)k * n + i];
         F[k] = A.F[(int64_t)k * n + i];
     }
-    solid_stress_point<D>(A, i, F, Bm);
+    solid_stress_point<D, LAW>(A, i, F, Bm);
 }
 
 template <int D>

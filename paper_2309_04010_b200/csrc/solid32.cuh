@@ -206,8 +206,8 @@ __global__ void __launch_bounds__(256) k32_stress_csr(Solid32Args A) {
 
 // k_solid_rmap in fp32 storage: F = I + H, C_p^-1 = I + Hc, the return map
 // in fp64, T~ = V0 P B stored in fp32
-template <int D>
-__global__ void __launch_bounds__(256) k32_rmap(Solid32Args A) {
+template <int D, int LAW>
+__global__ void __launch_bounds__(256, 2) k32_rmap(Solid32Args A) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= A.n) return;
     Ctrl *c = A.ctrl;
@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(256) k32_rmap(Solid32Args A) {
         alpha = (double)A.alpha[i];
     }
     double P[D * D];
-    const int rc = return_map_dev<D>(F, cp, alpha, A.mat, P);
+    const int rc = return_map_dev<D, LAW>(F, cp, alpha, A.mat, P);
     if (rc) {
         const unsigned long long id = (unsigned long long)A.perm[i];
         if (rc == 1) atomicMin(&c->err_inv, id);

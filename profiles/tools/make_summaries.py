@@ -1,6 +1,6 @@
 """Summarise ncu output into the files bench.py and DESIGN.md cite.
 
-    python profiles/make_summaries.py LAUNCHES_CSV FULL_RAW_CSV TAG
+    python profiles/tools/make_summaries.py LAUNCHES_CSV FULL_RAW_CSV TAG
 
 LAUNCHES_CSV: `ncu --metrics gpu__time_duration.sum --csv --log-file` of a
 bench command (per-launch, cold-cache, serialised: compare SHARES only).
@@ -17,11 +17,14 @@ import json
 import os
 import sys
 
-HERE = os.path.dirname(os.path.abspath(__file__))
+HERE = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))  # profiles/
 
-CLASS_OF = {"k_solid_stress": "stress", "k_solid_stress_csr": "stress", "k_solid_rmap": "stress",
+CLASS_OF = {"k32_stress_csr": "stress32", "k32_rmap": "stress32", "k32_accel_csr": "accel32",
+            "k32_kick_drift": "kick_drift32", "k32_vmax": "reduce32",
+            "k_solid_stress": "stress", "k_solid_stress_csr": "stress", "k_solid_rmap": "stress",
             "k_solid_accel": "accel", "k_solid_accel_csr": "accel",
             "k_sweep_tiled": "sweep", "k_sweep_flow": "sweep",
+            "k_sweep_tiled32": "sweep32", "k_sweep_flow32": "sweep32",
             "k_solid_kick_drift": "kick_drift", "k_solid_vmax": "reduce", "k_ctrl": "reduce"}
 KEY = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
        "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
@@ -42,7 +45,10 @@ SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
 
 
 def short(name):
-    return name.split("(")[0].replace("void ", "").replace("mtsph::", "").split("<")[0].strip()
+    base = name.split("(")[0].replace("void ", "").replace("mtsph::", "")
+    s = base.split("<")[0].strip()
+    # the fp32 instantiation of the shared sweep kernels
+    return s + "32" if s.startswith("k_sweep") and "float" in base else s
 
 
 def launches(path):
