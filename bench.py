@@ -147,6 +147,71 @@ def algorithmic_bytes(d, nnz_pp, pairs_pp, groups_pp, sweep="tiled", w=8):
     }
 
 
+def outer_bytes(d, nnz_pp):
+    """Compulsory HBM bytes per particle of one outer diffusion step
+    (PorousProblem.advance_slow: prep, flux, mass, prep, flux, post,
+    flux-rate; fp64).  Gathered neighbour fields count once per particle,
+    the CSR index 4 B per entry and pass.  See DESIGN.md §4."""
+    w, dd = 8, d * d
+    xv, vec, ten = w * (d + 1), w * d, w * dd
+    idx = 4 * nnz_pp
+    prep_a = ten + w + xv + ten + 4 * w + ten      # F, m_l, X|V0, B -> volc sat coeff J, A
+    flux = xv + 2 * w + ten + w + idx + vec         # X|V0, sat, volc, A, coeff -> q
+    mass = xv + ten + vec + w + 2 * w + 1 + idx     # X|V0, A, q, volc, m_l r/w, flags
+    prep = ten + w + xv + 4 * w
+    post = w + xv + w + 1 + w + 2 * vec + vec + 4 * w + 2 * vec   # -> pres mix 1/mix rho_l, M, v_l
+    frate = xv + ten + 2 * vec + w + idx + vec
+    return prep_a + flux + mass + prep + flux + post + frate
+
+
+def membrane_leg(args):
+    """Outer-loop diffusion + porous inner relaxation on the reference's 3D
+    porous film (fsi_3d) widened to ~10 M particles (north star item 4)."""
+    from paper_2309_04010_b200.config import resolve
+    from paper_2309_04010_b200.scenarios import build_problem, make_policy
+    side = args.membrane_side
+    params = resolve({"scenario": "fsi_3d", "length": side, "breadth": side,
+                      "damping_sweep": "tiled"}).params
+    t0 = time.perf_counter()
+    prob = build_problem(params, sweep="tiled")
+    setup_s = time.perf_counter() - t0
+    pol = make_policy(params, prob.h_min)
+    dev, n = prob.dev, prob.lattice.n
+    d = prob.lattice.pos.shape[1]
+    k_out = max(3, min(args.steps, 10))
+    k_in = max(args.steps, 4)
+    for _ in range(args.warmup):
+        dev.advance_slow(pol.dt_outer, 0.0)
+        dev.relax(pol.eta, pol.cfl, -1.0, pol.dt_outer, max_inner=k_in, min_inner=k_in)
+    outer_ms = []
+    t0 = time.perf_counter()
+    for k in range(k_out):
+        dev.advance_slow(pol.dt_outer, (k + 1) * pol.dt_outer)
+        outer_ms.append(dev.outer_ms())
+    outer_wall = (time.perf_counter() - t0) / k_out
+    t0 = time.perf_counter()
+    r = dev.relax(pol.eta, pol.cfl, -1.0, pol.dt_outer, max_inner=k_in, min_inner=k_in)
+    inner_s = time.perf_counter() - t0
+    ms = float(np.mean(outer_ms))
+    nnz_pp = dev.sizes()["nnz"] / n
+    model = outer_bytes(d, nnz_pp)
+    peak, _ = load_peaks()
+    out = {"workload": f"fsi_3d porous film {side:g} x {side:g} x {params['thickness']:g} m, "
+                       f"anisotropy {params['anisotropy']:g} ({n} particles), tiled sweep, fp64",
+           "particles": n, "setup_s": setup_s,
+           "inner": {"value": n * int(r.n_inner) / inner_s, "unit": "particle-steps/s",
+                     "ms_per_step": 1e3 * inner_s / max(int(r.n_inner), 1),
+                     "timing": "wall clock around the device loop (graph chunks)"},
+           "outer_diffusion": {"value": n / (ms / 1e3), "unit": "particle-steps/s",
+                               "ms_per_step": ms, "wall_ms_per_step": 1e3 * outer_wall,
+                               "timing": "CUDA events around the 7 kernels of advance_slow"}}
+    gbs = model * n / (ms / 1e3) / 1e9
+    out["outer_diffusion"].update({"bytes_per_particle": model, "achieved_gbs": gbs,
+                                   "frac_of_hbm_peak": gbs / peak,
+                                   "neighbours_per_particle": nnz_pp})
+    return out
+
+
 def build_solid(params, sweep):
     from paper_2309_04010_b200 import lattices
     from paper_2309_04010_b200.device import DeviceSolid
@@ -266,6 +331,9 @@ def run_ours(args):
         "gpu_launches": launches,
         "clocks": clk,
     }
+    if not args.no_membrane and world == 1:
+        del dev
+        line["membrane"] = membrane_leg(args)
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(params, args, budget_s=args.cpu_budget)
     if rank == 0:
@@ -384,6 +452,9 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-fp32", action="store_true", help="skip the fp32 variant")
+    ap.add_argument("--no-membrane", action="store_true", help="skip the porous membrane leg")
+    ap.add_argument("--membrane-side", type=float, default=0.14,
+                    help="fsi_3d film edge (m); 0.14 gives ~10 M particles")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

@@ -98,6 +98,8 @@ SIGNATURES = {
     "mtsph_solid_launches": (c_int, [c_vp, c_vp]),
     "mtsph_solid_sizes": (c_int, [c_vp, c_vp]),
     "mtsph_solid_set_precision": (c_int, [c_vp, c_int]),
+    "mtsph_porous_outer_ms": (c_int, [c_vp, c_vp]),
+    "mtsph_porous_sizes": (c_int, [c_vp, c_vp]),
     "mtsph_solid_precision": (c_int, [c_vp, c_vp]),
     "mtsph_porous_create": (c_int, [c_vp, c_vp]),
     "mtsph_porous_destroy": (c_int, [c_vp]),

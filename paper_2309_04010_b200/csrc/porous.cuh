@@ -12,15 +12,23 @@
 //   k_por_fluxrate  advected-momentum rate -sum V_b (vq_a+vq_b).(A_a gradW) (:574)
 // Inner step = PorousProblem.relax_step (scenarios.py:278):
 //   k_por_kick1     M += dt/2 rate, clamps, v_s, x += dt v_s
-//   k_por_stress    SELL gather dF/dt, F += dt dF/dt, Almansi mixture
+//   k_por_stress    gather dF/dt, F += dt dF/dt, Almansi mixture
 //                   stress, nominal stress, T = Pm B                   (_accel.py:240)
-//   k_por_accel     SELL gather of (T_a + T_b).gradW + flux rate, kick,
+//   k_por_accel     gather of (T_a + T_b).gradW + flux rate, kick,
 //                   energy-density / |a| partials
 //   sweep           damping with mixture masses
 //   k_por_post_step momentum rebuild, |v|max partial
+//
+// Every neighbour gather is row-parallel (gather_csr.cuh): kPorLanes lanes
+// per particle walk its sorted CSR row with stride kPorLanes, the partial
+// sums are combined by a fixed xor-shuffle tree, and lane 0 of the group
+// runs the particle's epilogue.  A block covers 256 particles in kPorLanes
+// rounds, so grids and per-block partials are those of one thread per
+// particle.
 #pragma once
 
 #include "damping.cuh"
+#include "gather_csr.cuh"
 #include "solid.cuh"
 
 namespace mtsph {
@@ -41,8 +49,8 @@ struct PorousArgs {
     double *T;
     const double *B;
     const uint8_t *flags;
-    const int64_t *slice_ptr;
-    const int32_t *slice_w, *nbr;
+    const int64_t *indptr;   // CSR rows (sorted)
+    const int32_t *csr;
     const int64_t *perm;
     double *part;
     int nblk;
@@ -50,6 +58,16 @@ struct PorousArgs {
     KSpec ks;
     PorMat m;
 };
+
+constexpr int kPorLanes = 4;
+
+// particle of round `it` for this lane, its lane within the group
+#define POR_ROWS_BEGIN                                                              \
+    const int sub = threadIdx.x % kPorLanes;                                         \
+    for (int it = 0; it < kPorLanes; ++it) {                                         \
+        const int64_t i = (int64_t)blockIdx.x * 256 + it * (256 / kPorLanes) + threadIdx.x / kPorLanes; \
+        const bool act = i < n;
+#define POR_ROWS_END }
 
 template <int D>
 __global__ void __launch_bounds__(256) k_por_prep(PorousArgs A, int with_amap) {
@@ -78,68 +96,70 @@ __global__ void __launch_bounds__(256) k_por_prep(PorousArgs A, int with_amap) {
     }
 }
 
+// q_a = D rho_l,a sum_b V_b (s_a - s_b) A_a gradW: A_a is per particle, so
+// the gather sums sum_b V_b (s_a - s_b) gradW and A_a is applied once
 template <int D>
 __global__ void __launch_bounds__(256) k_por_flux(PorousArgs A) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= A.n) return;
     const int64_t n = A.n;
-    double xa[3], am[D * D], acc[D];
-    xget<D>(A.XV[i], xa);
-#pragma unroll
-    for (int k = 0; k < D * D; ++k) am[k] = A.amap[(int64_t)k * n + i];
+    POR_ROWS_BEGIN
+    double acc[D];
 #pragma unroll
     for (int k = 0; k < D; ++k) acc[k] = 0.0;
-    const double sa = A.sat[i];
-    const int64_t base = A.slice_ptr[i >> 5] + (i & 31);
-    const int w = A.slice_w[i >> 5];
-    for (int m = 0; m < w; ++m) {
-        const int32_t b = __ldg(A.nbr + base + (int64_t)m * 32);
-        const double4 xvb = ldg4(A.XV + b);
-        double xb[3], rel[D], g[D];
-        xget<D>(xvb, xb);
+    if (act) {
+        double xa[3];
+        xget<D>(ldg4(A.XV + i), xa);
+        const double sa = A.sat[i];
+        const int64_t k1 = A.indptr[i + 1];
+        for (int64_t k = A.indptr[i] + sub; k < k1; k += kPorLanes) {
+            const int32_t b = __ldg(A.csr + k);
+            const double4 xvb = ldg4(A.XV + b);
+            double xb[3], rel[D], g[D];
+            xget<D>(xvb, xb);
 #pragma unroll
-        for (int k = 0; k < D; ++k) rel[k] = xb[k] - xa[k];
-        grad_w<D>(rel, A.ks, g);
-        const double wgt = A.volc[b] * (sa - A.sat[b]);
+            for (int q = 0; q < D; ++q) rel[q] = xb[q] - xa[q];
+            grad_w<D>(rel, A.ks, g);
+            const double wgt = A.volc[b] * (sa - A.sat[b]);
+#pragma unroll
+            for (int c = 0; c < D; ++c) acc[c] += wgt * g[c];
+        }
+    }
+    group_sum<kPorLanes>(acc);
+    if (act && sub == 0) {
+        const double cf = A.coeff[i];
 #pragma unroll
         for (int r = 0; r < D; ++r) {
             double s = 0.0;
 #pragma unroll
-            for (int c = 0; c < D; ++c) s += am[r * D + c] * g[c];
-            acc[r] += wgt * s;
+            for (int c = 0; c < D; ++c) s += A.amap[(int64_t)(r * D + c) * n + i] * acc[c];
+            A.q[(int64_t)r * n + i] = s * cf;
         }
     }
-    const double cf = A.coeff[i];
-#pragma unroll
-    for (int r = 0; r < D; ++r) A.q[(int64_t)r * n + i] = acc[r] * cf;
+    POR_ROWS_END
 }
 
 // mass update + clamp + contact/evaporation; partial[0][blk] = clamp count
 template <int D>
 __global__ void __launch_bounds__(256) k_por_mass(PorousArgs A, double dt, int contact_on, double evap_factor) {
     __shared__ double sh[32];
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t n = A.n;
     double clamped = 0.0;
-    if (i < n) {
+    POR_ROWS_BEGIN
+    double rate[1] = {0.0};
+    if (act) {
         double xa[3], ama[D * D], qa[D];
-        xget<D>(A.XV[i], xa);
+        xget<D>(ldg4(A.XV + i), xa);
 #pragma unroll
         for (int k = 0; k < D * D; ++k) ama[k] = A.amap[(int64_t)k * n + i];
 #pragma unroll
         for (int k = 0; k < D; ++k) qa[k] = A.q[(int64_t)k * n + i];
-        const double va = A.volc[i];
-        double rate = 0.0;
-        const int64_t base = A.slice_ptr[i >> 5] + (i & 31);
-        const int w = A.slice_w[i >> 5];
-        for (int m = 0; m < w; ++m) {
-            const int32_t b = __ldg(A.nbr + base + (int64_t)m * 32);
-            if (b == i) continue;
+        const int64_t k1 = A.indptr[i + 1];
+        for (int64_t k = A.indptr[i] + sub; k < k1; k += kPorLanes) {
+            const int32_t b = __ldg(A.csr + k);
             const double4 xvb = ldg4(A.XV + b);
             double xb[3], rel[D], g[D];
             xget<D>(xvb, xb);
 #pragma unroll
-            for (int k = 0; k < D; ++k) rel[k] = xb[k] - xa[k];
+            for (int q = 0; q < D; ++q) rel[q] = xb[q] - xa[q];
             grad_w<D>(rel, A.ks, g);
             double acc = 0.0;
 #pragma unroll
@@ -149,11 +169,15 @@ __global__ void __launch_bounds__(256) k_por_mass(PorousArgs A, double dt, int c
                 for (int c = 0; c < D; ++c) s += 0.5 * (ama[r * D + c] + A.amap[(int64_t)(r * D + c) * n + b]) * g[c];
                 acc += (qa[r] + A.q[(int64_t)r * n + b]) * s;
             }
-            rate -= va * A.volc[b] * acc;
+            rate[0] -= A.volc[b] * acc;
         }
-        double mass = A.mass_l[i] + dt * rate;
+    }
+    group_sum<kPorLanes>(rate);
+    if (act && sub == 0) {
+        const double va = A.volc[i];
+        double mass = A.mass_l[i] + dt * (va * rate[0]);
         const double cap = A.m.porosity * A.m.rho_l0 * va;
-        if (mass < 0.0 || mass > cap) clamped = 1.0;
+        if (mass < 0.0 || mass > cap) clamped += 1.0;
         mass = fmin(fmax(mass, 0.0), cap);
         if (contact_on) {
             if (A.flags[i] & PF_CONTACT) mass = A.m.porosity * A.m.rho_l0 * va;
@@ -162,6 +186,7 @@ __global__ void __launch_bounds__(256) k_por_mass(PorousArgs A, double dt, int c
         }
         A.mass_l[i] = mass;
     }
+    POR_ROWS_END
     const double s = block_sum<256>(clamped, sh);
     if (threadIdx.x == 0) A.part[blockIdx.x] = s;
 }
@@ -225,48 +250,53 @@ __global__ void __launch_bounds__(256) k_por_post(PorousArgs A) {
 
 template <int D>
 __global__ void __launch_bounds__(256) k_por_fluxrate(PorousArgs A) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= A.n) return;
     const int64_t n = A.n;
-    double xa[3], am[D * D], vqa[D * D], acc[D];
-    xget<D>(A.XV[i], xa);
-#pragma unroll
-    for (int k = 0; k < D * D; ++k) am[k] = -A.amap[(int64_t)k * n + i];
-#pragma unroll
-    for (int r = 0; r < D; ++r)
-#pragma unroll
-        for (int c = 0; c < D; ++c) vqa[r * D + c] = A.vl[(int64_t)r * n + i] * A.q[(int64_t)c * n + i];
+    POR_ROWS_BEGIN
+    double acc[D];
 #pragma unroll
     for (int k = 0; k < D; ++k) acc[k] = 0.0;
-    const int64_t base = A.slice_ptr[i >> 5] + (i & 31);
-    const int w = A.slice_w[i >> 5];
-    for (int m = 0; m < w; ++m) {
-        const int32_t b = __ldg(A.nbr + base + (int64_t)m * 32);
-        const double4 xvb = ldg4(A.XV + b);
-        double xb[3], rel[D], g0[D], g[D];
-        xget<D>(xvb, xb);
+    if (act) {
+        double xa[3], am[D * D], vqa[D * D];
+        xget<D>(ldg4(A.XV + i), xa);
 #pragma unroll
-        for (int k = 0; k < D; ++k) rel[k] = xb[k] - xa[k];
-        grad_w<D>(rel, A.ks, g0);
+        for (int k = 0; k < D * D; ++k) am[k] = -A.amap[(int64_t)k * n + i];
 #pragma unroll
-        for (int r = 0; r < D; ++r) {
-            double s = 0.0;
+        for (int r = 0; r < D; ++r)
 #pragma unroll
-            for (int c = 0; c < D; ++c) s += am[r * D + c] * g0[c];
-            g[r] = s;
-        }
-        const double vb = A.volc[b];
+            for (int c = 0; c < D; ++c) vqa[r * D + c] = A.vl[(int64_t)r * n + i] * A.q[(int64_t)c * n + i];
+        const int64_t k1 = A.indptr[i + 1];
+        for (int64_t k = A.indptr[i] + sub; k < k1; k += kPorLanes) {
+            const int32_t b = __ldg(A.csr + k);
+            const double4 xvb = ldg4(A.XV + b);
+            double xb[3], rel[D], g0[D], g[D];
+            xget<D>(xvb, xb);
 #pragma unroll
-        for (int r = 0; r < D; ++r) {
-            double s = 0.0;
+            for (int q = 0; q < D; ++q) rel[q] = xb[q] - xa[q];
+            grad_w<D>(rel, A.ks, g0);
 #pragma unroll
-            for (int c = 0; c < D; ++c)
-                s += (vqa[r * D + c] + A.vl[(int64_t)r * n + b] * A.q[(int64_t)c * n + b]) * g[c];
-            acc[r] += vb * s;
+            for (int r = 0; r < D; ++r) {
+                double s = 0.0;
+#pragma unroll
+                for (int c = 0; c < D; ++c) s += am[r * D + c] * g0[c];
+                g[r] = s;
+            }
+            const double vb = A.volc[b];
+#pragma unroll
+            for (int r = 0; r < D; ++r) {
+                double s = 0.0;
+#pragma unroll
+                for (int c = 0; c < D; ++c)
+                    s += (vqa[r * D + c] + A.vl[(int64_t)r * n + b] * A.q[(int64_t)c * n + b]) * g[c];
+                acc[r] += vb * s;
+            }
         }
     }
+    group_sum<kPorLanes>(acc);
+    if (act && sub == 0) {
 #pragma unroll
-    for (int r = 0; r < D; ++r) A.frate[(int64_t)r * n + i] = acc[r];
+        for (int r = 0; r < D; ++r) A.frate[(int64_t)r * n + i] = acc[r];
+    }
+    POR_ROWS_END
 }
 
 // ---------------------------------------------------------- inner step
@@ -297,40 +327,12 @@ __global__ void __launch_bounds__(256) k_por_kick1(PorousArgs A) {
     reinterpret_cast<V_t *>(A.V)[i] = w;
 }
 
+// F update, Almansi mixture stress, nominal stress, T = Pm B (lane 0 of
+// the particle's group)
 template <int D>
-__global__ void __launch_bounds__(256) k_por_stress(PorousArgs A) {
-    using V_t = typename VT<D>::T;
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= A.n) return;
+__device__ __forceinline__ void por_stress_point(const PorousArgs &A, int64_t i, const double *acc, double dt) {
     Ctrl *c = A.ctrl;
-    if (c->done) return;
-    const double dt = c->dt;
     const int64_t n = A.n;
-    const V_t *V = reinterpret_cast<const V_t *>(A.V);
-    double xa[3], va[3], acc[D * D];
-    xget<D>(A.XV[i], xa);
-    vget(V[i], va);
-#pragma unroll
-    for (int k = 0; k < D * D; ++k) acc[k] = 0.0;
-    const int64_t base = A.slice_ptr[i >> 5] + (i & 31);
-    const int w = A.slice_w[i >> 5];
-    for (int m = 0; m < w; ++m) {
-        const int32_t b = __ldg(A.nbr + base + (int64_t)m * 32);
-        const double4 xvb = ldg4(A.XV + b);
-        double xb[3], vb[3], rel[D], g[D];
-        xget<D>(xvb, xb);
-        vget(V[b], vb);
-#pragma unroll
-        for (int k = 0; k < D; ++k) rel[k] = xb[k] - xa[k];
-        grad_w<D>(rel, A.ks, g);
-        const double volb = volof<D>(xvb);
-#pragma unroll
-        for (int r = 0; r < D; ++r) {
-            const double dv = volb * (vb[r] - va[r]);
-#pragma unroll
-            for (int cc = 0; cc < D; ++cc) acc[r * D + cc] += dv * g[cc];
-        }
-    }
     double Bm[D * D], F[D * D], L[D * D];
 #pragma unroll
     for (int k = 0; k < D * D; ++k) {
@@ -381,48 +383,98 @@ __global__ void __launch_bounds__(256) k_por_stress(PorousArgs A) {
 }
 
 template <int D>
+__global__ void __launch_bounds__(256) k_por_stress(PorousArgs A) {
+    using V_t = typename VT<D>::T;
+    Ctrl *c = A.ctrl;
+    if (c->done) return;
+    const double dt = c->dt;
+    const int64_t n = A.n;
+    const V_t *V = reinterpret_cast<const V_t *>(A.V);
+    POR_ROWS_BEGIN
+    double acc[D * D];
+#pragma unroll
+    for (int k = 0; k < D * D; ++k) acc[k] = 0.0;
+    if (act) {
+        double xa[3], va[3];
+        xget<D>(ldg4(A.XV + i), xa);
+        vget(vldg(V + i), va);
+        const int64_t k1 = A.indptr[i + 1];
+        for (int64_t k = A.indptr[i] + sub; k < k1; k += kPorLanes) {
+            const int32_t b = __ldg(A.csr + k);
+            const double4 xvb = ldg4(A.XV + b);
+            double xb[3], vb[3], rel[D], g[D];
+            xget<D>(xvb, xb);
+            vget(vldg(V + b), vb);
+#pragma unroll
+            for (int q = 0; q < D; ++q) rel[q] = xb[q] - xa[q];
+            grad_w<D>(rel, A.ks, g);
+            const double volb = volof<D>(xvb);
+#pragma unroll
+            for (int r = 0; r < D; ++r) {
+                const double dv = volb * (vb[r] - va[r]);
+#pragma unroll
+                for (int cc = 0; cc < D; ++cc) acc[r * D + cc] += dv * g[cc];
+            }
+        }
+    }
+    group_sum<kPorLanes>(acc);
+    if (act && sub == 0) por_stress_point<D>(A, i, acc, dt);
+    POR_ROWS_END
+}
+
+
+template <int D>
 __global__ void __launch_bounds__(256) k_por_accel(PorousArgs A) {
     using V_t = typename VT<D>::T;
     __shared__ double sh[32];
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const Ctrl *c = A.ctrl;
     if (c->done) return;
     const int64_t n = A.n;
+    const double dt = c->dt;
     double ek = 0.0, a2m = 0.0;
-    if (i < n) {
-        const double dt = c->dt;
-        double xa[3], Ta[D * D], acc[D];
-        xget<D>(A.XV[i], xa);
-        tload<D>(A.T, A.n, i, Ta);
+    POR_ROWS_BEGIN
+    // sum_b V_b (T_a + T_b) gradW = sum_b V_b T_b gradW + T_a sum_b V_b gradW
+    double acc[D + D];
 #pragma unroll
-        for (int k = 0; k < D; ++k) acc[k] = 0.0;
-        const int64_t base = A.slice_ptr[i >> 5] + (i & 31);
-        const int w = A.slice_w[i >> 5];
-        for (int m = 0; m < w; ++m) {
-            const int32_t b = __ldg(A.nbr + base + (int64_t)m * 32);
+    for (int k = 0; k < 2 * D; ++k) acc[k] = 0.0;
+    if (act) {
+        double xa[3];
+        xget<D>(ldg4(A.XV + i), xa);
+        const int64_t k1 = A.indptr[i + 1];
+        for (int64_t k = A.indptr[i] + sub; k < k1; k += kPorLanes) {
+            const int32_t b = __ldg(A.csr + k);
             const double4 xvb = ldg4(A.XV + b);
             double xb[3], Tb[D * D], rel[D], g[D];
             xget<D>(xvb, xb);
             tload<D>(A.T, A.n, b, Tb);
 #pragma unroll
-            for (int k = 0; k < D; ++k) rel[k] = xb[k] - xa[k];
+            for (int q = 0; q < D; ++q) rel[q] = xb[q] - xa[q];
             grad_w<D>(rel, A.ks, g);
             const double volb = volof<D>(xvb);
 #pragma unroll
             for (int r = 0; r < D; ++r) {
                 double s = 0.0;
 #pragma unroll
-                for (int cc = 0; cc < D; ++cc) s += (Ta[r * D + cc] + Tb[r * D + cc]) * g[cc];
+                for (int cc = 0; cc < D; ++cc) s += Tb[r * D + cc] * g[cc];
                 acc[r] += volb * s;
+                acc[D + r] += volb * g[r];
             }
         }
+    }
+    group_sum<kPorLanes>(acc);
+    if (act && sub == 0) {
+        double Ta[D * D];
+        tload<D>(A.T, A.n, i, Ta);
         const bool movable = A.flags[i] & PF_MOVABLE;
         const double rho = A.m.rho_s0 / A.J[i] + A.rho_lf[i];
-        const double rmix = A.mix[i] / volof<D>(A.XV[i]);
+        const double rmix = A.mix[i] / volof<D>(ldg4(A.XV + i));
         double v[3] = {0, 0, 0}, v2 = 0.0, aa = 0.0;
 #pragma unroll
         for (int k = 0; k < D; ++k) {
-            const double rt = acc[k] + A.frate[(int64_t)k * n + i];
+            double ta = 0.0;
+#pragma unroll
+            for (int cc = 0; cc < D; ++cc) ta += Ta[k * D + cc] * acc[D + cc];
+            const double rt = acc[k] + ta + A.frate[(int64_t)k * n + i];
             A.rate[(int64_t)k * n + i] = rt;
             const double q = A.q[(int64_t)k * n + i];
             double M = A.M[(int64_t)k * n + i] + 0.5 * dt * rt;
@@ -436,10 +488,11 @@ __global__ void __launch_bounds__(256) k_por_accel(PorousArgs A) {
         vset(w2, v);
         reinterpret_cast<V_t *>(A.V)[i] = w2;
         if (movable) {
-            ek = A.mix[i] * v2;
-            a2m = aa / (rmix * rmix);
+            ek += A.mix[i] * v2;
+            a2m = fmax(a2m, aa / (rmix * rmix));
         }
     }
+    POR_ROWS_END
     const double se = block_sum<256>(ek, sh);
     const double sa = block_max<256>(a2m, sh);
     if (threadIdx.x == 0) {

@@ -22,7 +22,9 @@ struct mtsph_porous {
     int per_step_launches = 0;
     cudaGraphExec_t graphs[3] = {nullptr, nullptr, nullptr};
     int graph_steps[3] = {4, 32, 128};
+    cudaEvent_t ev_outer[2] = {nullptr, nullptr};   // brackets the last advance_slow
     ~mtsph_porous() {
+        for (auto e : ev_outer) if (e) cudaEventDestroy(e);
         for (auto &g : graphs) if (g) cudaGraphExecDestroy(g);
         if (hc) cudaFreeHost(hc);
         if (s) cudaStreamDestroy(s);
@@ -33,8 +35,8 @@ struct mtsph_porous {
         A.x = x.p; A.F = F.p; A.M = M.p; A.q = q.p; A.vl = vl.p; A.rate = rate.p; A.frate = frate.p;
         A.mass_l = mass_l.p; A.sat = sat.p; A.pres = pres.p; A.J = J.p; A.rho_lf = rho_lf.p;
         A.mix = mix.p; A.inv_mix = inv_mix.p; A.volc = volc.p; A.coeff = coeff.p; A.amap = amap.p;
-        A.mrate = mrate.p; A.T = T.p; A.B = nb.B.p; A.flags = flags.p; A.slice_ptr = nb.slice_ptr.p;
-        A.slice_w = nb.slice_w.p; A.nbr = nb.nbr.p; A.perm = nb.perm.p; A.part = part.p; A.nblk = nblk;
+        A.mrate = mrate.p; A.T = T.p; A.B = nb.B.p; A.flags = flags.p; A.indptr = nb.indptr.p;
+        A.csr = nb.csr.p; A.perm = nb.perm.p; A.part = part.p; A.nblk = nblk;
         A.ctrl = ctrl.p; A.ks = nb.ks; A.m = m;
         return A;
     }
@@ -184,6 +186,9 @@ template <int D> static int64_t porous_advance(mtsph_porous *P, double dt, doubl
     PorousArgs A = P->args();
     const unsigned nb = blocks_for(P->n);
     cudaStream_t s = P->s;
+    if (!P->ev_outer[0])
+        for (auto &e : P->ev_outer) MT_CUDA(cudaEventCreate(&e));
+    MT_CUDA(cudaEventRecord(P->ev_outer[0], s));
     k_por_prep<D><<<nb, 256, 0, s>>>(A, 1);
     k_por_flux<D><<<nb, 256, 0, s>>>(A);
     const int contact_on = t <= P->contact_time * (1.0 + 1e-12) ? 1 : 0;
@@ -194,6 +199,7 @@ template <int D> static int64_t porous_advance(mtsph_porous *P, double dt, doubl
     k_por_post<D><<<nb, 256, 0, s>>>(A);
     k_por_fluxrate<D><<<nb, 256, 0, s>>>(A);
     MT_LAUNCH_CHECK();
+    MT_CUDA(cudaEventRecord(P->ev_outer[1], s));
     P->launches += 7;
     std::vector<double> part(P->nblk);
     P->part.download(part.data(), P->nblk, s);
@@ -211,6 +217,24 @@ extern "C" mtsph_status mtsph_porous_advance_slow(mtsph_porous *P, double dt_out
     P->push_ctrl();
     *clamped = P->d == 2 ? porous_advance<2>(P, dt_outer, t) : porous_advance<3>(P, dt_outer, t);
     check_porous_errors(P);
+    API_END
+}
+
+extern "C" mtsph_status mtsph_porous_sizes(const mtsph_porous *P, int64_t out[4]) {
+    const NbhDev &nb = P->nb;
+    out[0] = nb.nnz;
+    out[1] = nb.sweep == 3 ? P->tiled.npairs : nb.npairs;
+    out[2] = nb.sweep == 3 ? P->tiled.npairs : nb.ngroups;
+    out[3] = nb.sweep == 3 ? (int64_t)P->tiled.colour_ptr.size() - 1 : 0;
+    return MTSPH_OK;
+}
+
+extern "C" mtsph_status mtsph_porous_outer_ms(const mtsph_porous *P, double *ms) {
+    API_BEGIN
+    if (!P->ev_outer[0]) throw Error(MTSPH_ERR_ARG, "no outer step has run");
+    float f = 0.f;
+    MT_CUDA(cudaEventElapsedTime(&f, P->ev_outer[0], P->ev_outer[1]));
+    *ms = f;
     API_END
 }
 

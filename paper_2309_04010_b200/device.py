@@ -293,6 +293,18 @@ class DevicePorous:
                                                   ctypes.byref(v)))
         return v.value
 
+    def sizes(self):
+        out = np.zeros(4, np.int64)
+        check(self._lib.mtsph_porous_sizes(self._h, ptr(out)))
+        return {"nnz": int(out[0]), "npairs": int(out[1]), "ngroups": int(out[2]),
+                "phases": int(out[3])}
+
+    def outer_ms(self):
+        """Device ms of the kernels of the last advance_slow (CUDA events)."""
+        v = ctypes.c_double()
+        check(self._lib.mtsph_porous_outer_ms(self._h, ctypes.byref(v)))
+        return v.value
+
     def stable_dt(self, cfl):
         v = ctypes.c_double()
         check(self._lib.mtsph_porous_stable_dt(self._h, float(cfl), ctypes.byref(v)))
