@@ -14,7 +14,9 @@ import numpy as np
 from . import errors
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmtsph_b200.so")
+# MTSPH_LIB: an alternative build of the same library (tuning variants,
+# e.g. a different compile-time sweep ring depth); default the in-tree one
+LIB_PATH = os.environ.get("MTSPH_LIB") or os.path.join(HERE, "libmtsph_b200.so")
 
 c_i64 = ctypes.c_int64
 c_dbl = ctypes.c_double

@@ -539,7 +539,10 @@ inline void build_tiled(const NbhDev &nb, int sh, TiledSched &t, cudaStream_t s)
             int col = 0;
             for (int k = d - 1; k >= 0; --k) { bc[k] = cc[k] >> lg[k]; col = col * P[k] + (int)(bc[k] % P[k]); }
             T.colour = col;
-            // halo ranges: cells of the block grown by one, z-y-x order
+            // halo ranges: cells of the block grown by one, z-y-x order.  The
+            // block owns the pairs (a, b), a < b, with a in it, so b >= lo:
+            // a ring cell that lies wholly before the block in the Morton
+            // order holds no partner and is left out (about half the ring)
             int local = 0;
             const int nz = d == 3 ? ext[2] + 2 : 1;
             for (int oz = 0; oz < nz; ++oz)
@@ -552,6 +555,7 @@ inline void build_tiled(const NbhDev &nb, int sh, TiledSched &t, cudaStream_t s)
                         if (!ok) continue;
                         int64_t a, e;
                         if (!cell_range(encode(q, d), a, e)) continue;
+                        if (e <= lo) continue;
                         T.ranges.push_back(make_int2((int)a, local));
                         local += (int)(e - a);
                     }
@@ -797,6 +801,12 @@ inline void build_tiled_auto(const NbhDev &nb, TiledSched &t, cudaStream_t s, in
             tiled_smem_bytes(t, d, 4)));
         t.flow_grid32 = sms * per;
     }
+    if (const char *e = std::getenv("MTSPH_VERBOSE"); e && e[0] == '1')
+        std::fprintf(stderr,
+                     "[mtsph] tiled sweep: %d Morton bits/block, %lld tasks, max halo %d, max sub-colour %d, "
+                     "%d threads, smem %zu B (fp64) %zu B (fp32), dataflow grid %d / %d, %d stages\n",
+                     t.sh, (long long)t.ntasks, t.max_halo, t.maxsub, t.threads, tiled_smem_bytes(t, d),
+                     tiled_smem_bytes(t, d, 4), t.flow_grid, t.flow_grid32, kSweepStages);
 }
 
 }  // namespace mtsph
