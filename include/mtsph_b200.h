@@ -229,6 +229,22 @@ enum {
     MTSPH_PHASE_VMAX = 5,        /* out[0] = max |v|^2 (owned)                       */
     MTSPH_PHASE_AMAX = 6,        /* out[0] = max |v|^2, out[1] = max |a|^2 (free)    */
 };
+/* Device-controlled multi-rank loop (no host synchronisation per phase):
+ * phase_async only enqueues a phase on the solid's stream (the reductions
+ * stay on the device); rank_partials writes this rank's {sum m v^2,
+ * max |a|^2, max |v|^2, error flag} (owned particles) to 4 doubles of
+ * device memory; the caller all-gathers them over the ranks (NCCL) into
+ * [nranks][4] and control_ranks applies the stopping rule and next step
+ * (stepping.py:369-385, solids.py:433) on the device, identically on every
+ * rank.  mode 0: initial step size (after the AMAX phase), 1: end of an
+ * inner step (after ACCEL ... VMAX).  begin_loop sets the loop parameters
+ * as mtsph_solid_relax does; loop_state reads the control block back.    */
+mtsph_status mtsph_solid_phase_async(mtsph_solid *s, int phase, int arg);
+mtsph_status mtsph_solid_begin_loop(mtsph_solid *s, const mtsph_inner_params *p);
+mtsph_status mtsph_solid_rank_partials(mtsph_solid *s, int mode, double *dev_out4);
+mtsph_status mtsph_solid_control_ranks(mtsph_solid *s, const double *dev_gathered, int nranks,
+                                       int mode);
+mtsph_status mtsph_solid_loop_state(mtsph_solid *s, mtsph_inner_result *r, int *done);
 /* set the step size and viscosity used by the next phases                */
 mtsph_status mtsph_solid_set_step(mtsph_solid *s, double dt, double eta);
 mtsph_status mtsph_solid_phase(mtsph_solid *s, int phase, int arg, double out[2]);

@@ -101,6 +101,11 @@ SIGNATURES = {
     "mtsph_solid_sizes": (c_int, [c_vp, c_vp]),
     "mtsph_solid_set_precision": (c_int, [c_vp, c_int]),
     "mtsph_porous_outer_ms": (c_int, [c_vp, c_vp]),
+    "mtsph_solid_phase_async": (c_int, [c_vp, c_int, c_int]),
+    "mtsph_solid_begin_loop": (c_int, [c_vp, c_vp]),
+    "mtsph_solid_rank_partials": (c_int, [c_vp, c_int, c_vp]),
+    "mtsph_solid_control_ranks": (c_int, [c_vp, c_vp, c_int, c_int]),
+    "mtsph_solid_loop_state": (c_int, [c_vp, c_vp, c_vp]),
     "mtsph_porous_sizes": (c_int, [c_vp, c_vp]),
     "mtsph_solid_precision": (c_int, [c_vp, c_vp]),
     "mtsph_porous_create": (c_int, [c_vp, c_vp]),

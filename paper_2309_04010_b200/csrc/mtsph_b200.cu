@@ -912,6 +912,113 @@ extern "C" mtsph_status mtsph_solid_phase(mtsph_solid *S, int phase, int arg, do
     API_END
 }
 
+// ---- device-controlled multi-rank loop: the phases are only enqueued on
+// the solid's stream (no host synchronisation), the rank reductions go
+// through a device buffer the caller all-gathers (NCCL), and the control
+// kernel applies the stopping rule on the device of every rank.
+
+template <int D> static void solid_phase_async(mtsph_solid *S, int phase, int arg) {
+    SolidArgs A = S->args();
+    const unsigned nb = blocks_for(S->n);
+    cudaStream_t s = S->s;
+    switch (phase) {
+    case MTSPH_PHASE_KICK_DRIFT:
+        k_solid_kick_drift<D><<<nb, 256, 0, s>>>(A);
+        S->launches += 1;
+        break;
+    case MTSPH_PHASE_STRESS:
+        launch_stress_gather<D>(S, A, s);
+        launch_rmap<D>(S, A, s);
+        S->launches += 2;
+        break;
+    case MTSPH_PHASE_ACCEL:
+        launch_accel_gather<D>(S, A, s);
+        S->launches += 1;
+        break;
+    case MTSPH_PHASE_SWEEP: {
+        if (S->nb.sweep != 3) throw Error(MTSPH_ERR_ARG, "sweep phases need the tiled schedule");
+        const int c = arg & 63, dir = arg >= 64 ? -1 : 1;
+        const TiledSched &t = S->tiled;
+        if (c + 1 >= (int)t.colour_ptr.size()) throw Error(MTSPH_ERR_ARG, "colour out of range");
+        const int64_t t0 = t.colour_ptr[c], t1 = t.colour_ptr[c + 1];
+        if (t1 > t0) {
+            k_sweep_tiled<D><<<(unsigned)(t1 - t0), t.threads, tiled_smem_bytes(t, D), s>>>(S->tiled_args(), t0, dir,
+                                                                                           S->ctrl.p);
+            S->launches += 1;
+        }
+        break;
+    }
+    case MTSPH_PHASE_VMAX:
+    case MTSPH_PHASE_AMAX:
+        k_solid_vmax<D><<<nb, 256, 0, s>>>(A, phase == MTSPH_PHASE_AMAX ? 1 : 0);
+        S->launches += 1;
+        break;
+    default:
+        throw Error(MTSPH_ERR_ARG, "unknown phase");
+    }
+    MT_LAUNCH_CHECK();
+}
+
+extern "C" mtsph_status mtsph_solid_phase_async(mtsph_solid *S, int phase, int arg) {
+    API_BEGIN
+    if (S->prec != 64) throw Error(MTSPH_ERR_ARG, "multi-rank phases run in fp64");
+    if (S->d == 2) solid_phase_async<2>(S, phase, arg); else solid_phase_async<3>(S, phase, arg);
+    API_END
+}
+
+extern "C" mtsph_status mtsph_solid_begin_loop(mtsph_solid *S, const mtsph_inner_params *p) {
+    API_BEGIN
+    S->pull_ctrl();
+    Ctrl *c = S->hc;
+    c->eta = p->eta;
+    c->cfl = p->cfl;
+    c->criterion = p->criterion;
+    c->dt_outer = p->dt_outer;
+    c->max_inner = p->max_inner;
+    c->min_inner = p->min_inner < 1 ? 1 : p->min_inner;
+    c->n_inner = 0;
+    c->done = 0;
+    c->cap_hit = 0;
+    c->min_dt = INFINITY;
+    c->err_inv = c->err_rm = ~0ull;
+    S->push_ctrl();
+    API_END
+}
+
+extern "C" mtsph_status mtsph_solid_rank_partials(mtsph_solid *S, int mode, double *dev_out) {
+    API_BEGIN
+    if (mode != CTRL_INIT && mode != CTRL_STEP) throw Error(MTSPH_ERR_ARG, "mode: 0 (initial step) or 1 (step)");
+    k_rank_partials<<<1, 256, 0, S->s>>>(S->ctrl.p, S->part.p, S->nblk, mode, dev_out);
+    MT_LAUNCH_CHECK();
+    S->launches += 1;
+    API_END
+}
+
+extern "C" mtsph_status mtsph_solid_control_ranks(mtsph_solid *S, const double *dev_gathered, int nranks,
+                                                  int mode) {
+    API_BEGIN
+    if (mode != CTRL_INIT && mode != CTRL_STEP) throw Error(MTSPH_ERR_ARG, "mode: 0 (initial step) or 1 (step)");
+    if (nranks < 1) throw Error(MTSPH_ERR_ARG, "nranks must be positive");
+    k_ctrl_ranks<<<1, 32, 0, S->s>>>(S->ctrl.p, dev_gathered, nranks, mode);
+    MT_LAUNCH_CHECK();
+    S->launches += 1;
+    API_END
+}
+
+extern "C" mtsph_status mtsph_solid_loop_state(mtsph_solid *S, mtsph_inner_result *r, int *done) {
+    API_BEGIN
+    S->pull_ctrl();
+    const Ctrl *c = S->hc;
+    *done = c->done;
+    r->n_inner = c->n_inner;
+    r->cap_hit = c->cap_hit;
+    r->ek = c->ek;
+    r->min_dt = c->min_dt;
+    r->last_dt = c->last_dt;
+    check_solid_errors(S);
+    API_END
+}
+
 static void pack_common(mtsph_solid *S, const char *field, int64_t m, const int64_t *ids, double *host,
                         const double *in, bool pack) {
     if (S->prec != 64) throw Error(MTSPH_ERR_ARG, "multi-rank exchanges run in fp64");

@@ -529,20 +529,9 @@ __device__ __forceinline__ double stable_dt(const Ctrl *c, double vmax2, double 
     return c->cfl * dt;
 }
 
-// one block of 256; fixed-order reduction of the per-block partials
-__global__ void __launch_bounds__(256) k_ctrl(Ctrl *c, const double *part, int nblk, int mode) {
-    __shared__ double sh[32];
-    if (mode == CTRL_STEP && c->done) return;
-    double e = 0.0, am = 0.0, vm = 0.0;
-    for (int b = threadIdx.x; b < nblk; b += 256) {
-        if (mode != CTRL_INIT) e += part[b];
-        am = fmax(am, part[nblk + b]);
-        vm = fmax(vm, part[2 * nblk + b]);
-    }
-    const double E = block_sum<256>(e, sh);
-    const double AM = block_max<256>(am, sh);
-    const double VM = block_max<256>(vm, sh);
-    if (threadIdx.x != 0) return;
+// the stopping rule and next step from the reduced E_k sum, |a|max^2 and
+// |v|max^2 (stepping.py:369-385, solids.py:433); one thread
+__device__ __forceinline__ void ctrl_apply(Ctrl *c, double E, double AM, double VM, int mode) {
     c->amax2 = AM;
     c->vmax2 = VM;
     if (mode == CTRL_INIT) {
@@ -564,6 +553,65 @@ __global__ void __launch_bounds__(256) k_ctrl(Ctrl *c, const double *part, int n
     if (conv && c->n_inner >= c->min_inner && c->ramp_left <= 0) { c->done = 1; return; }
     if (c->n_inner >= cap) { c->done = 1; c->cap_hit = 1; return; }
     c->dt = stable_dt(c, VM, AM);
+}
+
+// one block of 256; fixed-order reduction of the per-block partials
+__global__ void __launch_bounds__(256) k_ctrl(Ctrl *c, const double *part, int nblk, int mode) {
+    __shared__ double sh[32];
+    if (mode == CTRL_STEP && c->done) return;
+    double e = 0.0, am = 0.0, vm = 0.0;
+    for (int b = threadIdx.x; b < nblk; b += 256) {
+        if (mode != CTRL_INIT) e += part[b];
+        am = fmax(am, part[nblk + b]);
+        vm = fmax(vm, part[2 * nblk + b]);
+    }
+    const double E = block_sum<256>(e, sh);
+    const double AM = block_max<256>(am, sh);
+    const double VM = block_max<256>(vm, sh);
+    if (threadIdx.x == 0) ctrl_apply(c, E, AM, VM, mode);
+}
+
+// Multi-rank device control.  k_rank_partials reduces this rank's
+// per-block partials (owned particles only) to out[4] = {sum m v^2,
+// max |a|^2, max |v|^2, error flag}; the ranks' quadruples are all-gathered
+// (NCCL) into [nranks][4] and k_ctrl_ranks reduces them in rank order -- the same
+// operations on every rank, so all ranks take identical control decisions
+// without the host.
+__global__ void __launch_bounds__(256) k_rank_partials(const Ctrl *c, const double *part, int nblk, int mode,
+                                                       double *out) {
+    __shared__ double sh[32];
+    if (mode == CTRL_STEP && c->done) return;
+    double e = 0.0, am = 0.0, vm = 0.0;
+    for (int b = threadIdx.x; b < nblk; b += 256) {
+        if (mode != CTRL_INIT) e += part[b];
+        am = fmax(am, part[nblk + b]);
+        vm = fmax(vm, part[2 * nblk + b]);
+    }
+    const double E = block_sum<256>(e, sh);
+    const double AM = block_max<256>(am, sh);
+    const double VM = block_max<256>(vm, sh);
+    if (threadIdx.x == 0) {
+        out[0] = E;
+        out[1] = AM;
+        out[2] = VM;
+        out[3] = (c->err_inv != ~0ull || c->err_rm != ~0ull) ? 1.0 : 0.0;
+    }
+}
+
+// gathered: [nranks][4] = {sum m v^2, max |a|^2, max |v|^2, error flag};
+// an error on any rank stops every rank
+__global__ void k_ctrl_ranks(Ctrl *c, const double *gathered, int nranks, int mode) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (mode == CTRL_STEP && c->done) return;
+    double E = 0.0, AM = 0.0, VM = 0.0, err = 0.0;
+    for (int r = 0; r < nranks; ++r) {
+        E += gathered[4 * r];
+        AM = fmax(AM, gathered[4 * r + 1]);
+        VM = fmax(VM, gathered[4 * r + 2]);
+        err = fmax(err, gathered[4 * r + 3]);
+    }
+    ctrl_apply(c, E, AM, VM, mode);
+    if (err > 0.0) c->done = 1;
 }
 
 // observables (NeckingProblem.measure) as per-block partials

@@ -178,6 +178,45 @@ class DeviceSolid:
         check(self._lib.mtsph_solid_phase(self._h, self.PHASES[name], int(arg), ptr(out)))
         return out
 
+    # -- device-controlled multi-rank loop (no host sync per phase) -------
+    def phase_async(self, name, arg=0):
+        """Enqueue a phase on stream_handle(); reductions stay on the device."""
+        check(self._lib.mtsph_solid_phase_async(self._h, self.PHASES[name], int(arg)))
+
+    def begin_loop(self, eta, cfl, criterion, dt_outer, max_inner=0, min_inner=1):
+        p = _lib.InnerParams(float(eta), float(cfl), float(criterion), float(dt_outer),
+                             int(max_inner), int(min_inner))
+        check(self._lib.mtsph_solid_begin_loop(self._h, ctypes.byref(p)))
+
+    def rank_partials(self, mode, dev_ptr):
+        """This rank's {sum m v^2, max |a|^2, max |v|^2, error} -> 4 doubles
+        at device address dev_ptr (mode 0: initial step, 1: end of step)."""
+        check(self._lib.mtsph_solid_rank_partials(self._h, int(mode), dev_ptr))
+
+    def control_ranks(self, dev_ptr, nranks, mode):
+        """Stopping rule + next step from the gathered [nranks][4] partials."""
+        check(self._lib.mtsph_solid_control_ranks(self._h, dev_ptr, int(nranks), int(mode)))
+
+    def rank_partials_host(self, mode):
+        import torch
+        buf = torch.zeros(4, dtype=torch.float64, device="cuda")
+        self.rank_partials(mode, buf.data_ptr())
+        torch.cuda.ExternalStream(self.stream_handle()).synchronize()
+        return buf.cpu().numpy()
+
+    def control_ranks_host(self, gathered, mode):
+        import torch
+        g = torch.from_numpy(np.ascontiguousarray(gathered, dtype=np.float64).ravel()).cuda()
+        torch.cuda.current_stream().synchronize()
+        self.control_ranks(g.data_ptr(), len(g) // 4, mode)
+        torch.cuda.ExternalStream(self.stream_handle()).synchronize()
+
+    def loop_state(self):
+        r = _lib.InnerResult()
+        done = ctypes.c_int()
+        check(self._lib.mtsph_solid_loop_state(self._h, ctypes.byref(r), ctypes.byref(done)))
+        return bool(done.value), r
+
     def colours(self):
         v = ctypes.c_int()
         check(self._lib.mtsph_solid_colours(self._h, ctypes.byref(v)))

@@ -85,6 +85,23 @@ class LocalGroup:
     def allmax(self, values):
         return float(max(values))
 
+    def control(self, mode):
+        """Device control step of every rank: the ranks' partials are
+        gathered into one device buffer ([nranks][4], rank order) and every
+        rank's control kernel reduces it (the all-gather of TorchGroup)."""
+        import torch
+        w = len(self.devices)
+        if getattr(self, "_gat", None) is None or self._gat.numel() != 4 * w:
+            self._gat = torch.zeros(4 * w, dtype=torch.float64, device="cuda")
+        for r, dev in enumerate(self.devices):
+            dev.rank_partials(mode, self._gat.data_ptr() + 32 * r)
+        for dev in self.devices:
+            torch.cuda.ExternalStream(dev.stream_handle()).synchronize()
+        for dev in self.devices:
+            dev.control_ranks(self._gat.data_ptr(), w, mode)
+        for dev in self.devices:
+            torch.cuda.ExternalStream(dev.stream_handle()).synchronize()
+
 
 class TorchGroup:
     """One rank per process; point-to-point exchanges and reductions through
@@ -132,10 +149,14 @@ class TorchGroup:
         with torch.cuda.stream(self.stream):
             for q, (ids, buf) in sorted(sends.items()):
                 dev.pack_device(field, len(ids), ids.data_ptr(), buf.data_ptr())
-            reqs = [dist.irecv(buf, src=q) for q, (ids, buf) in sorted(recvs.items())]
-            reqs += [dist.isend(buf, dst=q) for q, (ids, buf) in sorted(sends.items())]
-            for r in reqs:
-                r.wait()          # NCCL: the stream waits, the host does not
+            # one NCCL group (ncclGroupStart/End): separate isend/irecv calls
+            # would each block their pair's stream until matched, and two
+            # ranks that both receive first would deadlock
+            ops = [dist.P2POp(dist.irecv, buf, q) for q, (ids, buf) in sorted(recvs.items())]
+            ops += [dist.P2POp(dist.isend, buf, q) for q, (ids, buf) in sorted(sends.items())]
+            if ops:
+                for r in dist.batch_isend_irecv(ops):
+                    r.wait()      # NCCL: the stream waits, the host does not
             for q, (ids, buf) in sorted(recvs.items()):
                 dev.unpack_device(field, len(ids), ids.data_ptr(), buf.data_ptr())
 
@@ -188,6 +209,28 @@ class TorchGroup:
 
     def allmax(self, values):
         return self._reduce(max(values), self.dist.ReduceOp.MAX)
+
+    def control(self, mode):
+        """Device control step: this rank's partials (4 doubles) are
+        all-gathered into [world][4] and the control kernel applies the
+        stopping rule and next step on every rank from the same numbers.
+        NCCL: all on the solid's stream, no host synchronisation.  gloo:
+        host-staged."""
+        torch, dist, dev = self.torch, self.dist, self.devices[0]
+        w = dist.get_world_size()
+        if self.on_device:
+            if getattr(self, "_loc", None) is None:
+                self._loc = torch.zeros(4, dtype=torch.float64, device=self.tdev)
+                self._gat = torch.zeros(4 * w, dtype=torch.float64, device=self.tdev)
+            with torch.cuda.stream(self.stream):
+                dev.rank_partials(mode, self._loc.data_ptr())
+                dist.all_gather_into_tensor(self._gat, self._loc, async_op=True).wait()
+                dev.control_ranks(self._gat.data_ptr(), w, mode)
+            return
+        loc = torch.from_numpy(np.ascontiguousarray(dev.rank_partials_host(mode), dtype=np.float64))
+        out = [torch.zeros(4, dtype=torch.float64) for _ in range(w)]
+        dist.all_gather(out, loc)
+        dev.control_ranks_host(np.concatenate([o.numpy() for o in out]), mode)
 
 
 def stable_dt(h, sound, cfl, vmax2, amax2):
@@ -289,6 +332,55 @@ class DecomposedSolid:
                 if n >= cap:
                     return n, ek, True, min_dt
             dt = stable_dt(self.h, self.sound, cfl, vmax2, amax2)
+
+    # -- device-controlled loop ------------------------------------------
+    def _step_async(self):
+        g = self.group
+        for dev in self.devices:
+            dev.phase_async("kick_drift")
+        g.refresh("vel")
+        for dev in self.devices:
+            dev.phase_async("stress")
+        g.refresh("T")
+        for dev in self.devices:
+            dev.phase_async("accel")
+        g.refresh("vel")
+        nc = self.ncolours
+        for rev in (False, True):
+            for q in range(nc):
+                c = nc - 1 - q if rev else q
+                for dev in self.devices:
+                    dev.phase_async("sweep", c + 64 if rev else c)
+                g.pushback(c)
+                g.refresh("vel")
+        for dev in self.devices:
+            dev.phase_async("vmax")
+        g.control(1)
+
+    def relax_device(self, eta, cfl, criterion, dt_outer, max_inner=0, min_inner=1,
+                     fixed_steps=None, check_every=8):
+        """The inner loop with the control on the device of every rank: the
+        phases and exchanges are enqueued without host synchronisation, the
+        ranks' reductions are all-gathered on the device and each rank's
+        control kernel takes the same decisions (stepping.py:347 rule); the
+        host reads the control block once every `check_every` steps.
+        Returns (n_inner, ek, cap_hit, min_dt) like relax()."""
+        if fixed_steps is not None:
+            criterion, max_inner, min_inner = -1.0, int(fixed_steps), int(fixed_steps)
+        for dev in self.devices:
+            dev.begin_loop(eta, cfl, criterion, dt_outer, max_inner, min_inner)
+            dev.set_ramp(self.end_disp, self.ramp_steps, self.ramp_left)
+            dev.phase_async("amax")
+        self.group.control(0)
+        while True:
+            for _ in range(max(int(check_every), 1)):
+                self._step_async()
+            states = [dev.loop_state() for dev in self.devices]
+            if all(done for done, _ in states):
+                break
+        self.ramp_left = self.devices[0].ramp_left()
+        r = states[0][1]
+        return int(r.n_inner), float(r.ek), bool(r.cap_hit), float(r.min_dt)
 
     def gather(self, field):
         """Owned values of `field` in global particle order (LocalGroup only)."""

@@ -94,6 +94,14 @@ class FakeDevice:
     def unpack(self, field, ids, vals):
         self.v[np.asarray(ids)] = vals
 
+    # device-control double: partials encode the rank, control records input
+    def rank_partials_host(self, mode):
+        r = float(self.rank)
+        return np.array([r + 1.0, 10.0 * r, 100.0 + r, 0.0])
+
+    def control_ranks_host(self, gathered, mode):
+        self.gathered = (np.asarray(gathered).copy(), mode)
+
 
 def _worker(rank, world, port, result_q):
     import torch.distributed as dist
@@ -109,6 +117,7 @@ def _worker(rank, world, port, result_q):
         vals = glob[p.local_ids].copy()
         vals[p.ghost] = -1.0
         dev = FakeDevice(vals, 3)
+        dev.rank = rank
         g = TorchGroup(p, dev, dist)
         g.refresh("vel")
         ok_refresh = bool(np.array_equal(dev.v, glob[p.local_ids]))
@@ -131,7 +140,11 @@ def _worker(rank, world, port, result_q):
         ok_push = bool(np.array_equal(dev.v[mine], expect[mine]))
         s = g.allsum([rank + 1.0])
         m = g.allmax([float(rank)])
-        result_q.put((rank, ok_refresh, ok_push, s, m, int(bump.sum())))
+        # device control: every rank receives all ranks' partials in rank order
+        g.control(1)
+        want = np.concatenate([[r + 1.0, 10.0 * r, 100.0 + r, 0.0] for r in range(world)])
+        ok_ctrl = bool(np.array_equal(dev.gathered[0], want)) and dev.gathered[1] == 1
+        result_q.put((rank, ok_refresh, ok_push, s, m, int(bump.sum()), ok_ctrl))
     finally:
         dist.destroy_process_group()
 
@@ -150,8 +163,9 @@ def test_gloo_two_ranks_exchange():
     for pr in procs:
         pr.join(timeout=60)
     assert [r[0] for r in res] == [0, 1]
-    for rank, ok_refresh, ok_push, s, m, nbump in res:
+    for rank, ok_refresh, ok_push, s, m, nbump, ok_ctrl in res:
         assert ok_refresh, rank
         assert ok_push, rank
+        assert ok_ctrl, rank
         assert s == 3.0 and m == 1.0
     assert sum(r[5] for r in res) > 0

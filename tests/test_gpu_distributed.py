@@ -49,3 +49,97 @@ def test_decomposed_matches_single_domain_tiled(group):
             scale = max(np.max(np.abs(w)), 1e-300)
             err = np.max(np.abs(got - w)) / scale
             assert err <= 1e-13, (nranks, f, err)
+
+
+@pytest.mark.parametrize("group", ["local", "local_device"])
+def test_device_controlled_loop_matches_single_domain(group):
+    """relax_device: phases enqueued without host synchronisation, rank
+    partials gathered on the device, the control kernel of every rank takes
+    the step decisions -- same trajectory as the single domain (fixed steps)
+    and the same stopping step as the host-controlled decomposed loop."""
+    from paper_2309_04010_b200.device import DeviceSolid
+    from paper_2309_04010_b200.distributed import DecomposedSolid
+    p, lat, el, hard = _setup()
+    law, hp = hard.device_params()
+    steps, eta, cfl = 25, p["eta"], p["cfl"]
+    end_disp = 0.02 * p["length"]
+    ref = DeviceSolid(lat.pos, lat.vol, el.density0, lat.constrained, lat.side, lat.mid_mask,
+                      lat.h_axes, el.shear_modulus, el.bulk_modulus, plastic=True,
+                      hardening_law=law, hard=hp, sweep="tiled")
+    ref.set_ramp(end_disp, 10, 10)
+    for _ in range(steps):
+        ref.relax_step(ref.stable_dt(cfl), eta)
+    want = {f: ref.get(f) for f in ("pos", "vel", "F", "alpha")}
+    for nranks in (1, 2, 3):
+        dec = DecomposedSolid(lat, el, hard, nranks, group=group, end_disp_per_outer=end_disp,
+                              ramp_steps=10)
+        dec.advance_slow()
+        n, ek, cap, _ = dec.relax_device(eta, cfl, 0.0, 1.0, fixed_steps=steps, check_every=4)
+        assert n == steps and dec.ramp_left == 0
+        for f, w in want.items():
+            got = dec.gather(f)
+            scale = max(np.max(np.abs(w)), 1e-300)
+            err = np.max(np.abs(got - w)) / scale
+            assert err <= 1e-13, (nranks, f, err)
+    # stopping rule: device-controlled and host-controlled loops agree
+    crit = None
+    for mode in ("host", "device"):
+        dec = DecomposedSolid(lat, el, hard, 2, group=group, end_disp_per_outer=end_disp,
+                              ramp_steps=10)
+        dec.advance_slow()
+        if crit is None:
+            # a criterion the loop reaches after a few dozen steps
+            n0, ek0, _, _ = dec.relax(eta, cfl, 0.0, 1.0, fixed_steps=40)
+            crit = ek0
+            continue
+        n, ek, cap, _ = dec.relax_device(eta, cfl, crit, 1.0, max_inner=400)
+        assert not cap and n <= 40 + 1
+    dec_h = DecomposedSolid(lat, el, hard, 2, group=group, end_disp_per_outer=end_disp,
+                            ramp_steps=10)
+    dec_h.advance_slow()
+    nh, ekh, caph, _ = dec_h.relax(eta, cfl, crit, 1.0, max_inner=400)
+    assert n == nh and not caph
+    assert abs(ek - ekh) <= 1e-12 * abs(ekh)
+
+
+def test_nccl_group_single_rank_device_loop():
+    """TorchGroup over a real NCCL communicator (world size 1 on this GPU):
+    device-resident exchanges (none for one rank) and the NCCL all-gather of
+    the control partials on the solid's stream, against the single domain."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2309_04010_b200.device import DeviceSolid
+    from paper_2309_04010_b200.distributed import DecomposedSolid
+    p, lat, el, hard = _setup()
+    law, hp = hard.device_params()
+    steps, eta, cfl = 20, p["eta"], p["cfl"]
+    end_disp = 0.02 * p["length"]
+    ref = DeviceSolid(lat.pos, lat.vol, el.density0, lat.constrained, lat.side, lat.mid_mask,
+                      lat.h_axes, el.shear_modulus, el.bulk_modulus, plastic=True,
+                      hardening_law=law, hard=hp, sweep="tiled")
+    ref.set_ramp(end_disp, 10, 10)
+    for _ in range(steps):
+        ref.relax_step(ref.stable_dt(cfl), eta)
+    want = {f: ref.get(f) for f in ("pos", "vel", "F")}
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        dec = DecomposedSolid(lat, el, hard, 1, ranks=[0], group="torch", dist=dist,
+                              tensor_device="cuda", end_disp_per_outer=end_disp, ramp_steps=10)
+        dec.advance_slow()
+        n, ek, cap, _ = dec.relax_device(eta, cfl, 0.0, 1.0, fixed_steps=steps, check_every=5)
+        assert n == steps
+        dev = dec.devices[0]
+        for f, w in want.items():
+            got = dev.get(f)
+            scale = max(np.max(np.abs(w)), 1e-300)
+            assert np.max(np.abs(got - w)) <= 1e-13 * scale, f
+    finally:
+        dist.destroy_process_group()
