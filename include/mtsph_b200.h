@@ -52,6 +52,9 @@ const char *mtsph_last_error(void);
 int64_t mtsph_last_error_ids(int64_t *ids, int64_t cap);
 /* number of CUDA devices visible (0 on a CPU-only host) */
 int mtsph_device_count(void);
+/* select the GPU new problems (and their streams) are created on; one
+ * process per GPU calls it with its local rank before creating any      */
+mtsph_status mtsph_set_device(int ordinal);
 
 /* ------------------------------------------------------------------ */
 /* Layer 1: _accel.py drop-ins (host pointers, reference layout)       */

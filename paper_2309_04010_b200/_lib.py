@@ -101,6 +101,7 @@ SIGNATURES = {
     "mtsph_solid_sizes": (c_int, [c_vp, c_vp]),
     "mtsph_solid_set_precision": (c_int, [c_vp, c_int]),
     "mtsph_porous_outer_ms": (c_int, [c_vp, c_vp]),
+    "mtsph_set_device": (c_int, [c_int]),
     "mtsph_solid_phase_async": (c_int, [c_vp, c_int, c_int]),
     "mtsph_solid_begin_loop": (c_int, [c_vp, c_vp]),
     "mtsph_solid_rank_partials": (c_int, [c_vp, c_int, c_vp]),

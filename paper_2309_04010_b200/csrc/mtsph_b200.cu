@@ -58,6 +58,19 @@ extern "C" int mtsph_device_count(void) {
     return c;
 }
 
+// the device this library's runtime places new problems on (one process
+// per GPU: the rank's local device).  The library carries its own CUDA
+// runtime, so torch.cuda.set_device does not select it.
+extern "C" mtsph_status mtsph_set_device(int ordinal) {
+    API_BEGIN
+    const int c = mtsph_device_count();
+    if (ordinal < 0 || ordinal >= c)
+        throw Error(MTSPH_ERR_ARG, "device ordinal " + std::to_string(ordinal) + " out of range (" +
+                                       std::to_string(c) + " devices)");
+    MT_CUDA(cudaSetDevice(ordinal));
+    API_END
+}
+
 static void require_device() {
     if (mtsph_device_count() <= 0) throw Error(MTSPH_ERR_CUDA, "no CUDA device available");
 }

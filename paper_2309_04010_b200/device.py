@@ -36,6 +36,12 @@ def _h3(h_axes):
     return (ctypes.c_double * 3)(*h[:3])
 
 
+def select_device(ordinal):
+    """Place the problems created from now on (and their streams) on GPU
+    `ordinal` -- one process per GPU calls this with its local rank."""
+    check(_lib.load_library().mtsph_set_device(int(ordinal)))
+
+
 class DeviceNeighborhood:
     """Fixed reference neighbourhood built on the GPU."""
 
