@@ -51,17 +51,32 @@ def short(name):
     return s + "32" if s.startswith("k_sweep") and "float" in base else s
 
 
-def launches(path):
+def launch_list(path):
+    """[(kernel, ms, segment)] in launch order; a new segment starts at each
+    neighbourhood build (its first kernel, k_cell_keys), so the solid
+    problem of bench.py is segment 1 and its membrane leg segment 2."""
     rows = [r for r in csv.reader(open(path)) if r]
     hdr_i = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     hdr = rows[hdr_i]
     k, m, u, v = (hdr.index(c) for c in ("Kernel Name", "Metric Name", "Metric Unit", "Metric Value"))
-    per = {}
+    out, seg, prev = [], 0, None
     for r in rows[hdr_i + 1:]:
         if len(r) <= v or r[m] != "gpu__time_duration.sum":
             continue
-        ms = float(r[v].replace(",", "")) * SCALE.get(r[u], 1.0)
-        e = per.setdefault(short(r[k]), {"launches": 0, "total_ms": 0.0})
+        name = short(r[k])
+        if name == "k_cell_keys" and prev != "k_cell_keys":
+            seg += 1
+        prev = name
+        out.append((name, float(r[v].replace(",", "")) * SCALE.get(r[u], 1.0), seg))
+    return out
+
+
+def launches(path, segment=None):
+    per = {}
+    for name, ms, seg in launch_list(path):
+        if segment is not None and seg != segment:
+            continue
+        e = per.setdefault(name, {"launches": 0, "total_ms": 0.0})
         e["launches"] += 1
         e["total_ms"] += ms
     tot = sum(e["total_ms"] for e in per.values())
@@ -102,6 +117,16 @@ def main():
             "note": "ncu gpu__time_duration.sum per launch (cold-cache, serialised, --clock-control none); "
                     "compare shares with bench.py's kernels[*].share, not absolute times",
             "kernels": launches(lpath)}
+    # shares within each step variant (the launch list also holds setup,
+    # the fp32 variant and the membrane leg)
+    solid = launches(lpath, segment=1)
+    for tagv, keep in (("fp64_step_shares", lambda k: k.startswith("k_solid_") or k in ("k_sweep_flow", "k_ctrl")),
+                       ("fp32_step_shares", lambda k: k.startswith("k32_") or k == "k_sweep_flow32")):
+        sel = {k: v["total_ms"] for k, v in solid.items()
+               if keep(k) and k not in ("k_solid_gsum", "k_solid_measure", "k32_static", "k32_narrow",
+                                        "k32_convert")}
+        tot = sum(sel.values())
+        summ[tagv] = {k: round(v / tot, 4) for k, v in sorted(sel.items(), key=lambda kv: -kv[1])} if tot else {}
     json.dump(summ, open(os.path.join(HERE, f"launches_{tag}_summary.json"), "w"), indent=1)
     recs = full(fpath)
     traffic = {}
