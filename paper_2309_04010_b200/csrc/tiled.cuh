@@ -34,11 +34,19 @@
 namespace mtsph {
 
 // depth of the cp.async ring that stages sub-colour chunks (prefetch
-// distance kSweepStages - 1 sub-colours)
-#ifndef MTSPH_SWEEP_STAGES
-#define MTSPH_SWEEP_STAGES 4  // measured: 6 and 8 are slower (10M, 3D)
+// distance stages - 1 sub-colours), per real type.  Measured at 10M (3D,
+// 512 threads, sub-colours <= 448 pairs): fp64 3 stages 6.58 ms (2 CTAs/SM
+// fit; 4 stages: 1 CTA/SM, 8.47 ms), fp32 4 stages 3.94 ms (3 CTAs/SM;
+// 3 stages 4.31 ms)
+#ifndef MTSPH_SWEEP_STAGES64
+#define MTSPH_SWEEP_STAGES64 3
 #endif
-constexpr int kSweepStages = MTSPH_SWEEP_STAGES;
+#ifndef MTSPH_SWEEP_STAGES32
+#define MTSPH_SWEEP_STAGES32 4
+#endif
+template <class R> struct SweepStages { static constexpr int n = MTSPH_SWEEP_STAGES64; };
+template <> struct SweepStages<float> { static constexpr int n = MTSPH_SWEEP_STAGES32; };
+inline int sweep_stages(int rsize) { return rsize == 8 ? MTSPH_SWEEP_STAGES64 : MTSPH_SWEEP_STAGES32; }
 
 struct TiledSched {
     int sh = 0;                      // low Morton bits per block (build_tiled)
@@ -146,6 +154,7 @@ __device__ __forceinline__ void sweep_task(const TiledArgsT<R> &T, int64_t task,
     const int64_t p0 = T.pair_off[task];
     const int64_t s0 = T.sub_off[task];
     const int nsub = (int)(T.sub_off[task + 1] - s0) - 1;
+    constexpr int kSweepStages = SweepStages<R>::n;
     // ring of kSweepStages (pair, coefficient) chunks staged with cp.async
     R *bd = reinterpret_cast<R *>(hal.end(H));                                 // ring of coefficients
     uint32_t *bp = reinterpret_cast<uint32_t *>(bd + kSweepStages * T.maxsub);  // ring of pairs
@@ -324,7 +333,7 @@ __global__ void __launch_bounds__(1024) k_sweep_flow(TiledArgsT<R> T, TiledFlow 
 inline size_t tiled_smem_bytes(const TiledSched &t, int d, int rsize = 8) {
     (void)d;
     return (size_t)((((t.max_ranges + 1) & ~1) + 3) / 4 * 4) * 8 + (size_t)t.max_halo * 4 * rsize +
-           (size_t)t.maxsub * kSweepStages * (4 + rsize) + (size_t)(t.max_nsub + 1) * 4;
+           (size_t)t.maxsub * sweep_stages(rsize) * (4 + rsize) + (size_t)(t.max_nsub + 1) * 4;
 }
 
 template <int D, class R = double>
@@ -471,6 +480,12 @@ inline void build_tiled(const NbhDev &nb, int sh, TiledSched &t, cudaStream_t s)
     using namespace tiled_detail;
     const int64_t n = nb.n;
     const int d = nb.d;
+    // largest sub-colour in pairs (multiple of 8; 0 = none).  3D default
+    // 448 = the pair lanes of a 512-thread CTA: with it the fp64 block fits
+    // two CTAs per SM (sweep 7.35 -> 6.58 ms at 10M) and fp32 three (4.22
+    // -> 3.94 ms); 2D keeps whole sub-colours.  MTSPH_SWEEP_SUBCAP overrides.
+    int subcap = d == 3 ? 448 : 0;
+    if (const char *e = std::getenv("MTSPH_SWEEP_SUBCAP")) subcap = std::max(0, std::atoi(e)) & ~7;
     int lg[3] = {0, 0, 0}, ext[3] = {1, 1, 1}, P[3] = {1, 1, 1};
     for (int i = 0; i < sh; ++i) ++lg[i % d];
     // block colour period per axis: same-coloured blocks must be two cells
@@ -611,8 +626,16 @@ inline void build_tiled(const NbhDev &nb, int sh, TiledSched &t, cudaStream_t s)
             T.pd.clear();
             T.sub.assign(1, 0);
             for (int c = 0; c < ncol; ++c) {
+                const int32_t start = (int32_t)T.pairs.size();
                 bank_order(sp.data() + cnt[c], sd.data() + cnt[c], cnt[c + 1] - cnt[c], T.pairs, T.pd);
-                T.sub.push_back((int32_t)T.pairs.size());
+                // optional cap on the sub-colour size (whole quarter-warp
+                // groups): a subset of a matching is a matching, so a split
+                // sub-colour is still independent pairs; smaller ring slots
+                // let more CTAs share an SM
+                const int32_t end = (int32_t)T.pairs.size();
+                if (subcap > 0)
+                    for (int32_t b = start + subcap; b < end; b += subcap) T.sub.push_back(b);
+                T.sub.push_back(end);
             }
         }
     };
@@ -773,6 +796,10 @@ inline void build_tiled_auto(const NbhDev &nb, TiledSched &t, cudaStream_t s, in
         // 1024) and the small fallback blocks (4^2 in 2D: 256 beat 1024 5x)
         const double avg = t.nsub_total ? (double)t.pairs.n / (double)t.nsub_total : 0.0;
         th = std::min(1024, std::max(128, ((int)(2.0 * avg) + 63) & ~63));
+        // 3D: 512 threads (64 staging + 448 pair lanes, the sub-colour cap):
+        // two (fp64) / three (fp32) CTAs per SM; measured 1024 threads with
+        // uncapped sub-colours 7.35 / 4.22 ms, 512 with the cap 6.58 / 3.94
+        if (d == 3 && !std::getenv("MTSPH_SWEEP_SUBCAP")) th = 512;
     }
     t.threads = th;
     // the attribute is per function, shared by every problem instance: allow
@@ -804,9 +831,9 @@ inline void build_tiled_auto(const NbhDev &nb, TiledSched &t, cudaStream_t s, in
     if (const char *e = std::getenv("MTSPH_VERBOSE"); e && e[0] == '1')
         std::fprintf(stderr,
                      "[mtsph] tiled sweep: %d Morton bits/block, %lld tasks, max halo %d, max sub-colour %d, "
-                     "%d threads, smem %zu B (fp64) %zu B (fp32), dataflow grid %d / %d, %d stages\n",
+                     "%d threads, smem %zu B (fp64) %zu B (fp32), dataflow grid %d / %d, %d stages (fp64)\n",
                      t.sh, (long long)t.ntasks, t.max_halo, t.maxsub, t.threads, tiled_smem_bytes(t, d),
-                     tiled_smem_bytes(t, d, 4), t.flow_grid, t.flow_grid32, kSweepStages);
+                     tiled_smem_bytes(t, d, 4), t.flow_grid, t.flow_grid32, sweep_stages(8));
 }
 
 }  // namespace mtsph

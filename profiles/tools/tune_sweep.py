@@ -1,7 +1,8 @@
 """Tuning sweep (GPU): tiled-sweep block size (MTSPH_TILE_BITS) and CTA
 size (MTSPH_TILE_THREADS); one solid per setting, both precisions.
 
-    python profiles/tools/tune_sweep.py --cases 6:0,7:0,7:1024
+    python profiles/tools/tune_sweep.py --cases 6:0,7:0,7:1024,6:512:448
+    (bits:threads[:sub-colour cap]; MTSPH_LIB selects a tuning build)
 """
 import argparse
 import json
@@ -25,8 +26,9 @@ def main():
     params = bench.workload_params(args)
     eta, cfl = params["eta"], params["cfl"]
     for case in args.cases.split(","):
-        bits, th = case.split(":")
+        bits, th, *rest = case.split(":")
         os.environ["MTSPH_TILE_BITS"] = bits
+        os.environ["MTSPH_SWEEP_SUBCAP"] = rest[0] if rest else "0"
         if th != "0":
             os.environ["MTSPH_TILE_THREADS"] = th
         else:
@@ -41,7 +43,7 @@ def main():
             dev.run_steps(args.steps, eta, cfl)
             t = dev.run_steps(args.steps, eta, cfl)
             out = {k: round(v / args.steps, 3) for k, v in t.items() if k.endswith("_ms")}
-            print(f"bits={bits} threads={th} fp{bits_p}", json.dumps(out), "setup", round(setup, 1),
+            print(f"case={case} fp{bits_p}", json.dumps(out), "setup", round(setup, 1),
                   flush=True)
         del dev
 
