@@ -28,7 +28,10 @@ def main():
     for case in args.cases.split(","):
         bits, th, *rest = case.split(":")
         os.environ["MTSPH_TILE_BITS"] = bits
-        os.environ["MTSPH_SWEEP_SUBCAP"] = rest[0] if rest else "0"
+        if rest:
+            os.environ["MTSPH_SWEEP_SUBCAP"] = rest[0]
+        else:
+            os.environ.pop("MTSPH_SWEEP_SUBCAP", None)   # the schedule's default
         if th != "0":
             os.environ["MTSPH_TILE_THREADS"] = th
         else:
