@@ -100,19 +100,21 @@ __device__ __forceinline__ int return_map_dev(const double *F, double *cp, doubl
 #pragma unroll
         for (int k = 0; k < D * D; ++k) sn2 += s[k] * s[k];
         const double sn = sqrt(sn2);
-        const double fpre = sn - SQ23_D * hard_k<LAW>(m, alpha);
+        double kp;
+        double kat = hard_k_kp<LAW>(m, alpha, kp);   // K, K' at the first iterate (x = 0)
+        const double fpre = sn - SQ23_D * kat;
         if (fpre > 0.0) {
             const double mue = (tr / D) * m.mu;
             // plasticity.py:118 Newton-bisection.  One hardening evaluation
-            // per iterate; when the loop stops on the tolerance the residual
-            // of the final x is the one just computed (same x), so only an
-            // exhausted loop re-evaluates it.
+            // per iterate (the first is the trial-state one above); when the
+            // loop stops on the tolerance the residual of the final x is the
+            // one just computed (same x), so only an exhausted loop
+            // re-evaluates it.
             double x = 0.0, lo = 0.0, hi = sn / (2.0 * mue), gf = 0.0;
             bool conv = false;
             for (int it = 0; it < m.max_iter; ++it) {
-                const double at = alpha + SQ23_D * x;
-                double kp;
-                const double g = sn - 2.0 * mue * x - SQ23_D * hard_k_kp<LAW>(m, at, kp);
+                if (it > 0) kat = hard_k_kp<LAW>(m, alpha + SQ23_D * x, kp);
+                const double g = sn - 2.0 * mue * x - SQ23_D * kat;
                 if (!(fabs(g) > m.tol)) { gf = g; conv = true; break; }
                 if (g > 0.0) lo = x;
                 if (g < 0.0) hi = x;
@@ -277,7 +279,14 @@ __device__ __forceinline__ void solid_stress_point(const SolidArgs &A, int64_t i
         A.alpha[i] = alpha;
     }
     double Tm[D * D];
-    mm<D>(P, Bm, Tm);
+    if (Bm) {
+        mm<D>(P, Bm, Tm);
+    } else {  // B read only now: not live across the return map (registers)
+        double Bl[D * D];
+#pragma unroll
+        for (int k = 0; k < D * D; ++k) Bl[k] = A.B[(int64_t)k * n + i];
+        mm<D>(P, Bl, Tm);
+    }
     const double4 xv = ldg4(A.XV + i);
     const double vol = volof<D>(xv);
 #pragma unroll
@@ -406,13 +415,10 @@ __global__ void __launch_bounds__(256, 2) k_solid_rmap(SolidArgs A) {
     if (A.ctrl->done) return;
     if (A.flags[i] & FL_GHOST) return;
     const int64_t n = A.n;
-    double Bm[D * D], F[D * D];
+    double F[D * D];
 #pragma unroll
-    for (int k = 0; k < D * D; ++k) {
-        Bm[k] = A.B[(int64_t)k * n + i];
-        F[k] = A.F[(int64_t)k * n + i];
-    }
-    solid_stress_point<D, LAW>(A, i, F, Bm);
+    for (int k = 0; k < D * D; ++k) F[k] = A.F[(int64_t)k * n + i];
+    solid_stress_point<D, LAW>(A, i, F, nullptr);
 }
 
 template <int D>

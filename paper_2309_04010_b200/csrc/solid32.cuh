@@ -213,13 +213,12 @@ __global__ void __launch_bounds__(256, 2) k32_rmap(Solid32Args A) {
     Ctrl *c = A.ctrl;
     if (c->done) return;
     const int64_t n = A.n;
-    double F[D * D], cp[D * D], Bm[D * D];
+    double F[D * D], cp[D * D];
 #pragma unroll
     for (int k = 0; k < D * D; ++k) {
         const double id = (k % (D + 1) == 0) ? 1.0 : 0.0;
         F[k] = id + (double)A.H[(int64_t)k * n + i];
         cp[k] = id;
-        Bm[k] = (double)A.B[(int64_t)k * n + i];
     }
     double alpha = 0.0;
     if (A.mat.plastic) {
@@ -240,7 +239,9 @@ __global__ void __launch_bounds__(256, 2) k32_rmap(Solid32Args A) {
         for (int k = 0; k < D * D; ++k) A.Hc[(int64_t)k * n + i] = (float)(cp[k] - ((k % (D + 1) == 0) ? 1.0 : 0.0));
         A.alpha[i] = (float)alpha;
     }
-    double Tm[D * D];
+    double Tm[D * D], Bm[D * D];
+#pragma unroll
+    for (int k = 0; k < D * D; ++k) Bm[k] = (double)A.B[(int64_t)k * n + i];
     mm<D>(P, Bm, Tm);
     const float4 xv = A.XV[i];
     const double vol = (double)volof32<D>(xv);

@@ -124,6 +124,9 @@ class TorchGroup:
         self.on_device = str(tensor_device).startswith("cuda")
         if self.on_device:
             self._setup_device_lists()
+            # a global collective first, so the grouped send/recv of the
+            # first exchange is never the first collective of the group
+            dist.barrier()
 
     # -- device-resident exchange -------------------------------------
     def _setup_device_lists(self):
