@@ -184,3 +184,41 @@ def test_parallel_sweeps_reach_the_serial_equilibrium(raw):
     print("equilibrium differences vs serial:", diffs)
     for sweep, (du, df) in diffs.items():
         assert du < tol and df < tol, (sweep, du, df, tol)
+
+
+@pytest.mark.parametrize("bits", [64, 32])
+def test_full_size_bench_workload_damping_invariants(bits):
+    """The benchmark's own 10 M-particle bar (BASELINE configs[2] geometry):
+    size-independent properties of the tiled damping sweep at full size --
+    with the elastic forces switched off (moduli 1e-30) the inner step is
+    kick/drift + damping, so total momentum is conserved to rounding and the
+    kinetic energy never increases, in fp64 and in the fp32 variant."""
+    from paper_2309_04010_b200 import lattices
+    from paper_2309_04010_b200.config import resolve
+    from paper_2309_04010_b200.device import DeviceSolid
+    p = resolve({"scenario": "bar_3d", "damping_sweep": "tiled"}).params
+    lat = lattices.build_lattice(p)
+    n = lat.n
+    assert n == 10_000_000
+    free = np.zeros(n, bool)
+    s = DeviceSolid(lat.pos, lat.vol, 1.0, free, np.zeros(n, np.int8), None, lat.h_axes,
+                    1e-30, 1e-30, plastic=False, sweep="tiled")
+    rng = np.random.default_rng(11)
+    vel = rng.normal(size=(n, 3))
+    s.set("vel", vel)
+    s.set_precision(bits)
+    mass = lat.vol * 1.0
+    v0 = s.get("vel")
+    p0 = mass @ v0
+    e0 = 0.5 * float(np.sum(mass[:, None] * v0 * v0))
+    first = e0
+    for _ in range(3):
+        s.relax_step(1e-9, 1e7)
+        v = s.get("vel")
+        e = 0.5 * float(np.sum(mass[:, None] * v * v))
+        assert e <= e0 * (1 + (1e-12 if bits == 64 else 1e-6))
+        e0 = e
+    scale = float(np.sum(mass * np.linalg.norm(vel, axis=1)))
+    tol = 1e-12 if bits == 64 else 1e-6
+    assert np.max(np.abs(mass @ s.get("vel") - p0)) <= tol * scale
+    assert e0 < 0.5 * first
