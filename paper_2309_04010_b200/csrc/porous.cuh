@@ -12,9 +12,11 @@
 //   k_por_fluxrate  advected-momentum rate -sum V_b (vq_a+vq_b).(A_a gradW) (:574)
 // Inner step = PorousProblem.relax_step (scenarios.py:278):
 //   k_por_kick1     M += dt/2 rate, clamps, v_s, x += dt v_s
-//   k_por_stress    gather dF/dt, F += dt dF/dt, Almansi mixture
-//                   stress, nominal stress, T = Pm B                   (_accel.py:240)
-//   k_por_accel     gather of (T_a + T_b).gradW + flux rate, kick,
+//   k_por_stress    gather dF/dt, F += dt dF/dt                        (_accel.py:240)
+//   k_por_constit   J, Almansi mixture stress, nominal stress, divergence
+//                   record T~ = V0 Pm B (solid.cuh DS layout, X included)
+//   k_por_accel     gather of sum_b T~_b.gradW + T_a sum_b V_b gradW
+//                   (static, G) + flux rate, kick,
 //                   energy-density / |a| partials
 //   sweep           damping with mixture masses
 //   k_por_post_step momentum rebuild, |v|max partial
@@ -46,7 +48,8 @@ struct PorousArgs {
     double *x, *F, *M, *q, *vl, *rate, *frate;
     double *mass_l, *sat, *pres, *J, *rho_lf, *mix, *inv_mix;
     double *volc, *coeff, *amap, *mrate;
-    double *T;
+    double *T;                      // divergence records (DS<D>)
+    const double *G;                // [d][n] sum_b V_b gradW_ab (static)
     const double *B;
     const uint8_t *flags;
     const int64_t *indptr;   // CSR rows (sorted)
@@ -327,24 +330,19 @@ __global__ void __launch_bounds__(256) k_por_kick1(PorousArgs A) {
     reinterpret_cast<V_t *>(A.V)[i] = w;
 }
 
-// F update, Almansi mixture stress, nominal stress, T = Pm B (lane 0 of
-// the particle's group)
+// J, Almansi mixture stress, nominal stress (porous.py / _accel.py:240),
+// divergence record T~ = V0 Pm B with the reference position; element-wise,
+// after the gather kernel updated F
 template <int D>
-__device__ __forceinline__ void por_stress_point(const PorousArgs &A, int64_t i, const double *acc, double dt) {
+__global__ void __launch_bounds__(256) k_por_constit(PorousArgs A) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= A.n) return;
     Ctrl *c = A.ctrl;
+    if (c->done) return;
     const int64_t n = A.n;
-    double Bm[D * D], F[D * D], L[D * D];
+    double F[D * D];
 #pragma unroll
-    for (int k = 0; k < D * D; ++k) {
-        Bm[k] = A.B[(int64_t)k * n + i];
-        F[k] = A.F[(int64_t)k * n + i];
-    }
-    mm<D>(acc, Bm, L);
-#pragma unroll
-    for (int k = 0; k < D * D; ++k) {
-        F[k] += dt * L[k];
-        A.F[(int64_t)k * n + i] = F[k];
-    }
+    for (int k = 0; k < D * D; ++k) F[k] = A.F[(int64_t)k * n + i];
     const double j = det_d<D>(F);
     A.J[i] = j;
     double Tm[D * D];
@@ -353,7 +351,7 @@ __device__ __forceinline__ void por_stress_point(const PorousArgs &A, int64_t i,
 #pragma unroll
         for (int k = 0; k < D * D; ++k) Tm[k] = 0.0;
     } else {
-        double fi[D * D], e[D * D], sg[D * D], pm[D * D];
+        double fi[D * D], e[D * D], sg[D * D], pm[D * D], Bm[D * D];
         inv_d<D>(F, j, fi);
         double tre = 0.0;
 #pragma unroll
@@ -377,9 +375,39 @@ __device__ __forceinline__ void por_stress_point(const PorousArgs &A, int64_t i,
         mmt<D>(sg, fi, tmp);  // sigma F^-T
 #pragma unroll
         for (int k = 0; k < D * D; ++k) pm[k] = j * tmp[k];
+#pragma unroll
+        for (int k = 0; k < D * D; ++k) Bm[k] = A.B[(int64_t)k * n + i];
         mm<D>(pm, Bm, Tm);
     }
-    tstore<D>(A.T, A.n, i, Tm);
+    const double4 xv = ldg4(A.XV + i);
+    const double vol = volof<D>(xv);
+#pragma unroll
+    for (int k = 0; k < D * D; ++k) Tm[k] *= vol;
+    dstore_raw<D>(A.T, n, i, Tm, xv);
+}
+
+// sum_b V_b gradW_ab per particle (static; once at setup), CSR row order
+template <int D>
+__global__ void __launch_bounds__(256) k_por_gsum(PorousArgs A, double *G) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= A.n) return;
+    double xa[3], s[D];
+    xget<D>(ldg4(A.XV + i), xa);
+#pragma unroll
+    for (int k = 0; k < D; ++k) s[k] = 0.0;
+    for (int64_t k = A.indptr[i]; k < A.indptr[i + 1]; ++k) {
+        const double4 xvb = ldg4(A.XV + A.csr[k]);
+        double xb[3], rel[D], g[D];
+        xget<D>(xvb, xb);
+#pragma unroll
+        for (int q = 0; q < D; ++q) rel[q] = xb[q] - xa[q];
+        grad_w<D>(rel, A.ks, g);
+        const double volb = volof<D>(xvb);
+#pragma unroll
+        for (int q = 0; q < D; ++q) s[q] += volb * g[q];
+    }
+#pragma unroll
+    for (int k = 0; k < D; ++k) G[(int64_t)k * A.n + i] = s[k];
 }
 
 template <int D>
@@ -418,7 +446,14 @@ __global__ void __launch_bounds__(256) k_por_stress(PorousArgs A) {
         }
     }
     group_sum<kPorLanes>(acc);
-    if (act && sub == 0) por_stress_point<D>(A, i, acc, dt);
+    if (act && sub == 0) {  // F += dt (acc B)
+        double Bm[D * D], L[D * D];
+#pragma unroll
+        for (int k = 0; k < D * D; ++k) Bm[k] = A.B[(int64_t)k * n + i];
+        mm<D>(acc, Bm, L);
+#pragma unroll
+        for (int k = 0; k < D * D; ++k) A.F[(int64_t)k * n + i] += dt * L[k];
+    }
     POR_ROWS_END
 }
 
@@ -433,38 +468,37 @@ __global__ void __launch_bounds__(256) k_por_accel(PorousArgs A) {
     const double dt = c->dt;
     double ek = 0.0, a2m = 0.0;
     POR_ROWS_BEGIN
-    // sum_b V_b (T_a + T_b) gradW = sum_b V_b T_b gradW + T_a sum_b V_b gradW
-    double acc[D + D];
+    // sum_b V_b (T_a + T_b) gradW = sum_b T~_b gradW + T_a G_a, with the
+    // divergence record T~_b = V_b T_b (three 256-bit loads per neighbour,
+    // X included) and G_a = sum_b V_b gradW static
+    double acc[D];
 #pragma unroll
-    for (int k = 0; k < 2 * D; ++k) acc[k] = 0.0;
+    for (int k = 0; k < D; ++k) acc[k] = 0.0;
     if (act) {
         double xa[3];
         xget<D>(ldg4(A.XV + i), xa);
         const int64_t k1 = A.indptr[i + 1];
         for (int64_t k = A.indptr[i] + sub; k < k1; k += kPorLanes) {
             const int32_t b = __ldg(A.csr + k);
-            const double4 xvb = ldg4(A.XV + b);
             double xb[3], Tb[D * D], rel[D], g[D];
-            xget<D>(xvb, xb);
-            tload<D>(A.T, A.n, b, Tb);
+            dload<D>(A.T, n, A.XV, b, Tb, xb);
 #pragma unroll
             for (int q = 0; q < D; ++q) rel[q] = xb[q] - xa[q];
             grad_w<D>(rel, A.ks, g);
-            const double volb = volof<D>(xvb);
 #pragma unroll
             for (int r = 0; r < D; ++r) {
                 double s = 0.0;
 #pragma unroll
                 for (int cc = 0; cc < D; ++cc) s += Tb[r * D + cc] * g[cc];
-                acc[r] += volb * s;
-                acc[D + r] += volb * g[r];
+                acc[r] += s;
             }
         }
     }
     group_sum<kPorLanes>(acc);
     if (act && sub == 0) {
-        double Ta[D * D];
-        tload<D>(A.T, A.n, i, Ta);
+        double Ta[D * D], xd[3];
+        dload<D>(A.T, n, A.XV, i, Ta, xd);
+        const double vola = volof<D>(ldg4(A.XV + i));
         const bool movable = A.flags[i] & PF_MOVABLE;
         const double rho = A.m.rho_s0 / A.J[i] + A.rho_lf[i];
         const double rmix = A.mix[i] / volof<D>(ldg4(A.XV + i));
@@ -473,8 +507,8 @@ __global__ void __launch_bounds__(256) k_por_accel(PorousArgs A) {
         for (int k = 0; k < D; ++k) {
             double ta = 0.0;
 #pragma unroll
-            for (int cc = 0; cc < D; ++cc) ta += Ta[k * D + cc] * acc[D + cc];
-            const double rt = acc[k] + ta + A.frate[(int64_t)k * n + i];
+            for (int cc = 0; cc < D; ++cc) ta += Ta[k * D + cc] * A.G[(int64_t)cc * n + i];
+            const double rt = acc[k] + ta / vola + A.frate[(int64_t)k * n + i];
             A.rate[(int64_t)k * n + i] = rt;
             const double q = A.q[(int64_t)k * n + i];
             double M = A.M[(int64_t)k * n + i] + 0.5 * dt * rt;

@@ -9,7 +9,7 @@ struct mtsph_porous {
     cudaStream_t s = nullptr;
     DBuf<unsigned char> V;
     DBuf<double> x, F, M, q, vl, rate, frate, mass_l, sat, pres, J, rho_lf, mix, inv_mix, volc, coeff,
-        amap, mrate, T, part;
+        amap, mrate, T, G, part;
     DBuf<uint8_t> flags;
     DBuf<Ctrl> ctrl;
     DBuf<int64_t> level_ptr;
@@ -35,7 +35,7 @@ struct mtsph_porous {
         A.x = x.p; A.F = F.p; A.M = M.p; A.q = q.p; A.vl = vl.p; A.rate = rate.p; A.frate = frate.p;
         A.mass_l = mass_l.p; A.sat = sat.p; A.pres = pres.p; A.J = J.p; A.rho_lf = rho_lf.p;
         A.mix = mix.p; A.inv_mix = inv_mix.p; A.volc = volc.p; A.coeff = coeff.p; A.amap = amap.p;
-        A.mrate = mrate.p; A.T = T.p; A.B = nb.B.p; A.flags = flags.p; A.indptr = nb.indptr.p;
+        A.mrate = mrate.p; A.T = T.p; A.G = G.p; A.B = nb.B.p; A.flags = flags.p; A.indptr = nb.indptr.p;
         A.csr = nb.csr.p; A.perm = nb.perm.p; A.part = part.p; A.nblk = nblk;
         A.ctrl = ctrl.p; A.ks = nb.ks; A.m = m;
         return A;
@@ -61,9 +61,10 @@ template <int D> static int porous_step(mtsph_porous *P, int mode) {
     const unsigned nb = blocks_for(P->n);
     k_por_kick1<D><<<nb, 256, 0, P->s>>>(A);
     k_por_stress<D><<<nb, 256, 0, P->s>>>(A);
+    k_por_constit<D><<<nb, 256, 0, P->s>>>(A);
     k_por_accel<D><<<nb, 256, 0, P->s>>>(A);
     MT_LAUNCH_CHECK();
-    int l = 3;
+    int l = 4;
     if (P->nb.sweep == 3) {
         TiledArgs T{P->tiled.range_off.p, P->tiled.ranges.p, P->tiled.halo_n.p, P->tiled.pair_off.p,
                     P->tiled.pairs.p, P->tiled.pd.p, P->tiled.sub_off.p, P->tiled.sub.p, P->inv_mix.p, P->V.p,
@@ -145,11 +146,15 @@ extern "C" mtsph_status mtsph_porous_create(const mtsph_porous_desc *dsc, mtsph_
     P->inv_mix.upload(inv.data(), n, P->s);
     P->amap.alloc((size_t)dd * n);
     P->amap.zero(P->s);
-    P->T.alloc((size_t)n * (d == 3 ? 9 : 4));
+    P->T.alloc((size_t)n * (d == 3 ? DS<3>::n : DS<2>::n));
     P->T.zero(P->s);
     P->flags.upload(flags.data(), n, P->s);
     P->nblk = (int)blocks_for(n);
     P->part.alloc((size_t)3 * P->nblk);
+    P->G.alloc((size_t)d * n);  // static sum_b V_b gradW_ab
+    if (d == 2) k_por_gsum<2><<<blocks_for(n), 256, 0, P->s>>>(P->args(), P->G.p);
+    else k_por_gsum<3><<<blocks_for(n), 256, 0, P->s>>>(P->args(), P->G.p);
+    MT_LAUNCH_CHECK();
     P->part.zero(P->s);
     if (P->nb.sweep == 1) P->level_ptr.upload(P->nb.level_ptr_h.data(), P->nb.level_ptr_h.size(), P->s);
     PorMat &m = P->m;
