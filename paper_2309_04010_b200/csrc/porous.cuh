@@ -49,6 +49,13 @@ struct PorousArgs {
     double *mass_l, *sat, *pres, *J, *rho_lf, *mix, *inv_mix;
     double *volc, *coeff, *amap, *mrate;
     double *T;                      // divergence records (DS<D>)
+    // planar gather records of the outer step: plane k of particle b is the
+    // 32 B at (k n + b), so the 4 lanes of a row group (4 consecutive
+    // neighbours) read one 128 B line per plane instead of one sector per
+    // scalar field.  rm (mass update): 3D (A00 A01 A02 A10) (A11 A12 A20 A21)
+    // (A22 q0 q1 q2) (X0 X1 X2 V); 2D (A00 A01 A10 A11) (q0 q1 V 0), X from
+    // XV.  rf (flux rate): (vl0 vl1 vl2|0 V) (q0 q1 q2|0 0), X from XV.
+    double *rm, *rf;
     const double *G;                // [d][n] sum_b V_b gradW_ab (static)
     const double *B;
     const uint8_t *flags;
@@ -63,6 +70,7 @@ struct PorousArgs {
 };
 
 constexpr int kPorLanes = 4;
+template <int D> struct PorRM { static constexpr int planes = D == 3 ? 4 : 2; };
 
 // particle of round `it` for this lane, its lane within the group
 #define POR_ROWS_BEGIN                                                              \
@@ -96,13 +104,24 @@ __global__ void __launch_bounds__(256) k_por_prep(PorousArgs A, int with_amap) {
         mmt<D>(fi, Bm, am);  // F^-1 B^T
 #pragma unroll
         for (int k = 0; k < D * D; ++k) A.amap[(int64_t)k * n + i] = am[k];
+        double4 *rm = reinterpret_cast<double4 *>(A.rm);
+        if (D == 3) {
+            const double4 xv = ldg4(A.XV + i);
+            st4(rm + i, make_double4(am[0], am[1], am[2], am[3]));
+            st4(rm + n + i, make_double4(am[4], am[5], am[6], am[7]));
+            st4(rm + 3 * n + i, make_double4(xv.x, xv.y, xv.z, vol));
+        } else {
+            st4(rm + i, make_double4(am[0], am[1], am[2], am[3]));
+        }
     }
 }
 
 // q_a = D rho_l,a sum_b V_b (s_a - s_b) A_a gradW: A_a is per particle, so
 // the gather sums sum_b V_b (s_a - s_b) gradW and A_a is applied once
+// pack: 1 = write q into the mass-update record (first flux of the outer
+// step), 0 = into the flux-rate record (second)
 template <int D>
-__global__ void __launch_bounds__(256) k_por_flux(PorousArgs A) {
+__global__ void __launch_bounds__(256) k_por_flux(PorousArgs A, int pack) {
     const int64_t n = A.n;
     POR_ROWS_BEGIN
     double acc[D];
@@ -129,12 +148,21 @@ __global__ void __launch_bounds__(256) k_por_flux(PorousArgs A) {
     group_sum<kPorLanes>(acc);
     if (act && sub == 0) {
         const double cf = A.coeff[i];
+        double qv[3] = {0.0, 0.0, 0.0};
 #pragma unroll
         for (int r = 0; r < D; ++r) {
             double s = 0.0;
 #pragma unroll
             for (int c = 0; c < D; ++c) s += A.amap[(int64_t)(r * D + c) * n + i] * acc[c];
-            A.q[(int64_t)r * n + i] = s * cf;
+            qv[r] = s * cf;
+            A.q[(int64_t)r * n + i] = qv[r];
+        }
+        if (pack) {
+            double4 *rm = reinterpret_cast<double4 *>(A.rm);
+            if (D == 3) st4(rm + 2 * n + i, make_double4(A.amap[(int64_t)8 * n + i], qv[0], qv[1], qv[2]));
+            else st4(rm + n + i, make_double4(qv[0], qv[1], A.volc[i], 0.0));
+        } else {
+            st4(reinterpret_cast<double4 *>(A.rf) + n + i, make_double4(qv[0], qv[1], qv[2], 0.0));
         }
     }
     POR_ROWS_END
@@ -156,11 +184,24 @@ __global__ void __launch_bounds__(256) k_por_mass(PorousArgs A, double dt, int c
 #pragma unroll
         for (int k = 0; k < D; ++k) qa[k] = A.q[(int64_t)k * n + i];
         const int64_t k1 = A.indptr[i + 1];
+        const double4 *rm = reinterpret_cast<const double4 *>(A.rm);
         for (int64_t k = A.indptr[i] + sub; k < k1; k += kPorLanes) {
             const int32_t b = __ldg(A.csr + k);
-            const double4 xvb = ldg4(A.XV + b);
-            double xb[3], rel[D], g[D];
-            xget<D>(xvb, xb);
+            // A_b, q_b, V_b (and X_b in 3D) from the planar record
+            double ab[D * D], qb[D], xb[3], vb;
+            const double4 p0 = ldg4(rm + b), p1 = ldg4(rm + n + b);
+            if (D == 3) {
+                const double4 p2 = ldg4(rm + 2 * n + b), p3 = ldg4(rm + 3 * n + b);
+                ab[0] = p0.x; ab[1] = p0.y; ab[2] = p0.z; ab[3] = p0.w;
+                ab[4] = p1.x; ab[5] = p1.y; ab[6] = p1.z; ab[7] = p1.w;
+                ab[8] = p2.x; qb[0] = p2.y; qb[1] = p2.z; qb[2] = p2.w;
+                xb[0] = p3.x; xb[1] = p3.y; xb[2] = p3.z; vb = p3.w;
+            } else {
+                ab[0] = p0.x; ab[1] = p0.y; ab[2] = p0.z; ab[3] = p0.w;
+                qb[0] = p1.x; qb[1] = p1.y; vb = p1.z;
+                xget<D>(ldg4(A.XV + b), xb);
+            }
+            double rel[D], g[D];
 #pragma unroll
             for (int q = 0; q < D; ++q) rel[q] = xb[q] - xa[q];
             grad_w<D>(rel, A.ks, g);
@@ -169,10 +210,10 @@ __global__ void __launch_bounds__(256) k_por_mass(PorousArgs A, double dt, int c
             for (int r = 0; r < D; ++r) {
                 double s = 0.0;
 #pragma unroll
-                for (int c = 0; c < D; ++c) s += 0.5 * (ama[r * D + c] + A.amap[(int64_t)(r * D + c) * n + b]) * g[c];
-                acc += (qa[r] + A.q[(int64_t)r * n + b]) * s;
+                for (int c = 0; c < D; ++c) s += 0.5 * (ama[r * D + c] + ab[r * D + c]) * g[c];
+                acc += (qa[r] + qb[r]) * s;
             }
-            rate[0] -= A.volc[b] * acc;
+            rate[0] -= vb * acc;
         }
     }
     group_sum<kPorLanes>(rate);
@@ -240,34 +281,36 @@ __global__ void __launch_bounds__(256) k_por_post(PorousArgs A) {
         A.M[(int64_t)k * n + i] = M[k];
     }
     split_vel<D>(A, i, j, M, q, vs, vl);
-    double v3[3] = {0, 0, 0};
+    double v3[3] = {0, 0, 0}, l3[3] = {0, 0, 0};
 #pragma unroll
     for (int k = 0; k < D; ++k) {
         v3[k] = vs[k];
+        l3[k] = vl[k];
         A.vl[(int64_t)k * n + i] = vl[k];
     }
+    st4(reinterpret_cast<double4 *>(A.rf) + i, make_double4(l3[0], l3[1], l3[2], A.volc[i]));
     V_t w;
     vset(w, v3);
     V[i] = w;
 }
 
+// -sum_b V_b (vl_a q_a^T + vl_b q_b^T) (A_a gradW) (porous.py:574), with the
+// neighbour loop carrying G = sum_b V_b g and sum_b V_b (q_b . g) vl_b,
+// g = -A_a gradW: the vl_a q_a^T term is applied once after the loop
 template <int D>
-__global__ void __launch_bounds__(256) k_por_fluxrate(PorousArgs A) {
+__global__ void __launch_bounds__(256, 3) k_por_fluxrate(PorousArgs A) {
     const int64_t n = A.n;
     POR_ROWS_BEGIN
-    double acc[D];
+    double acc[2 * D];   // [0, D): sum V_b (q_b.g) vl_b ; [D, 2D): sum V_b g
 #pragma unroll
-    for (int k = 0; k < D; ++k) acc[k] = 0.0;
+    for (int k = 0; k < 2 * D; ++k) acc[k] = 0.0;
     if (act) {
-        double xa[3], am[D * D], vqa[D * D];
+        double xa[3], am[D * D];
         xget<D>(ldg4(A.XV + i), xa);
 #pragma unroll
         for (int k = 0; k < D * D; ++k) am[k] = -A.amap[(int64_t)k * n + i];
-#pragma unroll
-        for (int r = 0; r < D; ++r)
-#pragma unroll
-            for (int c = 0; c < D; ++c) vqa[r * D + c] = A.vl[(int64_t)r * n + i] * A.q[(int64_t)c * n + i];
         const int64_t k1 = A.indptr[i + 1];
+        const double4 *rf = reinterpret_cast<const double4 *>(A.rf);
         for (int64_t k = A.indptr[i] + sub; k < k1; k += kPorLanes) {
             const int32_t b = __ldg(A.csr + k);
             const double4 xvb = ldg4(A.XV + b);
@@ -283,21 +326,30 @@ __global__ void __launch_bounds__(256) k_por_fluxrate(PorousArgs A) {
                 for (int c = 0; c < D; ++c) s += am[r * D + c] * g0[c];
                 g[r] = s;
             }
-            const double vb = A.volc[b];
+            const double4 f0 = ldg4(rf + b), f1 = ldg4(rf + n + b);
+            const double vlb[3] = {f0.x, f0.y, f0.z}, qb[3] = {f1.x, f1.y, f1.z};
+            const double vb = f0.w;
+            double qg = 0.0;
+#pragma unroll
+            for (int c = 0; c < D; ++c) qg += qb[c] * g[c];
+            const double w = vb * qg;
 #pragma unroll
             for (int r = 0; r < D; ++r) {
-                double s = 0.0;
-#pragma unroll
-                for (int c = 0; c < D; ++c)
-                    s += (vqa[r * D + c] + A.vl[(int64_t)r * n + b] * A.q[(int64_t)c * n + b]) * g[c];
-                acc[r] += vb * s;
+                acc[r] += w * vlb[r];
+                acc[D + r] += vb * g[r];
             }
         }
     }
     group_sum<kPorLanes>(acc);
     if (act && sub == 0) {
+        double qa[D], qG = 0.0;
 #pragma unroll
-        for (int r = 0; r < D; ++r) A.frate[(int64_t)r * n + i] = acc[r];
+        for (int c = 0; c < D; ++c) {
+            qa[c] = A.q[(int64_t)c * n + i];
+            qG += qa[c] * acc[D + c];
+        }
+#pragma unroll
+        for (int r = 0; r < D; ++r) A.frate[(int64_t)r * n + i] = A.vl[(int64_t)r * n + i] * qG + acc[r];
     }
     POR_ROWS_END
 }

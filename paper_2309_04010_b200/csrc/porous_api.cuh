@@ -9,7 +9,7 @@ struct mtsph_porous {
     cudaStream_t s = nullptr;
     DBuf<unsigned char> V;
     DBuf<double> x, F, M, q, vl, rate, frate, mass_l, sat, pres, J, rho_lf, mix, inv_mix, volc, coeff,
-        amap, mrate, T, G, part;
+        amap, mrate, T, G, part, rm, rf;
     DBuf<uint8_t> flags;
     DBuf<Ctrl> ctrl;
     DBuf<int64_t> level_ptr;
@@ -35,7 +35,7 @@ struct mtsph_porous {
         A.x = x.p; A.F = F.p; A.M = M.p; A.q = q.p; A.vl = vl.p; A.rate = rate.p; A.frate = frate.p;
         A.mass_l = mass_l.p; A.sat = sat.p; A.pres = pres.p; A.J = J.p; A.rho_lf = rho_lf.p;
         A.mix = mix.p; A.inv_mix = inv_mix.p; A.volc = volc.p; A.coeff = coeff.p; A.amap = amap.p;
-        A.mrate = mrate.p; A.T = T.p; A.G = G.p; A.B = nb.B.p; A.flags = flags.p; A.indptr = nb.indptr.p;
+        A.mrate = mrate.p; A.T = T.p; A.G = G.p; A.rm = rm.p; A.rf = rf.p; A.B = nb.B.p; A.flags = flags.p; A.indptr = nb.indptr.p;
         A.csr = nb.csr.p; A.perm = nb.perm.p; A.part = part.p; A.nblk = nblk;
         A.ctrl = ctrl.p; A.ks = nb.ks; A.m = m;
         return A;
@@ -146,6 +146,8 @@ extern "C" mtsph_status mtsph_porous_create(const mtsph_porous_desc *dsc, mtsph_
     P->inv_mix.upload(inv.data(), n, P->s);
     P->amap.alloc((size_t)dd * n);
     P->amap.zero(P->s);
+    P->rm.alloc((size_t)4 * (d == 3 ? PorRM<3>::planes : PorRM<2>::planes) * n);
+    P->rf.alloc((size_t)8 * n);
     P->T.alloc((size_t)n * (d == 3 ? DS<3>::n : DS<2>::n));
     P->T.zero(P->s);
     P->flags.upload(flags.data(), n, P->s);
@@ -195,12 +197,12 @@ template <int D> static int64_t porous_advance(mtsph_porous *P, double dt, doubl
         for (auto &e : P->ev_outer) MT_CUDA(cudaEventCreate(&e));
     MT_CUDA(cudaEventRecord(P->ev_outer[0], s));
     k_por_prep<D><<<nb, 256, 0, s>>>(A, 1);
-    k_por_flux<D><<<nb, 256, 0, s>>>(A);
+    k_por_flux<D><<<nb, 256, 0, s>>>(A, 1);
     const int contact_on = t <= P->contact_time * (1.0 + 1e-12) ? 1 : 0;
     const double evap_factor = (!contact_on && P->evap > 0.0) ? std::exp(-P->evap * dt) : 1.0;
     k_por_mass<D><<<nb, 256, 0, s>>>(A, dt, contact_on, evap_factor);
     k_por_prep<D><<<nb, 256, 0, s>>>(A, 0);
-    k_por_flux<D><<<nb, 256, 0, s>>>(A);
+    k_por_flux<D><<<nb, 256, 0, s>>>(A, 0);
     k_por_post<D><<<nb, 256, 0, s>>>(A);
     k_por_fluxrate<D><<<nb, 256, 0, s>>>(A);
     MT_LAUNCH_CHECK();
