@@ -480,11 +480,11 @@ inline void build_tiled(const NbhDev &nb, int sh, TiledSched &t, cudaStream_t s)
     using namespace tiled_detail;
     const int64_t n = nb.n;
     const int d = nb.d;
-    // largest sub-colour in pairs (multiple of 8; 0 = none).  3D default
-    // 448 = the pair lanes of a 512-thread CTA: with it the fp64 block fits
-    // two CTAs per SM (sweep 7.35 -> 6.58 ms at 10M) and fp32 three (4.22
-    // -> 3.94 ms); 2D keeps whole sub-colours.  MTSPH_SWEEP_SUBCAP overrides.
-    int subcap = d == 3 ? 448 : 0;
+    // largest sub-colour in pairs (multiple of 8; 0 = none).  Default 448 =
+    // the pair lanes of a 512-thread CTA: with it the fp64 block fits two
+    // CTAs per SM (3D sweep 7.35 -> 6.58 ms at 10M, 2D 2.01 -> 1.78) and fp32
+    // three (3D 4.22 -> 3.94, 2D 1.14 -> 1.05).  MTSPH_SWEEP_SUBCAP overrides.
+    int subcap = 448;
     if (const char *e = std::getenv("MTSPH_SWEEP_SUBCAP")) subcap = std::max(0, std::atoi(e)) & ~7;
     int lg[3] = {0, 0, 0}, ext[3] = {1, 1, 1}, P[3] = {1, 1, 1};
     for (int i = 0; i < sh; ++i) ++lg[i % d];
@@ -796,10 +796,11 @@ inline void build_tiled_auto(const NbhDev &nb, TiledSched &t, cudaStream_t s, in
         // 1024) and the small fallback blocks (4^2 in 2D: 256 beat 1024 5x)
         const double avg = t.nsub_total ? (double)t.pairs.n / (double)t.nsub_total : 0.0;
         th = std::min(1024, std::max(128, ((int)(2.0 * avg) + 63) & ~63));
-        // 3D: 512 threads (64 staging + 448 pair lanes, the sub-colour cap):
-        // two (fp64) / three (fp32) CTAs per SM; measured 1024 threads with
-        // uncapped sub-colours 7.35 / 4.22 ms, 512 with the cap 6.58 / 3.94
-        if (d == 3 && !std::getenv("MTSPH_SWEEP_SUBCAP")) th = 512;
+        // 512 threads (64 staging + 448 pair lanes, the sub-colour cap):
+        // two (fp64) / three (fp32) CTAs per SM; measured (10M, 3D) 1024
+        // threads with uncapped sub-colours 7.35 / 4.22 ms, 512 with the cap
+        // 6.58 / 3.94 (2D 2.01 / 1.14 -> 1.78 / 1.05)
+        if (!std::getenv("MTSPH_SWEEP_SUBCAP")) th = 512;
     }
     t.threads = th;
     // the attribute is per function, shared by every problem instance: allow
