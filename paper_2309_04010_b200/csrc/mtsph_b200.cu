@@ -520,6 +520,12 @@ extern "C" mtsph_status mtsph_solid_create(const mtsph_solid_desc *dsc, mtsph_so
             S->nb.grid_hi[k] = dsc->grid[3 + k];
         }
     }
+    if (const char *e = std::getenv("MTSPH_GATHER_LANES")) {
+        const int g = std::atoi(e);
+        if (g != 0 && g != 2 && g != 4 && g != 8) throw Error(MTSPH_ERR_ARG, "MTSPH_GATHER_LANES: 0, 2, 4 or 8");
+        S->gather_g = g;
+    }
+    S->nb.want_sell = S->gather_g == 0;
     if (dsc->ghost && dsc->sweep != 3 && dsc->sweep != 0)
         throw Error(MTSPH_ERR_ARG, "ghost particles (multi-rank) need the tiled sweep");
     if (dsc->ghost) {
@@ -583,11 +589,6 @@ extern "C" mtsph_status mtsph_solid_create(const mtsph_solid_desc *dsc, mtsph_so
     if (d == 2) k_solid_gsum<2><<<blocks_for(n), 256, 0, S->s>>>(S->args(), S->G.p);
     else k_solid_gsum<3><<<blocks_for(n), 256, 0, S->s>>>(S->args(), S->G.p);
     MT_LAUNCH_CHECK();
-    if (const char *e = std::getenv("MTSPH_GATHER_LANES")) {
-        const int g = std::atoi(e);
-        if (g != 0 && g != 2 && g != 4 && g != 8) throw Error(MTSPH_ERR_ARG, "MTSPH_GATHER_LANES: 0, 2, 4 or 8");
-        S->gather_g = g;
-    }
     S->part.alloc((size_t)3 * S->nblk);
     S->part.zero(S->s);
     S->meas.alloc((size_t)5 * S->nblk);

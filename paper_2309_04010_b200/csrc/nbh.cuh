@@ -75,6 +75,7 @@ struct NbhDev {
     int64_t nnz = 0;             // directed entries (2 * pairs)
     DBuf<int64_t> indptr;        // CSR over internal ids
     DBuf<int32_t> csr;
+    bool want_sell = false;      // SELL-32 only for the opt-in one-lane gathers
     int64_t nslices = 0, sell_size = 0;
     DBuf<int64_t> slice_ptr;
     DBuf<int32_t> slice_w;
@@ -663,7 +664,8 @@ void build_nbh_impl(NbhDev &nb, const double *pos_h, const double *vol_h, cudaSt
     k_neigh<D, true><<<blocks_for(n), kThreads, 0, s>>>(n, U.p, cell_of.p, cell_start.p, ncell, cnb.p,
                                                         nb.perm.p, nullptr, nb.indptr.p, nb.csr.p, nullptr);
     MT_LAUNCH_CHECK();
-    // SELL-32
+    // SELL-32 (only for the one-lane-per-particle gathers, MTSPH_GATHER_LANES=0)
+    if (nb.want_sell) {
     nb.nslices = (n + 31) / 32;
     nb.slice_w.alloc(nb.nslices);
     nb.slice_ptr.alloc(nb.nslices + 1);
@@ -679,6 +681,7 @@ void build_nbh_impl(NbhDev &nb, const double *pos_h, const double *vol_h, cudaSt
     k_fill_sell<<<blocks_for(nb.nslices * 32), kThreads, 0, s>>>(n, nb.indptr.p, nb.csr.p, nb.slice_ptr.p,
                                                                  nb.slice_w.p, nb.nbr.p);
     MT_LAUNCH_CHECK();
+    }
     // corrections
     nb.B.alloc(n * D * D);
     DBuf<uint8_t> sing(n);

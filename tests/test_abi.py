@@ -70,3 +70,12 @@ def test_product_never_imports_oracle():
             if f.endswith((".py", ".cu", ".cuh")):
                 src = open(os.path.join(dirpath, f)).read()
                 assert "from oracle" not in src and "import oracle" not in src, f
+
+
+def test_select_device_without_gpu_fails_loudly():
+    from paper_2309_04010_b200 import _lib, errors
+    from paper_2309_04010_b200.device import select_device
+    if _lib.load_library(require_device=False).mtsph_device_count() > 0:
+        pytest.skip("a GPU is visible")
+    with pytest.raises(errors.BackendError):
+        select_device(0)

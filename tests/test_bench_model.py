@@ -1,0 +1,46 @@
+"""CPU: the benchmark's byte models and the profile summariser (host logic
+behind bench.py's roofline and profiles/launches_*_summary.json)."""
+
+import os
+import sys
+
+from conftest import ROOT
+
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "profiles", "tools"))
+
+
+def test_algorithmic_bytes_fp64_and_fp32():
+    import bench
+    m64 = bench.algorithmic_bytes(3, 78.37, 39.19, 39.19, "tiled", w=8)
+    m32 = bench.algorithmic_bytes(3, 78.37, 39.19, 39.19, "tiled", w=4)
+    # the sweep: v r/w + 1/m + (2 x 16-bit ids + coefficient) per pair and pass
+    assert abs(m64["sweep"] - (2 * 24 + 8 + 2 * 12 * 39.19)) < 1e-9
+    assert abs(m32["sweep"] - (2 * 12 + 4 + 2 * 8 * 39.19)) < 1e-9
+    for k in ("kick_drift", "stress", "accel", "reduce"):
+        assert m32[k] < m64[k]
+    # the index table (4 B per neighbour) is the same in both precisions
+    assert m64["stress"] - m32["stress"] > 0
+    assert abs((m64["accel"] - m32["accel"]) - (4 * 4 + 4 * 9 + 4 + 4 + 4 * 3 * 4)) < 1e-9
+
+
+def test_outer_bytes_counts_index_per_gather_pass():
+    import bench
+    a, b = bench.outer_bytes(3, 70.0), bench.outer_bytes(3, 71.0)
+    assert abs((b - a) - 4 * 4) < 1e-9          # flux x 2, mass, flux rate
+
+
+def test_launch_list_segments(tmp_path):
+    import make_summaries as ms
+    hdr = '"ID","Kernel Name","Metric Name","Metric Unit","Metric Value"\n'
+    rows = ["k_cell_keys", "void k_solid_stress_csr<3, 4>(SolidArgs)", "k_sweep_flow<3, double>(x)",
+            "k_sweep_flow<3, float>(x)", "k_cell_keys", "void k_por_accel<3>(PorousArgs)"]
+    text = hdr + "".join(f'"{i}","{k}","gpu__time_duration.sum","ms","1.5"\n' for i, k in enumerate(rows))
+    p = tmp_path / "l.csv"
+    p.write_text(text)
+    L = ms.launch_list(str(p))
+    assert [seg for _, _, seg in L] == [1, 1, 1, 1, 2, 2]
+    assert [k for k, _, _ in L][2:4] == ["k_sweep_flow", "k_sweep_flow32"]
+    solid = ms.launches(str(p), segment=1)
+    assert set(solid) == {"k_cell_keys", "k_solid_stress_csr", "k_sweep_flow", "k_sweep_flow32"}
+    assert abs(sum(v["share"] for v in solid.values()) - 1.0) < 1e-12
