@@ -188,19 +188,25 @@ struct KSpec {
     double inv_h[3];
     double pref;   // sigma_d / prod(h)
     double h_min;
+    double inv_h2[3];  // 1 / h_k^2
+    double pref5;      // -5 pref
 };
 
+// Evaluated as w_k = r_k / h_k^2, q^2 = sum r_k w_k, grad_k = -5 pref
+// (1-q/2)^3 w_k: the same value as the form above up to rounding, with
+// fewer FP64 operations in the neighbour loops (9 instead of 13 besides
+// the square root).
 template <int D>
 __device__ __forceinline__ void grad_w(const double *rel, const KSpec &ks, double *g) {
-    double u[D];
+    double w[D];
     double q2 = 0.0;
 #pragma unroll
-    for (int k = 0; k < D; ++k) { u[k] = rel[k] * ks.inv_h[k]; q2 += u[k] * u[k]; }
+    for (int k = 0; k < D; ++k) { w[k] = rel[k] * ks.inv_h2[k]; q2 = fma(rel[k], w[k], q2); }
     const double q = sqrt(q2);
     const double t = 1.0 - 0.5 * q;
-    const double mag = (q < 2.0) ? ks.pref * (-5.0 * t * t * t) : 0.0;
+    const double mag = (q < 2.0) ? ks.pref5 * (t * t * t) : 0.0;
 #pragma unroll
-    for (int k = 0; k < D; ++k) g[k] = mag * (u[k] * ks.inv_h[k]);
+    for (int k = 0; k < D; ++k) g[k] = mag * w[k];
 }
 
 // 32 B accesses.  sm_100 has 256-bit global loads/stores (SASS

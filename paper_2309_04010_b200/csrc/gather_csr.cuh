@@ -121,12 +121,9 @@ __global__ void __launch_bounds__(256, MTSPH_ACCEL_CTAS) k_solid_accel_csr(Solid
                 for (int q = 0; q < D; ++q) rel[q] = xb[q] - xa[q];
                 grad_w<D>(rel, A.ks, g);
 #pragma unroll
-                for (int r = 0; r < D; ++r) {
-                    double sum = 0.0;
+                for (int r = 0; r < D; ++r)
 #pragma unroll
-                    for (int cc = 0; cc < D; ++cc) sum += Tb[r * D + cc] * g[cc];
-                    acc[r] += sum;
-                }
+                    for (int cc = 0; cc < D; ++cc) acc[r] = fma(Tb[r * D + cc], g[cc], acc[r]);
             }
         }
         group_sum<G>(acc);

@@ -562,14 +562,16 @@ inline KSpec make_kspec(int d, const double *h_axes) {
     const double sigma[4] = {0.0, 3.0 / 4.0, 7.0 / (4.0 * PI), 21.0 / (16.0 * PI)};
     KSpec ks{};
     double prod = 1.0, hmin = h_axes[0];
-    for (int k = 0; k < 3; ++k) { ks.inv_h[k] = 1.0; ks.h[k] = 1.0; }
+    for (int k = 0; k < 3; ++k) { ks.inv_h[k] = 1.0; ks.h[k] = 1.0; ks.inv_h2[k] = 1.0; }
     for (int k = 0; k < d; ++k) {
         ks.h[k] = h_axes[k];
         ks.inv_h[k] = 1.0 / h_axes[k];
+        ks.inv_h2[k] = ks.inv_h[k] * ks.inv_h[k];
         prod *= h_axes[k];
         hmin = std::min(hmin, h_axes[k]);
     }
     ks.pref = sigma[d] / prod;
+    ks.pref5 = -5.0 * ks.pref;
     ks.h_min = hmin;
     return ks;
 }

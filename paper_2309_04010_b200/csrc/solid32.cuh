@@ -29,29 +29,29 @@
 namespace mtsph {
 
 struct KSpec32 {
-    float inv_h[3];
-    float pref;
+    float inv_h2[3];
+    float pref5;   // -5 pref
 };
 
 inline KSpec32 kspec32(const KSpec &k) {
     KSpec32 r;
-    for (int q = 0; q < 3; ++q) r.inv_h[q] = (float)k.inv_h[q];
-    r.pref = (float)k.pref;
+    for (int q = 0; q < 3; ++q) r.inv_h2[q] = (float)k.inv_h2[q];
+    r.pref5 = (float)k.pref5;
     return r;
 }
 
 // grad_w (common.cuh) in fp32
 template <int D>
 __device__ __forceinline__ void grad_w32(const float *rel, const KSpec32 &ks, float *g) {
-    float u[D];
+    float w[D];
     float q2 = 0.f;
 #pragma unroll
-    for (int k = 0; k < D; ++k) { u[k] = rel[k] * ks.inv_h[k]; q2 += u[k] * u[k]; }
+    for (int k = 0; k < D; ++k) { w[k] = rel[k] * ks.inv_h2[k]; q2 = fmaf(rel[k], w[k], q2); }
     const float q = sqrtf(q2);
     const float t = 1.f - 0.5f * q;
-    const float mag = (q < 2.f) ? ks.pref * (-5.f * t * t * t) : 0.f;
+    const float mag = (q < 2.f) ? ks.pref5 * (t * t * t) : 0.f;
 #pragma unroll
-    for (int k = 0; k < D; ++k) g[k] = mag * (u[k] * ks.inv_h[k]);
+    for (int k = 0; k < D; ++k) g[k] = mag * w[k];
 }
 
 struct Solid32Args {
@@ -280,12 +280,9 @@ __global__ void __launch_bounds__(256) k32_accel_csr(Solid32Args A) {
                 for (int q = 0; q < D; ++q) rel[q] = xb[q] - xa[q];
                 grad_w32<D>(rel, A.ks, g);
 #pragma unroll
-                for (int r = 0; r < D; ++r) {
-                    float sum = 0.f;
+                for (int r = 0; r < D; ++r)
 #pragma unroll
-                    for (int cc = 0; cc < D; ++cc) sum += Tb[r * D + cc] * g[cc];
-                    acc[r] += sum;
-                }
+                    for (int cc = 0; cc < D; ++cc) acc[r] = fmaf(Tb[r * D + cc], g[cc], acc[r]);
             }
         }
         group_sum32<G>(acc);
