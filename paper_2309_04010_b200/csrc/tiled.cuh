@@ -831,9 +831,12 @@ inline void build_tiled_auto(const NbhDev &nb, TiledSched &t, cudaStream_t s, in
     }
     if (const char *e = std::getenv("MTSPH_VERBOSE"); e && e[0] == '1')
         std::fprintf(stderr,
-                     "[mtsph] tiled sweep: %d Morton bits/block, %lld tasks, max halo %d, max sub-colour %d, "
+                     "[mtsph] tiled sweep: %d Morton bits/block, %lld tasks, %lld pairs in %lld slots (%.1f %% "
+                     "padding), %lld sub-colours, max halo %d, max sub-colour %d, "
                      "%d threads, smem %zu B (fp64) %zu B (fp32), dataflow grid %d / %d, %d stages (fp64)\n",
-                     t.sh, (long long)t.ntasks, t.max_halo, t.maxsub, t.threads, tiled_smem_bytes(t, d),
+                     t.sh, (long long)t.ntasks, (long long)t.npairs, (long long)t.pairs.n,
+                     t.pairs.n ? 100.0 * (1.0 - (double)t.npairs / (double)t.pairs.n) : 0.0,
+                     (long long)t.nsub_total, t.max_halo, t.maxsub, t.threads, tiled_smem_bytes(t, d),
                      tiled_smem_bytes(t, d, 4), t.flow_grid, t.flow_grid32, sweep_stages(8));
 }
 
