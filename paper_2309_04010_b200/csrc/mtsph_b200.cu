@@ -357,7 +357,7 @@ template <int D> static int solid_step(mtsph_solid *S, int ctrl_mode, cudaEvent_
                                    : launch_sweep<D>(S->nb, S->sweep_args(), S->level_ptr.p, S->ctrl.p, S->s));
     mark(4);
     k_solid_vmax<D><<<nb, 256, 0, S->s>>>(A, 0);
-    k_ctrl<<<1, 256, 0, S->s>>>(S->ctrl.p, S->part.p, S->nblk, ctrl_mode);
+    k_ctrl<<<1, kCtrlThreads, 0, S->s>>>(S->ctrl.p, S->part.p, S->nblk, ctrl_mode);
     MT_LAUNCH_CHECK();
     mark(5);
     return l + 2;
@@ -392,7 +392,7 @@ template <int D> static int solid_step32(mtsph_solid *S, int ctrl_mode, cudaEven
     int l = 3 + launch_tiled_sweep<D, float>(S->tiled, S->tiled_args32(), S->ctrl.p, S->s);
     mark(4);
     k32_vmax<D><<<nb, 256, 0, S->s>>>(A, 0);
-    k_ctrl<<<1, 256, 0, S->s>>>(S->ctrl.p, S->part.p, S->nblk, ctrl_mode);
+    k_ctrl<<<1, kCtrlThreads, 0, S->s>>>(S->ctrl.p, S->part.p, S->nblk, ctrl_mode);
     MT_LAUNCH_CHECK();
     mark(5);
     S->dirty32 = true;
@@ -407,7 +407,7 @@ static int solid_step_any(mtsph_solid *S, int mode, cudaEvent_t *ev = nullptr) {
 template <int D> static void solid_init_dt(mtsph_solid *S) {
     if (S->prec == 32) k32_vmax<D><<<blocks_for(S->n), 256, 0, S->s>>>(S->args32(), 1);
     else k_solid_vmax<D><<<blocks_for(S->n), 256, 0, S->s>>>(S->args(), 1);
-    k_ctrl<<<1, 256, 0, S->s>>>(S->ctrl.p, S->part.p, S->nblk, CTRL_INIT);
+    k_ctrl<<<1, kCtrlThreads, 0, S->s>>>(S->ctrl.p, S->part.p, S->nblk, CTRL_INIT);
     MT_LAUNCH_CHECK();
     S->launches += 2;
 }

@@ -538,12 +538,9 @@ __global__ void __launch_bounds__(256) k_por_accel(PorousArgs A) {
             for (int q = 0; q < D; ++q) rel[q] = xb[q] - xa[q];
             grad_w<D>(rel, A.ks, g);
 #pragma unroll
-            for (int r = 0; r < D; ++r) {
-                double s = 0.0;
+            for (int r = 0; r < D; ++r)
 #pragma unroll
-                for (int cc = 0; cc < D; ++cc) s += Tb[r * D + cc] * g[cc];
-                acc[r] += s;
-            }
+                for (int cc = 0; cc < D; ++cc) acc[r] = fma(Tb[r * D + cc], g[cc], acc[r]);
         }
     }
     group_sum<kPorLanes>(acc);

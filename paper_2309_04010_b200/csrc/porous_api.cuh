@@ -74,7 +74,7 @@ template <int D> static int porous_step(mtsph_porous *P, int mode) {
         l += launch_sweep<D>(P->nb, P->sweep_args(), P->level_ptr.p, P->ctrl.p, P->s);
     }
     k_por_post_step<D><<<nb, 256, 0, P->s>>>(A, 0);
-    k_ctrl<<<1, 256, 0, P->s>>>(P->ctrl.p, P->part.p, P->nblk, mode);
+    k_ctrl<<<1, kCtrlThreads, 0, P->s>>>(P->ctrl.p, P->part.p, P->nblk, mode);
     MT_LAUNCH_CHECK();
     return l + 2;
 }
@@ -86,7 +86,7 @@ static int porous_step_any(mtsph_porous *P, int mode) {
 template <int D> static void porous_init_dt(mtsph_porous *P) {
     PorousArgs A = P->args();
     k_por_post_step<D><<<blocks_for(P->n), 256, 0, P->s>>>(A, 1);
-    k_ctrl<<<1, 256, 0, P->s>>>(P->ctrl.p, P->part.p, P->nblk, CTRL_INIT);
+    k_ctrl<<<1, kCtrlThreads, 0, P->s>>>(P->ctrl.p, P->part.p, P->nblk, CTRL_INIT);
     MT_LAUNCH_CHECK();
     P->launches += 2;
 }

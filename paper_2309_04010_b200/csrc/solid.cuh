@@ -561,19 +561,20 @@ __device__ __forceinline__ void ctrl_apply(Ctrl *c, double E, double AM, double 
     c->dt = stable_dt(c, VM, AM);
 }
 
-// one block of 256; fixed-order reduction of the per-block partials
-__global__ void __launch_bounds__(256) k_ctrl(Ctrl *c, const double *part, int nblk, int mode) {
+// one block of kCtrlThreads; fixed-order reduction of the per-block partials
+constexpr int kCtrlThreads = 1024;
+__global__ void __launch_bounds__(kCtrlThreads) k_ctrl(Ctrl *c, const double *part, int nblk, int mode) {
     __shared__ double sh[32];
     if (mode == CTRL_STEP && c->done) return;
     double e = 0.0, am = 0.0, vm = 0.0;
-    for (int b = threadIdx.x; b < nblk; b += 256) {
+    for (int b = threadIdx.x; b < nblk; b += kCtrlThreads) {
         if (mode != CTRL_INIT) e += part[b];
         am = fmax(am, part[nblk + b]);
         vm = fmax(vm, part[2 * nblk + b]);
     }
-    const double E = block_sum<256>(e, sh);
-    const double AM = block_max<256>(am, sh);
-    const double VM = block_max<256>(vm, sh);
+    const double E = block_sum<kCtrlThreads>(e, sh);
+    const double AM = block_max<kCtrlThreads>(am, sh);
+    const double VM = block_max<kCtrlThreads>(vm, sh);
     if (threadIdx.x == 0) ctrl_apply(c, E, AM, VM, mode);
 }
 
