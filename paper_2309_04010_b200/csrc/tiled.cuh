@@ -419,15 +419,21 @@ inline void bank_order(const uint32_t *pairs, const double *pd, int64_t m, std::
         std::sort(rows, rows + 8, [&](int x, int y) { return rowtot[x] > rowtot[y]; });
         std::sort(cols, cols + 8, [&](int x, int y) { return coltot[x] > coltot[y]; });
         unsigned vis = 0;
-        std::function<bool(int)> augment = [&](int a) -> bool {
-            for (int k = 0; k < 8; ++k) {
-                const int b = cols[k];
-                if (bk[a * 8 + b].empty() || (vis >> b & 1)) continue;
-                vis |= 1u << b;
-                if (mc[b] < 0 || augment(mc[b])) { mc[b] = a; return true; }
+        struct Aug {  // Kuhn's augmenting path (depth <= 8)
+            const std::vector<int32_t> *bk;
+            const int *cols;
+            int *mc;
+            unsigned *vis;
+            bool operator()(int a) const {
+                for (int k = 0; k < 8; ++k) {
+                    const int b = cols[k];
+                    if (bk[a * 8 + b].empty() || (*vis >> b & 1)) continue;
+                    *vis |= 1u << b;
+                    if (mc[b] < 0 || (*this)(mc[b])) { mc[b] = a; return true; }
+                }
+                return false;
             }
-            return false;
-        };
+        } augment{bk, cols, mc, &vis};
         for (int k = 0; k < 8; ++k) { vis = 0; augment(rows[k]); }
         int g = 0;
         for (int b = 0; b < 8; ++b) {
@@ -591,17 +597,19 @@ inline void build_tiled(const NbhDev &nb, int sh, TiledSched &t, cudaStream_t s)
             std::vector<double> pdv;
             colour.clear();
             int ncol = 0;
-            for (int64_t a = lo; a < hi; ++a)
+            for (int64_t a = lo; a < hi; ++a) {
+                const int la = local_of(a);
                 for (int64_t k = indptr[a]; k < indptr[a + 1]; ++k) {
                     const int64_t b = csr[k];
                     if (b <= a) continue;
-                    const int la = local_of(a), lbb = local_of(b);
-                    int c = 0;
-                    for (;; ++c) {
-                        if (c >= 256) throw Error(1, "tiled sweep: more than 256 sub-colours");
-                        const uint64_t bit = 1ull << (c & 63);
-                        if (!((mask[la][c >> 6] | mask[lbb][c >> 6]) & bit)) break;
+                    const int lbb = local_of(b);
+                    // lowest colour free at both ends (first zero bit)
+                    int c = 256;
+                    for (int wd = 0; wd < 4; ++wd) {
+                        const uint64_t used = mask[la][wd] | mask[lbb][wd];
+                        if (~used) { c = wd * 64 + __builtin_ctzll(~used); break; }
                     }
+                    if (c >= 256) throw Error(1, "tiled sweep: more than 256 sub-colours");
                     mask[la][c >> 6] |= 1ull << (c & 63);
                     mask[lbb][c >> 6] |= 1ull << (c & 63);
                     pr.push_back((uint32_t)la | ((uint32_t)lbb << 16));
@@ -609,6 +617,7 @@ inline void build_tiled(const NbhDev &nb, int sh, TiledSched &t, cudaStream_t s)
                     colour.push_back(c);
                     ncol = std::max(ncol, c + 1);
                 }
+            }
             // stable counting sort by sub-colour, then each sub-colour in
             // bank-conflict-free quarter-warp groups (padded)
             std::vector<int32_t> cnt(ncol + 1, 0);
