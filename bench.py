@@ -393,14 +393,18 @@ def run_decomposed(args, world, rank, local):
     """N > 1: the workload split into N x-slabs (partition.py), one per GPU,
     halo exchanges over NCCL each phase, rank reductions all-gathered on the
     device and the stopping rule applied by every rank's control kernel
-    (DecomposedSolid.relax_device).  Strong scaling: the same 10 M-particle
-    bar as N = 1, so value is directly comparable across N."""
+    (DecomposedSolid.relax_device).  --scaling weak (default): the bar is N
+    times longer (10 M particles per GPU, the N = 1 workload per slab);
+    strong: the same 10 M-particle bar split N ways."""
     import torch
     import torch.distributed as dist
     from paper_2309_04010_b200 import lattices
     from paper_2309_04010_b200.distributed import DecomposedSolid
     from paper_2309_04010_b200.scenarios import _necking_materials
     params = workload_params(args)
+    if args.scaling == "weak" and world > 1:
+        params = dict(params)
+        params["length"] = params["length"] * world
     lat = lattices.build_lattice(params)
     elastic, hard = _necking_materials(params)
     eta, cfl = params["eta"], params["cfl"]
@@ -453,9 +457,13 @@ def run_decomposed(args, world, rank, local):
         "metric": "inner solid-relaxation particle-steps/sec",
         "value": n_total * args.steps / (ms / 1e3), "unit": "particle-steps/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": args.scaling if world > 1 else "weak",
+        "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": f"{args.workload} (BASELINE configs[2])", "particles": n_total,
+        "config": {"workload": f"{args.workload} (BASELINE configs[2])"
+                               + (f", {world}x longer (weak scaling)" if args.scaling == "weak" and world > 1
+                                  else ""),
+                   "particles": n_total, "particles_per_gpu": n_total // world,
                    "dp": params["dp"], "h_over_dp": params["h_factor"],
                    "material": "rho 1, E 200, nu 0.3, J2 power-law s0 0.25 e0 0.01 n 0.2",
                    "prestrain": PRESTRAIN, "damping_sweep": "tiled",
@@ -553,6 +561,9 @@ def main():
                     help="auto: N = 1 single domain, N > 1 slab decomposition with NCCL halos; "
                          "decomposed forces the decomposed path (also at N = 1); replicas: "
                          "independent copies of the 1-GPU workload")
+    ap.add_argument("--scaling", default="weak", choices=("weak", "strong"),
+                    help="N > 1 decomposed runs: weak = 10 M particles per GPU (bar N times "
+                         "longer), strong = the 10 M bar split N ways")
     ap.add_argument("--no-membrane", action="store_true", help="skip the porous membrane leg")
     ap.add_argument("--membrane-side", type=float, default=0.14,
                     help="fsi_3d film edge (m); 0.14 gives ~10 M particles")

@@ -250,8 +250,11 @@ class DecomposedSolid:
 
     def __init__(self, lat, elastic, hardening, nranks, ranks=None, group="local",
                  dist=None, tensor_device="cpu", end_disp_per_outer=0.0, ramp_steps=1):
-        self.plans, self.grid, self.owner = make_plans(lat.pos, lat.h_axes, nranks)
         ranks = list(range(nranks)) if ranks is None else list(ranks)
+        # one process per GPU builds only its own plan (and its neighbours'
+        # exchange lists); the in-process emulation builds all of them
+        self.plans, self.grid, self.owner = make_plans(
+            lat.pos, lat.h_axes, nranks, ranks=None if group in ("local", "local_device") else ranks)
         law, hp = hardening.device_params() if hardening is not None else (0, (1.0, 1.0, 1.0, 0.0))
         devices = {}
         for r in ranks:

@@ -88,8 +88,23 @@ def block_colour_and_halo(cells, B, d):
     return col, bc
 
 
-def make_plans(pos, h_axes, nranks, tile_B=None):
-    """Partition into `nranks` x-slabs; returns (plans, grid(6), owner)."""
+def _block_keys(bc, d):
+    """int64 key per block coordinate row (coordinates >= -1 after shifts)."""
+    bc = np.asarray(bc, np.int64) + 2
+    key = np.zeros(len(bc), np.int64)
+    for k in range(d):
+        key = key * (1 << 21) + bc[:, k]
+    return key
+
+
+def make_plans(pos, h_axes, nranks, tile_B=None, ranks=None):
+    """Partition into `nranks` x-slabs; returns (plans, grid(6), owner).
+
+    ranks: build complete plans only for these ranks (one process per GPU
+    needs its own); their neighbours' lists are computed as far as the
+    exchange lists need them, other entries of `plans` are None.  All
+    steps are vectorised (searchsorted on the sorted local id lists), so a
+    rank of a many-rank run costs O(n) numpy work."""
     pos = np.asarray(pos, float)
     n, d = pos.shape
     if tile_B is None:
@@ -99,58 +114,70 @@ def make_plans(pos, h_axes, nranks, tile_B=None):
     align = max(SLAB_ALIGN, tile_B)     # every sweep block inside one slab
     u, lo, hi = scaled_grid(pos, h_axes)
     cells = cell_coords(u, lo)
+    del u
     ncx = int(cells[:, 0].max()) + 1
     counts = np.bincount(cells[:, 0], minlength=ncx)
     cuts = _cuts(ncx, counts, nranks, align)
     owner = np.searchsorted(cuts, cells[:, 0], side="right") - 1
     grid = np.concatenate([np.pad(lo, (0, 3 - d)), np.pad(hi, (0, 3 - d))])
-    col, bc = block_colour_and_halo(cells, tile_B, d)
-    plans = []
-    gid = np.arange(n)
-    for r in range(nranks):
+    wanted = list(range(nranks)) if ranks is None else sorted(int(r) for r in ranks)
+    # slabs are >= 4 cells wide and ghosts lie within one cell: only
+    # adjacent ranks exchange
+    need = sorted({q for r in wanted for q in (r - 1, r, r + 1) if 0 <= q < nranks})
+    plans = [None] * nranks
+    for r in need:
         x0, x1 = int(cuts[r]), int(cuts[r + 1])
-        near = (cells[:, 0] >= x0 - 1) & (cells[:, 0] <= x1)
-        local = gid[near]                                   # ascending global ids
-        ghost = owner[local] != r
-        plans.append(RankPlan(r, local, ghost, owner[local], (x0, x1), tile_B=tile_B))
+        local = np.flatnonzero((cells[:, 0] >= x0 - 1) & (cells[:, 0] <= x1))  # ascending ids
+        plans[r] = RankPlan(r, local, owner[local] != r, owner[local], (x0, x1), tile_B=tile_B)
+
+    def at(p, gids):
+        """positions of global ids (all present) in p.local_ids"""
+        return np.searchsorted(p.local_ids, gids).astype(np.int64)
+
     # refresh lists: ghosts of r owned by q <-> owned of q that are ghosts on r
-    pos_in = [{int(g): i for i, g in enumerate(p.local_ids)} for p in plans]
-    for p in plans:
-        for q in range(nranks):
-            if q == p.rank:
+    for r in wanted:
+        p = plans[r]
+        for q in (r - 1, r + 1):
+            if not 0 <= q < nranks:
                 continue
-            gh = p.local_ids[p.ghost & (p.owner == q)]
-            if len(gh) == 0:
-                continue
-            p.refresh_recv[q] = np.array([pos_in[p.rank][int(g)] for g in gh], np.int64)
-            plans[q].refresh_send[p.rank] = np.array([pos_in[q][int(g)] for g in gh], np.int64)
-    # sweep push-back lists: ghosts of r inside the halo of r's blocks of colour c
-    span_lo = np.zeros(d, np.int64)
-    for p in plans:
-        owned = ~p.ghost
+            mine = np.flatnonzero(p.ghost & (p.owner == q))
+            if len(mine):
+                p.refresh_recv[q] = mine.astype(np.int64)
+            pq = plans[q]
+            theirs = pq.local_ids[pq.ghost & (pq.owner == r)]
+            if len(theirs):
+                p.refresh_send[q] = at(p, theirs)
+    # sweep push-back lists: ghosts of r inside the halo (block grown by one
+    # cell) of r's blocks of colour c, per owner; needed for the wanted ranks
+    # and, as receive lists, for their neighbours
+    shift = int(np.log2(tile_B))
+    send = {}
+    for r in need:
+        p = plans[r]
         loc_cells = cells[p.local_ids]
-        blk = bc[p.local_ids]
+        col, bc = block_colour_and_halo(loc_cells, tile_B, d)
+        gidx = np.flatnonzero(p.ghost)
+        gc = loc_cells[gidx]
+        owned = ~p.ghost
         for c in range(1 << d):
-            sel = owned & (col[p.local_ids] == c)
-            if not np.any(sel):
+            sel = owned & (col == c)
+            if not np.any(sel) or len(gidx) == 0:
                 continue
-            blocks = np.unique(blk[sel], axis=0)
-            # a ghost cell is in the halo of block b iff each coordinate lies
-            # within [b*B - 1, b*B + B]
-            gmask = p.ghost.copy()
-            hit = np.zeros(len(p.local_ids), bool)
-            gc = loc_cells[gmask]
-            if len(gc):
-                inside = np.zeros(len(gc), bool)
-                for b in blocks:
-                    lo_c = b * tile_B - 1 + span_lo
-                    hi_c = b * tile_B + tile_B
-                    inside |= np.all((gc >= lo_c) & (gc <= hi_c), axis=1)
-                hit[np.flatnonzero(gmask)[inside]] = True
-            for q in np.unique(p.owner[hit]):
+            keys = np.unique(_block_keys(bc[sel], d))
+            hit = np.zeros(len(gidx), bool)
+            # candidate blocks of a ghost cell g: (g-1)>>s, g>>s, (g+1)>>s per
+            # axis; g lies in the halo of block b iff b B - 1 <= g <= b B + B
+            offs = np.stack(np.meshgrid(*[[-1, 0, 1]] * d, indexing="ij"), -1).reshape(-1, d)
+            for o in offs:
+                cand = (gc + o) >> shift
+                inside = np.all((gc >= cand * tile_B - 1) & (gc <= cand * tile_B + tile_B), axis=1)
+                hit |= inside & np.isin(_block_keys(cand, d), keys)
+            for q in np.unique(p.owner[gidx[hit]]):
                 q = int(q)
-                idx = np.flatnonzero(hit & (p.owner == q))
-                p.pushback_send[(c, q)] = idx.astype(np.int64)
-                plans[q].pushback_recv[(c, p.rank)] = np.array(
-                    [pos_in[q][int(g)] for g in p.local_ids[idx]], np.int64)
+                send[(r, c, q)] = gidx[hit & (p.owner[gidx] == q)].astype(np.int64)
+    for (r, c, q), idx in send.items():
+        if plans[r] is not None and r in wanted:
+            plans[r].pushback_send[(c, q)] = idx
+        if q in wanted:
+            plans[q].pushback_recv[(c, r)] = at(plans[q], plans[r].local_ids[idx])
     return plans, grid, owner

@@ -169,3 +169,21 @@ def test_gloo_two_ranks_exchange():
         assert ok_ctrl, rank
         assert s == 3.0 and m == 1.0
     assert sum(r[5] for r in res) > 0
+
+
+@pytest.mark.parametrize("nranks", [2, 3, 4])
+def test_single_rank_plans_equal_full_plans(nranks):
+    """One process per GPU builds only its own plan (ranks=[r]); it must be
+    the full decomposition's plan for r, exchange lists included."""
+    lat = _lattice(1.2)
+    full, grid, owner = make_plans(lat.pos, lat.h_axes, nranks)
+    for r in range(nranks):
+        sub, g2, o2 = make_plans(lat.pos, lat.h_axes, nranks, ranks=[r])
+        a, b = full[r], sub[r]
+        assert np.array_equal(a.local_ids, b.local_ids) and np.array_equal(a.ghost, b.ghost)
+        for name in ("refresh_recv", "refresh_send", "pushback_send", "pushback_recv"):
+            da, db = getattr(a, name), getattr(b, name)
+            assert sorted(da) == sorted(db), (r, name)
+            for k in da:
+                assert np.array_equal(da[k], db[k]), (r, name, k)
+        assert np.array_equal(grid, g2) and np.array_equal(owner, o2)
