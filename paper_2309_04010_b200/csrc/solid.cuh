@@ -38,11 +38,16 @@ struct Mat {
     int plastic;
 };
 
+// t^m for t >= 1 (the power law's 1 + a/e0): exp2(m log2 t) is within a
+// few 1e-17 of pow here (m log2 t is small) and cheaper than pow's
+// extra-precise path
+__device__ __forceinline__ double pow_ge1(double t, double m) { return exp2(m * log2(t)); }
+
 // LAW: the hardening law as a compile-time constant (0, 1), or -1 to
 // read m.law at run time.  The split return-map kernels are instantiated
 // per law, so each carries one law's code and registers.
 template <int LAW = -1> __device__ __forceinline__ double hard_k(const Mat &m, double a) {
-    if (LAW == 1 || (LAW < 0 && m.law == 1)) return m.p[0] * pow(1.0 + a / m.p[1], m.p[2]);
+    if (LAW == 1 || (LAW < 0 && m.law == 1)) return m.p[0] * pow_ge1(1.0 + a / m.p[1], m.p[2]);
     return m.p[0] + (m.p[1] - m.p[0]) * (1.0 - exp(-m.p[2] * a)) + m.p[3] * a;
 }
 // K(a) and K'(a) from one pow / exp (the Newton iterate needs both):
@@ -51,7 +56,7 @@ template <int LAW = -1> __device__ __forceinline__ double hard_k(const Mat &m, d
 template <int LAW = -1> __device__ __forceinline__ double hard_k_kp(const Mat &m, double a, double &kp) {
     if (LAW == 1 || (LAW < 0 && m.law == 1)) {
         const double t = 1.0 + a / m.p[1];
-        const double k = m.p[0] * pow(t, m.p[2]);
+        const double k = m.p[0] * pow_ge1(t, m.p[2]);
         kp = k * m.p[2] / (m.p[1] * t);
         return k;
     }
