@@ -547,7 +547,17 @@ inline void build_tiled(const NbhDev &nb, int sh, TiledSched &t, cudaStream_t s)
         const double vi = d == 3 ? xv[i].w : xv[i].z, vj = d == 3 ? xv[j].w : xv[j].z;
         return 2.0 * vi * vj * radial / r;
     };
+    struct ColBank {
+        int row[8] = {0, 0, 0, 0, 0, 0, 0, 0}, col[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        int maxrow = 0, maxcol = 0;
+    };
+    // MTSPH_SWEEP_BALANCE=<window>: free colours considered per pair (0 =
+    // plain first-fit colouring)
+    int kBalanceWindow = 8;
+    if (const char *e = std::getenv("MTSPH_SWEEP_BALANCE")) kBalanceWindow = std::max(0, std::atoi(e));
+    const bool balance = kBalanceWindow > 1;
     auto work = [&](int64_t b0, int64_t b1) {
+        std::vector<ColBank> cbank(256);
         std::vector<std::array<uint64_t, 4>> mask;
         std::vector<int> colour;
         std::vector<std::pair<int64_t, int>> sorted_ranges;
@@ -597,19 +607,39 @@ inline void build_tiled(const NbhDev &nb, int sh, TiledSched &t, cudaStream_t s)
             std::vector<double> pdv;
             colour.clear();
             int ncol = 0;
+            for (auto &bk : cbank) bk = ColBank();
             for (int64_t a = lo; a < hi; ++a) {
                 const int la = local_of(a);
                 for (int64_t k = indptr[a]; k < indptr[a + 1]; ++k) {
                     const int64_t b = csr[k];
                     if (b <= a) continue;
                     const int lbb = local_of(b);
-                    // lowest colour free at both ends (first zero bit)
+                    // lowest colour free at both ends (first zero bit); with
+                    // balancing, the first free colour among the lowest
+                    // kBalanceWindow free ones whose bank rows (li % 8) and
+                    // columns (lj % 8) this pair does not push past the
+                    // colour's fullest row / column -- the padding bank_order
+                    // needs is set by those maxima
                     int c = 256;
-                    for (int wd = 0; wd < 4; ++wd) {
-                        const uint64_t used = mask[la][wd] | mask[lbb][wd];
-                        if (~used) { c = wd * 64 + __builtin_ctzll(~used); break; }
+                    const int ra = la & 7, cb = lbb & 7;
+                    int seen = 0;
+                    for (int wd = 0; wd < 4 && seen < (balance ? kBalanceWindow : 1); ++wd) {
+                        uint64_t freeb = ~(mask[la][wd] | mask[lbb][wd]);
+                        while (freeb && seen < (balance ? kBalanceWindow : 1)) {
+                            const int cc = wd * 64 + __builtin_ctzll(freeb);
+                            freeb &= freeb - 1;
+                            if (seen++ == 0) c = cc;
+                            if (!balance) break;
+                            const ColBank &bk = cbank[cc];
+                            if (bk.row[ra] < bk.maxrow && bk.col[cb] < bk.maxcol) { c = cc; break; }
+                        }
                     }
                     if (c >= 256) throw Error(1, "tiled sweep: more than 256 sub-colours");
+                    if (balance) {
+                        ColBank &bk = cbank[c];
+                        bk.maxrow = std::max(bk.maxrow, ++bk.row[ra]);
+                        bk.maxcol = std::max(bk.maxcol, ++bk.col[cb]);
+                    }
                     mask[la][c >> 6] |= 1ull << (c & 63);
                     mask[lbb][c >> 6] |= 1ull << (c & 63);
                     pr.push_back((uint32_t)la | ((uint32_t)lbb << 16));
