@@ -556,8 +556,19 @@ inline void build_tiled(const NbhDev &nb, int sh, TiledSched &t, cudaStream_t s)
     int kBalanceWindow = 8;
     if (const char *e = std::getenv("MTSPH_SWEEP_BALANCE")) kBalanceWindow = std::max(0, std::atoi(e));
     const bool balance = kBalanceWindow > 1;
+    struct Cand {
+        int32_t la, lb;
+        int64_t a, b;
+    };
+    // colour the pairs by decreasing endpoint degree (MTSPH_SWEEP_ORDER=row:
+    // row order): 1.381 -> 1.358 M sub-colours per pass, padding 8.5 -> 7.5 %,
+    // sweep 6.20 -> 6.13 ms at 10M
+    bool degree_order = true;
+    if (const char *e = std::getenv("MTSPH_SWEEP_ORDER")) degree_order = std::string(e) != "row";
     auto work = [&](int64_t b0, int64_t b1) {
         std::vector<ColBank> cbank(256);
+        std::vector<Cand> cand;
+        std::vector<int32_t> deg;
         std::vector<std::array<uint64_t, 4>> mask;
         std::vector<int> colour;
         std::vector<std::pair<int64_t, int>> sorted_ranges;
@@ -608,12 +619,28 @@ inline void build_tiled(const NbhDev &nb, int sh, TiledSched &t, cudaStream_t s)
             colour.clear();
             int ncol = 0;
             for (auto &bk : cbank) bk = ColBank();
+            // the block's pairs (a, b), a < b, a in the block, in row order
+            cand.clear();
             for (int64_t a = lo; a < hi; ++a) {
                 const int la = local_of(a);
                 for (int64_t k = indptr[a]; k < indptr[a + 1]; ++k) {
                     const int64_t b = csr[k];
                     if (b <= a) continue;
-                    const int lbb = local_of(b);
+                    cand.push_back({(int32_t)la, (int32_t)local_of(b), a, b});
+                }
+            }
+            if (degree_order) {
+                // colour the pairs of high-degree particles first (fewer colours)
+                deg.assign(local, 0);
+                for (const auto &e : cand) { ++deg[e.la]; ++deg[e.lb]; }
+                std::stable_sort(cand.begin(), cand.end(), [&](const Cand &x, const Cand &y) {
+                    return std::max(deg[x.la], deg[x.lb]) > std::max(deg[y.la], deg[y.lb]);
+                });
+            }
+            for (const auto &e : cand) {
+                {
+                    const int la = e.la, lbb = e.lb;
+                    const int64_t a = e.a, b = e.b;
                     // lowest colour free at both ends (first zero bit); with
                     // balancing, the first free colour among the lowest
                     // kBalanceWindow free ones whose bank rows (li % 8) and
