@@ -239,9 +239,9 @@ struct mtsph_solid {
     cudaGraphExec_t graphs[3] = {nullptr, nullptr, nullptr};
     int graph_steps[3] = {4, 32, 128};
     // fp32 variant (solid32.cuh): prec 32 = the fp32 arrays below hold the
-    // state and the fp64 ones are a mirror, refreshed on demand (dirty32)
+    // state and the fp64 ones are a mirror, refreshed whenever the host reads
+    // them (a steps counter cannot tell: steps also run inside CUDA graphs)
     int prec = 64;
-    bool dirty32 = false;
     int gather_g32 = 4;  // lanes per particle of the fp32 gathers (MTSPH_GATHER_LANES32)
     DBuf<float> XV32, B32, G32, mass32, rho032, inv_m32, pd32, u32, a32, H32, Hc32, alpha32, T32;
     DBuf<unsigned char> V32;
@@ -395,7 +395,6 @@ template <int D> static int solid_step32(mtsph_solid *S, int ctrl_mode, cudaEven
     k_ctrl<<<1, kCtrlThreads, 0, S->s>>>(S->ctrl.p, S->part.p, S->nblk, ctrl_mode);
     MT_LAUNCH_CHECK();
     mark(5);
-    S->dirty32 = true;
     return l + 2;
 }
 
@@ -417,13 +416,12 @@ static void g_timed_drop(const mtsph_solid *owner);
 
 // fp32 state -> the fp64 mirror (before anything reads the fp64 arrays)
 static void sync64(mtsph_solid *S) {
-    if (S->prec != 32 || !S->dirty32) return;
+    if (S->prec != 32) return;
     const unsigned nb = blocks_for(S->n);
     if (S->d == 2) k32_convert<2><<<nb, 256, 0, S->s>>>(S->args(), S->args32(), 0);
     else k32_convert<3><<<nb, 256, 0, S->s>>>(S->args(), S->args32(), 0);
     MT_LAUNCH_CHECK();
     S->launches += 1;
-    S->dirty32 = false;
 }
 // the fp64 arrays -> the fp32 state (after the host wrote the fp64 ones)
 static void sync32(mtsph_solid *S) {
@@ -433,7 +431,6 @@ static void sync32(mtsph_solid *S) {
     else k32_convert<3><<<nb, 256, 0, S->s>>>(S->args(), S->args32(), 1);
     MT_LAUNCH_CHECK();
     S->launches += 1;
-    S->dirty32 = false;
 }
 
 extern "C" mtsph_status mtsph_solid_set_precision(mtsph_solid *S, int bits) {

@@ -1,0 +1,57 @@
+"""Application run at benchmark scale (GPU): the reference driver protocol
+(stepping.run_outer_inner) on BASELINE configs[2] -- the 10 M-particle 3D
+power-law bar, left end clamped, right end pulled at the BASELINE rate, outer
+dt 0.01 -- with every inner loop on the device (graph chunks, stopping rule
+in the control kernel).  Prints one JSON line: inner steps per outer step,
+wall time, observables.
+
+    python profiles/tools/app_run.py [--n-outer 3] [--sweep tiled] [--fp32]
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n-outer", type=int, default=3)
+    ap.add_argument("--sweep", default="tiled")
+    ap.add_argument("--fp32", action="store_true")
+    args = ap.parse_args()
+    from paper_2309_04010_b200 import scenarios
+    from paper_2309_04010_b200.config import resolve
+    from paper_2309_04010_b200.stepping import run_outer_inner
+    base = resolve({"scenario": "bar_3d"}).params
+    dt_outer = base["t_total"] / base["n_outer"]
+    raw = {"scenario": "bar_3d", "n_outer": args.n_outer, "t_total": args.n_outer * dt_outer,
+           "stretch_per_end": base["stretch_per_end"] * args.n_outer / base["n_outer"],
+           "damping_sweep": args.sweep}
+    p = resolve(raw).params
+    t0 = time.perf_counter()
+    problem, policy = scenarios.build(p, sweep=args.sweep)
+    setup = time.perf_counter() - t0
+    if args.fp32:
+        problem.dev.set_precision(32)
+    t0 = time.perf_counter()
+    obs, counters = run_outer_inner(problem, policy)
+    wall = time.perf_counter() - t0
+    n = problem.lattice.n
+    print(json.dumps({
+        "workload": f"bar_3d (BASELINE configs[2]), {n} particles, {args.sweep} sweep, "
+                    f"{'fp32 variant' if args.fp32 else 'fp64'}",
+        "dt_outer": policy.dt_outer, "energy_criterion": policy.energy_criterion,
+        "n_outer": counters.n_outer, "n_inner": [int(x) for x in obs.n_inner],
+        "cap_hits": counters.cap_hits, "setup_s": setup, "wall_s": wall,
+        "inner_steps_per_s": counters.n_inner / wall,
+        "particle_steps_per_s": n * counters.n_inner / wall,
+        "reaction_force": [float(x) for x in obs.reaction_force],
+        "min_dt_inner": counters.min_dt_inner}))
+
+
+if __name__ == "__main__":
+    main()

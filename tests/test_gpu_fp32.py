@@ -140,3 +140,27 @@ def test_fp32_run_steps():
     s.set_precision(64)
     t = s.run_steps(8, p["eta"], p["cfl"])
     assert t["total_ms"] > 0
+
+
+def test_fp32_repeated_device_loops_read_back_current_state():
+    """Several device-loop calls in fp32 (steps run inside cached CUDA
+    graphs): every read-back (get / measure) sees the current state, and it
+    tracks the fp64 run call by call."""
+    out = {}
+    for bits in (64, 32):
+        s, lat, p = _bar(3)
+        s.set_precision(bits)
+        s.set_ramp(0.01 * p["length"], 30, 30)
+        hist = []
+        for _ in range(3):
+            s.relax(eta=p["eta"], cfl=p["cfl"], criterion=-1.0, dt_outer=1.0, max_inner=40,
+                    min_inner=40)
+            hist.append((s.get("vel"), s.get("pos") - lat.pos))
+        out[bits] = hist
+    for k in range(3):
+        v64, u64 = out[64][k]
+        v32, u32 = out[32][k]
+        assert _scaled_err(u32, u64) < FP32_TRAJ_TOL, k
+        assert _scaled_err(v32, v64) < 1e-3, k
+    # the state moved between the calls (not a stale copy)
+    assert np.max(np.abs(out[32][2][1] - out[32][0][1])) > 0
