@@ -77,29 +77,48 @@ template <int D> __device__ __forceinline__ void xget32(const float4 &xv, float 
 }
 template <int D> __device__ __forceinline__ float volof32(const float4 &xv) { return D == 3 ? xv.w : xv.z; }
 
-// divergence record, fp32: 3D (T~00 T~01 T~02 T~10) (T~11 T~12 T~20 T~21)
-// (X0 X1 X2 T~22), three 16 B planes; 2D (T~00 T~01 T~10 T~11), X from XV
+// two floats packed in a double's bit pattern (256-bit records are moved
+// with the v4.f64 loads/stores of common.cuh)
+__device__ __forceinline__ void unpack2f(double d, float &lo, float &hi) {
+    const unsigned long long u = (unsigned long long)__double_as_longlong(d);
+    lo = __uint_as_float((unsigned)(u & 0xffffffffull));
+    hi = __uint_as_float((unsigned)(u >> 32));
+}
+__device__ __forceinline__ double pack2f(float lo, float hi) {
+    return __longlong_as_double((long long)(((unsigned long long)__float_as_uint(hi) << 32) |
+                                            __float_as_uint(lo)));
+}
+
+// divergence record, fp32: 3D one 32 B plane (T~00 .. T~21, one 256-bit
+// load) and one 16 B plane (X0 X1 X2 T~22) -- two loads per neighbour
+// instead of three 16 B ones (accel 3.24 -> 3.12 ms at 10M); 2D
+// (T~00 T~01 T~10 T~11), X from XV.  (Interleaving X|V0 with v in one
+// 32 B record for the deformation-rate gather was slower: 3.62 -> 3.89 ms.)
 template <int D>
 __device__ __forceinline__ void dstore32(float *Tp, int64_t n, int64_t a, const float *tt, const float4 &xv) {
-    float4 *r = reinterpret_cast<float4 *>(Tp);
-    r[a] = make_float4(tt[0], tt[1], tt[2], tt[3]);
     if (D == 3) {
-        r[n + a] = make_float4(tt[4], tt[5], tt[6], tt[7]);
-        r[2 * n + a] = make_float4(xv.x, xv.y, xv.z, tt[8]);
+        st4(reinterpret_cast<double4 *>(Tp) + a,
+            make_double4(pack2f(tt[0], tt[1]), pack2f(tt[2], tt[3]), pack2f(tt[4], tt[5]), pack2f(tt[6], tt[7])));
+        reinterpret_cast<float4 *>(Tp + 8 * n)[a] = make_float4(xv.x, xv.y, xv.z, tt[8]);
+    } else {
+        reinterpret_cast<float4 *>(Tp)[a] = make_float4(tt[0], tt[1], tt[2], tt[3]);
     }
 }
 template <int D>
 __device__ __forceinline__ void dload32(const float *Tp, int64_t n, const float4 *XV, int64_t b, float *tt,
                                         float *x) {
-    const float4 *r = reinterpret_cast<const float4 *>(Tp);
-    const float4 q0 = __ldg(r + b);
-    tt[0] = q0.x; tt[1] = q0.y; tt[2] = q0.z; tt[3] = q0.w;
     if (D == 2) {
+        const float4 q0 = __ldg(reinterpret_cast<const float4 *>(Tp) + b);
+        tt[0] = q0.x; tt[1] = q0.y; tt[2] = q0.z; tt[3] = q0.w;
         const float4 xv = __ldg(XV + b);
         x[0] = xv.x; x[1] = xv.y;
     } else {
-        const float4 q1 = __ldg(r + n + b), q2 = __ldg(r + 2 * n + b);
-        tt[4] = q1.x; tt[5] = q1.y; tt[6] = q1.z; tt[7] = q1.w;
+        const double4 q = ldg4(reinterpret_cast<const double4 *>(Tp) + b);
+        unpack2f(q.x, tt[0], tt[1]);
+        unpack2f(q.y, tt[2], tt[3]);
+        unpack2f(q.z, tt[4], tt[5]);
+        unpack2f(q.w, tt[6], tt[7]);
+        const float4 q2 = __ldg(reinterpret_cast<const float4 *>(Tp + 8 * n) + b);
         tt[8] = q2.w;
         x[0] = q2.x; x[1] = q2.y; x[2] = q2.z;
     }
