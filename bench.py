@@ -48,6 +48,15 @@ FALLBACK_HBM_GBS = 6650.0
 PRESTRAIN = 0.005
 
 
+_OUT = None   # the real stdout: the JSON line is the only thing written there
+
+
+def emit(line):
+    out = _OUT if _OUT is not None else sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
 def load_peaks():
     try:
         with open(PEAKS_PATH) as fh:
@@ -346,7 +355,7 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(params, args, budget_s=args.cpu_budget)
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
@@ -481,7 +490,7 @@ def run_decomposed(args, world, rank, local):
         "clocks": clk,
     }
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line)
     dist.destroy_process_group()
 
 
@@ -541,7 +550,7 @@ def run_reference(args):
         "e2e": {"value": base["value"], "unit": "particle-steps/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def main():
@@ -569,6 +578,11 @@ def main():
                     help="fsi_3d film edge (m); 0.14 gives ~10 M particles")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    # keep stdout for the JSON line alone: library output on fd 1 (NCCL's
+    # version banner, ...) goes to stderr
+    global _OUT
+    _OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     if args.impl == "reference":
         run_reference(args)
     else:
