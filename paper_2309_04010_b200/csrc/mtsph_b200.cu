@@ -517,6 +517,10 @@ extern "C" mtsph_status mtsph_solid_create(const mtsph_solid_desc *dsc, mtsph_so
             S->nb.grid_hi[k] = dsc->grid[3 + k];
         }
     }
+    // lanes per particle: 4 in 3D (~78 neighbours), 2 in 2D (~21):
+    // measured 2D 10M fp64 4.99 -> 4.94 ms/step, fp32 3.14 -> 2.95
+    S->gather_g = d == 2 ? 2 : 4;
+    S->gather_g32 = d == 2 ? 2 : 4;
     if (const char *e = std::getenv("MTSPH_GATHER_LANES")) {
         const int g = std::atoi(e);
         if (g != 0 && g != 2 && g != 4 && g != 8) throw Error(MTSPH_ERR_ARG, "MTSPH_GATHER_LANES: 0, 2, 4 or 8");

@@ -63,12 +63,13 @@ def test_necking_trajectory_100_steps(gold_traj, prefix):
     _check_trajectory(gold_traj, prefix)
 
 
-@pytest.mark.parametrize("lanes", ["0", "2", "8"])
+@pytest.mark.parametrize("lanes", ["0", "2", "4", "8"])
 @pytest.mark.parametrize("prefix", ["n2_", "n3_"])
 def test_necking_trajectory_gather_modes(gold_traj, prefix, lanes, monkeypatch):
     """The same 100-step bar for every neighbour-gather mode: SELL (0) and the
-    row-parallel CSR gathers with 2 / 8 lanes per particle (4 is the default,
-    covered above).  Only the summation order differs between them."""
+    row-parallel CSR gathers with 2 / 4 / 8 lanes per particle (the defaults,
+    2 in 2D and 4 in 3D, are also covered above).  Only the summation order
+    differs between them."""
     monkeypatch.setenv("MTSPH_GATHER_LANES", lanes)
     _check_trajectory(gold_traj, prefix)
 
