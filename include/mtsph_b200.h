@@ -297,6 +297,10 @@ typedef struct {
            bulk_modulus, porosity, fluid_density0, initial_saturation;
     double contact_time, evaporation_rate;
     int sweep;
+    /* multi-rank (NULL for a single domain), as in mtsph_solid_desc:   */
+    const uint8_t *ghost;       /* (n,) 1 = halo copy of another rank's particle */
+    const double *grid;         /* 6 doubles: global scaled-space grid bounds    */
+    int tile;                   /* tiled sweep block edge in cells (0: auto)     */
 } mtsph_porous_desc;
 
 typedef struct mtsph_porous mtsph_porous;
@@ -323,6 +327,36 @@ mtsph_status mtsph_porous_refresh_velocities(mtsph_porous *p);
 mtsph_status mtsph_porous_get(mtsph_porous *p, const char *field, double *host);
 mtsph_status mtsph_porous_set(mtsph_porous *p, const char *field, const double *host);
 mtsph_status mtsph_porous_launches(const mtsph_porous *p, int64_t *count);
+/* --- multi-rank porous phases (slab decomposition, tiled sweep; driver
+ * paper_2309_04010_b200/distributed.py DecomposedPorous).  Ghost particles
+ * are never updated and never reduced; their fields come from exchanges. */
+enum {
+    MTSPH_POR_KICK = 1,       /* M += dt/2 rate, v_s, x += dt v_s (owned)            */
+    MTSPH_POR_STRESS = 2,     /* dF/dt gather + F update, constitutive, T~ (owned)   */
+    MTSPH_POR_ACCEL = 3,      /* divergence + flux rate + kick; out = sum m v^2, max |a|^2 */
+    MTSPH_POR_SWEEP = 4,      /* damping, colour arg (reverse when arg >= 64)        */
+    MTSPH_POR_POSTSTEP = 5,   /* momentum rebuild; out[0] = max |v|^2                */
+    MTSPH_POR_AMAX = 6,       /* before the loop: out = max |v|^2, max |a|^2         */
+    MTSPH_POR_PREP_MAP = 7,   /* outer: J, V, s, D rho_l and the map A (owned)       */
+    MTSPH_POR_FLUX_MASS = 8,  /* outer: flux q, packed for the mass update           */
+    MTSPH_POR_MASS = 9,       /* outer: mass update; out[0] = clamped particles      */
+    MTSPH_POR_PREP = 10,      /* outer: J, V, s, D rho_l                             */
+    MTSPH_POR_FLUX = 11,      /* outer: flux q, packed for the flux rate             */
+    MTSPH_POR_POST = 12,      /* outer: pressure, masses, momentum, velocity split   */
+    MTSPH_POR_FLUXRATE = 13,  /* outer: advected-momentum rate                       */
+};
+/* step size / viscosity of the inner phases; dt and time of the outer ones */
+mtsph_status mtsph_porous_set_step(mtsph_porous *p, double dt, double eta);
+mtsph_status mtsph_porous_set_outer(mtsph_porous *p, double dt_outer, double t);
+mtsph_status mtsph_porous_phase(mtsph_porous *p, int phase, int arg, double out[2]);
+/* host-staged field exchange for the listed particles (ORIGINAL local
+ * ids): "vel" (d), "T" (d*d), "satvol" (2), "rm" (16 in 3D, 8 in 2D),
+ * "rf" (8), "inv_mix" (1) doubles per particle                          */
+mtsph_status mtsph_porous_pack(mtsph_porous *p, const char *field, int64_t m,
+                               const int64_t *ids, double *host);
+mtsph_status mtsph_porous_unpack(mtsph_porous *p, const char *field, int64_t m,
+                                 const int64_t *ids, const double *host);
+mtsph_status mtsph_porous_colours(const mtsph_porous *p, int *ncolours);
 
 #ifdef __cplusplus
 }

@@ -43,7 +43,8 @@ class PorousDesc(ctypes.Structure):
                 ("density0", c_dbl), ("diffusivity", c_dbl), ("pressure_coeff", c_dbl),
                 ("shear_modulus", c_dbl), ("lame_lambda", c_dbl), ("bulk_modulus", c_dbl),
                 ("porosity", c_dbl), ("fluid_density0", c_dbl), ("initial_saturation", c_dbl),
-                ("contact_time", c_dbl), ("evaporation_rate", c_dbl), ("sweep", c_int)]
+                ("contact_time", c_dbl), ("evaporation_rate", c_dbl), ("sweep", c_int),
+                ("ghost", c_vp), ("grid", c_vp), ("tile", c_int)]
 
 
 class InnerParams(ctypes.Structure):
@@ -108,6 +109,12 @@ SIGNATURES = {
     "mtsph_solid_control_ranks": (c_int, [c_vp, c_vp, c_int, c_int]),
     "mtsph_solid_loop_state": (c_int, [c_vp, c_vp, c_vp]),
     "mtsph_porous_sizes": (c_int, [c_vp, c_vp]),
+    "mtsph_porous_set_step": (c_int, [c_vp, c_dbl, c_dbl]),
+    "mtsph_porous_set_outer": (c_int, [c_vp, c_dbl, c_dbl]),
+    "mtsph_porous_phase": (c_int, [c_vp, c_int, c_int, c_vp]),
+    "mtsph_porous_pack": (c_int, [c_vp, ctypes.c_char_p, c_i64, c_vp, c_vp]),
+    "mtsph_porous_unpack": (c_int, [c_vp, ctypes.c_char_p, c_i64, c_vp, c_vp]),
+    "mtsph_porous_colours": (c_int, [c_vp, c_vp]),
     "mtsph_solid_precision": (c_int, [c_vp, c_vp]),
     "mtsph_porous_create": (c_int, [c_vp, c_vp]),
     "mtsph_porous_destroy": (c_int, [c_vp]),

@@ -35,7 +35,9 @@
 
 namespace mtsph {
 
-enum { PF_MOVABLE = 1, PF_CONTACT = 2 };
+// PF_GHOST: a halo copy of another rank's particle (multi-rank): never
+// updated here (its fields come from exchanges), never reduced
+enum { PF_MOVABLE = 1, PF_CONTACT = 2, PF_GHOST = 4 };
 
 struct PorMat {
     double rho_s0, D, C, mu, lam, porosity, rho_l0, sat0;
@@ -84,6 +86,7 @@ template <int D>
 __global__ void __launch_bounds__(256) k_por_prep(PorousArgs A, int with_amap) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= A.n) return;
+    if (A.flags[i] & PF_GHOST) return;
     const int64_t n = A.n;
     double F[D * D];
 #pragma unroll
@@ -146,7 +149,7 @@ __global__ void __launch_bounds__(256) k_por_flux(PorousArgs A, int pack) {
         }
     }
     group_sum<kPorLanes>(acc);
-    if (act && sub == 0) {
+    if (act && sub == 0 && !(A.flags[i] & PF_GHOST)) {
         const double cf = A.coeff[i];
         double qv[3] = {0.0, 0.0, 0.0};
 #pragma unroll
@@ -217,7 +220,7 @@ __global__ void __launch_bounds__(256) k_por_mass(PorousArgs A, double dt, int c
         }
     }
     group_sum<kPorLanes>(rate);
-    if (act && sub == 0) {
+    if (act && sub == 0 && !(A.flags[i] & PF_GHOST)) {
         const double va = A.volc[i];
         double mass = A.mass_l[i] + dt * (va * rate[0]);
         const double cap = A.m.porosity * A.m.rho_l0 * va;
@@ -260,6 +263,7 @@ __global__ void __launch_bounds__(256) k_por_post(PorousArgs A) {
     using V_t = typename VT<D>::T;
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= A.n) return;
+    if (A.flags[i] & PF_GHOST) return;
     const int64_t n = A.n;
     const double sat = A.sat[i];
     A.pres[i] = A.m.C * (sat - A.m.sat0);
@@ -341,7 +345,7 @@ __global__ void __launch_bounds__(256, 3) k_por_fluxrate(PorousArgs A) {
         }
     }
     group_sum<kPorLanes>(acc);
-    if (act && sub == 0) {
+    if (act && sub == 0 && !(A.flags[i] & PF_GHOST)) {
         double qa[D], qG = 0.0;
 #pragma unroll
         for (int c = 0; c < D; ++c) {
@@ -361,6 +365,7 @@ __global__ void __launch_bounds__(256) k_por_kick1(PorousArgs A) {
     using V_t = typename VT<D>::T;
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= A.n) return;
+    if (A.flags[i] & PF_GHOST) return;
     const Ctrl *c = A.ctrl;
     if (c->done) return;
     const double dt = c->dt;
@@ -389,6 +394,7 @@ template <int D>
 __global__ void __launch_bounds__(256) k_por_constit(PorousArgs A) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= A.n) return;
+    if (A.flags[i] & PF_GHOST) return;
     Ctrl *c = A.ctrl;
     if (c->done) return;
     const int64_t n = A.n;
@@ -498,7 +504,7 @@ __global__ void __launch_bounds__(256) k_por_stress(PorousArgs A) {
         }
     }
     group_sum<kPorLanes>(acc);
-    if (act && sub == 0) {  // F += dt (acc B)
+    if (act && sub == 0 && !(A.flags[i] & PF_GHOST)) {  // F += dt (acc B)
         double Bm[D * D], L[D * D];
 #pragma unroll
         for (int k = 0; k < D * D; ++k) Bm[k] = A.B[(int64_t)k * n + i];
@@ -544,7 +550,7 @@ __global__ void __launch_bounds__(256) k_por_accel(PorousArgs A) {
         }
     }
     group_sum<kPorLanes>(acc);
-    if (act && sub == 0) {
+    if (act && sub == 0 && !(A.flags[i] & PF_GHOST)) {
         double Ta[D * D], xd[3];
         dload<D>(A.T, n, A.XV, i, Ta, xd);
         const double vola = volof<D>(ldg4(A.XV + i));
@@ -594,7 +600,7 @@ __global__ void __launch_bounds__(256) k_por_post_step(PorousArgs A, int pre_loo
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t n = A.n;
     double v2 = 0.0, a2 = 0.0;
-    if (i < n) {
+    if (i < n && !(A.flags[i] & PF_GHOST)) {
         double v[3];
         vget(reinterpret_cast<const V_t *>(A.V)[i], v);
         const bool movable = A.flags[i] & PF_MOVABLE;
@@ -652,6 +658,73 @@ __global__ void __launch_bounds__(256) k_por_refresh(PorousArgs A) {
     V_t w;
     vset(w, v3);
     reinterpret_cast<V_t *>(A.V)[i] = w;
+}
+
+}  // namespace mtsph
+
+namespace mtsph {
+
+// multi-rank field exchange: 0 vel (d), 1 T~ (d*d; the receiver keeps its
+// own copy of X), 2 (s, V) (2), 3 mass-update record (16 / 8), 4 flux-rate
+// record (8), 5 1/m_mix (1)
+inline int por_field_width(int which, int d) {
+    switch (which) {
+    case 0: return d;
+    case 1: return d * d;
+    case 2: return 2;
+    case 3: return d == 3 ? 16 : 8;
+    case 4: return 8;
+    default: return 1;
+    }
+}
+
+template <int D>
+__global__ void k_por_pack(PorousArgs A, int64_t m, const int64_t *__restrict__ ids, int which, int w,
+                           double *buf, int unpack) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= m) return;
+    const int64_t i = ids[k], n = A.n;
+    double *e = buf + k * w;
+    using V_t = typename VT<D>::T;
+    if (which == 0) {
+        V_t *V = reinterpret_cast<V_t *>(A.V);
+        if (unpack) {
+            double v[3] = {0, 0, 0};
+            for (int c = 0; c < D; ++c) v[c] = e[c];
+            V_t o;
+            vset(o, v);
+            V[i] = o;
+        } else {
+            double v[3];
+            vget(V[i], v);
+            for (int c = 0; c < D; ++c) e[c] = v[c];
+        }
+    } else if (which == 1) {
+        double t[D * D], x[3];
+        if (unpack) {
+            for (int c = 0; c < D * D; ++c) t[c] = e[c];
+            dstore_raw<D>(A.T, n, i, t, A.XV[i]);
+        } else {
+            dload<D>(A.T, n, A.XV, i, t, x);
+            for (int c = 0; c < D * D; ++c) e[c] = t[c];
+        }
+    } else if (which == 2) {
+        if (unpack) { A.sat[i] = e[0]; A.volc[i] = e[1]; }
+        else { e[0] = A.sat[i]; e[1] = A.volc[i]; }
+    } else if (which == 3 || which == 4) {
+        const int planes = w / 4;
+        double4 *r = reinterpret_cast<double4 *>(which == 3 ? A.rm : A.rf);
+        for (int p = 0; p < planes; ++p) {
+            if (unpack) r[p * n + i] = make_double4(e[4 * p], e[4 * p + 1], e[4 * p + 2], e[4 * p + 3]);
+            else {
+                const double4 q = r[p * n + i];
+                e[4 * p] = q.x; e[4 * p + 1] = q.y; e[4 * p + 2] = q.z; e[4 * p + 3] = q.w;
+            }
+        }
+    } else {
+        if (unpack) A.inv_mix[i] = e[0];
+        else e[0] = A.inv_mix[i];
+    }
 }
 
 }  // namespace mtsph

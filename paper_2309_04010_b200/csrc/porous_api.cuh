@@ -18,6 +18,8 @@ struct mtsph_porous {
     PorMat m{};
     double contact_time = 0.0, evap = 0.0;
     int nblk = 0;
+    double outer_dt = 0.0, outer_t = 0.0;   // multi-rank outer phases
+    std::vector<int64_t> iperm_h;           // original -> internal (pack/unpack)
     int64_t launches = 0;
     int per_step_launches = 0;
     cudaGraphExec_t graphs[3] = {nullptr, nullptr, nullptr};
@@ -108,8 +110,30 @@ extern "C" mtsph_status mtsph_porous_create(const mtsph_porous_desc *dsc, mtsph_
     P->n = n;
     P->d = d;
     MT_CUDA(cudaStreamCreateWithFlags(&P->s, cudaStreamNonBlocking));
-    build_nbh(P->nb, n, d, dsc->pos, dsc->vol, dsc->h_axes, dsc->sweep, P->s);
-    if (dsc->sweep == 3) build_tiled_auto(P->nb, P->tiled, P->s);
+    if (dsc->grid) {
+        P->nb.has_grid = true;
+        for (int k = 0; k < 3; ++k) {
+            P->nb.grid_lo[k] = dsc->grid[k];
+            P->nb.grid_hi[k] = dsc->grid[3 + k];
+        }
+    }
+    if (dsc->ghost && dsc->sweep != 3) throw Error(MTSPH_ERR_ARG, "ghost particles (multi-rank) need the tiled sweep");
+    if (dsc->ghost) {
+        // as mtsph_solid_create: ghost flags in the internal order feed the
+        // tiled schedule, so the schedule waits for the neighbour build
+        P->nb.ghost_orig = dsc->ghost;
+        build_nbh(P->nb, n, d, dsc->pos, dsc->vol, dsc->h_axes, 0, P->s);
+        P->nb.ghost_orig = nullptr;
+        P->nb.sweep = dsc->sweep;
+        std::vector<int64_t> pm(n);
+        P->nb.perm.download(pm.data(), n, P->s);
+        MT_CUDA(cudaStreamSynchronize(P->s));
+        P->nb.ghost_internal.resize(n);
+        for (int64_t k = 0; k < n; ++k) P->nb.ghost_internal[k] = dsc->ghost[pm[k]] ? 1 : 0;
+    } else {
+        build_nbh(P->nb, n, d, dsc->pos, dsc->vol, dsc->h_axes, dsc->sweep, P->s);
+    }
+    if (dsc->sweep == 3) build_tiled_auto(P->nb, P->tiled, P->s, dsc->tile);
     std::vector<int64_t> perm(n);
     P->nb.perm.download(perm.data(), n, P->s);
     MT_CUDA(cudaStreamSynchronize(P->s));
@@ -122,7 +146,8 @@ extern "C" mtsph_status mtsph_porous_create(const mtsph_porous_desc *dsc, mtsph_
         for (int c = 0; c < d; ++c) x[(size_t)c * n + k] = dsc->pos[o * d + c];
         for (int c = 0; c < d; ++c) F[(size_t)(c * d + c) * n + k] = 1.0;
         const bool movable = !dsc->constrained[o];
-        flags[k] = (movable ? PF_MOVABLE : 0) | ((dsc->contact && dsc->contact[o]) ? PF_CONTACT : 0);
+        flags[k] = (movable ? PF_MOVABLE : 0) | ((dsc->contact && dsc->contact[o]) ? PF_CONTACT : 0) |
+                   ((dsc->ghost && dsc->ghost[o]) ? PF_GHOST : 0);
         mix[k] = dsc->density0 * dsc->vol[o];
         inv[k] = movable ? 1.0 / mix[k] : 0.0;
     }
@@ -225,6 +250,161 @@ extern "C" mtsph_status mtsph_porous_advance_slow(mtsph_porous *P, double dt_out
     *clamped = P->d == 2 ? porous_advance<2>(P, dt_outer, t) : porous_advance<3>(P, dt_outer, t);
     check_porous_errors(P);
     API_END
+}
+
+// ---- multi-rank phases
+template <int D> static void porous_phase(mtsph_porous *P, int phase, int arg, double out[2]) {
+    PorousArgs A = P->args();
+    const unsigned nb = blocks_for(P->n);
+    cudaStream_t s = P->s;
+    out[0] = out[1] = 0.0;
+    auto partials = [&](int segs) {
+        std::vector<double> h((size_t)segs * P->nblk);
+        P->part.download(h.data(), h.size(), s);
+        MT_CUDA(cudaStreamSynchronize(s));
+        return h;
+    };
+    switch (phase) {
+    case MTSPH_POR_KICK: k_por_kick1<D><<<nb, 256, 0, s>>>(A); break;
+    case MTSPH_POR_STRESS:
+        k_por_stress<D><<<nb, 256, 0, s>>>(A);
+        k_por_constit<D><<<nb, 256, 0, s>>>(A);
+        break;
+    case MTSPH_POR_ACCEL: {
+        P->part.zero(s);
+        k_por_accel<D><<<nb, 256, 0, s>>>(A);
+        MT_LAUNCH_CHECK();
+        const auto h = partials(2);
+        for (int b = 0; b < P->nblk; ++b) {
+            out[0] += h[b];
+            out[1] = std::max(out[1], h[P->nblk + b]);
+        }
+        break;
+    }
+    case MTSPH_POR_SWEEP: {
+        if (P->nb.sweep != 3) throw Error(MTSPH_ERR_ARG, "sweep phases need the tiled schedule");
+        const int c = arg & 63, dir = arg >= 64 ? -1 : 1;
+        const TiledSched &t = P->tiled;
+        if (c + 1 >= (int)t.colour_ptr.size()) throw Error(MTSPH_ERR_ARG, "colour out of range");
+        const int64_t t0 = t.colour_ptr[c], t1 = t.colour_ptr[c + 1];
+        if (t1 > t0) {
+            TiledArgs T{t.range_off.p, t.ranges.p, t.halo_n.p, t.pair_off.p, t.pairs.p, t.pd.p, t.sub_off.p,
+                        t.sub.p, P->inv_mix.p, P->V.p, t.maxsub};
+            k_sweep_tiled<D><<<(unsigned)(t1 - t0), t.threads, tiled_smem_bytes(t, D), s>>>(T, t0, dir, P->ctrl.p);
+        }
+        break;
+    }
+    case MTSPH_POR_POSTSTEP:
+    case MTSPH_POR_AMAX: {
+        P->part.zero(s);
+        k_por_post_step<D><<<nb, 256, 0, s>>>(A, phase == MTSPH_POR_AMAX ? 1 : 0);
+        MT_LAUNCH_CHECK();
+        const auto h = partials(3);
+        for (int b = 0; b < P->nblk; ++b) {
+            out[0] = std::max(out[0], h[2 * P->nblk + b]);
+            out[1] = std::max(out[1], h[P->nblk + b]);
+        }
+        break;
+    }
+    case MTSPH_POR_PREP_MAP: k_por_prep<D><<<nb, 256, 0, s>>>(A, 1); break;
+    case MTSPH_POR_FLUX_MASS: k_por_flux<D><<<nb, 256, 0, s>>>(A, 1); break;
+    case MTSPH_POR_MASS: {
+        const double dt = P->outer_dt, t = P->outer_t;
+        const int contact_on = t <= P->contact_time * (1.0 + 1e-12) ? 1 : 0;
+        const double evap_factor = (!contact_on && P->evap > 0.0) ? std::exp(-P->evap * dt) : 1.0;
+        P->part.zero(s);
+        k_por_mass<D><<<nb, 256, 0, s>>>(A, dt, contact_on, evap_factor);
+        MT_LAUNCH_CHECK();
+        const auto h = partials(1);
+        for (int b = 0; b < P->nblk; ++b) out[0] += h[b];
+        break;
+    }
+    case MTSPH_POR_PREP: k_por_prep<D><<<nb, 256, 0, s>>>(A, 0); break;
+    case MTSPH_POR_FLUX: k_por_flux<D><<<nb, 256, 0, s>>>(A, 0); break;
+    case MTSPH_POR_POST: k_por_post<D><<<nb, 256, 0, s>>>(A); break;
+    case MTSPH_POR_FLUXRATE: k_por_fluxrate<D><<<nb, 256, 0, s>>>(A); break;
+    default: throw Error(MTSPH_ERR_ARG, "unknown porous phase");
+    }
+    MT_LAUNCH_CHECK();
+    P->launches += 1;
+    MT_CUDA(cudaStreamSynchronize(s));
+}
+
+extern "C" mtsph_status mtsph_porous_set_step(mtsph_porous *P, double dt, double eta) {
+    API_BEGIN
+    P->pull_ctrl();
+    P->hc->dt = dt;
+    P->hc->eta = eta;
+    P->hc->done = 0;
+    P->hc->err_inv = ~0ull;
+    P->push_ctrl();
+    API_END
+}
+
+extern "C" mtsph_status mtsph_porous_set_outer(mtsph_porous *P, double dt_outer, double t) {
+    P->outer_dt = dt_outer;
+    P->outer_t = t;
+    return MTSPH_OK;
+}
+
+extern "C" mtsph_status mtsph_porous_phase(mtsph_porous *P, int phase, int arg, double out[2]) {
+    API_BEGIN
+    if (P->d == 2) porous_phase<2>(P, phase, arg, out); else porous_phase<3>(P, phase, arg, out);
+    if (phase == MTSPH_POR_STRESS || phase == MTSPH_POR_PREP_MAP || phase == MTSPH_POR_PREP) {
+        P->pull_ctrl();
+        check_porous_errors(P);
+    }
+    API_END
+}
+
+static void porous_pack_common(mtsph_porous *P, const char *field, int64_t m, const int64_t *ids, double *host,
+                               const double *in, bool pack) {
+    const std::string f(field);
+    const int which = f == "vel" ? 0 : f == "T" ? 1 : f == "satvol" ? 2 : f == "rm" ? 3 : f == "rf" ? 4
+                    : f == "inv_mix" ? 5 : -1;
+    if (which < 0) throw Error(MTSPH_ERR_ARG, "porous pack fields: vel, T, satvol, rm, rf, inv_mix");
+    if (m <= 0) return;
+    if (P->iperm_h.empty()) {
+        P->iperm_h.resize(P->n);
+        P->nb.iperm.download(P->iperm_h.data(), P->n, P->s);
+        MT_CUDA(cudaStreamSynchronize(P->s));
+    }
+    std::vector<int64_t> internal(m);
+    for (int64_t k = 0; k < m; ++k) {
+        if (ids[k] < 0 || ids[k] >= P->n) throw Error(MTSPH_ERR_ARG, "particle id out of range");
+        internal[k] = P->iperm_h[ids[k]];
+    }
+    const int w = por_field_width(which, P->d);
+    DBuf<int64_t> dids(m);
+    DBuf<double> buf((size_t)m * w);
+    dids.upload(internal.data(), m, P->s);
+    if (!pack) buf.upload(in, (size_t)m * w, P->s);
+    PorousArgs A = P->args();
+    if (P->d == 2) k_por_pack<2><<<blocks_for(m), 256, 0, P->s>>>(A, m, dids.p, which, w, buf.p, pack ? 0 : 1);
+    else k_por_pack<3><<<blocks_for(m), 256, 0, P->s>>>(A, m, dids.p, which, w, buf.p, pack ? 0 : 1);
+    MT_LAUNCH_CHECK();
+    P->launches += 1;
+    if (pack) buf.download(host, (size_t)m * w, P->s);
+    MT_CUDA(cudaStreamSynchronize(P->s));
+}
+
+extern "C" mtsph_status mtsph_porous_pack(mtsph_porous *P, const char *field, int64_t m, const int64_t *ids,
+                                          double *host) {
+    API_BEGIN
+    porous_pack_common(P, field, m, ids, host, nullptr, true);
+    API_END
+}
+
+extern "C" mtsph_status mtsph_porous_unpack(mtsph_porous *P, const char *field, int64_t m, const int64_t *ids,
+                                            const double *host) {
+    API_BEGIN
+    porous_pack_common(P, field, m, ids, nullptr, host, false);
+    API_END
+}
+
+extern "C" mtsph_status mtsph_porous_colours(const mtsph_porous *P, int *nc) {
+    *nc = P->nb.sweep == 3 ? (int)P->tiled.colour_ptr.size() - 1 : 0;
+    return MTSPH_OK;
 }
 
 extern "C" mtsph_status mtsph_porous_sizes(const mtsph_porous *P, int64_t out[4]) {

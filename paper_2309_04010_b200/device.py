@@ -311,14 +311,21 @@ class DevicePorous:
     FIELDS_DD = {"F"}
     FIELDS_1 = {"fluid_mass", "saturation", "pressure"}
 
+    PHASES = {"kick": 1, "stress": 2, "accel": 3, "sweep": 4, "post_step": 5, "amax": 6,
+              "prep_map": 7, "flux_mass": 8, "mass": 9, "prep": 10, "flux": 11, "post": 12,
+              "fluxrate": 13}
+    WIDTH = {"vel": None, "T": None, "satvol": 2, "rm": None, "rf": 8, "inv_mix": 1}
+
     def __init__(self, pos, vol, constrained, contact, h_axes, model, contact_time,
-                 evaporation_rate, sweep="serial"):
+                 evaporation_rate, sweep="serial", ghost=None, grid=None, tile=0):
         lib = _lib.load_library()
         pos = _f64(pos)
         n, d = pos.shape
         self.n, self.d = n, d
         self._keep = {"pos": pos, "vol": _f64(vol, (n,)), "constrained": _u8(constrained, n),
-                      "contact": _u8(contact, n)}
+                      "contact": _u8(contact, n),
+                      "ghost": _u8(ghost, n) if ghost is not None else None,
+                      "grid": _f64(grid, (6,)) if grid is not None else None}
         k = self._keep
         m = model
         desc = _lib.PorousDesc(
@@ -326,7 +333,9 @@ class DevicePorous:
             ptr(k["contact"]).value, _h3(h_axes), m.density0, m.diffusivity, m.pressure_coeff,
             m.shear_modulus, m.lame_lambda, m.bulk_modulus, m.porosity, m.fluid_density0,
             m.initial_saturation, float(contact_time), float(evaporation_rate),
-            _lib.SWEEPS[sweep])
+            _lib.SWEEPS[sweep],
+            ptr(k["ghost"]).value if k["ghost"] is not None else None,
+            ptr(k["grid"]).value if k["grid"] is not None else None, int(tile))
         handle = ctypes.c_void_p()
         check(lib.mtsph_porous_create(ctypes.byref(desc), ctypes.byref(handle)))
         self._h = handle
@@ -337,6 +346,43 @@ class DevicePorous:
         check(self._lib.mtsph_porous_advance_slow(self._h, float(dt_outer), float(t),
                                                   ctypes.byref(v)))
         return v.value
+
+    # -- multi-rank phases (slab decomposition) -------------------------
+    def set_step(self, dt, eta):
+        check(self._lib.mtsph_porous_set_step(self._h, float(dt), float(eta)))
+
+    def set_outer(self, dt_outer, t):
+        check(self._lib.mtsph_porous_set_outer(self._h, float(dt_outer), float(t)))
+
+    def phase(self, name, arg=0):
+        out = np.zeros(2)
+        check(self._lib.mtsph_porous_phase(self._h, self.PHASES[name], int(arg), ptr(out)))
+        return out
+
+    def colours(self):
+        v = ctypes.c_int()
+        check(self._lib.mtsph_porous_colours(self._h, ctypes.byref(v)))
+        return v.value
+
+    def _width(self, field):
+        if field == "vel":
+            return self.d
+        if field == "T":
+            return self.d * self.d
+        if field == "rm":
+            return 16 if self.d == 3 else 8
+        return self.WIDTH[field]
+
+    def pack(self, field, ids):
+        ids = np.ascontiguousarray(ids, dtype=np.int64)
+        out = np.zeros((len(ids), self._width(field)))
+        check(self._lib.mtsph_porous_pack(self._h, field.encode(), len(ids), ptr(ids), ptr(out)))
+        return out
+
+    def unpack(self, field, ids, values):
+        ids = np.ascontiguousarray(ids, dtype=np.int64)
+        vals = _f64(values)
+        check(self._lib.mtsph_porous_unpack(self._h, field.encode(), len(ids), ptr(ids), ptr(vals)))
 
     def sizes(self):
         out = np.zeros(4, np.int64)

@@ -399,3 +399,128 @@ class DecomposedSolid:
             own = ~p.ghost
             out[p.local_ids[own]] = vals[own]
         return out
+
+
+class DecomposedPorous:
+    """A porous membrane (PorousProblem) split into x-slabs: the outer
+    diffusion step and the inner relaxation as device phases separated by
+    ghost exchanges, with the host-side control of DecomposedSolid.relax.
+
+    Exchanges per outer step: (s, V) after each preparation, the mass-update
+    record after the first flux, the flux-rate record, 1/m_mix and v after
+    the velocity split.  Per inner step: v after the kick, T~ after the
+    constitutive update, v after the divergence, and per sweep colour the
+    push-back and refresh of v, as in the solid.  Host-staged exchanges
+    (LocalGroup, or TorchGroup with tensor_device="cpu")."""
+
+    def __init__(self, lat, model, contact_time, evaporation_rate, nranks, ranks=None,
+                 group="local", dist=None, tensor_device="cpu"):
+        from .device import DevicePorous
+        ranks = list(range(nranks)) if ranks is None else list(ranks)
+        self.plans, self.grid, self.owner = make_plans(
+            lat.pos, lat.h_axes, nranks, ranks=None if group == "local" else ranks)
+        devices = {}
+        for r in ranks:
+            p = self.plans[r]
+            ids = p.local_ids
+            devices[r] = DevicePorous(lat.pos[ids], lat.vol[ids], lat.constrained[ids],
+                                      lat.contact[ids], lat.h_axes, model, contact_time,
+                                      evaporation_rate, sweep="tiled", ghost=p.ghost,
+                                      grid=self.grid, tile=p.tile_B)
+        if group == "local":
+            self.group = LocalGroup(self.plans, [devices[r] for r in range(nranks)])
+        else:
+            (r,) = ranks
+            if str(tensor_device).startswith("cuda"):
+                raise ValueError("porous exchanges are host-staged: tensor_device='cpu'")
+            self.group = TorchGroup(self.plans[r], devices[r], dist, tensor_device)
+        self.devices = self.group.devices
+        self.h = float(np.min(lat.h_axes))
+        self.sound = math.sqrt(model.bulk_modulus / model.density0)
+        # the reference sums the free volumes in original order
+        self.vol_movable = float(np.sum(lat.vol[~np.asarray(lat.constrained, bool)]))
+        self.ncolours = max(dev.colours() for dev in self.devices)
+        self.n_global = len(lat.vol)
+
+    def advance_slow(self, dt_outer, t):
+        """PorousProblem.advance_slow: returns the number of clamped particles."""
+        g = self.group
+        for dev in self.devices:
+            dev.set_outer(dt_outer, t)
+            dev.phase("prep_map")
+        g.refresh("satvol")
+        for dev in self.devices:
+            dev.phase("flux_mass")
+        g.refresh("rm")
+        clamped = g.allsum([dev.phase("mass")[0] for dev in self.devices])
+        for dev in self.devices:
+            dev.phase("prep")
+        g.refresh("satvol")
+        for dev in self.devices:
+            dev.phase("flux")
+            dev.phase("post")
+        g.refresh("rf")
+        g.refresh("inv_mix")
+        g.refresh("vel")
+        for dev in self.devices:
+            dev.phase("fluxrate")
+        return int(round(clamped))
+
+    def step(self, dt, eta):
+        g = self.group
+        for dev in self.devices:
+            dev.set_step(dt, eta)
+            dev.phase("kick")
+        g.refresh("vel")
+        for dev in self.devices:
+            dev.phase("stress")
+        g.refresh("T")
+        parts = [dev.phase("accel") for dev in self.devices]
+        ek = 0.5 * g.allsum([p[0] for p in parts]) / self.vol_movable
+        amax2 = g.allmax([p[1] for p in parts])
+        g.refresh("vel")
+        nc = self.ncolours
+        for rev in (False, True):
+            for q in range(nc):
+                c = nc - 1 - q if rev else q
+                for dev in self.devices:
+                    dev.phase("sweep", c + 64 if rev else c)
+                g.pushback(c)
+                g.refresh("vel")
+        vmax2 = g.allmax([dev.phase("post_step")[0] for dev in self.devices])
+        return ek, vmax2, amax2
+
+    def initial_dt(self, cfl):
+        vals = [dev.phase("amax") for dev in self.devices]
+        return stable_dt(self.h, self.sound, cfl, self.group.allmax([v[0] for v in vals]),
+                         self.group.allmax([v[1] for v in vals]))
+
+    def relax(self, eta, cfl, criterion, dt_outer, max_inner=0, min_inner=1, fixed_steps=None):
+        """Inner loop with the reference's stopping rule (or exactly
+        `fixed_steps` steps).  Returns (n_inner, ek, cap_hit, min_dt)."""
+        dt = self.initial_dt(cfl)
+        n, min_dt = 0, math.inf
+        while True:
+            n += 1
+            min_dt = min(min_dt, dt)
+            ek, vmax2, amax2 = self.step(dt, eta)
+            if fixed_steps is not None:
+                if n >= fixed_steps:
+                    return n, ek, False, min_dt
+            else:
+                cap = max_inner if max_inner > 0 else 10 * int(math.ceil(dt_outer / dt))
+                if ek <= criterion and n >= min_inner:
+                    return n, ek, False, min_dt
+                if n >= cap:
+                    return n, ek, True, min_dt
+            dt = stable_dt(self.h, self.sound, cfl, vmax2, amax2)
+
+    def gather(self, field):
+        """Owned values of `field` in global particle order (LocalGroup only)."""
+        sample = self.devices[0].get(field)
+        out = np.zeros((self.n_global,) + sample.shape[1:])
+        for p, dev in zip(self.plans, self.devices):
+            vals = dev.get(field)
+            own = ~p.ghost
+            out[p.local_ids[own]] = vals[own]
+        return out
