@@ -357,6 +357,23 @@ mtsph_status mtsph_porous_pack(mtsph_porous *p, const char *field, int64_t m,
 mtsph_status mtsph_porous_unpack(mtsph_porous *p, const char *field, int64_t m,
                                  const int64_t *ids, const double *host);
 mtsph_status mtsph_porous_colours(const mtsph_porous *p, int *ncolours);
+/* device-resident exchange and device-controlled inner loop, as the
+ * mtsph_solid_* functions of the same names; begin_loop also takes the
+ * whole problem's free volume (the E_k normaliser) when > 0             */
+mtsph_status mtsph_porous_phase_async(mtsph_porous *p, int phase, int arg);
+mtsph_status mtsph_porous_begin_loop(mtsph_porous *p, const mtsph_inner_params *ip,
+                                     double vol_movable);
+mtsph_status mtsph_porous_rank_partials(mtsph_porous *p, int mode, double *dev_out4);
+mtsph_status mtsph_porous_control_ranks(mtsph_porous *p, const double *dev_gathered,
+                                        int nranks, int mode);
+mtsph_status mtsph_porous_loop_state(mtsph_porous *p, mtsph_inner_result *r, int *done);
+mtsph_status mtsph_porous_internal_ids(mtsph_porous *p, int64_t m, const int64_t *ids,
+                                       int64_t *internal);
+mtsph_status mtsph_porous_stream(const mtsph_porous *p, void **stream);
+mtsph_status mtsph_porous_pack_device(mtsph_porous *p, const char *field, int64_t m,
+                                      const int64_t *ids_dev, double *out_dev);
+mtsph_status mtsph_porous_unpack_device(mtsph_porous *p, const char *field, int64_t m,
+                                        const int64_t *ids_dev, const double *in_dev);
 
 #ifdef __cplusplus
 }

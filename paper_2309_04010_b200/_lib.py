@@ -115,6 +115,15 @@ SIGNATURES = {
     "mtsph_porous_pack": (c_int, [c_vp, ctypes.c_char_p, c_i64, c_vp, c_vp]),
     "mtsph_porous_unpack": (c_int, [c_vp, ctypes.c_char_p, c_i64, c_vp, c_vp]),
     "mtsph_porous_colours": (c_int, [c_vp, c_vp]),
+    "mtsph_porous_phase_async": (c_int, [c_vp, c_int, c_int]),
+    "mtsph_porous_begin_loop": (c_int, [c_vp, c_vp, c_dbl]),
+    "mtsph_porous_rank_partials": (c_int, [c_vp, c_int, c_vp]),
+    "mtsph_porous_control_ranks": (c_int, [c_vp, c_vp, c_int, c_int]),
+    "mtsph_porous_loop_state": (c_int, [c_vp, c_vp, c_vp]),
+    "mtsph_porous_internal_ids": (c_int, [c_vp, c_i64, c_vp, c_vp]),
+    "mtsph_porous_stream": (c_int, [c_vp, ctypes.POINTER(c_vp)]),
+    "mtsph_porous_pack_device": (c_int, [c_vp, ctypes.c_char_p, c_i64, c_vp, c_vp]),
+    "mtsph_porous_unpack_device": (c_int, [c_vp, ctypes.c_char_p, c_i64, c_vp, c_vp]),
     "mtsph_solid_precision": (c_int, [c_vp, c_vp]),
     "mtsph_porous_create": (c_int, [c_vp, c_vp]),
     "mtsph_porous_destroy": (c_int, [c_vp]),

@@ -253,7 +253,9 @@ extern "C" mtsph_status mtsph_porous_advance_slow(mtsph_porous *P, double dt_out
 }
 
 // ---- multi-rank phases
-template <int D> static void porous_phase(mtsph_porous *P, int phase, int arg, double out[2]) {
+// sync = false: only enqueue (device-controlled loop; reductions stay in
+// the per-block partials for mtsph_porous_rank_partials)
+template <int D> static void porous_phase(mtsph_porous *P, int phase, int arg, double out[2], bool sync = true) {
     PorousArgs A = P->args();
     const unsigned nb = blocks_for(P->n);
     cudaStream_t s = P->s;
@@ -271,9 +273,10 @@ template <int D> static void porous_phase(mtsph_porous *P, int phase, int arg, d
         k_por_constit<D><<<nb, 256, 0, s>>>(A);
         break;
     case MTSPH_POR_ACCEL: {
-        P->part.zero(s);
+        if (sync) P->part.zero(s);
         k_por_accel<D><<<nb, 256, 0, s>>>(A);
         MT_LAUNCH_CHECK();
+        if (!sync) break;
         const auto h = partials(2);
         for (int b = 0; b < P->nblk; ++b) {
             out[0] += h[b];
@@ -296,9 +299,10 @@ template <int D> static void porous_phase(mtsph_porous *P, int phase, int arg, d
     }
     case MTSPH_POR_POSTSTEP:
     case MTSPH_POR_AMAX: {
-        P->part.zero(s);
+        if (sync) P->part.zero(s);
         k_por_post_step<D><<<nb, 256, 0, s>>>(A, phase == MTSPH_POR_AMAX ? 1 : 0);
         MT_LAUNCH_CHECK();
+        if (!sync) break;
         const auto h = partials(3);
         for (int b = 0; b < P->nblk; ++b) {
             out[0] = std::max(out[0], h[2 * P->nblk + b]);
@@ -315,7 +319,7 @@ template <int D> static void porous_phase(mtsph_porous *P, int phase, int arg, d
         P->part.zero(s);
         k_por_mass<D><<<nb, 256, 0, s>>>(A, dt, contact_on, evap_factor);
         MT_LAUNCH_CHECK();
-        const auto h = partials(1);
+        const auto h = partials(1);   // one host read per outer step
         for (int b = 0; b < P->nblk; ++b) out[0] += h[b];
         break;
     }
@@ -327,7 +331,7 @@ template <int D> static void porous_phase(mtsph_porous *P, int phase, int arg, d
     }
     MT_LAUNCH_CHECK();
     P->launches += 1;
-    MT_CUDA(cudaStreamSynchronize(s));
+    if (sync) MT_CUDA(cudaStreamSynchronize(s));
 }
 
 extern "C" mtsph_status mtsph_porous_set_step(mtsph_porous *P, double dt, double eta) {
@@ -399,6 +403,126 @@ extern "C" mtsph_status mtsph_porous_unpack(mtsph_porous *P, const char *field, 
                                             const double *host) {
     API_BEGIN
     porous_pack_common(P, field, m, ids, nullptr, host, false);
+    API_END
+}
+
+extern "C" mtsph_status mtsph_porous_phase_async(mtsph_porous *P, int phase, int arg) {
+    API_BEGIN
+    double out[2];
+    if (P->d == 2) porous_phase<2>(P, phase, arg, out, false); else porous_phase<3>(P, phase, arg, out, false);
+    API_END
+}
+
+extern "C" mtsph_status mtsph_porous_begin_loop(mtsph_porous *P, const mtsph_inner_params *p,
+                                                double vol_movable) {
+    API_BEGIN
+    P->pull_ctrl();
+    Ctrl *c = P->hc;
+    c->eta = p->eta;
+    c->cfl = p->cfl;
+    c->criterion = p->criterion;
+    c->dt_outer = p->dt_outer;
+    c->max_inner = p->max_inner;
+    c->min_inner = p->min_inner < 1 ? 1 : p->min_inner;
+    c->n_inner = 0;
+    c->done = 0;
+    c->cap_hit = 0;
+    c->min_dt = INFINITY;
+    c->err_inv = c->err_rm = ~0ull;
+    if (vol_movable > 0.0) c->vol_movable = vol_movable;   // the whole problem's, for E_k
+    P->push_ctrl();
+    API_END
+}
+
+extern "C" mtsph_status mtsph_porous_rank_partials(mtsph_porous *P, int mode, double *dev_out) {
+    API_BEGIN
+    if (mode != CTRL_INIT && mode != CTRL_STEP) throw Error(MTSPH_ERR_ARG, "mode: 0 (initial step) or 1 (step)");
+    k_rank_partials<<<1, 256, 0, P->s>>>(P->ctrl.p, P->part.p, P->nblk, mode, dev_out);
+    MT_LAUNCH_CHECK();
+    P->launches += 1;
+    API_END
+}
+
+extern "C" mtsph_status mtsph_porous_control_ranks(mtsph_porous *P, const double *dev_gathered, int nranks,
+                                                   int mode) {
+    API_BEGIN
+    if (mode != CTRL_INIT && mode != CTRL_STEP) throw Error(MTSPH_ERR_ARG, "mode: 0 (initial step) or 1 (step)");
+    if (nranks < 1) throw Error(MTSPH_ERR_ARG, "nranks must be positive");
+    k_ctrl_ranks<<<1, 32, 0, P->s>>>(P->ctrl.p, dev_gathered, nranks, mode);
+    MT_LAUNCH_CHECK();
+    P->launches += 1;
+    API_END
+}
+
+extern "C" mtsph_status mtsph_porous_loop_state(mtsph_porous *P, mtsph_inner_result *r, int *done) {
+    API_BEGIN
+    P->pull_ctrl();
+    const Ctrl *c = P->hc;
+    *done = c->done;
+    r->n_inner = c->n_inner;
+    r->cap_hit = c->cap_hit;
+    r->ek = c->ek;
+    r->min_dt = c->min_dt;
+    r->last_dt = c->last_dt;
+    check_porous_errors(P);
+    API_END
+}
+
+extern "C" mtsph_status mtsph_porous_internal_ids(mtsph_porous *P, int64_t m, const int64_t *ids,
+                                                  int64_t *internal) {
+    API_BEGIN
+    if (P->iperm_h.empty()) {
+        P->iperm_h.resize(P->n);
+        P->nb.iperm.download(P->iperm_h.data(), P->n, P->s);
+        MT_CUDA(cudaStreamSynchronize(P->s));
+    }
+    for (int64_t k = 0; k < m; ++k) {
+        if (ids[k] < 0 || ids[k] >= P->n) throw Error(MTSPH_ERR_ARG, "particle id out of range");
+        internal[k] = P->iperm_h[ids[k]];
+    }
+    API_END
+}
+
+extern "C" mtsph_status mtsph_porous_stream(const mtsph_porous *P, void **stream) {
+    *stream = (void *)P->s;
+    return MTSPH_OK;
+}
+
+static int porous_field(const char *field) {
+    const std::string f(field ? field : "");
+    const int which = f == "vel" ? 0 : f == "T" ? 1 : f == "satvol" ? 2 : f == "rm" ? 3 : f == "rf" ? 4
+                    : f == "inv_mix" ? 5 : -1;
+    if (which < 0) throw Error(MTSPH_ERR_ARG, "porous pack fields: vel, T, satvol, rm, rf, inv_mix");
+    return which;
+}
+
+// device-resident exchange: internal ids and the buffer are device memory,
+// the kernel is enqueued on the problem's stream (no host synchronisation)
+extern "C" mtsph_status mtsph_porous_pack_device(mtsph_porous *P, const char *field, int64_t m,
+                                                 const int64_t *ids, double *out) {
+    API_BEGIN
+    const int which = porous_field(field);
+    if (m <= 0) return MTSPH_OK;
+    const int w = por_field_width(which, P->d);
+    if (P->d == 2) k_por_pack<2><<<blocks_for(m), 256, 0, P->s>>>(P->args(), m, ids, which, w, out, 0);
+    else k_por_pack<3><<<blocks_for(m), 256, 0, P->s>>>(P->args(), m, ids, which, w, out, 0);
+    MT_LAUNCH_CHECK();
+    P->launches += 1;
+    API_END
+}
+
+extern "C" mtsph_status mtsph_porous_unpack_device(mtsph_porous *P, const char *field, int64_t m,
+                                                   const int64_t *ids, const double *in) {
+    API_BEGIN
+    const int which = porous_field(field);
+    if (m <= 0) return MTSPH_OK;
+    const int w = por_field_width(which, P->d);
+    if (P->d == 2)
+        k_por_pack<2><<<blocks_for(m), 256, 0, P->s>>>(P->args(), m, ids, which, w, const_cast<double *>(in), 1);
+    else
+        k_por_pack<3><<<blocks_for(m), 256, 0, P->s>>>(P->args(), m, ids, which, w, const_cast<double *>(in), 1);
+    MT_LAUNCH_CHECK();
+    P->launches += 1;
     API_END
 }
 

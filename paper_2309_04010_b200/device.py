@@ -228,9 +228,13 @@ class DeviceSolid:
         check(self._lib.mtsph_solid_colours(self._h, ctypes.byref(v)))
         return v.value
 
+    def field_width(self, field):
+        """doubles per particle of an exchanged field ("vel", "T")"""
+        return self.d if field == "vel" else self.d * self.d
+
     def pack(self, field, ids):
         ids = np.ascontiguousarray(ids, dtype=np.int64)
-        w = self.d if field == "vel" else self.d * self.d
+        w = self.field_width(field)
         out = np.zeros((len(ids), w))
         check(self._lib.mtsph_solid_pack(self._h, field.encode(), len(ids), ptr(ids), ptr(out)))
         return out
@@ -315,6 +319,7 @@ class DevicePorous:
               "prep_map": 7, "flux_mass": 8, "mass": 9, "prep": 10, "flux": 11, "post": 12,
               "fluxrate": 13}
     WIDTH = {"vel": None, "T": None, "satvol": 2, "rm": None, "rf": 8, "inv_mix": 1}
+    EXCHANGED = ("vel", "T", "satvol", "rm", "rf", "inv_mix")
 
     def __init__(self, pos, vol, constrained, contact, h_axes, model, contact_time,
                  evaporation_rate, sweep="serial", ghost=None, grid=None, tile=0):
@@ -364,7 +369,8 @@ class DevicePorous:
         check(self._lib.mtsph_porous_colours(self._h, ctypes.byref(v)))
         return v.value
 
-    def _width(self, field):
+    def field_width(self, field):
+        """doubles per particle of an exchanged field"""
         if field == "vel":
             return self.d
         if field == "T":
@@ -375,7 +381,7 @@ class DevicePorous:
 
     def pack(self, field, ids):
         ids = np.ascontiguousarray(ids, dtype=np.int64)
-        out = np.zeros((len(ids), self._width(field)))
+        out = np.zeros((len(ids), self.field_width(field)))
         check(self._lib.mtsph_porous_pack(self._h, field.encode(), len(ids), ptr(ids), ptr(out)))
         return out
 
@@ -383,6 +389,58 @@ class DevicePorous:
         ids = np.ascontiguousarray(ids, dtype=np.int64)
         vals = _f64(values)
         check(self._lib.mtsph_porous_unpack(self._h, field.encode(), len(ids), ptr(ids), ptr(vals)))
+
+    # -- device-resident exchange and device-controlled loop ------------
+    def internal_ids(self, ids):
+        ids = np.ascontiguousarray(ids, dtype=np.int64)
+        out = np.zeros(len(ids), np.int64)
+        check(self._lib.mtsph_porous_internal_ids(self._h, len(ids), ptr(ids), ptr(out)))
+        return out
+
+    def stream_handle(self):
+        st = ctypes.c_void_p()
+        check(self._lib.mtsph_porous_stream(self._h, ctypes.byref(st)))
+        return st.value or 0
+
+    def pack_device(self, field, m, ids_ptr, out_ptr):
+        check(self._lib.mtsph_porous_pack_device(self._h, field.encode(), int(m), ids_ptr, out_ptr))
+
+    def unpack_device(self, field, m, ids_ptr, in_ptr):
+        check(self._lib.mtsph_porous_unpack_device(self._h, field.encode(), int(m), ids_ptr, in_ptr))
+
+    def phase_async(self, name, arg=0):
+        check(self._lib.mtsph_porous_phase_async(self._h, self.PHASES[name], int(arg)))
+
+    def begin_loop(self, eta, cfl, criterion, dt_outer, max_inner=0, min_inner=1, vol_movable=0.0):
+        p = _lib.InnerParams(float(eta), float(cfl), float(criterion), float(dt_outer),
+                             int(max_inner), int(min_inner))
+        check(self._lib.mtsph_porous_begin_loop(self._h, ctypes.byref(p), float(vol_movable)))
+
+    def rank_partials(self, mode, dev_ptr):
+        check(self._lib.mtsph_porous_rank_partials(self._h, int(mode), dev_ptr))
+
+    def control_ranks(self, dev_ptr, nranks, mode):
+        check(self._lib.mtsph_porous_control_ranks(self._h, dev_ptr, int(nranks), int(mode)))
+
+    def rank_partials_host(self, mode):
+        import torch
+        buf = torch.zeros(4, dtype=torch.float64, device="cuda")
+        self.rank_partials(mode, buf.data_ptr())
+        torch.cuda.ExternalStream(self.stream_handle()).synchronize()
+        return buf.cpu().numpy()
+
+    def control_ranks_host(self, gathered, mode):
+        import torch
+        g = torch.from_numpy(np.ascontiguousarray(gathered, dtype=np.float64).ravel()).cuda()
+        torch.cuda.current_stream().synchronize()
+        self.control_ranks(g.data_ptr(), len(g) // 4, mode)
+        torch.cuda.ExternalStream(self.stream_handle()).synchronize()
+
+    def loop_state(self):
+        r = _lib.InnerResult()
+        done = ctypes.c_int()
+        check(self._lib.mtsph_porous_loop_state(self._h, ctypes.byref(r), ctypes.byref(done)))
+        return bool(done.value), r
 
     def sizes(self):
         out = np.zeros(4, np.int64)

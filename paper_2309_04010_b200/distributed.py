@@ -56,7 +56,7 @@ class LocalGroup:
         key = (field, src, dst, id(src_idx))
         if key not in self._cache:
             s, t = self.devices[src], self.devices[dst]
-            w = s.d if field == "vel" else s.d * s.d
+            w = s.field_width(field)
             self._cache[key] = (torch.from_numpy(s.internal_ids(src_idx)).cuda(),
                                 torch.from_numpy(t.internal_ids(dst_idx)).cuda(),
                                 torch.empty((len(src_idx), w), dtype=torch.float64, device="cuda"))
@@ -139,7 +139,8 @@ class TorchGroup:
             return ids, torch.empty((len(idx), width), dtype=torch.float64, device=self.tdev)
 
         self.dl = {}
-        for field, width in (("vel", d), ("T", d * d)):
+        fields = getattr(dev, "EXCHANGED", ("vel", "T"))
+        for field, width in ((f, dev.field_width(f)) for f in fields):
             self.dl[("refresh_send", field)] = {q: entry(i, width) for q, i in p.refresh_send.items()}
             self.dl[("refresh_recv", field)] = {q: entry(i, width) for q, i in p.refresh_recv.items()}
         self.dl["push_send"] = {k: entry(i, d) for k, i in p.pushback_send.items()}
@@ -183,7 +184,7 @@ class TorchGroup:
                                   self.dl[("refresh_recv", field)])
             return
         p, dev = self.plans[0], self.devices[0]
-        width = dev.d if field == "vel" else dev.d * dev.d
+        width = dev.field_width(field)
         sends = {q: dev.pack(field, idx) for q, idx in p.refresh_send.items()}
         got = self._swap(sends, {q: len(i) for q, i in p.refresh_recv.items()}, width)
         for q, vals in got.items():
@@ -418,7 +419,7 @@ class DecomposedPorous:
         from .device import DevicePorous
         ranks = list(range(nranks)) if ranks is None else list(ranks)
         self.plans, self.grid, self.owner = make_plans(
-            lat.pos, lat.h_axes, nranks, ranks=None if group == "local" else ranks)
+            lat.pos, lat.h_axes, nranks, ranks=None if group in ("local", "local_device") else ranks)
         devices = {}
         for r in ranks:
             p = self.plans[r]
@@ -427,12 +428,11 @@ class DecomposedPorous:
                                       lat.contact[ids], lat.h_axes, model, contact_time,
                                       evaporation_rate, sweep="tiled", ghost=p.ghost,
                                       grid=self.grid, tile=p.tile_B)
-        if group == "local":
-            self.group = LocalGroup(self.plans, [devices[r] for r in range(nranks)])
+        if group in ("local", "local_device"):
+            self.group = LocalGroup(self.plans, [devices[r] for r in range(nranks)],
+                                    device_buffers=group == "local_device")
         else:
             (r,) = ranks
-            if str(tensor_device).startswith("cuda"):
-                raise ValueError("porous exchanges are host-staged: tensor_device='cpu'")
             self.group = TorchGroup(self.plans[r], devices[r], dist, tensor_device)
         self.devices = self.group.devices
         self.h = float(np.min(lat.h_axes))
@@ -514,6 +514,51 @@ class DecomposedPorous:
                 if n >= cap:
                     return n, ek, True, min_dt
             dt = stable_dt(self.h, self.sound, cfl, vmax2, amax2)
+
+    # -- device-controlled inner loop (as DecomposedSolid.relax_device) -----
+    def _step_async(self):
+        g = self.group
+        for dev in self.devices:
+            dev.phase_async("kick")
+        g.refresh("vel")
+        for dev in self.devices:
+            dev.phase_async("stress")
+        g.refresh("T")
+        for dev in self.devices:
+            dev.phase_async("accel")
+        g.refresh("vel")
+        nc = self.ncolours
+        for rev in (False, True):
+            for q in range(nc):
+                c = nc - 1 - q if rev else q
+                for dev in self.devices:
+                    dev.phase_async("sweep", c + 64 if rev else c)
+                g.pushback(c)
+                g.refresh("vel")
+        for dev in self.devices:
+            dev.phase_async("post_step")
+        g.control(1)
+
+    def relax_device(self, eta, cfl, criterion, dt_outer, max_inner=0, min_inner=1,
+                     fixed_steps=None, check_every=8):
+        """Inner loop with phases enqueued without host synchronisation and
+        the stopping rule applied on every rank's device from all-gathered
+        partials; E_k normalised by the whole problem's free volume."""
+        if fixed_steps is not None:
+            criterion, max_inner, min_inner = -1.0, int(fixed_steps), int(fixed_steps)
+        for dev in self.devices:
+            dev.begin_loop(eta, cfl, criterion, dt_outer, max_inner, min_inner,
+                           vol_movable=self.vol_movable)
+            dev.phase_async("amax")
+        self.group.control(0)
+        while True:
+            for _ in range(max(int(check_every), 1)):
+                self._step_async()
+            states = [dev.loop_state() for dev in self.devices]
+            if all(done for done, _ in states):
+                break
+        r = states[0][1]
+        return int(r.n_inner), float(r.ek), bool(r.cap_hit), float(r.min_dt)
 
     def gather(self, field):
         """Owned values of `field` in global particle order (LocalGroup only)."""

@@ -88,6 +88,9 @@ class FakeDevice:
         self.v = values.copy()
         self.d = d
 
+    def field_width(self, field):
+        return self.d if field == "vel" else self.d * self.d
+
     def pack(self, field, ids):
         return self.v[np.asarray(ids)].copy()
 

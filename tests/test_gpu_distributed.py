@@ -153,9 +153,10 @@ POROUS_CASES = {
 }
 
 
+@pytest.mark.parametrize("group", ["local", "local_device"])
 @pytest.mark.parametrize("case", sorted(POROUS_CASES))
 @pytest.mark.parametrize("nranks", [1, 2, 3])
-def test_decomposed_porous_matches_single_domain(nranks, case):
+def test_decomposed_porous_matches_single_domain(nranks, case, group):
     """The porous membrane (BASELINE configs[1] strip, wetted top face; the
     reference's 3D film, wetted centre) split into x-slabs: outer diffusion steps and inner relaxation as device phases
     with host-staged ghost exchanges reproduce the single domain (same tiled
@@ -173,7 +174,8 @@ def test_decomposed_porous_matches_single_domain(nranks, case):
         dt_outer = 1.0
     ref = DevicePorous(lat.pos, lat.vol, lat.constrained, lat.contact, lat.h_axes, model,
                        p["contact_time"], p["evaporation_rate"], sweep="tiled")
-    dec = DecomposedPorous(lat, model, p["contact_time"], p["evaporation_rate"], nranks)
+    dec = DecomposedPorous(lat, model, p["contact_time"], p["evaporation_rate"], nranks,
+                           group=group)
     assert sum((~pl.ghost).sum() for pl in dec.plans) == lat.n
     eta, cfl = p["eta"], p["cfl"]
     for step in (1, 2):
@@ -194,3 +196,36 @@ def test_decomposed_porous_matches_single_domain(nranks, case):
         err = float(np.max(np.abs(got - want))) / scale
         assert err <= 1e-12, (nranks, field, err)
     assert float(np.max(ref.get("fluid_mass"))) > 0
+
+
+@pytest.mark.parametrize("group", ["local", "local_device"])
+def test_decomposed_porous_device_loop(group):
+    """Device-controlled porous inner loop (phases enqueued, rank partials
+    gathered on the device, per-rank control kernel) against the single
+    domain's device loop: same steps, same state to 1e-12."""
+    from paper_2309_04010_b200 import lattices
+    from paper_2309_04010_b200.config import resolve
+    from paper_2309_04010_b200.device import DevicePorous
+    from paper_2309_04010_b200.distributed import DecomposedPorous
+    from paper_2309_04010_b200.scenarios import _membrane
+    p = resolve({"scenario": "membrane_2d"}).params
+    lat = lattices.build_lattice(p)
+    model = _membrane(p)
+    dt_outer = p["t_total"] / p["n_outer"]
+    ref = DevicePorous(lat.pos, lat.vol, lat.constrained, lat.contact, lat.h_axes, model,
+                       p["contact_time"], p["evaporation_rate"], sweep="tiled")
+    dec = DecomposedPorous(lat, model, p["contact_time"], p["evaporation_rate"], 3, group=group)
+    for step in (1, 2):
+        t = step * dt_outer
+        ref.advance_slow(dt_outer, t)
+        dec.advance_slow(dt_outer, t)
+        r = ref.relax(p["eta"], p["cfl"], -1.0, dt_outer, max_inner=15, min_inner=15)
+        n, ek, cap, _ = dec.relax_device(p["eta"], p["cfl"], -1.0, dt_outer, fixed_steps=15,
+                                         check_every=4)
+        assert n == r.n_inner == 15
+        assert abs(ek - r.ek) <= 1e-10 * max(abs(r.ek), 1e-300)
+    for field in ("fluid_mass", "pos", "F"):
+        want = ref.get(field)
+        got = dec.gather(field)
+        scale = max(float(np.max(np.abs(want))), 1e-300)
+        assert float(np.max(np.abs(got - want))) / scale <= 1e-12, field
