@@ -642,11 +642,16 @@ inline void build_tiled(const NbhDev &nb, int sh, TiledSched &t, cudaStream_t s)
                     const int la = e.la, lbb = e.lb;
                     const int64_t a = e.a, b = e.b;
                     // lowest colour free at both ends (first zero bit); with
-                    // balancing, the first free colour among the lowest
-                    // kBalanceWindow free ones whose bank rows (li % 8) and
+                    // balancing, a free colour whose bank rows (li % 8) and
                     // columns (lj % 8) this pair does not push past the
-                    // colour's fullest row / column -- the padding bank_order
-                    // needs is set by those maxima
+                    // colour's fullest row / column (the padding bank_order
+                    // needs is set by those maxima): the first such colour of
+                    // each 64-colour word, words scanned while fewer than
+                    // kBalanceWindow free colours have been seen, the last
+                    // one found wins (else the lowest free colour).  Stopping
+                    // at the first fit across words measured worse (1.43 M vs
+                    // 1.36 M sub-colours, 6.27 vs 6.13 ms), as did a soft
+                    // size cap preferring colours under 400-440 pairs.
                     int c = 256;
                     const int ra = la & 7, cb = lbb & 7;
                     int seen = 0;
