@@ -489,6 +489,17 @@ def run_decomposed(args, world, rank, local):
         "gpu_launches": launches,
         "clocks": clk,
     }
+    # roofline of the whole per-rank step (the decomposed loop has no
+    # per-class events): algorithmic bytes of every class for the rank's
+    # owned particles over the step time
+    sz = dev.sizes()
+    nl = len(plan.local_ids)
+    model = algorithmic_bytes(d, sz["nnz"] / nl, sz["npairs"] / nl, sz["ngroups"] / nl, "tiled")
+    peak, peak_kind = load_peaks()
+    gbs = sum(model.values()) * (n_total / world) / (ms / args.steps / 1e3) / 1e9
+    line["roofline"] = {"kernel": "whole inner step per rank", "bound": "hbm", "achieved": gbs,
+                        "peak": peak, "unit": "GB/s", "frac": gbs / peak, "traffic": None,
+                        "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"}
     if rank == 0:
         emit(line)
     dist.destroy_process_group()
