@@ -298,7 +298,9 @@ def run_ours(args):
         dev.relax_step(dt, eta)
     e2e_s = time.perf_counter() - t0
     e2e = world * n * e2e_steps / e2e_s
-    ctrl_bytes = 160
+    # sizeof(Ctrl) (csrc/damping.cuh): 14 doubles, 4 int64, 4 int, 2 uint64;
+    # per step stable_dt + relax_step move it 2x host->device, 4x back
+    ctrl_bytes = 14 * 8 + 4 * 8 + 4 * 4 + 2 * 8
     # roofline of the dominant kernel class
     peak, peak_kind = load_peaks()
     model = algorithmic_bytes(d, sz["nnz"] / n, sz["npairs"] / n, sz["ngroups"] / n, args.sweep)
