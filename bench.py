@@ -502,9 +502,72 @@ def run_decomposed(args, world, rank, local):
     line["roofline"] = {"kernel": "whole inner step per rank", "bound": "hbm", "achieved": gbs,
                         "peak": peak, "unit": "GB/s", "frac": gbs / peak, "traffic": None,
                         "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"}
+    del dec, dev
+    if not args.no_membrane:
+        try:
+            line["membrane"] = membrane_decomposed(args, world, rank, local)
+        except Exception as e:   # the solid line above stands on its own
+            line["membrane"] = {"error": f"{type(e).__name__}: {e}"}
     if rank == 0:
         emit(line)
     dist.destroy_process_group()
+
+
+def membrane_decomposed(args, world, rank, local):
+    """BASELINE configs[3] on N GPUs: the porous film (fsi_3d, 10 M particles
+    per GPU under weak scaling: the film N times longer along x) on x-slabs,
+    porous inner steps device-controlled (DecomposedPorous.relax_device, NCCL
+    halos and all-gather), one outer diffusion step with its exchanges."""
+    import torch
+    import torch.distributed as dist
+    from paper_2309_04010_b200 import lattices
+    from paper_2309_04010_b200.config import resolve
+    from paper_2309_04010_b200.distributed import DecomposedPorous
+    from paper_2309_04010_b200.scenarios import _membrane, make_policy
+    side = args.membrane_side
+    length = side * (world if args.scaling == "weak" else 1)
+    params = resolve({"scenario": "fsi_3d", "length": length, "breadth": side,
+                      "damping_sweep": "tiled"}).params
+    lat = lattices.build_lattice(params)
+    pol = make_policy(params, float(np.min(lat.h_axes)))
+    t0 = time.perf_counter()
+    dec = DecomposedPorous(lat, _membrane(params), params["contact_time"],
+                           params["evaporation_rate"], world, ranks=[rank], group="torch",
+                           dist=dist, tensor_device=f"cuda:{local}")
+    setup_s = time.perf_counter() - t0
+    dev = dec.devices[0]
+    stream = torch.cuda.ExternalStream(dev.stream_handle())
+    k_in = max(args.steps, 4)
+    dec.advance_slow(pol.dt_outer, pol.dt_outer)
+    dec.relax_device(pol.eta, pol.cfl, -1.0, pol.dt_outer, fixed_steps=3, check_every=3)
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    dec.relax_device(pol.eta, pol.cfl, -1.0, pol.dt_outer, fixed_steps=k_in, check_every=k_in)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    inner_ms = float(t.item()) / k_in
+    dist.barrier()
+    w0 = time.perf_counter()
+    dec.advance_slow(pol.dt_outer, 2 * pol.dt_outer)
+    torch.cuda.synchronize()
+    w = torch.tensor([time.perf_counter() - w0], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(w, op=dist.ReduceOp.MAX)
+    n = lat.n
+    return {"workload": f"fsi_3d porous film {length:g} x {side:g} x {params['thickness']:g} m "
+                        f"({n} particles, {n // world} per GPU), tiled sweep, fp64, {world} x-slabs",
+            "setup_s": setup_s,
+            "inner": {"value": n / (inner_ms / 1e3), "unit": "particle-steps/s",
+                      "ms_per_step": inner_ms,
+                      "timing": "CUDA events on each rank's stream around the device-controlled "
+                                "steps; max over ranks"},
+            "outer_diffusion": {"value": n / float(w.item()), "unit": "particle-steps/s",
+                                "ms_per_step": 1e3 * float(w.item()),
+                                "timing": "wall clock of one outer step (host-synchronised "
+                                          "phases and exchanges); max over ranks"}}
 
 
 def cpu_baseline(params, args, budget_s=20.0, steps=None):
