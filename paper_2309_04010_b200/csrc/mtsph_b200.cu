@@ -101,6 +101,7 @@ extern "C" mtsph_status mtsph_nbh_destroy(mtsph_nbh *nb) {
 
 extern "C" mtsph_status mtsph_nbh_sizes(const mtsph_nbh *h, int64_t *nnz, int64_t *npairs, int64_t *ngroups,
                                         int64_t *nphases) {
+    if (!h) return fail(MTSPH_ERR_ARG, "mtsph_nbh_sizes: null handle");
     const NbhDev &nb = h->nb;
     if (nnz) *nnz = nb.nnz;
     if (npairs) *npairs = nb.npairs;
@@ -118,6 +119,7 @@ extern "C" mtsph_status mtsph_nbh_sizes(const mtsph_nbh *h, int64_t *nnz, int64_
 }
 
 extern "C" mtsph_status mtsph_nbh_permutation(const mtsph_nbh *h, int64_t *perm) {
+    if (!h) return fail(MTSPH_ERR_ARG, "mtsph_nbh_permutation: null handle");
     API_BEGIN
     h->nb.perm.download(perm, h->nb.n, h->s);
     MT_CUDA(cudaStreamSynchronize(h->s));
@@ -136,6 +138,7 @@ static void grad_host(int d, const double *rel, const KSpec &ks, double *g) {
 extern "C" mtsph_status mtsph_nbh_export(const mtsph_nbh *h, int64_t *indptr, int64_t *idx, double *grad0,
                                          int64_t *pair_i, int64_t *pair_j, double *pair_damp,
                                          double *pair_grad, int64_t *pair_group, double *corr) {
+    if (!h) return fail(MTSPH_ERR_ARG, "mtsph_nbh_export: null handle");
     API_BEGIN
     const NbhDev &nb = h->nb;
     const int64_t n = nb.n;
@@ -434,6 +437,7 @@ static void sync32(mtsph_solid *S) {
 }
 
 extern "C" mtsph_status mtsph_solid_set_precision(mtsph_solid *S, int bits) {
+    if (!S) return fail(MTSPH_ERR_ARG, "mtsph_solid_set_precision: null handle");
     API_BEGIN
     if (bits != 32 && bits != 64) throw Error(MTSPH_ERR_ARG, "precision must be 32 or 64 bits");
     if (bits == S->prec) return MTSPH_OK;
@@ -484,6 +488,7 @@ extern "C" mtsph_status mtsph_solid_set_precision(mtsph_solid *S, int bits) {
 }
 
 extern "C" mtsph_status mtsph_solid_precision(const mtsph_solid *S, int *bits) {
+    if (!S) return fail(MTSPH_ERR_ARG, "mtsph_solid_precision: null handle");
     *bits = S->prec;
     return MTSPH_OK;
 }
@@ -625,6 +630,7 @@ extern "C" mtsph_status mtsph_solid_destroy(mtsph_solid *s) {
 
 extern "C" mtsph_status mtsph_solid_set_ramp(mtsph_solid *S, double end_disp, int64_t ramp_steps,
                                              int64_t ramp_left) {
+    if (!S) return fail(MTSPH_ERR_ARG, "mtsph_solid_set_ramp: null handle");
     API_BEGIN
     S->pull_ctrl();
     S->hc->ramp_disp = end_disp / (double)(ramp_steps > 0 ? ramp_steps : 1);
@@ -634,6 +640,7 @@ extern "C" mtsph_status mtsph_solid_set_ramp(mtsph_solid *S, double end_disp, in
 }
 
 extern "C" mtsph_status mtsph_solid_ramp_left(const mtsph_solid *S, int64_t *ramp_left) {
+    if (!S) return fail(MTSPH_ERR_ARG, "mtsph_solid_ramp_left: null handle");
     API_BEGIN
     const_cast<mtsph_solid *>(S)->pull_ctrl();
     *ramp_left = S->hc->ramp_left;
@@ -641,6 +648,7 @@ extern "C" mtsph_status mtsph_solid_ramp_left(const mtsph_solid *S, int64_t *ram
 }
 
 extern "C" mtsph_status mtsph_solid_stable_dt(mtsph_solid *S, double cfl, double *dt) {
+    if (!S) return fail(MTSPH_ERR_ARG, "mtsph_solid_stable_dt: null handle");
     API_BEGIN
     S->pull_ctrl();
     S->hc->cfl = cfl;
@@ -652,6 +660,7 @@ extern "C" mtsph_status mtsph_solid_stable_dt(mtsph_solid *S, double cfl, double
 }
 
 extern "C" mtsph_status mtsph_solid_relax_step(mtsph_solid *S, double dt, double eta, double *ek) {
+    if (!S) return fail(MTSPH_ERR_ARG, "mtsph_solid_relax_step: null handle");
     API_BEGIN
     S->pull_ctrl();
     S->hc->dt = dt;
@@ -679,6 +688,7 @@ static cudaGraphExec_t solid_graph(mtsph_solid *S, int which) {
 }
 
 extern "C" mtsph_status mtsph_solid_relax(mtsph_solid *S, const mtsph_inner_params *p, mtsph_inner_result *r) {
+    if (!S) return fail(MTSPH_ERR_ARG, "mtsph_solid_relax: null handle");
     API_BEGIN
     S->pull_ctrl();
     Ctrl *c = S->hc;
@@ -733,6 +743,7 @@ static void g_timed_drop(const mtsph_solid *owner) {
 
 extern "C" mtsph_status mtsph_solid_run_steps(mtsph_solid *S, const mtsph_inner_params *p, int64_t nsteps,
                                               double timing[7]) {
+    if (!S) return fail(MTSPH_ERR_ARG, "mtsph_solid_run_steps: null handle");
     API_BEGIN
     if (nsteps <= 0) throw Error(MTSPH_ERR_ARG, "nsteps must be positive");
     S->pull_ctrl();
@@ -826,6 +837,7 @@ template <int D> __global__ void k_unpack(int64_t n, int64_t m, const int64_t *_
 }
 
 extern "C" mtsph_status mtsph_solid_set_step(mtsph_solid *S, double dt, double eta) {
+    if (!S) return fail(MTSPH_ERR_ARG, "mtsph_solid_set_step: null handle");
     API_BEGIN
     S->pull_ctrl();
     S->hc->dt = dt;
@@ -837,6 +849,7 @@ extern "C" mtsph_status mtsph_solid_set_step(mtsph_solid *S, double dt, double e
 }
 
 extern "C" mtsph_status mtsph_solid_colours(const mtsph_solid *S, int *nc) {
+    if (!S) return fail(MTSPH_ERR_ARG, "mtsph_solid_colours: null handle");
     *nc = S->nb.sweep == 3 ? (int)S->tiled.colour_ptr.size() - 1 : 0;
     return MTSPH_OK;
 }
@@ -917,6 +930,7 @@ template <int D> static void solid_phase(mtsph_solid *S, int phase, int arg, dou
 }
 
 extern "C" mtsph_status mtsph_solid_phase(mtsph_solid *S, int phase, int arg, double out[2]) {
+    if (!S) return fail(MTSPH_ERR_ARG, "mtsph_solid_phase: null handle");
     API_BEGIN
     if (S->prec != 64) throw Error(MTSPH_ERR_ARG, "multi-rank phases run in fp64");
     if (S->d == 2) solid_phase<2>(S, phase, arg, out); else solid_phase<3>(S, phase, arg, out);
@@ -975,6 +989,7 @@ template <int D> static void solid_phase_async(mtsph_solid *S, int phase, int ar
 }
 
 extern "C" mtsph_status mtsph_solid_phase_async(mtsph_solid *S, int phase, int arg) {
+    if (!S) return fail(MTSPH_ERR_ARG, "mtsph_solid_phase_async: null handle");
     API_BEGIN
     if (S->prec != 64) throw Error(MTSPH_ERR_ARG, "multi-rank phases run in fp64");
     if (S->d == 2) solid_phase_async<2>(S, phase, arg); else solid_phase_async<3>(S, phase, arg);
@@ -982,6 +997,7 @@ extern "C" mtsph_status mtsph_solid_phase_async(mtsph_solid *S, int phase, int a
 }
 
 extern "C" mtsph_status mtsph_solid_begin_loop(mtsph_solid *S, const mtsph_inner_params *p) {
+    if (!S) return fail(MTSPH_ERR_ARG, "mtsph_solid_begin_loop: null handle");
     API_BEGIN
     S->pull_ctrl();
     Ctrl *c = S->hc;
@@ -1001,6 +1017,7 @@ extern "C" mtsph_status mtsph_solid_begin_loop(mtsph_solid *S, const mtsph_inner
 }
 
 extern "C" mtsph_status mtsph_solid_rank_partials(mtsph_solid *S, int mode, double *dev_out) {
+    if (!S) return fail(MTSPH_ERR_ARG, "mtsph_solid_rank_partials: null handle");
     API_BEGIN
     if (mode != CTRL_INIT && mode != CTRL_STEP) throw Error(MTSPH_ERR_ARG, "mode: 0 (initial step) or 1 (step)");
     k_rank_partials<<<1, 256, 0, S->s>>>(S->ctrl.p, S->part.p, S->nblk, mode, dev_out);
@@ -1011,6 +1028,7 @@ extern "C" mtsph_status mtsph_solid_rank_partials(mtsph_solid *S, int mode, doub
 
 extern "C" mtsph_status mtsph_solid_control_ranks(mtsph_solid *S, const double *dev_gathered, int nranks,
                                                   int mode) {
+    if (!S) return fail(MTSPH_ERR_ARG, "mtsph_solid_control_ranks: null handle");
     API_BEGIN
     if (mode != CTRL_INIT && mode != CTRL_STEP) throw Error(MTSPH_ERR_ARG, "mode: 0 (initial step) or 1 (step)");
     if (nranks < 1) throw Error(MTSPH_ERR_ARG, "nranks must be positive");
@@ -1021,6 +1039,7 @@ extern "C" mtsph_status mtsph_solid_control_ranks(mtsph_solid *S, const double *
 }
 
 extern "C" mtsph_status mtsph_solid_loop_state(mtsph_solid *S, mtsph_inner_result *r, int *done) {
+    if (!S) return fail(MTSPH_ERR_ARG, "mtsph_solid_loop_state: null handle");
     API_BEGIN
     S->pull_ctrl();
     const Ctrl *c = S->hc;
@@ -1076,6 +1095,7 @@ static void pack_common(mtsph_solid *S, const char *field, int64_t m, const int6
 
 extern "C" mtsph_status mtsph_solid_pack(mtsph_solid *S, const char *field, int64_t m, const int64_t *ids,
                                          double *host) {
+    if (!S) return fail(MTSPH_ERR_ARG, "mtsph_solid_pack: null handle");
     API_BEGIN
     pack_common(S, field, m, ids, host, nullptr, true);
     API_END
@@ -1083,6 +1103,7 @@ extern "C" mtsph_status mtsph_solid_pack(mtsph_solid *S, const char *field, int6
 
 extern "C" mtsph_status mtsph_solid_unpack(mtsph_solid *S, const char *field, int64_t m, const int64_t *ids,
                                            const double *host) {
+    if (!S) return fail(MTSPH_ERR_ARG, "mtsph_solid_unpack: null handle");
     API_BEGIN
     pack_common(S, field, m, ids, nullptr, host, false);
     API_END
@@ -1099,6 +1120,7 @@ static int pack_field(const char *field) {
 
 extern "C" mtsph_status mtsph_solid_internal_ids(mtsph_solid *S, int64_t m, const int64_t *ids,
                                                  int64_t *internal) {
+    if (!S) return fail(MTSPH_ERR_ARG, "mtsph_solid_internal_ids: null handle");
     API_BEGIN
     if (S->iperm_h.empty()) {
         S->iperm_h.resize(S->n);
@@ -1113,12 +1135,14 @@ extern "C" mtsph_status mtsph_solid_internal_ids(mtsph_solid *S, int64_t m, cons
 }
 
 extern "C" mtsph_status mtsph_solid_stream(const mtsph_solid *S, void **stream) {
+    if (!S) return fail(MTSPH_ERR_ARG, "mtsph_solid_stream: null handle");
     *stream = (void *)S->s;
     return MTSPH_OK;
 }
 
 extern "C" mtsph_status mtsph_solid_pack_device(mtsph_solid *S, const char *field, int64_t m,
                                                 const int64_t *ids, double *out) {
+    if (!S) return fail(MTSPH_ERR_ARG, "mtsph_solid_pack_device: null handle");
     API_BEGIN
     if (S->prec != 64) throw Error(MTSPH_ERR_ARG, "multi-rank exchanges run in fp64");
     const int which = pack_field(field);
@@ -1132,6 +1156,7 @@ extern "C" mtsph_status mtsph_solid_pack_device(mtsph_solid *S, const char *fiel
 
 extern "C" mtsph_status mtsph_solid_unpack_device(mtsph_solid *S, const char *field, int64_t m,
                                                   const int64_t *ids, const double *in) {
+    if (!S) return fail(MTSPH_ERR_ARG, "mtsph_solid_unpack_device: null handle");
     API_BEGIN
     if (S->prec != 64) throw Error(MTSPH_ERR_ARG, "multi-rank exchanges run in fp64");
     const int which = pack_field(field);
@@ -1144,6 +1169,7 @@ extern "C" mtsph_status mtsph_solid_unpack_device(mtsph_solid *S, const char *fi
 }
 
 extern "C" mtsph_status mtsph_solid_measure(mtsph_solid *S, double out[5]) {
+    if (!S) return fail(MTSPH_ERR_ARG, "mtsph_solid_measure: null handle");
     API_BEGIN
     sync64(S);
     SolidArgs A = S->args();
@@ -1174,6 +1200,7 @@ extern "C" mtsph_status mtsph_solid_measure(mtsph_solid *S, double out[5]) {
 enum FieldKind { FK_SOA_VEC, FK_SOA_TEN, FK_SCALAR, FK_VEL, FK_REF };
 
 extern "C" mtsph_status mtsph_solid_get(mtsph_solid *S, const char *field, double *host) {
+    if (!S) return fail(MTSPH_ERR_ARG, "mtsph_solid_get: null handle");
     API_BEGIN
     sync64(S);
     const int64_t n = S->n;
@@ -1207,6 +1234,7 @@ extern "C" mtsph_status mtsph_solid_get(mtsph_solid *S, const char *field, doubl
 }
 
 extern "C" mtsph_status mtsph_solid_set(mtsph_solid *S, const char *field, const double *host) {
+    if (!S) return fail(MTSPH_ERR_ARG, "mtsph_solid_set: null handle");
     API_BEGIN
     sync64(S);
     const int64_t n = S->n;
@@ -1240,6 +1268,7 @@ extern "C" mtsph_status mtsph_solid_set(mtsph_solid *S, const char *field, const
 }
 
 extern "C" mtsph_status mtsph_solid_sizes(const mtsph_solid *S, int64_t out[4]) {
+    if (!S) return fail(MTSPH_ERR_ARG, "mtsph_solid_sizes: null handle");
     const NbhDev &nb = S->nb;
     out[0] = nb.nnz;
     out[1] = nb.sweep == 3 ? S->tiled.npairs : nb.npairs;
@@ -1255,6 +1284,7 @@ extern "C" mtsph_status mtsph_solid_sizes(const mtsph_solid *S, int64_t out[4]) 
 }
 
 extern "C" mtsph_status mtsph_solid_launches(const mtsph_solid *S, int64_t *count) {
+    if (!S) return fail(MTSPH_ERR_ARG, "mtsph_solid_launches: null handle");
     *count = S->launches;
     return MTSPH_OK;
 }

@@ -243,6 +243,7 @@ template <int D> static int64_t porous_advance(mtsph_porous *P, double dt, doubl
 
 extern "C" mtsph_status mtsph_porous_advance_slow(mtsph_porous *P, double dt_outer, double t,
                                                   int64_t *clamped) {
+    if (!P) return fail(MTSPH_ERR_ARG, "mtsph_porous_advance_slow: null handle");
     API_BEGIN
     P->pull_ctrl();
     P->hc->err_inv = ~0ull;
@@ -335,6 +336,7 @@ template <int D> static void porous_phase(mtsph_porous *P, int phase, int arg, d
 }
 
 extern "C" mtsph_status mtsph_porous_set_step(mtsph_porous *P, double dt, double eta) {
+    if (!P) return fail(MTSPH_ERR_ARG, "mtsph_porous_set_step: null handle");
     API_BEGIN
     P->pull_ctrl();
     P->hc->dt = dt;
@@ -346,12 +348,14 @@ extern "C" mtsph_status mtsph_porous_set_step(mtsph_porous *P, double dt, double
 }
 
 extern "C" mtsph_status mtsph_porous_set_outer(mtsph_porous *P, double dt_outer, double t) {
+    if (!P) return fail(MTSPH_ERR_ARG, "mtsph_porous_set_outer: null handle");
     P->outer_dt = dt_outer;
     P->outer_t = t;
     return MTSPH_OK;
 }
 
 extern "C" mtsph_status mtsph_porous_phase(mtsph_porous *P, int phase, int arg, double out[2]) {
+    if (!P) return fail(MTSPH_ERR_ARG, "mtsph_porous_phase: null handle");
     API_BEGIN
     if (P->d == 2) porous_phase<2>(P, phase, arg, out); else porous_phase<3>(P, phase, arg, out);
     if (phase == MTSPH_POR_STRESS || phase == MTSPH_POR_PREP_MAP || phase == MTSPH_POR_PREP) {
@@ -394,6 +398,7 @@ static void porous_pack_common(mtsph_porous *P, const char *field, int64_t m, co
 
 extern "C" mtsph_status mtsph_porous_pack(mtsph_porous *P, const char *field, int64_t m, const int64_t *ids,
                                           double *host) {
+    if (!P) return fail(MTSPH_ERR_ARG, "mtsph_porous_pack: null handle");
     API_BEGIN
     porous_pack_common(P, field, m, ids, host, nullptr, true);
     API_END
@@ -401,12 +406,14 @@ extern "C" mtsph_status mtsph_porous_pack(mtsph_porous *P, const char *field, in
 
 extern "C" mtsph_status mtsph_porous_unpack(mtsph_porous *P, const char *field, int64_t m, const int64_t *ids,
                                             const double *host) {
+    if (!P) return fail(MTSPH_ERR_ARG, "mtsph_porous_unpack: null handle");
     API_BEGIN
     porous_pack_common(P, field, m, ids, nullptr, host, false);
     API_END
 }
 
 extern "C" mtsph_status mtsph_porous_phase_async(mtsph_porous *P, int phase, int arg) {
+    if (!P) return fail(MTSPH_ERR_ARG, "mtsph_porous_phase_async: null handle");
     API_BEGIN
     double out[2];
     if (P->d == 2) porous_phase<2>(P, phase, arg, out, false); else porous_phase<3>(P, phase, arg, out, false);
@@ -415,6 +422,7 @@ extern "C" mtsph_status mtsph_porous_phase_async(mtsph_porous *P, int phase, int
 
 extern "C" mtsph_status mtsph_porous_begin_loop(mtsph_porous *P, const mtsph_inner_params *p,
                                                 double vol_movable) {
+    if (!P) return fail(MTSPH_ERR_ARG, "mtsph_porous_begin_loop: null handle");
     API_BEGIN
     P->pull_ctrl();
     Ctrl *c = P->hc;
@@ -435,6 +443,7 @@ extern "C" mtsph_status mtsph_porous_begin_loop(mtsph_porous *P, const mtsph_inn
 }
 
 extern "C" mtsph_status mtsph_porous_rank_partials(mtsph_porous *P, int mode, double *dev_out) {
+    if (!P) return fail(MTSPH_ERR_ARG, "mtsph_porous_rank_partials: null handle");
     API_BEGIN
     if (mode != CTRL_INIT && mode != CTRL_STEP) throw Error(MTSPH_ERR_ARG, "mode: 0 (initial step) or 1 (step)");
     k_rank_partials<<<1, 256, 0, P->s>>>(P->ctrl.p, P->part.p, P->nblk, mode, dev_out);
@@ -445,6 +454,7 @@ extern "C" mtsph_status mtsph_porous_rank_partials(mtsph_porous *P, int mode, do
 
 extern "C" mtsph_status mtsph_porous_control_ranks(mtsph_porous *P, const double *dev_gathered, int nranks,
                                                    int mode) {
+    if (!P) return fail(MTSPH_ERR_ARG, "mtsph_porous_control_ranks: null handle");
     API_BEGIN
     if (mode != CTRL_INIT && mode != CTRL_STEP) throw Error(MTSPH_ERR_ARG, "mode: 0 (initial step) or 1 (step)");
     if (nranks < 1) throw Error(MTSPH_ERR_ARG, "nranks must be positive");
@@ -455,6 +465,7 @@ extern "C" mtsph_status mtsph_porous_control_ranks(mtsph_porous *P, const double
 }
 
 extern "C" mtsph_status mtsph_porous_loop_state(mtsph_porous *P, mtsph_inner_result *r, int *done) {
+    if (!P) return fail(MTSPH_ERR_ARG, "mtsph_porous_loop_state: null handle");
     API_BEGIN
     P->pull_ctrl();
     const Ctrl *c = P->hc;
@@ -470,6 +481,7 @@ extern "C" mtsph_status mtsph_porous_loop_state(mtsph_porous *P, mtsph_inner_res
 
 extern "C" mtsph_status mtsph_porous_internal_ids(mtsph_porous *P, int64_t m, const int64_t *ids,
                                                   int64_t *internal) {
+    if (!P) return fail(MTSPH_ERR_ARG, "mtsph_porous_internal_ids: null handle");
     API_BEGIN
     if (P->iperm_h.empty()) {
         P->iperm_h.resize(P->n);
@@ -484,6 +496,7 @@ extern "C" mtsph_status mtsph_porous_internal_ids(mtsph_porous *P, int64_t m, co
 }
 
 extern "C" mtsph_status mtsph_porous_stream(const mtsph_porous *P, void **stream) {
+    if (!P) return fail(MTSPH_ERR_ARG, "mtsph_porous_stream: null handle");
     *stream = (void *)P->s;
     return MTSPH_OK;
 }
@@ -500,6 +513,7 @@ static int porous_field(const char *field) {
 // the kernel is enqueued on the problem's stream (no host synchronisation)
 extern "C" mtsph_status mtsph_porous_pack_device(mtsph_porous *P, const char *field, int64_t m,
                                                  const int64_t *ids, double *out) {
+    if (!P) return fail(MTSPH_ERR_ARG, "mtsph_porous_pack_device: null handle");
     API_BEGIN
     const int which = porous_field(field);
     if (m <= 0) return MTSPH_OK;
@@ -513,6 +527,7 @@ extern "C" mtsph_status mtsph_porous_pack_device(mtsph_porous *P, const char *fi
 
 extern "C" mtsph_status mtsph_porous_unpack_device(mtsph_porous *P, const char *field, int64_t m,
                                                    const int64_t *ids, const double *in) {
+    if (!P) return fail(MTSPH_ERR_ARG, "mtsph_porous_unpack_device: null handle");
     API_BEGIN
     const int which = porous_field(field);
     if (m <= 0) return MTSPH_OK;
@@ -527,11 +542,13 @@ extern "C" mtsph_status mtsph_porous_unpack_device(mtsph_porous *P, const char *
 }
 
 extern "C" mtsph_status mtsph_porous_colours(const mtsph_porous *P, int *nc) {
+    if (!P) return fail(MTSPH_ERR_ARG, "mtsph_porous_colours: null handle");
     *nc = P->nb.sweep == 3 ? (int)P->tiled.colour_ptr.size() - 1 : 0;
     return MTSPH_OK;
 }
 
 extern "C" mtsph_status mtsph_porous_sizes(const mtsph_porous *P, int64_t out[4]) {
+    if (!P) return fail(MTSPH_ERR_ARG, "mtsph_porous_sizes: null handle");
     const NbhDev &nb = P->nb;
     out[0] = nb.nnz;
     out[1] = nb.sweep == 3 ? P->tiled.npairs : nb.npairs;
@@ -541,6 +558,7 @@ extern "C" mtsph_status mtsph_porous_sizes(const mtsph_porous *P, int64_t out[4]
 }
 
 extern "C" mtsph_status mtsph_porous_outer_ms(const mtsph_porous *P, double *ms) {
+    if (!P) return fail(MTSPH_ERR_ARG, "mtsph_porous_outer_ms: null handle");
     API_BEGIN
     if (!P->ev_outer[0]) throw Error(MTSPH_ERR_ARG, "no outer step has run");
     float f = 0.f;
@@ -550,6 +568,7 @@ extern "C" mtsph_status mtsph_porous_outer_ms(const mtsph_porous *P, double *ms)
 }
 
 extern "C" mtsph_status mtsph_porous_stable_dt(mtsph_porous *P, double cfl, double *dt) {
+    if (!P) return fail(MTSPH_ERR_ARG, "mtsph_porous_stable_dt: null handle");
     API_BEGIN
     P->pull_ctrl();
     P->hc->cfl = cfl;
@@ -561,6 +580,7 @@ extern "C" mtsph_status mtsph_porous_stable_dt(mtsph_porous *P, double cfl, doub
 }
 
 extern "C" mtsph_status mtsph_porous_relax_step(mtsph_porous *P, double dt, double eta, double *ek) {
+    if (!P) return fail(MTSPH_ERR_ARG, "mtsph_porous_relax_step: null handle");
     API_BEGIN
     P->pull_ctrl();
     P->hc->dt = dt;
@@ -589,6 +609,7 @@ static cudaGraphExec_t porous_graph(mtsph_porous *P, int which) {
 
 extern "C" mtsph_status mtsph_porous_relax(mtsph_porous *P, const mtsph_inner_params *p,
                                            mtsph_inner_result *r) {
+    if (!P) return fail(MTSPH_ERR_ARG, "mtsph_porous_relax: null handle");
     API_BEGIN
     P->pull_ctrl();
     Ctrl *c = P->hc;
@@ -624,6 +645,7 @@ extern "C" mtsph_status mtsph_porous_relax(mtsph_porous *P, const mtsph_inner_pa
 }
 
 extern "C" mtsph_status mtsph_porous_refresh_velocities(mtsph_porous *P) {
+    if (!P) return fail(MTSPH_ERR_ARG, "mtsph_porous_refresh_velocities: null handle");
     API_BEGIN
     PorousArgs A = P->args();
     if (P->d == 2) k_por_refresh<2><<<blocks_for(P->n), 256, 0, P->s>>>(A);
@@ -648,6 +670,7 @@ static DBuf<double> *porous_field(mtsph_porous *P, const std::string &f, int &co
 }
 
 extern "C" mtsph_status mtsph_porous_get(mtsph_porous *P, const char *field, double *host) {
+    if (!P) return fail(MTSPH_ERR_ARG, "mtsph_porous_get: null handle");
     API_BEGIN
     const int64_t n = P->n;
     const int d = P->d;
@@ -677,6 +700,7 @@ extern "C" mtsph_status mtsph_porous_get(mtsph_porous *P, const char *field, dou
 }
 
 extern "C" mtsph_status mtsph_porous_set(mtsph_porous *P, const char *field, const double *host) {
+    if (!P) return fail(MTSPH_ERR_ARG, "mtsph_porous_set: null handle");
     API_BEGIN
     const int64_t n = P->n;
     const int d = P->d;
@@ -705,6 +729,7 @@ extern "C" mtsph_status mtsph_porous_set(mtsph_porous *P, const char *field, con
 }
 
 extern "C" mtsph_status mtsph_porous_launches(const mtsph_porous *P, int64_t *count) {
+    if (!P) return fail(MTSPH_ERR_ARG, "mtsph_porous_launches: null handle");
     *count = P->launches;
     return MTSPH_OK;
 }

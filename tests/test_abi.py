@@ -79,3 +79,26 @@ def test_select_device_without_gpu_fails_loudly():
         pytest.skip("a GPU is visible")
     with pytest.raises(errors.BackendError):
         select_device(0)
+
+
+def test_null_handles_are_rejected():
+    """Every entry point that takes a problem / neighbourhood handle returns
+    MTSPH_ERR_ARG with a message for a null handle (destroy: a no-op, like
+    free(NULL)) -- no device needed, nothing is dereferenced."""
+    import ctypes
+    from paper_2309_04010_b200 import _lib
+    lib = _lib.load_library(require_device=False)
+    text = re.sub(r"/\*.*?\*/", "", open(HEADER).read(), flags=re.S)
+    names = sorted(set(re.findall(
+        r"\b(mtsph_[a-z0-9_]+)\s*\(\s*(?:const\s+)?mtsph_(?:solid|porous|nbh)\s*\*", text)))
+    assert len(names) >= 50
+    for name in names:
+        _, argtypes = _lib.SIGNATURES[name]
+        args = [0.0 if t is ctypes.c_double else 0 if t in (ctypes.c_int, ctypes.c_int64)
+                else None for t in argtypes]
+        st = getattr(lib, name)(*args)
+        if name.endswith("_destroy"):
+            assert st == 0, name
+        else:
+            assert st == 1, name
+            assert b"null handle" in lib.mtsph_last_error(), name
