@@ -859,15 +859,6 @@ template <int D> static void solid_phase(mtsph_solid *S, int phase, int arg, dou
     const unsigned nb = blocks_for(S->n);
     cudaStream_t s = S->s;
     out[0] = out[1] = 0.0;
-    auto reduce_parts = [&](int seg, bool is_sum) {
-        std::vector<double> h(S->nblk);
-        S->part.download(h.data(), S->nblk, s);
-        MT_CUDA(cudaStreamSynchronize(s));
-        double r = 0.0;
-        for (double v : h) r = is_sum ? r + v : std::max(r, v);
-        (void)seg;
-        return r;
-    };
     switch (phase) {
     case MTSPH_PHASE_KICK_DRIFT:
         k_solid_kick_drift<D><<<nb, 256, 0, s>>>(A);
@@ -924,7 +915,6 @@ template <int D> static void solid_phase(mtsph_solid *S, int phase, int arg, dou
     default:
         throw Error(MTSPH_ERR_ARG, "unknown phase");
     }
-    (void)reduce_parts;
     MT_LAUNCH_CHECK();
     MT_CUDA(cudaStreamSynchronize(s));
 }
