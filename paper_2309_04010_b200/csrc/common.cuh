@@ -318,17 +318,34 @@ template <int BT> __device__ __forceinline__ double block_sum(double v, double *
     return r;  // valid in thread 0
 }
 
+// (the lanes past the block's warp count pad with -inf / +inf, so any sign
+// of value reduces correctly)
 template <int BT> __device__ __forceinline__ double block_max(double v, double *sh) {
     const int t = threadIdx.x;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_down_sync(0xffffffffu, v, o));
     if ((t & 31) == 0) sh[t >> 5] = v;
     __syncthreads();
-    double r = 0.0;
+    double r = -INFINITY;
     if (t < 32) {
-        r = (t < BT / 32) ? sh[t] : 0.0;
+        r = (t < BT / 32) ? sh[t] : -INFINITY;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) r = fmax(r, __shfl_down_sync(0xffffffffu, r, o));
+    }
+    __syncthreads();
+    return r;
+}
+template <int BT> __device__ __forceinline__ double block_min(double v, double *sh) {
+    const int t = threadIdx.x;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_down_sync(0xffffffffu, v, o));
+    if ((t & 31) == 0) sh[t >> 5] = v;
+    __syncthreads();
+    double r = INFINITY;
+    if (t < 32) {
+        r = (t < BT / 32) ? sh[t] : INFINITY;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) r = fmin(r, __shfl_down_sync(0xffffffffu, r, o));
     }
     __syncthreads();
     return r;

@@ -1182,7 +1182,7 @@ extern "C" mtsph_status mtsph_solid_measure(mtsph_solid *S, double out[5]) {
     out[0] = -fx;
     out[1] = rad;
     out[2] = S->mat.plastic ? amax : 0.0;
-    out[3] = S->mat.plastic ? amin : 0.0;
+    out[3] = S->mat.plastic && amin < 1e308 ? amin : 0.0;   // no mid-span particles: 0
     out[4] = bad > 0 ? 0.0 : 1.0;
     API_END
 }

@@ -655,7 +655,7 @@ __global__ void __launch_bounds__(256) k_solid_measure(SolidArgs A, double *out 
     const double s0 = block_sum<256>(fx, sh);
     const double s1 = block_max<256>(rad, sh);
     const double s2 = block_max<256>(amax, sh);
-    const double s3 = -block_max<256>(-amin, sh);
+    const double s3 = block_min<256>(amin, sh);
     const double s4 = block_max<256>(bad, sh);
     if (threadIdx.x == 0) {
         const int nb = gridDim.x;

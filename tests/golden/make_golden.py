@@ -7,6 +7,7 @@ committed so that tests can pin the oracle and the CUDA path without the
 reference being present.
 
     python tests/golden/make_golden.py            # rewrites tests/golden/*.npz
+    python tests/golden/make_golden.py runs       # only runs.npz (any maker name)
 
 Every case records both the inputs and the reference outputs, so the
 fixtures are self-describing.  Reference call sites used (file:line of
@@ -337,14 +338,51 @@ def make_runs(m):
     print("runs.npz", len(out), "arrays")
 
 
+# the acceptance-suite configurations (reference tests/test_acceptance.py:246
+# desk necking, :323 paper-scale FSI), first outer steps only
+ACCEPT_NECK = {"scenario": "necking_2d", "dp": 12.826e-3 / 25, "n_outer": 1000}
+ACCEPT_FSI = {"scenario": "fsi_2d"}
+ACCEPT_STEPS = {"an2_": 12, "af2_": 125}  # necking: through mid-span yield (step 11); FSI: whole run
+
+
+def make_acceptance_heads(m):
+    """First outer steps of the acceptance configurations (observables and
+    the final state), for parity at the reference's own acceptance sizes."""
+    import dataclasses
+    from mtsph.config import resolve
+    from mtsph.scenarios import build
+    from mtsph.stepping import run_outer_inner
+
+    out = {}
+    for prefix, raw in (("an2_", ACCEPT_NECK), ("af2_", ACCEPT_FSI)):
+        problem, policy = build(resolve(raw).params)
+        obs, counters = run_outer_inner(
+            problem, dataclasses.replace(policy, n_outer=ACCEPT_STEPS[prefix]))
+        st = problem.state
+        out.update({prefix + k: getattr(obs, k) for k in
+                    ("time", "reaction_force", "neck_disp", "amplitude", "ek_ratio", "n_inner")})
+        out[prefix + "pos"] = st.pos
+        for k, v in obs.extras.items():
+            out[prefix + k] = v
+        if hasattr(st, "vel_solid"):
+            out.update({prefix + "vel": st.vel_solid, prefix + "fluid_mass": st.fluid_mass,
+                        prefix + "saturation": st.saturation})
+        else:
+            out.update({prefix + "vel": st.vel, prefix + "alpha": problem.plastic.alpha})
+        print(prefix, "n", st.n, "n_inner", obs.n_inner.tolist())
+    np.savez_compressed(os.path.join(HERE, "acceptance_heads.npz"), **out)
+    print("acceptance_heads.npz", len(out), "arrays")
+
+
+MAKERS = ("neighborhoods", "operators", "constitutive", "porous", "trajectories", "runs",
+          "acceptance_heads")
+
+
 def main():
+    """make_golden.py [name ...]: all fixtures, or only the named ones."""
     m = _import_reference()
-    make_neighborhoods(m)
-    make_operators(m)
-    make_constitutive(m)
-    make_porous(m)
-    make_trajectories(m)
-    make_runs(m)
+    for name in sys.argv[1:] or MAKERS:
+        globals()["make_" + name](m)
 
 
 if __name__ == "__main__":
