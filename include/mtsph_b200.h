@@ -314,7 +314,8 @@ mtsph_status mtsph_porous_advance_slow(mtsph_porous *p, double dt_outer, double 
 /* device time (CUDA events on the problem's stream) of the kernels of the
  * last advance_slow, in ms (benchmark instrumentation)                   */
 mtsph_status mtsph_porous_outer_ms(const mtsph_porous *p, double *ms);
-/* neighbour entries, damping pairs, groups, sweep colours (as mtsph_solid_sizes) */
+/* neighbour entries, damping pairs, groups, sweep colours (tiled) or
+   dependency levels (serial), as mtsph_solid_sizes                      */
 mtsph_status mtsph_porous_sizes(const mtsph_porous *p, int64_t out[4]);
 mtsph_status mtsph_porous_stable_dt(mtsph_porous *p, double cfl, double *dt);
 mtsph_status mtsph_porous_relax_step(mtsph_porous *p, double dt, double eta, double *ek);

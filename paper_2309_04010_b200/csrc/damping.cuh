@@ -202,6 +202,286 @@ __global__ void __launch_bounds__(1024) k_sweep_serial(SweepArgs A, const int64_
     }
 }
 
+// ---- exact serial order, small problems: velocities and the level table
+// in shared memory.  The global kernel above pays a chain of dependent L2
+// loads per level (level table -> group -> pair -> positions -> velocity)
+// before its barrier; here the velocities live in shared memory and each
+// thread's single-pair entries of the next levels (i, j and the static
+// pair_damp, precomputed in level order by k_serial_entries) are loaded
+// ahead through a register ring, so a level costs a shared-memory exchange
+// and a barrier.  Same operations in the same order: bit-identical to
+// k_sweep_serial (tests/test_gpu_solid.py).  Multi-pair groups
+// (simultaneous solves) take the global path's solver on the shared copy.
+
+// entry k (level order): a single pair -> (i | j << 32, pair_damp); a group
+// of 2..kGroupMax pairs -> (-2 - (side offset << 8 | count), 0) with its
+// pairs' (i | j << 32, pair_damp) at side[offset ...]; a larger group ->
+// (-2 - (g << 8), 0) (count 0: the global solver)
+constexpr int kGroupMax = 8;
+
+__device__ __forceinline__ double2 pair_entry(int32_t i, int32_t j, double pd) {
+    const unsigned long long ij = (unsigned long long)(uint32_t)i | ((unsigned long long)(uint32_t)j << 32);
+    return make_double2(__longlong_as_double((long long)ij), pd);
+}
+
+template <int D>
+__global__ void k_serial_entries(SweepArgs A, const int64_t *__restrict__ level_groups, int64_t ng,
+                                 const int64_t *__restrict__ side_off, double2 *out, double2 *side) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= ng) return;
+    const int64_t g = level_groups[k];
+    const int64_t lo = A.gptr[g], hi = A.gptr[g + 1];
+    if (hi - lo == 1) {
+        const int32_t i = A.pi[lo], j = A.pj[lo];
+        out[k] = pair_entry(i, j, pair_damp<D>(A.XV[i], A.XV[j], A.ks));
+    } else if (hi - lo <= kGroupMax) {
+        const int64_t o = side_off[k];
+        for (int64_t q = lo; q < hi; ++q) {
+            const int32_t i = A.pi[q], j = A.pj[q];
+            side[o + (q - lo)] = pair_entry(i, j, pair_damp<D>(A.XV[i], A.XV[j], A.ks));
+        }
+        out[k] = make_double2(__longlong_as_double(-2 - ((o << 8) | (hi - lo))), 0.0);
+    } else {
+        out[k] = make_double2(__longlong_as_double(-2 - (g << 8)), 0.0);
+    }
+}
+
+// the simultaneous solve of a small group from its precomputed pair
+// entries, local arrays instead of the global scratch (same arithmetic as
+// visit_group)
+template <int D>
+__device__ void group_solve_entries(const double2 *__restrict__ pe, int cnt, const double *__restrict__ inv_m,
+                                    double half, double *sv, int n) {
+    constexpr int NB = 2 * kGroupMax;
+    double2 e[kGroupMax];
+    for (int q = 0; q < cnt; ++q) e[q] = __ldg(pe + q);
+    int ii[kGroupMax], jj[kGroupMax];
+    double imi[kGroupMax], imj[kGroupMax];
+    for (int q = 0; q < cnt; ++q) {
+        const unsigned long long key = (unsigned long long)__double_as_longlong(e[q].x);
+        ii[q] = (int)(uint32_t)key;
+        jj[q] = (int)(uint32_t)(key >> 32);
+    }
+    for (int q = 0; q < cnt; ++q) {
+        imi[q] = __ldg(inv_m + ii[q]);
+        imj[q] = __ldg(inv_m + jj[q]);
+    }
+    int loc[NB];
+    int nb = 0;
+    for (int q = 0; q < cnt; ++q) {
+        const int ep[2] = {ii[q], jj[q]};
+        for (int s = 0; s < 2; ++s) {
+            bool found = false;
+            for (int t = 0; t < nb; ++t) if (loc[t] == ep[s]) { found = true; break; }
+            if (!found) loc[nb++] = ep[s];
+        }
+    }
+    double Am[NB * NB], rhs[NB * 3];
+    for (int r = 0; r < nb; ++r) {
+        for (int c = 0; c < nb; ++c) Am[r * nb + c] = (r == c) ? 1.0 : 0.0;
+        for (int m = 0; m < D; ++m) rhs[r * 3 + m] = sv[m * n + loc[r]];
+    }
+    for (int q = 0; q < cnt; ++q) {
+        const double c = half * e[q].y;
+        int ia = 0, ib = 0;
+        for (int t = 0; t < nb; ++t) {
+            if (loc[t] == ii[q]) ia = t;
+            if (loc[t] == jj[q]) ib = t;
+        }
+        const double ca = c * imi[q], cb = c * imj[q];
+        Am[ia * nb + ia] += ca;
+        Am[ia * nb + ib] -= ca;
+        Am[ib * nb + ib] += cb;
+        Am[ib * nb + ia] -= cb;
+    }
+    for (int col = 0; col < nb - 1; ++col) {
+        const double piv = Am[col * nb + col];
+        for (int r = col + 1; r < nb; ++r) {
+            const double f = Am[r * nb + col] / piv;
+            if (f != 0.0) {
+                for (int c = col; c < nb; ++c) Am[r * nb + c] -= f * Am[col * nb + c];
+                for (int m = 0; m < D; ++m) rhs[r * 3 + m] -= f * rhs[col * 3 + m];
+            }
+        }
+    }
+    for (int r = nb - 1; r >= 0; --r)
+        for (int m = 0; m < D; ++m) {
+            double s = rhs[r * 3 + m];
+            for (int c = r + 1; c < nb; ++c) s -= Am[r * nb + c] * rhs[c * 3 + m];
+            rhs[r * 3 + m] = s / Am[r * nb + r];
+        }
+    for (int t = 0; t < nb; ++t)
+        for (int m = 0; m < D; ++m) sv[m * n + loc[t]] = rhs[t * 3 + m];
+}
+
+// velocity accessor of the shared copy: planar [D][n]
+struct SmemV {
+    double *sv;
+    int n;
+    __device__ void get(int64_t i, double *a, int D) const { for (int m = 0; m < D; ++m) a[m] = sv[m * n + i]; }
+    __device__ void set(int64_t i, const double *a, int D) const { for (int m = 0; m < D; ++m) sv[m * n + i] = a[m]; }
+};
+
+// visit_group's simultaneous solve on the shared copy (same arithmetic)
+template <int D>
+__device__ void group_solve_smem(const SweepArgs &A, int64_t g, double half, const SmemV &V) {
+    const int64_t lo = A.gptr[g], hi = A.gptr[g + 1];
+    double *S = A.scratch + A.gscr[g];
+    const int nbmax = (int)(2 * (hi - lo));
+    double *Am = S;
+    double *rhs = S + nbmax * nbmax;
+    long long *loc = reinterpret_cast<long long *>(rhs + 3 * nbmax);
+    int nb = 0;
+    for (int64_t k = lo; k < hi; ++k) {
+        const int32_t e[2] = {A.pi[k], A.pj[k]};
+        for (int s = 0; s < 2; ++s) {
+            bool found = false;
+            for (int t = 0; t < nb; ++t) if (loc[t] == e[s]) { found = true; break; }
+            if (!found) loc[nb++] = e[s];
+        }
+    }
+    for (int r = 0; r < nb; ++r) {
+        for (int c = 0; c < nb; ++c) Am[r * nb + c] = (r == c) ? 1.0 : 0.0;
+        double v[3];
+        V.get(loc[r], v, D);
+        for (int m = 0; m < D; ++m) rhs[r * 3 + m] = v[m];
+    }
+    for (int64_t k = lo; k < hi; ++k) {
+        const int32_t i = A.pi[k], j = A.pj[k];
+        const double c = half * pair_damp<D>(A.XV[i], A.XV[j], A.ks);
+        int ia = 0, ib = 0;
+        for (int t = 0; t < nb; ++t) {
+            if (loc[t] == i) ia = t;
+            if (loc[t] == j) ib = t;
+        }
+        const double ca = c * A.inv_m[i], cb = c * A.inv_m[j];
+        Am[ia * nb + ia] += ca;
+        Am[ia * nb + ib] -= ca;
+        Am[ib * nb + ib] += cb;
+        Am[ib * nb + ia] -= cb;
+    }
+    for (int col = 0; col < nb - 1; ++col) {
+        const double piv = Am[col * nb + col];
+        for (int r = col + 1; r < nb; ++r) {
+            const double f = Am[r * nb + col] / piv;
+            if (f != 0.0) {
+                for (int c = col; c < nb; ++c) Am[r * nb + c] -= f * Am[col * nb + c];
+                for (int m = 0; m < D; ++m) rhs[r * 3 + m] -= f * rhs[col * 3 + m];
+            }
+        }
+    }
+    for (int r = nb - 1; r >= 0; --r)
+        for (int m = 0; m < D; ++m) {
+            double s = rhs[r * 3 + m];
+            for (int c = r + 1; c < nb; ++c) s -= Am[r * nb + c] * rhs[c * 3 + m];
+            rhs[r * 3 + m] = s / Am[r * nb + r];
+        }
+    for (int t = 0; t < nb; ++t) {
+        const double v[3] = {rhs[t * 3], rhs[t * 3 + 1], rhs[t * 3 + 2]};
+        V.set(loc[t], v, D);
+    }
+}
+
+constexpr int kSerialThreads = 1024;
+constexpr size_t kSerialSmemMax = 200 * 1024;
+
+inline size_t serial_smem_bytes(int64_t n, int d, int64_t nlevels) {
+    return (size_t)n * d * sizeof(double) + (size_t)(nlevels + 1) * sizeof(int64_t);
+}
+
+template <int D>
+__global__ void __launch_bounds__(kSerialThreads, 1)
+    k_sweep_serial_smem(SweepArgs A, const double2 *__restrict__ ent, const double2 *__restrict__ side,
+                        const int64_t *__restrict__ level_ptr, int64_t nlevels, int n, const Ctrl *ctrl) {
+    if (ctrl->done) return;
+    extern __shared__ double smem_serial[];
+    using V_t = typename VT<D>::T;
+    V_t *Vg = reinterpret_cast<V_t *>(A.V);
+    const SmemV V{smem_serial, n};
+    int64_t *lp = reinterpret_cast<int64_t *>(smem_serial + (size_t)D * n);
+    const double half = 0.5 * ctrl->dt * ctrl->eta;
+    const int t = threadIdx.x;
+    for (int i = t; i < n; i += kSerialThreads) {
+        double a[3];
+        vget(Vg[i], a);
+        V.set(i, a, D);
+    }
+    for (int64_t L = t; L <= nlevels; L += kSerialThreads) lp[L] = level_ptr[L];
+    __syncthreads();
+    const double2 none = make_double2(__longlong_as_double(-1ll), 0.0);   // no entry
+    auto apply = [&](const double2 &e, double imi, double imj) {
+        const long long key = __double_as_longlong(e.x);
+        if (key == -1) return;
+        if (key < 0) {
+            const long long code = -2 - key;
+            const int cnt = (int)(code & 0xff);
+            if (cnt) group_solve_entries<D>(side + (code >> 8), cnt, A.inv_m, half, smem_serial, n);
+            else group_solve_smem<D>(A, code >> 8, half, V);
+            return;
+        }
+        const int i = (int)(uint32_t)key, j = (int)(uint32_t)((unsigned long long)key >> 32);
+        const double c = half * e.y;
+        const double ca = c * imi, cb = c * imj;
+        const double den = 1.0 + ca + cb;
+        double a[3], b[3];
+        V.get(i, a, D);
+        V.get(j, b, D);
+#pragma unroll
+        for (int m = 0; m < D; ++m) {
+            const double u = (a[m] - b[m]) / den;
+            a[m] -= ca * u;
+            b[m] += cb * u;
+        }
+        V.set(i, a, D);
+        V.set(j, b, D);
+    };
+    auto inv_of = [&](const double2 &e, double &imi, double &imj) {
+        const long long key = __double_as_longlong(e.x);
+        imi = imj = 0.0;
+        if (key >= 0) {
+            imi = __ldg(A.inv_m + (uint32_t)key);
+            imj = __ldg(A.inv_m + (uint32_t)((unsigned long long)key >> 32));
+        }
+    };
+    for (int pass = 0; pass < 2; ++pass) {
+        // step s visits level s (forward) or nlevels - 1 - s (reverse)
+        auto level = [&](int64_t s) { return pass == 0 ? s : nlevels - 1 - s; };
+        auto fetch = [&](int64_t s) {
+            if (s >= nlevels) return none;
+            const int64_t L = level(s), k = lp[L] + t;
+            return k < lp[L + 1] ? __ldg(ent + k) : none;
+        };
+        // ring: entries of steps s..s+3, inverse masses of steps s and s+1
+        double2 e0 = fetch(0), e1 = fetch(1), e2 = fetch(2), e3 = fetch(3);
+        double i0a, i0b, i1a, i1b;
+        inv_of(e0, i0a, i0b);
+        inv_of(e1, i1a, i1b);
+        for (int64_t s = 0; s < nlevels; ++s) {
+            apply(e0, i0a, i0b);
+            const int64_t L = level(s);
+            for (int64_t k = lp[L] + t + kSerialThreads; k < lp[L + 1]; k += kSerialThreads) {
+                const double2 e = __ldg(ent + k);
+                double a, b;
+                inv_of(e, a, b);
+                apply(e, a, b);
+            }
+            e0 = e1; i0a = i1a; i0b = i1b;
+            e1 = e2;
+            inv_of(e1, i1a, i1b);
+            e2 = e3;
+            e3 = fetch(s + 4);
+            __syncthreads();
+        }
+    }
+    for (int i = t; i < n; i += kSerialThreads) {
+        double a[3];
+        V.get(i, a, D);
+        V_t w = Vg[i];
+        vset(w, a);
+        Vg[i] = w;
+    }
+}
+
 // one colour phase: thread per task, groups in task order (dir>0) or
 // reversed (dir<0)
 template <int D>
@@ -218,12 +498,53 @@ __global__ void __launch_bounds__(128) k_sweep_colour(SweepArgs A, int64_t t0, i
         for (int64_t g = g1 - 1; g >= g0; --g) visit_group<D>(A, g, half);
 }
 
+// the level-ordered entries of the shared-memory serial sweep (setup, once;
+// MTSPH_SERIAL_SMEM=0 keeps the global-memory kernel)
+template <int D> void build_serial_entries(NbhDev &nb, const SweepArgs &A, cudaStream_t s) {
+    const char *env = getenv("MTSPH_SERIAL_SMEM");
+    if (nb.sweep != 1 || (env && atoi(env) == 0)) return;
+    const int64_t ng = nb.level_groups.n;
+    if (ng == 0 || serial_smem_bytes(nb.n, D, nb.nlevels) > kSerialSmemMax) return;
+    // side-table offsets of the small groups, in level order
+    std::vector<int64_t> lg(ng), gp(nb.ngroups + 1), off(ng, 0);
+    nb.level_groups.download(lg.data(), ng, s);
+    nb.gptr.download(gp.data(), nb.ngroups + 1, s);
+    MT_CUDA(cudaStreamSynchronize(s));
+    int64_t tot = 0;
+    for (int64_t k = 0; k < ng; ++k) {
+        const int64_t c = gp[lg[k] + 1] - gp[lg[k]];
+        off[k] = tot;
+        if (c > 1 && c <= kGroupMax) tot += c;
+    }
+    DBuf<int64_t> off_d;
+    off_d.upload(off.data(), ng, s);
+    nb.serial_ent.alloc(ng);
+    nb.serial_side.alloc(std::max<int64_t>(tot, 1));
+    k_serial_entries<D><<<(unsigned)((ng + 255) / 256), 256, 0, s>>>(A, nb.level_groups.p, ng, off_d.p,
+                                                                     nb.serial_ent.p, nb.serial_side.p);
+    MT_LAUNCH_CHECK();
+    MT_CUDA(cudaStreamSynchronize(s));   // off_d is freed on return
+}
+
 // launch one full sweep on stream s; returns the number of kernel launches
 template <int D>
 int launch_sweep(const NbhDev &nb, const SweepArgs &A, const int64_t *level_ptr_d, const Ctrl *ctrl,
                  cudaStream_t s) {
     if (nb.npairs == 0) return 0;
     if (nb.sweep == 1) {
+        const size_t sm = serial_smem_bytes(nb.n, D, nb.nlevels);
+        if (nb.serial_ent.n && sm <= kSerialSmemMax) {
+            static bool attr = false;   // per template instance
+            if (!attr) {
+                MT_CUDA(cudaFuncSetAttribute(k_sweep_serial_smem<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)kSerialSmemMax));
+                attr = true;
+            }
+            k_sweep_serial_smem<D><<<1, kSerialThreads, sm, s>>>(A, nb.serial_ent.p, nb.serial_side.p, level_ptr_d,
+                                                                 nb.nlevels, (int)nb.n, ctrl);
+            MT_LAUNCH_CHECK();
+            return 1;
+        }
         k_sweep_serial<D><<<1, 1024, 0, s>>>(A, level_ptr_d, nb.nlevels, nb.level_groups.p, ctrl);
         MT_LAUNCH_CHECK();
         return 1;

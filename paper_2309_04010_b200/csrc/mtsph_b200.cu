@@ -598,7 +598,11 @@ extern "C" mtsph_status mtsph_solid_create(const mtsph_solid_desc *dsc, mtsph_so
     S->part.alloc((size_t)3 * S->nblk);
     S->part.zero(S->s);
     S->meas.alloc((size_t)5 * S->nblk);
-    if (S->nb.sweep == 1) S->level_ptr.upload(S->nb.level_ptr_h.data(), S->nb.level_ptr_h.size(), S->s);
+    if (S->nb.sweep == 1) {
+        S->level_ptr.upload(S->nb.level_ptr_h.data(), S->nb.level_ptr_h.size(), S->s);
+        if (d == 2) build_serial_entries<2>(S->nb, S->sweep_args(), S->s);
+        else build_serial_entries<3>(S->nb, S->sweep_args(), S->s);
+    }
     Mat &m = S->mat;
     m.mu = dsc->shear_modulus;
     m.K = dsc->bulk_modulus;

@@ -99,6 +99,8 @@ struct NbhDev {
     int64_t nlevels = 0;
     std::vector<int64_t> level_ptr_h;
     DBuf<int64_t> level_groups;
+    DBuf<double2> serial_ent;    // level-ordered sweep entries (damping.cuh k_serial_entries)
+    DBuf<double2> serial_side;   // pair entries of the small simultaneous-solve groups
     // COLOURED: phases (colours) -> tasks -> groups
     std::vector<int64_t> colour_task_ptr;  // ncolours+1 over tasks
     DBuf<int64_t> task_ptr;                // ntasks+1 over groups

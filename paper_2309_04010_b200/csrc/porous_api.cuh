@@ -183,7 +183,11 @@ extern "C" mtsph_status mtsph_porous_create(const mtsph_porous_desc *dsc, mtsph_
     else k_por_gsum<3><<<blocks_for(n), 256, 0, P->s>>>(P->args(), P->G.p);
     MT_LAUNCH_CHECK();
     P->part.zero(P->s);
-    if (P->nb.sweep == 1) P->level_ptr.upload(P->nb.level_ptr_h.data(), P->nb.level_ptr_h.size(), P->s);
+    if (P->nb.sweep == 1) {
+        P->level_ptr.upload(P->nb.level_ptr_h.data(), P->nb.level_ptr_h.size(), P->s);
+        if (d == 2) build_serial_entries<2>(P->nb, P->sweep_args(), P->s);
+        else build_serial_entries<3>(P->nb, P->sweep_args(), P->s);
+    }
     PorMat &m = P->m;
     m.rho_s0 = dsc->density0;
     m.D = dsc->diffusivity;
@@ -553,7 +557,7 @@ extern "C" mtsph_status mtsph_porous_sizes(const mtsph_porous *P, int64_t out[4]
     out[0] = nb.nnz;
     out[1] = nb.sweep == 3 ? P->tiled.npairs : nb.npairs;
     out[2] = nb.sweep == 3 ? P->tiled.npairs : nb.ngroups;
-    out[3] = nb.sweep == 3 ? (int64_t)P->tiled.colour_ptr.size() - 1 : 0;
+    out[3] = nb.sweep == 3 ? (int64_t)P->tiled.colour_ptr.size() - 1 : nb.sweep == 1 ? nb.nlevels : 0;
     return MTSPH_OK;
 }
 

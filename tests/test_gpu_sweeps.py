@@ -110,6 +110,59 @@ def test_dataflow_sweep_is_bit_identical_to_colour_launches(dim, monkeypatch):
         np.testing.assert_array_equal(x, y)
 
 
+@pytest.mark.parametrize("dim", [2, 3])
+def test_serial_sweep_shared_memory_kernel_is_bit_identical(dim, monkeypatch):
+    """The reference-order sweep of small problems runs from shared memory
+    (velocities and level table staged, pair entries prefetched); it applies
+    the same operations in the same order as the global-memory kernel."""
+    from paper_2309_04010_b200 import lattices
+    from paper_2309_04010_b200.config import resolve
+    from paper_2309_04010_b200.device import DeviceSolid
+    from paper_2309_04010_b200.scenarios import _necking_materials
+    raw = {"scenario": "block_3d", "length": 0.2, "width": 0.08, "breadth": 0.08, "dp": 0.01} \
+        if dim == 3 else {"scenario": "bar_2d", "length": 2.0, "width": 0.4, "dp": 0.025}
+    p = resolve(raw).params
+    lat = lattices.build_lattice(p)
+    el, hard = _necking_materials(p)
+    law, hp = hard.device_params()
+    runs = {}
+    for smem in ("1", "0"):
+        monkeypatch.setenv("MTSPH_SERIAL_SMEM", smem)
+        s = DeviceSolid(lat.pos, lat.vol, el.density0, lat.constrained, lat.side, lat.mid_mask,
+                        lat.h_axes, el.shear_modulus, el.bulk_modulus, plastic=True,
+                        hardening_law=law, hard=hp, sweep="serial")
+        s.set_ramp(0.01 * p["length"], 10, 10)
+        for _ in range(30):
+            s.relax_step(s.stable_dt(0.2), p["eta"])
+        r = s.relax(eta=p["eta"], cfl=p["cfl"], criterion=-1.0, dt_outer=1.0, max_inner=20,
+                    min_inner=20)
+        assert r.n_inner == 20
+        runs[smem] = [s.get(f) for f in ("pos", "vel", "F", "alpha")]
+    assert np.max(np.abs(runs["1"][1])) > 0
+    for x, y in zip(runs["1"], runs["0"]):
+        np.testing.assert_array_equal(x, y)
+
+
+def test_serial_sweep_shared_memory_kernel_is_bit_identical_porous(monkeypatch):
+    """Same for the membrane (anisotropic kernel, simultaneous group solves
+    included where the reference groups pairs)."""
+    from paper_2309_04010_b200.config import resolve
+    from paper_2309_04010_b200.scenarios import build
+    from paper_2309_04010_b200.stepping import run_outer_inner
+    p = resolve({"scenario": "fsi_2d", "length": 2e-3, "t_total": 2.4, "n_outer": 3,
+                 "max_inner": 40}).params
+    runs = {}
+    for smem in ("1", "0"):
+        monkeypatch.setenv("MTSPH_SERIAL_SMEM", smem)
+        problem, policy = build(p, sweep="serial")
+        obs, _ = run_outer_inner(problem, policy)
+        runs[smem] = (obs.n_inner, [problem.dev.get(f) for f in ("pos", "vel_solid", "fluid_mass")])
+    np.testing.assert_array_equal(runs["1"][0], runs["0"][0])
+    assert np.max(np.abs(runs["1"][1][1])) > 0
+    for x, y in zip(runs["1"][1], runs["0"][1]):
+        np.testing.assert_array_equal(x, y)
+
+
 @pytest.mark.parametrize("flow", ["1", "0"])
 @pytest.mark.parametrize("dim", [2, 3])
 @pytest.mark.parametrize("shape", ["tiny", "thin"])
