@@ -151,3 +151,32 @@ def test_porous_run_observables(gold_runs):
     assert rel_err(prob.fluid_mass, gold_runs["rf2_fluid_mass"]) < 1e-10
     assert rel_err(prob.pos - lat.pos, gold_runs["rf2_pos"] - lat.pos) < 1e-8
     assert rel_err(np.array([r["profile"] for r in rows]), gold_runs["rf2_profile"]) < 1e-8
+
+
+def test_desk_necking_acceptance_head():
+    """The oracle against the reference's own run of its acceptance
+    configuration (desk necking bar, dp = PH/25; tests/golden/
+    acceptance_heads.npz): 12 outer steps through first mid-span yield."""
+    from conftest import golden
+    from paper_2309_04010_b200 import lattices
+    from paper_2309_04010_b200.config import resolve
+    from paper_2309_04010_b200.scenarios import _necking_materials, make_policy
+    gold = golden("acceptance_heads.npz")
+    p = resolve({"scenario": "necking_2d", "dp": 12.826e-3 / 25, "n_outer": 1000}).params
+    lat = lattices.build_lattice(p)
+    el, hard = _necking_materials(p)
+    law, hp = hard.device_params()
+    policy = make_policy(p, float(np.min(lat.h_axes)))
+    prob = NeckingOracle(lat.pos, lat.vol, el.density0, lat.constrained, lat.side < 0,
+                         lat.side > 0, lat.mid_mask, el.shear_modulus, el.bulk_modulus, hp,
+                         float(lat.h_axes[0]), end_disp_per_outer=p["stretch_per_end"] / p["n_outer"],
+                         ramp_steps=p["ramp_steps"], hardening_law=law)
+    n_outer = len(gold["an2_n_inner"])
+    rows = run_outer_inner(prob, policy.dt_outer, n_outer, policy.eta, policy.energy_criterion,
+                           cfl=policy.cfl, max_inner=policy.max_inner, min_inner=policy.min_inner)
+    np.testing.assert_array_equal([r["n_inner"] for r in rows], gold["an2_n_inner"])
+    for key in ("reaction_force", "mid_alpha_min"):
+        got = np.array([r[key] for r in rows])
+        assert rel_err(got, gold["an2_" + key]) < 1e-9, key
+    assert np.max(gold["an2_mid_alpha_min"]) > 0
+    assert rel_err(prob.pos - lat.pos, gold["an2_pos"] - lat.pos) < 1e-9
