@@ -208,10 +208,14 @@ __global__ void __launch_bounds__(1024) k_sweep_serial(SweepArgs A, const int64_
 // before its barrier; here the velocities live in shared memory and each
 // thread's single-pair entries of the next levels (i, j and the static
 // pair_damp, precomputed in level order by k_serial_entries) are loaded
-// ahead through a register ring, so a level costs a shared-memory exchange
-// and a barrier.  Same operations in the same order: bit-identical to
-// k_sweep_serial (tests/test_gpu_solid.py).  Multi-pair groups
-// (simultaneous solves) take the global path's solver on the shared copy.
+// ahead through a register ring.  Groups of 2..kGroupMax pairs (the
+// reference's simultaneous solves of mirror pairs) are solved from their
+// precomputed entries in local arrays; larger ones take the global path's
+// solver on the shared copy.  Same operations in the same order:
+// bit-identical to k_sweep_serial (tests/test_gpu_sweeps.py
+// test_serial_sweep_shared_memory_kernel_is_bit_identical*).  Most levels
+// hold one small group, whose dependent solve (~3 us) is now the critical
+// path between two barriers.
 
 // entry k (level order): a single pair -> (i | j << 32, pair_damp); a group
 // of 2..kGroupMax pairs -> (-2 - (side offset << 8 | count), 0) with its
