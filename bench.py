@@ -337,7 +337,7 @@ def run_ours(args):
                    "sweep_phases": sz["phases"], "neighbours_per_particle": sz["nnz"] / n,
                    "pairs": sz["npairs"], "groups": sz["ngroups"],
                    "l2": "state >> 126 MB L2 (no flush needed)",
-                   "parallelism": "replicas" if world > 1 else "1 GPU",
+                   "parallelism": "1 GPU",
                    "setup_s": setup_s},
         "e2e": {"value": e2e, "unit": "particle-steps/s", "h2d_bytes_per_step": 2 * ctrl_bytes,
                 "d2h_bytes_per_step": 4 * ctrl_bytes,
@@ -400,22 +400,37 @@ def fp32_variant(dev, args, params, n, d, sz, world, peak):
             "kernels": kernels}
 
 
+def scale_params(args, world):
+    """BASELINE configs[4]: the seeded +-5 % jittered power-law block
+    (config-0 material, dp 0.02, 2 x 2 cross-section = 100 x 100 particles),
+    lengthened along x to the requested count: 32 M particles split over the
+    N GPUs (strong scaling) or 4 M per GPU (weak scaling)."""
+    from paper_2309_04010_b200.config import resolve
+    if args.scaling == "strong":
+        total = args.scale_particles or 32e6
+    else:
+        total = (args.scale_particles or 4e6) * world
+    base = resolve({"scenario": "block_3d", "damping_sweep": "tiled"}).params
+    per_col = round(base["width"] / base["dp"]) * round(base["breadth"] / base["dp"])
+    cols = max(int(round(total / per_col)), 8)
+    return resolve({"scenario": "block_3d", "damping_sweep": "tiled",
+                    "length": cols * base["dp"]}).params
+
+
 def run_decomposed(args, world, rank, local):
-    """N > 1: the workload split into N x-slabs (partition.py), one per GPU,
-    halo exchanges over NCCL each phase, rank reductions all-gathered on the
-    device and the stopping rule applied by every rank's control kernel
-    (DecomposedSolid.relax_device).  --scaling weak (default): the bar is N
-    times longer (10 M particles per GPU, the N = 1 workload per slab);
-    strong: the same 10 M-particle bar split N ways."""
+    """N > 1 (or --mode decomposed): BASELINE configs[4] split into N x-slabs
+    (partition.py), one per GPU, halo exchanges over NCCL each phase, rank
+    reductions all-gathered on the device and the stopping rule applied by
+    every rank's control kernel (DecomposedSolid.relax_device).  --scaling
+    strong (default): the 32 M-particle block split N ways; weak: 4 M
+    particles per GPU (the block N times longer)."""
     import torch
     import torch.distributed as dist
     from paper_2309_04010_b200 import lattices
     from paper_2309_04010_b200.distributed import DecomposedSolid
     from paper_2309_04010_b200.scenarios import _necking_materials
-    params = workload_params(args)
-    if args.scaling == "weak" and world > 1:
-        params = dict(params)
-        params["length"] = params["length"] * world
+    from paper_2309_04010_b200.config import resolve
+    params = scale_params(args, world)
     lat = lattices.build_lattice(params)
     elastic, hard = _necking_materials(params)
     eta, cfl = params["eta"], params["cfl"]
@@ -468,12 +483,11 @@ def run_decomposed(args, world, rank, local):
         "metric": "inner solid-relaxation particle-steps/sec",
         "value": n_total * args.steps / (ms / 1e3), "unit": "particle-steps/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-        "higher_is_better": True, "scaling": args.scaling if world > 1 else "weak",
+        "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": f"{args.workload} (BASELINE configs[2])"
-                               + (f", {world}x longer (weak scaling)" if args.scaling == "weak" and world > 1
-                                  else ""),
+        "config": {"workload": f"block_3d (BASELINE configs[4], jittered +-5 %, seed "
+                               f"{params['seed']}), {args.scaling} scaling",
                    "particles": n_total, "particles_per_gpu": n_total // world,
                    "dp": params["dp"], "h_over_dp": params["h_factor"],
                    "material": "rho 1, E 200, nu 0.3, J2 power-law s0 0.25 e0 0.01 n 0.2",
@@ -613,6 +627,10 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    # rank 0 alone does the work, with every host thread (torchrun exports
+    # OMP_NUM_THREADS=1 to each rank)
+    from oracle import oracle as O
+    O.lib().or_set_num_threads(len(os.sched_getaffinity(0)))
     params = workload_params(args)
     steps = max(args.steps, 1)
     base = cpu_baseline(params, args, steps=steps + args.warmup)
@@ -642,18 +660,38 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-fp32", action="store_true", help="skip the fp32 variant")
-    ap.add_argument("--mode", default="auto", choices=("auto", "decomposed", "replicas"),
+    ap.add_argument("--mode", default="auto", choices=("auto", "decomposed"),
                     help="auto: N = 1 single domain, N > 1 slab decomposition with NCCL halos; "
-                         "decomposed forces the decomposed path (also at N = 1); replicas: "
-                         "independent copies of the 1-GPU workload")
-    ap.add_argument("--scaling", default="weak", choices=("weak", "strong"),
-                    help="N > 1 decomposed runs: weak = 10 M particles per GPU (bar N times "
-                         "longer), strong = the 10 M bar split N ways")
+                         "decomposed forces the decomposed path (also at N = 1)")
+    ap.add_argument("--scaling", default="strong", choices=("weak", "strong"),
+                    help="decomposed runs (BASELINE configs[4], the jittered power-law "
+                         "block): strong = 32 M particles split N ways, weak = 4 M per GPU")
+    ap.add_argument("--scale-particles", type=float, default=0.0,
+                    help="decomposed runs: total (strong) or per-GPU (weak) particle count; "
+                         "default 32e6 / 4e6")
     ap.add_argument("--no-membrane", action="store_true", help="skip the porous membrane leg")
     ap.add_argument("--membrane-side", type=float, default=0.14,
                     help="fsi_3d film edge (m); 0.14 gives ~10 M particles")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # one process per GPU: re-launch this command under torchrun
+        # (127.0.0.1 rendezvous); the ranks see WORLD_SIZE and do not recurse
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+               "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+        sys.stdout.flush()
+        os.execv(sys.executable, cmd)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; "
+                         "launch with matching --nproc-per-node")
     # keep stdout for the JSON line alone: library output on fd 1 (NCCL's
     # version banner, ...) goes to stderr
     global _OUT

@@ -19,7 +19,7 @@
  *  2. Device-resident problems (neighbourhood, necking solid, porous
  *     membrane) whose state stays in HBM for the whole run; one call runs
  *     a complete inner relaxation loop (scenarios.py relax_step repeated
- *     under stepping.py:347's kinetic-energy criterion) without host
+ *     under stepping.py:158's kinetic-energy criterion) without host
  *     round trips.  These back the drop-in Problem objects of the Python
  *     package (paper_2309_04010_b200.scenarios).
  */
@@ -39,11 +39,11 @@ enum {
     MTSPH_OK = 0,
     MTSPH_ERR_ARG = 1,          /* bad argument / unsupported dimension      */
     MTSPH_ERR_CUDA = 2,         /* CUDA runtime failure or no device         */
-    MTSPH_ERR_GEOMETRY = 3,     /* errors.py:266 GeometryError               */
-    MTSPH_ERR_SINGULAR = 4,     /* errors.py:270 SingularMomentMatrixError   */
-    MTSPH_ERR_INVERSION = 5,    /* errors.py:283 ElementInversionError       */
-    MTSPH_ERR_RETURN_MAP = 6,   /* errors.py:295 ReturnMapError              */
-    MTSPH_ERR_NONFINITE = 7,    /* errors.py:308 SimulationError             */
+    MTSPH_ERR_GEOMETRY = 3,     /* errors.py:12  GeometryError               */
+    MTSPH_ERR_SINGULAR = 4,     /* errors.py:16  SingularMomentMatrixError   */
+    MTSPH_ERR_INVERSION = 5,    /* errors.py:29  ElementInversionError       */
+    MTSPH_ERR_RETURN_MAP = 6,   /* errors.py:41  ReturnMapError              */
+    MTSPH_ERR_NONFINITE = 7,    /* errors.py:54  SimulationError             */
 };
 
 int mtsph_abi_version(void);
@@ -155,7 +155,7 @@ typedef struct {
     const uint8_t *mid_mask;    /* (n,) mid-span section (neck radius)      */
     double h_axes[3];
     double shear_modulus, bulk_modulus;
-    int plastic;                /* 0: Neo-Hookean only (solids.py:394)      */
+    int plastic;                /* 0: Neo-Hookean only (solids.py:148)      */
     int hardening_law;          /* 0: reference saturation+linear (plasticity.py:64)
                                    1: power law s0 (1 + a/e0)^m             */
     double hard[4];             /* law 0: s0, sinf, delta, H; law 1: s0, e0, m, - */
@@ -197,7 +197,7 @@ mtsph_status mtsph_solid_destroy(mtsph_solid *s);
 mtsph_status mtsph_solid_set_ramp(mtsph_solid *s, double end_disp, int64_t ramp_steps,
                                   int64_t ramp_left);
 mtsph_status mtsph_solid_ramp_left(const mtsph_solid *s, int64_t *ramp_left);
-/* solids.py:433 stable step                                              */
+/* solids.py:187 stable step                                              */
 mtsph_status mtsph_solid_stable_dt(mtsph_solid *s, double cfl, double *dt);
 /* one relax_step at a host-chosen dt; returns the pre-damping E_k        */
 mtsph_status mtsph_solid_relax_step(mtsph_solid *s, double dt, double eta, double *ek);
@@ -238,7 +238,7 @@ enum {
  * max |a|^2, max |v|^2, error flag} (owned particles) to 4 doubles of
  * device memory; the caller all-gathers them over the ranks (NCCL) into
  * [nranks][4] and control_ranks applies the stopping rule and next step
- * (stepping.py:369-385, solids.py:433) on the device, identically on every
+ * (stepping.py:177-195, solids.py:187) on the device, identically on every
  * rank.  mode 0: initial step size (after the AMAX phase), 1: end of an
  * inner step (after ACCEL ... VMAX).  begin_loop sets the loop parameters
  * as mtsph_solid_relax does; loop_state reads the control block back.    */

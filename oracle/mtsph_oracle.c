@@ -8,7 +8,7 @@
  * order so results are thread-count independent), the algorithms of the
  * upstream package (paths relative to /root/reference/pkg/src/mtsph):
  *
- *   kernels.py:121      Wendland C2 kernel gradient (anisotropic map)
+ *   kernels.py:110      Wendland C2 kernel gradient (anisotropic map)
  *   _accel.py:16        velocity_gradient_gather
  *   _accel.py:34        pair_tensor_divergence
  *   _accel.py:52        pair_tensor_divergence_mapped
@@ -17,9 +17,9 @@
  *   _accel.py:210       conservative_mass_rate
  *   _accel.py:240       porous_stress_rhs
  *   plasticity.py:118   return_map (+ _solve_consistency :89)
- *   solids.py:394/410   kirchhoff_stress / first_pk
+ *   solids.py:148/164   kirchhoff_stress / first_pk
  *   scenarios.py:113    NeckingProblem.relax_step (fused here as one call)
- *   solids.py:433       solid_time_step
+ *   solids.py:187       solid_time_step
  *
  * Arrays follow the reference (numpy, C order): vectors (n,d), tensors
  * (n,d,d) row-major, CSR indptr/idx as int64.
@@ -80,7 +80,7 @@ static void matmul_nt(int d, const double *a, const double *b, double *o) {
 
 /* ----------------------------------------------------------------- kernel */
 
-/* dW/dr_vec of the anisotropic Wendland C2 kernel (kernels.py:121).
+/* dW/dr_vec of the anisotropic Wendland C2 kernel (kernels.py:110).
  * prefactor = sigma_d / prod(h_axes). */
 void or_kernel_grad(int d, const double *rel, const double *h_axes,
                     double prefactor, double *out) {
@@ -685,7 +685,7 @@ double or_necking_relax_step(or_necking *s, double dt, double eta,
     return ek;
 }
 
-/* solid_time_step (solids.py:433) on the necking state */
+/* solid_time_step (solids.py:187) on the necking state */
 double or_necking_stable_dt(const or_necking *s, double h, double c, double cfl) {
     const int d = s->d;
     double vmax2 = 0.0, amax2 = 0.0;
@@ -710,5 +710,16 @@ int or_num_threads(void) {
     return omp_get_max_threads();
 #else
     return 1;
+#endif
+}
+
+/* thread count of the parallel loops (the reference arm of bench.py runs
+   under torchrun, which exports OMP_NUM_THREADS=1) */
+void or_set_num_threads(int n) {
+#ifdef _OPENMP
+    extern void omp_set_num_threads(int);
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
 #endif
 }

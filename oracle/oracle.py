@@ -69,7 +69,7 @@ def kernel_prefactor(h_axes) -> float:
 
 
 def kernel_gradient(rel, h_axes):
-    """Vectorised dW/d(rel) (kernels.py:121)."""
+    """Vectorised dW/d(rel) (kernels.py:110)."""
     rel = np.asarray(rel, dtype=float)
     h_axes = np.asarray(h_axes, dtype=float)
     u = rel / h_axes
@@ -315,7 +315,7 @@ def _amap(F, corr):
 
 
 def saturation_and_flux(F, fluid_mass, vol0, nbh: Nbh, m: Membrane):
-    """porous.py:503: saturation from mass, Fick flux down its gradient."""
+    """porous.py:168: saturation from mass, Fick flux down its gradient."""
     n, d = fluid_mass.shape[0], F.shape[1]
     j = det(F)
     if np.any(j <= 0):
@@ -332,7 +332,7 @@ def saturation_and_flux(F, fluid_mass, vol0, nbh: Nbh, m: Membrane):
 
 
 def fluid_mass_update(F, fluid_mass, flux, vol0, nbh: Nbh, m: Membrane, dt):
-    """porous.py:476 (conservative pair form + clamp); returns mass, clamped."""
+    """porous.py:141 (conservative pair form + clamp); returns mass, clamped."""
     n, d = fluid_mass.shape[0], F.shape[1]
     j = det(F)
     vol = np.ascontiguousarray(vol0 * j)
@@ -362,7 +362,7 @@ def porous_stress_rhs(F, pressure, nbh: Nbh, m: Membrane):
 
 
 def momentum_flux_rate(F, vel_fluid, flux, vol0, nbh: Nbh):
-    """porous.py:574: -sum_b V_b ((vq)_a + (vq)_b) . (F_a^-1 B_a^T grad)."""
+    """porous.py:239: -sum_b V_b ((vq)_a + (vq)_b) . (F_a^-1 B_a^T grad)."""
     n, d = flux.shape
     out = np.zeros((n, d))
     vq = np.ascontiguousarray(vel_fluid[:, :, None] * flux[:, None, :])
@@ -376,7 +376,7 @@ def momentum_flux_rate(F, vel_fluid, flux, vol0, nbh: Nbh):
 
 
 def split_velocities(F, fluid_mass, momentum, flux, vol0, m: Membrane):
-    """porous.py:601 with the dry-region guard."""
+    """porous.py:266 with the dry-region guard."""
     j = det(F)
     rho_s = m.density0 / j
     rho_l = fluid_mass / (vol0 * j)

@@ -6,7 +6,7 @@ the CUDA path:
 
   NeckingOracle  ~ scenarios.py:41  NeckingProblem
   PorousOracle   ~ scenarios.py:171 PorousProblem
-  run_outer_inner ~ stepping.py:347
+  run_outer_inner ~ stepping.py:158
 """
 
 from __future__ import annotations
@@ -278,7 +278,7 @@ class PorousOracle:
 
 def run_outer_inner(problem, dt_outer, n_outer, eta, criterion, cfl=0.6,
                     max_inner=0, min_inner=1):
-    """stepping.py:347 restated; returns per-outer-step records."""
+    """stepping.py:158 restated; returns per-outer-step records."""
     rows = []
     for step in range(1, n_outer + 1):
         t = step * dt_outer

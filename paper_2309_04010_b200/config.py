@@ -88,7 +88,8 @@ KEYS = {
     "t_total": _k(float, _P), "n_outer": _k(int, _NN), "eta": _k(float, _NN),
     "energy_pct": _k(float, _P), "energy_ref": _k(float, _NN), "max_inner": _k(int, _NN),
     "min_inner": _k(int, _P), "ramp_steps": _k(int, _P), "cfl": _k(float, _P),
-    "damping_sweep": Key(str, lambda v: v in ("serial", "coloured"), "serial or coloured"),
+    "damping_sweep": Key(str, lambda v: v in ("serial", "coloured", "tiled"),
+                         "serial, coloured or tiled"),
     "ref_force": _k(float, _P), "ref_displacement": _k(float, _P),
 }
 
@@ -210,6 +211,25 @@ def _convert(key: str, text: str, line_no: int):
     return value
 
 
+def _check_value(key: str, value, line_no=None):
+    """Type and range check of one merged value (dict input and CLI
+    overrides get the same validation as config-file lines)."""
+    spec = KEYS.get(key)
+    at = f"line {line_no}: " if line_no else ""
+    if spec is None:
+        raise ConfigError(f"{at}unknown key {key!r}")
+    kind = spec.kind
+    ok_type = (isinstance(value, bool) if kind is bool else
+               isinstance(value, int) and not isinstance(value, bool) if kind is int else
+               isinstance(value, (int, float)) and not isinstance(value, bool) if kind is float else
+               isinstance(value, str))
+    if not ok_type:
+        raise ConfigError(f"{at}value {value!r} for key {key!r} is not a valid {kind.__name__}")
+    if spec.check is not None and not spec.check(value):
+        what = "out of range" if kind in (int, float) else "invalid"
+        raise ConfigError(f"{at}value {value!r} for key {key!r} {what} ({spec.rule})")
+
+
 def parse_file(path: str):
     """(raw key/value dict, key -> line number) of a config file."""
     raw, where = {}, {}
@@ -250,6 +270,9 @@ def resolve(raw: dict, path: str = "<memory>", lines: dict | None = None,
         if key != "scenario" and key not in defaults:
             at = f"line {lines[key]}: " if lines and key in lines else ""
             raise ConfigError(f"{at}key {key!r} does not apply to scenario {name!r}")
+    for key, value in merged.items():
+        if key != "scenario":
+            _check_value(key, value, lines.get(key) if lines else None)
     params = {**defaults, **merged, "scenario": name}
     _derive(params)
     return RunConfig(path=path, raw=merged, params=params, lines=dict(lines or {}))

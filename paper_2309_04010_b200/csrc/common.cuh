@@ -179,7 +179,7 @@ template <class T> struct DBuf {
 
 // ---------------------------------------------------------------- kernel
 
-// Anisotropic Wendland C2 kernel, support 2h (kernels.py:91-129).  Scaled
+// Anisotropic Wendland C2 kernel, support 2h (kernels.py:76-118).  Scaled
 // separation u_k = r_k / h_k, q = |u|:
 //   w(q) = (1 - q/2)^4 (1 + 2q),  dw/dq = -5 q (1 - q/2)^3
 //   grad_k = pref * dw/dq / q * u_k / h_k = pref * (-5 (1-q/2)^3) u_k / h_k

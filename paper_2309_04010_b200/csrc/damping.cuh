@@ -30,7 +30,8 @@ struct Ctrl {
     double ramp_disp, h, sound;
     double vol_movable;   // porous energy density normaliser
     long long n_inner, min_inner, max_inner, ramp_left;
-    int done, cap_hit, mode, pad;
+    int done, cap_hit, mode;
+    int remote_err;       // multi-rank: another rank reported an error (k_ctrl_ranks)
     unsigned long long err_inv, err_rm;  // min original id per error class
 };
 
@@ -509,6 +510,10 @@ template <int D> void build_serial_entries(NbhDev &nb, const SweepArgs &A, cudaS
     if (nb.sweep != 1 || (env && atoi(env) == 0)) return;
     const int64_t ng = nb.level_groups.n;
     if (ng == 0 || serial_smem_bytes(nb.n, D, nb.nlevels) > kSerialSmemMax) return;
+    // the shared-memory opt-in is a per-device function attribute: set it on
+    // every build (on the device this problem lives on), not once per process
+    MT_CUDA(cudaFuncSetAttribute(k_sweep_serial_smem<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kSerialSmemMax));
     // side-table offsets of the small groups, in level order
     std::vector<int64_t> lg(ng), gp(nb.ngroups + 1), off(ng, 0);
     nb.level_groups.download(lg.data(), ng, s);
@@ -538,12 +543,6 @@ int launch_sweep(const NbhDev &nb, const SweepArgs &A, const int64_t *level_ptr_
     if (nb.sweep == 1) {
         const size_t sm = serial_smem_bytes(nb.n, D, nb.nlevels);
         if (nb.serial_ent.n && sm <= kSerialSmemMax) {
-            static bool attr = false;   // per template instance
-            if (!attr) {
-                MT_CUDA(cudaFuncSetAttribute(k_sweep_serial_smem<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)kSerialSmemMax));
-                attr = true;
-            }
             k_sweep_serial_smem<D><<<1, kSerialThreads, sm, s>>>(A, nb.serial_ent.p, nb.serial_side.p, level_ptr_d,
                                                                  nb.nlevels, (int)nb.n, ctrl);
             MT_LAUNCH_CHECK();

@@ -502,6 +502,8 @@ static void check_solid_errors(mtsph_solid *S) {
         throw Error(MTSPH_ERR_RETURN_MAP, "return mapping did not converge (first id " +
                                               std::to_string(S->hc->err_rm) + ")",
                     {(int64_t)S->hc->err_rm});
+    if (S->hc->remote_err)
+        throw Error(MTSPH_ERR_NONFINITE, "inner loop stopped by an error on another rank");
 }
 
 extern "C" mtsph_status mtsph_solid_create(const mtsph_solid_desc *dsc, mtsph_solid **out) {
@@ -618,6 +620,7 @@ extern "C" mtsph_status mtsph_solid_create(const mtsph_solid_desc *dsc, mtsph_so
     S->hc->cfl = 0.6;
     S->hc->min_dt = INFINITY;
     S->hc->err_inv = S->hc->err_rm = ~0ull;
+    S->hc->remote_err = 0;
     S->hc->vol_movable = 0.0;
     S->ctrl.alloc(1);
     S->push_ctrl();
@@ -707,6 +710,7 @@ extern "C" mtsph_status mtsph_solid_relax(mtsph_solid *S, const mtsph_inner_para
     c->cap_hit = 0;
     c->min_dt = INFINITY;
     c->err_inv = c->err_rm = ~0ull;
+    c->remote_err = 0;
     S->push_ctrl();
     if (S->d == 2) solid_init_dt<2>(S); else solid_init_dt<3>(S);
     int which = 0;
@@ -763,6 +767,7 @@ extern "C" mtsph_status mtsph_solid_run_steps(mtsph_solid *S, const mtsph_inner_
     c->cap_hit = 0;
     c->min_dt = INFINITY;
     c->err_inv = c->err_rm = ~0ull;
+    c->remote_err = 0;
     S->push_ctrl();
     if (!g_timed || g_timed->steps != nsteps || g_timed->owner != S) {
         g_timed = std::make_unique<TimedGraph>();
@@ -848,6 +853,7 @@ extern "C" mtsph_status mtsph_solid_set_step(mtsph_solid *S, double dt, double e
     S->hc->eta = eta;
     S->hc->done = 0;
     S->hc->err_inv = S->hc->err_rm = ~0ull;
+    S->hc->remote_err = 0;
     S->push_ctrl();
     API_END
 }
@@ -1006,6 +1012,7 @@ extern "C" mtsph_status mtsph_solid_begin_loop(mtsph_solid *S, const mtsph_inner
     c->cap_hit = 0;
     c->min_dt = INFINITY;
     c->err_inv = c->err_rm = ~0ull;
+    c->remote_err = 0;
     S->push_ctrl();
     API_END
 }

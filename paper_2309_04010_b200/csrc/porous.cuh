@@ -2,7 +2,7 @@
 //
 // Outer (slow) step = PorousProblem.advance_slow (scenarios.py:226):
 //   k_por_prep      J, current volume, rho_l, saturation, D rho_l, and the
-//                   gradient map A = F^-1 B^T              (porous.py:456-473)
+//                   gradient map A = F^-1 B^T              (porous.py:133-139)
 //   k_por_flux      q_a = D rho_l,a sum_b V_b (s_a - s_b) (A_a gradW)    (:503)
 //   k_por_mass      conservative pair-form mass rate, gathered per
 //                   particle (no atomics, fixed order), clamp + counting,
@@ -238,7 +238,7 @@ __global__ void __launch_bounds__(256) k_por_mass(PorousArgs A, double dt, int c
     if (threadIdx.x == 0) A.part[blockIdx.x] = s;
 }
 
-// split_velocities (porous.py:601) for particle i; returns v_s, v_l
+// split_velocities (porous.py:266) for particle i; returns v_s, v_l
 template <int D>
 __device__ __forceinline__ void split_vel(const PorousArgs &A, int64_t i, double j, const double *M,
                                           const double *q, double *vs, double *vl) {
@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(256) k_por_post(PorousArgs A) {
     V[i] = w;
 }
 
-// -sum_b V_b (vl_a q_a^T + vl_b q_b^T) (A_a gradW) (porous.py:574), with the
+// -sum_b V_b (vl_a q_a^T + vl_b q_b^T) (A_a gradW) (porous.py:239), with the
 // neighbour loop carrying G = sum_b V_b g and sum_b V_b (q_b . g) vl_b,
 // g = -A_a gradW: the vl_a q_a^T term is applied once after the loop
 template <int D>

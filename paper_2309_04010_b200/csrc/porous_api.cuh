@@ -98,6 +98,8 @@ static void check_porous_errors(mtsph_porous *P) {
         throw Error(MTSPH_ERR_INVERSION, "non-positive deformation determinant (first id " +
                                              std::to_string(P->hc->err_inv) + ")",
                     {(int64_t)P->hc->err_inv});
+    if (P->hc->remote_err)
+        throw Error(MTSPH_ERR_NONFINITE, "inner loop stopped by an error on another rank");
 }
 
 extern "C" mtsph_status mtsph_porous_create(const mtsph_porous_desc *dsc, mtsph_porous **out) {
@@ -206,6 +208,7 @@ extern "C" mtsph_status mtsph_porous_create(const mtsph_porous_desc *dsc, mtsph_
     P->hc->cfl = 0.6;
     P->hc->min_dt = INFINITY;
     P->hc->err_inv = P->hc->err_rm = ~0ull;
+    P->hc->remote_err = 0;
     P->hc->vol_movable = vol_movable;
     P->ctrl.alloc(1);
     P->push_ctrl();
@@ -251,6 +254,7 @@ extern "C" mtsph_status mtsph_porous_advance_slow(mtsph_porous *P, double dt_out
     API_BEGIN
     P->pull_ctrl();
     P->hc->err_inv = ~0ull;
+    P->hc->remote_err = 0;
     P->push_ctrl();
     *clamped = P->d == 2 ? porous_advance<2>(P, dt_outer, t) : porous_advance<3>(P, dt_outer, t);
     check_porous_errors(P);
@@ -347,6 +351,7 @@ extern "C" mtsph_status mtsph_porous_set_step(mtsph_porous *P, double dt, double
     P->hc->eta = eta;
     P->hc->done = 0;
     P->hc->err_inv = ~0ull;
+    P->hc->remote_err = 0;
     P->push_ctrl();
     API_END
 }
@@ -441,6 +446,7 @@ extern "C" mtsph_status mtsph_porous_begin_loop(mtsph_porous *P, const mtsph_inn
     c->cap_hit = 0;
     c->min_dt = INFINITY;
     c->err_inv = c->err_rm = ~0ull;
+    c->remote_err = 0;
     if (vol_movable > 0.0) c->vol_movable = vol_movable;   // the whole problem's, for E_k
     P->push_ctrl();
     API_END
@@ -629,6 +635,7 @@ extern "C" mtsph_status mtsph_porous_relax(mtsph_porous *P, const mtsph_inner_pa
     c->min_dt = INFINITY;
     c->ramp_left = 0;
     c->err_inv = c->err_rm = ~0ull;
+    c->remote_err = 0;
     P->push_ctrl();
     if (P->d == 2) porous_init_dt<2>(P); else porous_init_dt<3>(P);
     int which = 0;

@@ -1,19 +1,19 @@
 // solid.cuh -- total-Lagrangian elastoplastic inner relaxation on the GPU.
 //
 // One inner step = NeckingProblem.relax_step (scenarios.py:113) + the
-// stepping.py:347 bookkeeping, as five kernels plus the damping sweep:
+// stepping.py:158 bookkeeping, as five kernels plus the damping sweep:
 //
 //   k_solid_kick_drift : v += dt/2 a (free), boundary ramp / clamps, x += dt v
 //   k_solid_stress     : SELL gather dF/dt = (sum_b V_b (v_b - v_a) (x) gradW) B
-//                        (solids.py:364), F += dt dF/dt, J2 return map or
-//                        Neo-Hookean stress (plasticity.py:118, solids.py:394),
+//                        (solids.py:118), F += dt dF/dt, J2 return map or
+//                        Neo-Hookean stress (plasticity.py:118, solids.py:148),
 //                        T = P B stored for the divergence
 //   k_solid_accel      : SELL gather a = 1/rho0 sum_b V_b (T_a + T_b) gradW
-//                        (solids.py:416), v += dt/2 a, E_k and |a|max partials
+//                        (solids.py:170), v += dt/2 a, E_k and |a|max partials
 //   sweep              : damping (damping.cuh)
 //   k_solid_vmax       : |v|max partial after damping
 //   k_solid_ctrl       : 1 block: fixed-order reductions, convergence test,
-//                        counters, next dt (solids.py:433) -- all on device
+//                        counters, next dt (solids.py:187) -- all on device
 //
 // State lives in HBM in the Morton order of the neighbourhood: own-access
 // fields SoA (coalesced), gathered fields AoS (X|vol and v as one 32 B
@@ -541,7 +541,7 @@ __device__ __forceinline__ double stable_dt(const Ctrl *c, double vmax2, double 
 }
 
 // the stopping rule and next step from the reduced E_k sum, |a|max^2 and
-// |v|max^2 (stepping.py:369-385, solids.py:433); one thread
+// |v|max^2 (stepping.py:177-195, solids.py:187); one thread
 __device__ __forceinline__ void ctrl_apply(Ctrl *c, double E, double AM, double VM, int mode) {
     c->amax2 = AM;
     c->vmax2 = VM;
@@ -623,7 +623,12 @@ __global__ void k_ctrl_ranks(Ctrl *c, const double *gathered, int nranks, int mo
         err = fmax(err, gathered[4 * r + 3]);
     }
     ctrl_apply(c, E, AM, VM, mode);
-    if (err > 0.0) c->done = 1;
+    if (err > 0.0) {
+        c->done = 1;
+        // a rank without an error of its own still has to fail (its host
+        // would otherwise enter the next outer step's exchanges alone)
+        if (c->err_inv == ~0ull && c->err_rm == ~0ull) c->remote_err = 1;
+    }
 }
 
 // observables (NeckingProblem.measure) as per-block partials

@@ -11,8 +11,8 @@ exchanges:
       sweep colour c    -> push modified ghosts back to their owners;
                            refresh ghost v
   |v|max                -> allreduce(max)
-  host: kinetic-energy criterion, ramp counter, next dt (stepping.py:369-385,
-        solids.py:433 -- same formulas as the device control kernel)
+  host: kinetic-energy criterion, ramp counter, next dt (stepping.py:177-195,
+        solids.py:187 -- same formulas as the device control kernel)
 
 Because every rank bins on the global cell grid, the decomposed run
 performs the single-domain tiled operations; `LocalGroup` runs all ranks in
@@ -238,7 +238,7 @@ class TorchGroup:
 
 
 def stable_dt(h, sound, cfl, vmax2, amax2):
-    """solids.py:433, evaluated like the device control kernel."""
+    """solids.py:187, evaluated like the device control kernel."""
     dt = h / (sound + math.sqrt(vmax2))
     amax = math.sqrt(amax2)
     if amax > 0.0:
@@ -369,7 +369,7 @@ class DecomposedSolid:
         """The inner loop with the control on the device of every rank: the
         phases and exchanges are enqueued without host synchronisation, the
         ranks' reductions are all-gathered on the device and each rank's
-        control kernel takes the same decisions (stepping.py:347 rule); the
+        control kernel takes the same decisions (stepping.py:158 rule); the
         host reads the control block once every `check_every` steps.
         Returns (n_inner, ek, cap_hit, min_dt) like relax()."""
         if fixed_steps is not None:

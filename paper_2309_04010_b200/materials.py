@@ -1,9 +1,9 @@
 """Material models of the drop-in API.
 
-ElasticModel   ~ reference solids.py:268  (mu, K, E, nu, rho0; sound speed)
+ElasticModel   ~ reference solids.py:23  (mu, K, E, nu, rho0; sound speed)
 HardeningModel ~ reference plasticity.py:27 (saturation + linear hardening),
                  plus the BASELINE power law  k(a) = s0 (1 + a/e0)^m
-MembraneModel  ~ reference porous.py:362  (Table 3 Nafion parameters)
+MembraneModel  ~ reference porous.py:27  (Table 3 Nafion parameters)
 """
 
 from __future__ import annotations

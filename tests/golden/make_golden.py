@@ -13,14 +13,14 @@ Every case records both the inputs and the reference outputs, so the
 fixtures are self-describing.  Reference call sites used (file:line of
 /root/reference/pkg/src/mtsph):
   neighbors.py:59   build_neighborhoods / neighbors.py:232 corrections
-  solids.py:364     deformation_rate      solids.py:416 stress divergence
-  solids.py:394     kirchhoff_stress      solids.py:410 first_pk
+  solids.py:118     deformation_rate      solids.py:170 stress divergence
+  solids.py:148     kirchhoff_stress      solids.py:164 first_pk
   plasticity.py:118 return_map
-  stepping.py:290   apply_damping_sweep (-> _accel.py:171 damping_sweep)
-  porous.py:476/503/529/574/601 diffusion, stress, flux, split
+  stepping.py:101   apply_damping_sweep (-> _accel.py:171 damping_sweep)
+  porous.py:141/168/194/239/266 diffusion, stress, flux, split
   _accel.py:240     porous_stress_rhs
   scenarios.py:113  NeckingProblem.relax_step, :278 PorousProblem.relax_step
-  stepping.py:347   run_outer_inner
+  stepping.py:158   run_outer_inner
 """
 
 from __future__ import annotations

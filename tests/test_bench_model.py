@@ -44,3 +44,33 @@ def test_launch_list_segments(tmp_path):
     solid = ms.launches(str(p), segment=1)
     assert set(solid) == {"k_cell_keys", "k_solid_stress_csr", "k_sweep_flow", "k_sweep_flow32"}
     assert abs(sum(v["share"] for v in solid.values()) - 1.0) < 1e-12
+
+
+def test_bench_gpus_n_launches_n_ranks():
+    """`bench.py --gpus 2` started without torchrun re-launches itself as two
+    ranks (127.0.0.1 rendezvous); the reference arm runs on rank 0 alone with
+    every host thread and reports n_gpus 2.  (The GPU arm's ranks are the
+    same launch; it needs the GPUs.)"""
+    import json
+    import subprocess
+    env = dict(os.environ)
+    env.pop("WORLD_SIZE", None)
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2",
+                          "--impl", "reference", "--steps", "1", "--warmup", "3",
+                          "--cpu-cols", "8"], capture_output=True, text=True, env=env,
+                         timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    rec = json.loads(lines[0])
+    assert rec["impl"] == "reference" and rec["n_gpus"] == 2
+    assert rec["cpu_baseline"]["cores"] == len(os.sched_getaffinity(0))
+
+
+def test_bench_rejects_mismatched_world_size():
+    import subprocess
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2",
+                          "--impl", "reference"], capture_output=True, text=True, env=env,
+                         timeout=300, cwd=ROOT)
+    assert out.returncode != 0 and "WORLD_SIZE" in out.stderr

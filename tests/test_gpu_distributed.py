@@ -229,3 +229,30 @@ def test_decomposed_porous_device_loop(group):
         got = dec.gather(field)
         scale = max(float(np.max(np.abs(want))), 1e-300)
         assert float(np.max(np.abs(got - want))) / scale <= 1e-12, field
+
+
+@pytest.mark.parametrize("group", ["local", "local_device"])
+def test_error_on_one_rank_fails_every_rank(group):
+    """An element inversion on rank 1 only: rank 1 raises
+    ElementInversionError with the particle's id, and rank 0 -- which has no
+    error of its own -- raises SimulationError instead of returning a normal
+    result (its host would otherwise go on to the next outer step's exchanges
+    alone and hang).  The flag travels in the all-gathered control partials."""
+    from paper_2309_04010_b200.distributed import DecomposedSolid
+    from paper_2309_04010_b200.errors import ElementInversionError, SimulationError
+    p, lat, el, hard = _setup()
+    dec = DecomposedSolid(lat, el, hard, 2, group=group)
+    plan = dec.plans[1]
+    own = np.flatnonzero(~plan.ghost & ~lat.constrained[plan.local_ids])
+    victim = int(own[len(own) // 2])
+    dev1 = dec.devices[1]
+    F = dev1.get("F")
+    F[victim] = np.diag([-1.0, 1.0, 1.0])
+    dev1.set("F", F)
+    with pytest.raises((ElementInversionError, SimulationError)):
+        dec.relax_device(p["eta"], p["cfl"], 0.0, 1.0, fixed_steps=4, check_every=2)
+    with pytest.raises(ElementInversionError) as e1:
+        dec.devices[1].loop_state()
+    assert int(plan.local_ids[victim]) in e1.value.particle_ids or victim in e1.value.particle_ids
+    with pytest.raises(SimulationError, match="another rank"):
+        dec.devices[0].loop_state()

@@ -74,7 +74,7 @@ def test_layer1_damping_sweep_matches_reference(gold_nbh, gold_ops, nb):
 
 @pytest.mark.parametrize("p", ["p2d_", "p3d_"])
 def test_layer1_porous_kernels_match_reference(gold_porous, p):
-    """porous.py:476/503/574 and _accel.py:240 through the drop-ins."""
+    """porous.py:141/168/239 and _accel.py:240 through the drop-ins."""
     from oracle import oracle as O
     lib, ptr, check = _lib()
     gp = gold_porous

@@ -39,6 +39,28 @@ def test_config_errors_name_the_problem(tmp_path, text, match):
         load_config(str(cfg))
 
 
+def test_every_damping_order_is_selectable_from_a_config_file(tmp_path):
+    for order in ("serial", "coloured", "tiled"):
+        cfg = tmp_path / f"{order}.cfg"
+        cfg.write_text(f"scenario = bar_3d\ndamping_sweep = {order}\n")
+        assert load_config(str(cfg)).params["damping_sweep"] == order
+
+
+@pytest.mark.parametrize("raw,match", [
+    ({"dp": -0.1}, "out of range"),
+    ({"damping_sweep": "random"}, "invalid"),
+    ({"n_outer": 2.5}, "not a valid int"),
+    ({"eta": "fast"}, "not a valid float"),
+    ({"h_factor": 0.0}, "out of range"),
+])
+def test_dict_input_and_overrides_are_validated_like_files(raw, match):
+    with pytest.raises(ConfigError, match=match):
+        resolve({"scenario": "bar_2d", **raw})
+    key, value = next(iter(raw.items()))
+    with pytest.raises(ConfigError, match=match):
+        resolve({"scenario": "bar_2d"}, overrides={key: value})
+
+
 def test_fsi_auto_outer_steps():
     p = resolve({"scenario": "fsi_3d", "dp": 0.125e-3 / 2}).params
     h = p["h_factor"] * p["dp"]
