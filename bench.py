@@ -173,14 +173,20 @@ def outer_bytes(d, nnz_pp):
     return prep_a + flux + mass + prep + flux + post + frate
 
 
-def membrane_leg(args):
-    """Outer-loop diffusion + porous inner relaxation on the reference's 3D
-    porous film (fsi_3d) widened to ~10 M particles (north star item 4)."""
+def membrane_params(length_factor=1.0):
+    """BASELINE configs[3]: the 40 x 40 x 1 cantilever plate (membrane_3d,
+    dp 1/22, 17.1 M particles), configs[1] material, wetted top face."""
     from paper_2309_04010_b200.config import resolve
+    base = resolve({"scenario": "membrane_3d"}).params
+    return resolve({"scenario": "membrane_3d", "damping_sweep": "tiled",
+                    "length": base["length"] * length_factor}).params
+
+
+def membrane_leg(args):
+    """Outer-loop diffusion + porous inner relaxation on BASELINE configs[3]
+    (the membrane_3d plate, 17.1 M particles; north star item 4)."""
     from paper_2309_04010_b200.scenarios import build_problem, make_policy
-    side = args.membrane_side
-    params = resolve({"scenario": "fsi_3d", "length": side, "breadth": side,
-                      "damping_sweep": "tiled"}).params
+    params = membrane_params()
     t0 = time.perf_counter()
     prob = build_problem(params, sweep="tiled")
     setup_s = time.perf_counter() - t0
@@ -205,8 +211,9 @@ def membrane_leg(args):
     nnz_pp = dev.sizes()["nnz"] / n
     model = outer_bytes(d, nnz_pp)
     peak, _ = load_peaks()
-    out = {"workload": f"fsi_3d porous film {side:g} x {side:g} x {params['thickness']:g} m, "
-                       f"anisotropy {params['anisotropy']:g} ({n} particles), tiled sweep, fp64",
+    out = {"workload": f"membrane_3d plate (BASELINE configs[3]) {params['length']:g} x "
+                       f"{params['breadth']:g} x {params['thickness']:g}, dp 1/22 ({n} particles), "
+                       "top face wetted, left edge clamped, tiled sweep, fp64",
            "particles": n, "setup_s": setup_s,
            "inner": {"value": n * int(r.n_inner) / inner_s, "unit": "particle-steps/s",
                      "ms_per_step": 1e3 * inner_s / max(int(r.n_inner), 1),
@@ -528,20 +535,18 @@ def run_decomposed(args, world, rank, local):
 
 
 def membrane_decomposed(args, world, rank, local):
-    """BASELINE configs[3] on N GPUs: the porous film (fsi_3d, 10 M particles
-    per GPU under weak scaling: the film N times longer along x) on x-slabs,
-    porous inner steps device-controlled (DecomposedPorous.relax_device, NCCL
-    halos and all-gather), one outer diffusion step with its exchanges."""
+    """BASELINE configs[3] on N GPUs: the membrane_3d plate (17.1 M
+    particles split N ways; --scaling weak: the plate N times longer) on
+    x-slabs, porous inner steps device-controlled (DecomposedPorous.
+    relax_device, NCCL halos and all-gather), one outer diffusion step with
+    its exchanges."""
     import torch
     import torch.distributed as dist
     from paper_2309_04010_b200 import lattices
     from paper_2309_04010_b200.config import resolve
     from paper_2309_04010_b200.distributed import DecomposedPorous
     from paper_2309_04010_b200.scenarios import _membrane, make_policy
-    side = args.membrane_side
-    length = side * (world if args.scaling == "weak" else 1)
-    params = resolve({"scenario": "fsi_3d", "length": length, "breadth": side,
-                      "damping_sweep": "tiled"}).params
+    params = membrane_params(world if args.scaling == "weak" else 1)
     lat = lattices.build_lattice(params)
     pol = make_policy(params, float(np.min(lat.h_axes)))
     t0 = time.perf_counter()
@@ -571,8 +576,9 @@ def membrane_decomposed(args, world, rank, local):
     w = torch.tensor([time.perf_counter() - w0], dtype=torch.float64, device=f"cuda:{local}")
     dist.all_reduce(w, op=dist.ReduceOp.MAX)
     n = lat.n
-    return {"workload": f"fsi_3d porous film {length:g} x {side:g} x {params['thickness']:g} m "
-                        f"({n} particles, {n // world} per GPU), tiled sweep, fp64, {world} x-slabs",
+    return {"workload": f"membrane_3d plate (BASELINE configs[3]) {params['length']:g} x "
+                        f"{params['breadth']:g} x {params['thickness']:g} ({n} particles, "
+                        f"{n // world} per GPU), tiled sweep, fp64, {world} x-slabs",
             "setup_s": setup_s,
             "inner": {"value": n / (inner_ms / 1e3), "unit": "particle-steps/s",
                       "ms_per_step": inner_ms,
@@ -670,8 +676,6 @@ def main():
                     help="decomposed runs: total (strong) or per-GPU (weak) particle count; "
                          "default 32e6 / 4e6")
     ap.add_argument("--no-membrane", action="store_true", help="skip the porous membrane leg")
-    ap.add_argument("--membrane-side", type=float, default=0.14,
-                    help="fsi_3d film edge (m); 0.14 gives ~10 M particles")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.gpus < 1:

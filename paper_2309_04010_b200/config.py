@@ -7,6 +7,8 @@ workloads used by the benchmarks:
   bar_2d       configs[0]  2D plane-strain power-law-hardening bar 20 x 2, dp 0.1
   membrane_2d  configs[1]  2D Nafion strip 10 x 0.5, dp 0.025, top-face wetting
   bar_3d       configs[2]  3D power-law-hardening bar 20 x 2 x 2, dp 0.02
+  membrane_3d  configs[3]  3D Nafion plate 40 x 40 x 1, dp 1/22 (17 M particles),
+                          top-face wetting, cantilever (left edge clamped)
   block_3d     configs[4]  3D jittered elastic-plastic block (scaling sweep)
 
 Format: one ``key = value`` per line, ``#`` comments, optional
@@ -165,8 +167,16 @@ SCENARIO_DEFAULTS = {
                     "n_outer": 400, "eta": 0.0, "energy_pct": 1.0e-8,
                     "evaporation_rate": 0.0, "h_factor": 1.3},
 }
+# BASELINE configs[3]: the configs[1] material and wetting on a 40 x 40 x 1
+# plate, clamped along its left edge.  BASELINE's dp = 0.01 would give
+# 1.6e9 particles, not its stated ~16 M; dp = 1/22 (880 x 880 x 22 plus the
+# clamp columns = 17.1 M) keeps the stated size and the geometry
+SCENARIO_DEFAULTS["membrane_3d"] = {
+    **SCENARIO_DEFAULTS["membrane_2d"], "length": 40.0, "breadth": 40.0, "thickness": 1.0,
+    "dp": 1.0 / 22.0, "t_total": 400 * 0.25 * (1.0 / 22.0) ** 2 / 1.0e-3, "n_outer": 400}
+del SCENARIO_DEFAULTS["membrane_3d"]["width"]
 
-FSI_SCENARIOS = ("fsi_2d", "fsi_3d", "membrane_2d")
+FSI_SCENARIOS = ("fsi_2d", "fsi_3d", "membrane_2d", "membrane_3d")
 
 
 @dataclass
@@ -288,14 +298,16 @@ def _derive(p: dict) -> None:
     if name in ("bar_2d", "bar_3d", "block_3d") and p["eta"] == 0.0:
         c = math.sqrt(p["bulk_modulus"] / p["density"])
         p["eta"] = 0.1 * p["density"] * c * p["h_factor"] * p["dp"]
-    if name == "membrane_2d":
+    if name in ("membrane_2d", "membrane_3d"):
         e, nu = p["youngs_modulus"], p["poisson_ratio"]
         mu = e / (2.0 * (1.0 + nu))
         lam = e / (3.0 * (1.0 - 2.0 * nu)) - 2.0 * mu / 3.0
         if p["pressure_coeff"] == 0.0:
-            # plane-strain free swelling: sigma = 2 mu e + lam tr(e) I - p I = 0
-            # with e = eps I  ->  p = 2 (mu + lam) eps;  eps = 0.05 at sat = a
-            p["pressure_coeff"] = 2.0 * (mu + lam) * 0.05 / p["porosity"]
+            # free swelling: sigma = 2 mu e + lam tr(e) I - p I = 0 with
+            # e = eps I  ->  p = 2 (mu + lam) eps (plane strain) or
+            # (2 mu + 3 lam) eps (3D);  eps = 0.05 at sat = porosity (c = 1)
+            k = 2.0 * (mu + lam) if name == "membrane_2d" else 2.0 * mu + 3.0 * lam
+            p["pressure_coeff"] = k * 0.05 / p["porosity"]
         if p["eta"] == 0.0:
             c = math.sqrt((e / (3.0 * (1.0 - 2.0 * nu))) / p["density"])
             p["eta"] = 0.1 * p["density"] * c * p["h_factor"] * p["dp"]

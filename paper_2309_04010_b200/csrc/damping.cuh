@@ -99,17 +99,20 @@ struct SweepArgs {
     KSpec ks;
 };
 
-template <int D>
+// CG: read the velocities through L2 (the multi-CTA serial kernel, where
+// other SMs wrote them at earlier levels)
+template <int D, bool CG = false>
 __device__ __forceinline__ void visit_group(const SweepArgs &A, int64_t g, double half) {
     using V_t = typename VT<D>::T;
     V_t *V = reinterpret_cast<V_t *>(A.V);
+    auto vload = [&](int64_t i) { return CG ? vldcg(V + i) : V[i]; };
     const int64_t lo = A.gptr[g], hi = A.gptr[g + 1];
     if (hi - lo == 1) {
         const int32_t i = A.pi[lo], j = A.pj[lo];
         const double c = half * pair_damp<D>(A.XV[i], A.XV[j], A.ks);
         const double ca = c * A.inv_m[i], cb = c * A.inv_m[j];
         const double den = 1.0 + ca + cb;
-        V_t vi = V[i], vj = V[j];
+        V_t vi = vload(i), vj = vload(j);
         double a[3], b[3];
         vget(vi, a);
         vget(vj, b);
@@ -143,7 +146,7 @@ __device__ __forceinline__ void visit_group(const SweepArgs &A, int64_t g, doubl
     for (int r = 0; r < nb; ++r) {
         for (int c = 0; c < nb; ++c) Am[r * nb + c] = (r == c) ? 1.0 : 0.0;
         double v[3];
-        vget(V[loc[r]], v);
+        vget(vload(loc[r]), v);
         for (int m = 0; m < D; ++m) rhs[r * 3 + m] = v[m];
     }
     for (int64_t k = lo; k < hi; ++k) {
@@ -254,9 +257,9 @@ __global__ void k_serial_entries(SweepArgs A, const int64_t *__restrict__ level_
 // the simultaneous solve of a small group from its precomputed pair
 // entries, local arrays instead of the global scratch (same arithmetic as
 // visit_group)
-template <int D>
-__device__ void group_solve_entries(const double2 *__restrict__ pe, int cnt, const double *__restrict__ inv_m,
-                                    double half, double *sv, int n) {
+template <int D, class Acc>
+__device__ void group_solve_entries_acc(const double2 *__restrict__ pe, int cnt, const double *__restrict__ inv_m,
+                                        double half, const Acc &V) {
     constexpr int NB = 2 * kGroupMax;
     double2 e[kGroupMax];
     for (int q = 0; q < cnt; ++q) e[q] = __ldg(pe + q);
@@ -284,7 +287,7 @@ __device__ void group_solve_entries(const double2 *__restrict__ pe, int cnt, con
     double Am[NB * NB], rhs[NB * 3];
     for (int r = 0; r < nb; ++r) {
         for (int c = 0; c < nb; ++c) Am[r * nb + c] = (r == c) ? 1.0 : 0.0;
-        for (int m = 0; m < D; ++m) rhs[r * 3 + m] = sv[m * n + loc[r]];
+        for (int m = 0; m < D; ++m) rhs[r * 3 + m] = V.get(loc[r], m);
     }
     for (int q = 0; q < cnt; ++q) {
         const double c = half * e[q].y;
@@ -316,7 +319,23 @@ __device__ void group_solve_entries(const double2 *__restrict__ pe, int cnt, con
             rhs[r * 3 + m] = s / Am[r * nb + r];
         }
     for (int t = 0; t < nb; ++t)
-        for (int m = 0; m < D; ++m) sv[m * n + loc[t]] = rhs[t * 3 + m];
+        for (int m = 0; m < D; ++m) V.set(loc[t], m, rhs[t * 3 + m]);
+}
+
+// velocity accessors of the entry solvers: the shared copy (planar [D][n])
+// and the global records read through L2 (multi-CTA kernel: other SMs
+// wrote them at earlier levels, so L1 may hold stale lines)
+struct PlanarV {
+    double *sv;
+    int n;
+    __device__ __forceinline__ double get(int i, int m) const { return sv[m * n + i]; }
+    __device__ __forceinline__ void set(int i, int m, double x) const { sv[m * n + i] = x; }
+};
+
+template <int D>
+__device__ void group_solve_entries(const double2 *__restrict__ pe, int cnt, const double *__restrict__ inv_m,
+                                    double half, double *sv, int n) {
+    group_solve_entries_acc<D>(pe, cnt, inv_m, half, PlanarV{sv, n});
 }
 
 // velocity accessor of the shared copy: planar [D][n]
@@ -487,6 +506,112 @@ __global__ void __launch_bounds__(kSerialThreads, 1)
     }
 }
 
+// ---- exact serial order, large problems: every level is spread over the
+// whole grid (one persistent launch, all CTAs co-resident) and a grid-wide
+// barrier separates consecutive levels.  The levels of the reference order
+// grow with the bar length (~30 per lattice column in 3D), the groups of one
+// level with the cross-section, so a level of a 10 M-particle bar holds ~1e4
+// groups: enough for every SM, where the one-CTA kernels above run them 1024
+// at a time.  Entries and arithmetic are those of k_sweep_serial_smem (single
+// pairs from the precomputed (i, j, pair_damp) entries, small groups from
+// local arrays, larger groups through visit_group); velocities are read
+// through L2 (ld.global.cg) because other SMs wrote them at earlier levels.
+// Bit-identical to k_sweep_serial (tests/test_gpu_sweeps.py).
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned *p, unsigned v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// bar[0]: arrivals (0 between barriers), bar[1]: generation.  The last CTA to
+// arrive resets the count and bumps the generation; the others spin on it.
+__device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned &gen) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+            atomicExch(bar, 0u);
+            __threadfence();
+            st_release_u32(bar + 1, gen + 1);
+        } else {
+            while (ld_acquire_u32(bar + 1) == gen) __nanosleep(20);
+        }
+    }
+    ++gen;
+    __syncthreads();
+}
+
+// global velocity records as an entry-solver accessor
+template <int D> struct GlobalV {
+    using V_t = typename VT<D>::T;
+    V_t *V;
+    __device__ __forceinline__ double get(int i, int m) const {
+        double a[3];
+        vget(vldcg(V + i), a);
+        return a[m];
+    }
+    __device__ __forceinline__ void set(int i, int m, double x) const {
+        double *r = reinterpret_cast<double *>(V + i);
+        __stcg(r + m, x);
+    }
+};
+
+constexpr int kSerialGridThreads = 256;
+
+template <int D>
+__global__ void __launch_bounds__(kSerialGridThreads)
+    k_sweep_serial_grid(SweepArgs A, const double2 *__restrict__ ent, const double2 *__restrict__ side,
+                        const int64_t *__restrict__ level_ptr, int64_t nlevels, unsigned *bar, const Ctrl *ctrl) {
+    if (ctrl->done) return;  // the same decision on every CTA
+    using V_t = typename VT<D>::T;
+    V_t *V = reinterpret_cast<V_t *>(A.V);
+    const double half = 0.5 * ctrl->dt * ctrl->eta;
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    unsigned gen = ld_acquire_u32(bar + 1);  // nobody bumps it before every CTA arrived once
+    const GlobalV<D> GV{V};
+    for (int pass = 0; pass < 2; ++pass) {
+        for (int64_t s = 0; s < nlevels; ++s) {
+            const int64_t L = pass == 0 ? s : nlevels - 1 - s;
+            const int64_t k1 = __ldg(level_ptr + L + 1);
+            for (int64_t k = __ldg(level_ptr + L) + tid; k < k1; k += nth) {
+                const double2 e = __ldg(ent + k);
+                const long long key = __double_as_longlong(e.x);
+                if (key < 0) {
+                    const long long code = -2 - key;
+                    const int cnt = (int)(code & 0xff);
+                    if (cnt) group_solve_entries_acc<D>(side + (code >> 8), cnt, A.inv_m, half, GV);
+                    else visit_group<D, true>(A, code >> 8, half);
+                    continue;
+                }
+                const int i = (int)(uint32_t)key, j = (int)(uint32_t)((unsigned long long)key >> 32);
+                const double c = half * e.y;
+                const double ca = c * __ldg(A.inv_m + i), cb = c * __ldg(A.inv_m + j);
+                const double den = 1.0 + ca + cb;
+                V_t vi = vldcg(V + i), vj = vldcg(V + j);
+                double a[3], b[3];
+                vget(vi, a);
+                vget(vj, b);
+#pragma unroll
+                for (int m = 0; m < D; ++m) {
+                    const double u = (a[m] - b[m]) / den;
+                    a[m] -= ca * u;
+                    b[m] += cb * u;
+                }
+                vset(vi, a);
+                vset(vj, b);
+                vst(V + i, vi);
+                vst(V + j, vj);
+            }
+            grid_barrier(bar, gen);
+        }
+    }
+}
+
 // one colour phase: thread per task, groups in task order (dir>0) or
 // reversed (dir<0)
 template <int D>
@@ -505,15 +630,42 @@ __global__ void __launch_bounds__(128) k_sweep_colour(SweepArgs A, int64_t t0, i
 
 // the level-ordered entries of the shared-memory serial sweep (setup, once;
 // MTSPH_SERIAL_SMEM=0 keeps the global-memory kernel)
+// Which reference-order kernel runs: the shared-memory one when velocities
+// and level table fit (MTSPH_SERIAL_SMEM=0 disables it), else the multi-CTA
+// one when a level averages more groups than one CTA has threads
+// (MTSPH_SERIAL_GRID=0 disables it, 1 forces it), else the one-CTA global
+// kernel.  All three are bit-identical.
 template <int D> void build_serial_entries(NbhDev &nb, const SweepArgs &A, cudaStream_t s) {
-    const char *env = getenv("MTSPH_SERIAL_SMEM");
-    if (nb.sweep != 1 || (env && atoi(env) == 0)) return;
+    if (nb.sweep != 1) return;
     const int64_t ng = nb.level_groups.n;
-    if (ng == 0 || serial_smem_bytes(nb.n, D, nb.nlevels) > kSerialSmemMax) return;
-    // the shared-memory opt-in is a per-device function attribute: set it on
-    // every build (on the device this problem lives on), not once per process
-    MT_CUDA(cudaFuncSetAttribute(k_sweep_serial_smem<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)kSerialSmemMax));
+    if (ng == 0) return;
+    const char *env = getenv("MTSPH_SERIAL_SMEM");
+    const char *genv = getenv("MTSPH_SERIAL_GRID");
+    const bool smem = !(env && atoi(env) == 0) && serial_smem_bytes(nb.n, D, nb.nlevels) <= kSerialSmemMax;
+    nb.serial_grid = 0;
+    if (!smem) {
+        const int gmode = genv ? atoi(genv) : -1;
+        const double per_level = (double)ng / (double)std::max<int64_t>(nb.nlevels, 1);
+        if (gmode == 1 || (gmode != 0 && per_level > 2.0 * kSerialGridThreads)) {
+            int dev = 0, sms = 0, per = 0;
+            MT_CUDA(cudaGetDevice(&dev));
+            MT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+            MT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sweep_serial_grid<D>,
+                                                                  kSerialGridThreads, 0));
+            // every CTA must be resident (grid barrier); enough CTAs for a
+            // level's groups, no more (the barrier's cost grows with the grid)
+            const int64_t want = (int64_t)std::ceil(per_level / kSerialGridThreads);
+            nb.serial_grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * std::max(per, 1)));
+            nb.serial_bar.alloc(2);
+            nb.serial_bar.zero(s);
+        }
+        if (!nb.serial_grid) return;
+    } else {
+        // the shared-memory opt-in is a per-device function attribute: set it
+        // on every build (on the device this problem lives on)
+        MT_CUDA(cudaFuncSetAttribute(k_sweep_serial_smem<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)kSerialSmemMax));
+    }
     // side-table offsets of the small groups, in level order
     std::vector<int64_t> lg(ng), gp(nb.ngroups + 1), off(ng, 0);
     nb.level_groups.download(lg.data(), ng, s);
@@ -542,6 +694,12 @@ int launch_sweep(const NbhDev &nb, const SweepArgs &A, const int64_t *level_ptr_
     if (nb.npairs == 0) return 0;
     if (nb.sweep == 1) {
         const size_t sm = serial_smem_bytes(nb.n, D, nb.nlevels);
+        if (nb.serial_grid > 0 && nb.serial_ent.n) {
+            k_sweep_serial_grid<D><<<(unsigned)nb.serial_grid, kSerialGridThreads, 0, s>>>(
+                A, nb.serial_ent.p, nb.serial_side.p, level_ptr_d, nb.nlevels, nb.serial_bar.p, ctrl);
+            MT_LAUNCH_CHECK();
+            return 1;
+        }
         if (nb.serial_ent.n && sm <= kSerialSmemMax) {
             k_sweep_serial_smem<D><<<1, kSerialThreads, sm, s>>>(A, nb.serial_ent.p, nb.serial_side.p, level_ptr_d,
                                                                  nb.nlevels, (int)nb.n, ctrl);

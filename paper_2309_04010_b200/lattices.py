@@ -200,9 +200,34 @@ def strip_2d(p) -> Lattice:
                    deflection_axis=1)
 
 
+def plate_3d(p) -> Lattice:
+    """Cantilever plate (membrane_3d, BASELINE configs[3]): the strip of
+    membrane_2d extruded along y -- ghost clamp columns left of x = 0 over the
+    whole breadth, saturation held on the top face (z), deflection (z)
+    measured at the free edge."""
+    dp = p["dp"]
+    n_span = spacing_count(p["length"], dp, "length")
+    ny = spacing_count(p["breadth"], dp, "breadth")
+    nz = spacing_count(p["thickness"], dp, "thickness")
+    lay = int(p["layers"])
+    icol = np.arange(-lay, n_span + 1)
+    xoff = icol * dp
+    yoff = centred(ny, dp)
+    zoff = centred(nz, dp)
+    xs, ys, zs = (a.ravel() for a in np.meshgrid(xoff, yoff, zoff, indexing="ij"))
+    col = np.repeat(np.arange(len(xoff)), ny * nz)
+    constrained = np.repeat(icol < 0, ny * nz)
+    contact = (zs == zoff.max()) & ~constrained
+    return Lattice(np.column_stack([xs, ys, zs]), np.full(len(xs), dp ** 3),
+                   np.array([p["h_factor"] * dp] * 3), constrained, np.zeros(len(xs), np.int8),
+                   contact=contact, column_id=col, column_x=xoff, center_column=len(xoff) - 1,
+                   deflection_axis=2)
+
+
 BUILDERS = {
     "necking_2d": bar_2d, "bar_2d": bar_2d, "necking_3d": cylinder_3d, "bar_3d": box_3d,
     "block_3d": box_3d, "fsi_2d": beam_2d, "fsi_3d": film_3d, "membrane_2d": strip_2d,
+    "membrane_3d": plate_3d,
 }
 
 
@@ -225,6 +250,10 @@ def particle_count(params) -> int:
         ghost = 2 * int(p["layers"]) + 1
         return (spacing_count(p["length"], dxy, "length") + ghost) * \
             (spacing_count(p["breadth"], dxy, "breadth") + ghost) * \
+            spacing_count(p["thickness"], p["dp"], "thickness")
+    if name == "membrane_3d":
+        return (spacing_count(p["length"], p["dp"], "length") + int(p["layers"]) + 1) * \
+            spacing_count(p["breadth"], p["dp"], "breadth") * \
             spacing_count(p["thickness"], p["dp"], "thickness")
     if name in ("bar_3d", "block_3d"):
         return spacing_count(p["length"], p["dp"], "length") * \

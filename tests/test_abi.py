@@ -102,3 +102,32 @@ def test_null_handles_are_rejected():
         else:
             assert st == 1, name
             assert b"null handle" in lib.mtsph_last_error(), name
+
+
+def test_accel_shim_has_the_reference_kernel_signatures():
+    """paper_2309_04010_b200.accel is a drop-in for mtsph/_accel.py: the
+    same seven public functions with the same parameter names and order.
+    The signatures are pinned here; when the reference package is present
+    (this container, not the GPU box) they are also compared with it."""
+    import inspect
+    import os
+    from paper_2309_04010_b200 import accel
+    want = {
+        "velocity_gradient_gather": "src indptr idx grad vol out",
+        "pair_tensor_divergence": "tens indptr idx grad vol out",
+        "pair_tensor_divergence_mapped": "tens amap indptr idx grad vol out",
+        "scalar_difference_flux": "sat coeff amap indptr idx vol grad out",
+        "damping_sweep": "vel pair_i pair_j pair_damp inv_mass_i inv_mass_j group_ptr eta dt",
+        "conservative_mass_rate": "flux amap pair_i pair_j pair_grad vol out",
+        "porous_stress_rhs": "def_grad pressure corr indptr idx grad0 vol0 mu lam tbuf out_j out_rate",
+    }
+    for name, params in want.items():
+        got = " ".join(inspect.signature(getattr(accel, name)).parameters)
+        assert got == params, name
+    src = "/root/reference/pkg/src/mtsph/_accel.py"
+    if os.path.exists(src):
+        import ast
+        tree = ast.parse(open(src).read())
+        ref = {f.name: " ".join(a.arg for a in f.args.args) for f in tree.body
+               if isinstance(f, ast.FunctionDef) and not f.name.startswith("_")}
+        assert ref == want

@@ -1,0 +1,130 @@
+"""GPU: the reference's 3D acceptance smoke tests
+(/root/reference/pkg/tests/test_acceptance.py:441-540), restated on the
+device-resident problems with the reference's damping order (serial):
+
+* necking_3d smoke (dp = L/53, 200 outer steps, 3 mm per end): no inner
+  cap hits, finite state, det F > 0, alpha >= 0, transverse mirror symmetry
+  of the displacement <= 1e-6 of its scale, neck at mid-span;
+* fsi_3d smoke (1.25 mm film, the reference's calibrated smoke parameters):
+  saturation bounds, two-plane mirror symmetry of the deflection <= 1e-6,
+  amplitude grows in contact (> 3x) and decays after (< 0.5 x peak,
+  monotone apart from sampling noise).
+
+The parallel orders are run on the same cases to report whether they keep
+the mirror symmetry: `coloured` merges mirror-image pairs into one task and
+keeps the reference's groups, so it is held to the same 1e-6; `tiled`
+(the throughput order) is not mirror-invariant -- its asymmetry is printed
+and bounded loosely.
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _mirror_gap(ref_pos, field, axis, flip=None):
+    """max |f(x) - M f(M x)| over the lattice, M = mirror across `axis`."""
+    mirrored = ref_pos.copy()
+    mirrored[:, axis] = -mirrored[:, axis]
+    order_a = np.lexsort((ref_pos[:, 2], ref_pos[:, 1], ref_pos[:, 0]))
+    order_m = np.lexsort((mirrored[:, 2], mirrored[:, 1], mirrored[:, 0]))
+    fa, fm = field[order_a], field[order_m]
+    if flip is not None:
+        fm = fm * flip
+    return float(np.max(np.abs(fa - fm)))
+
+
+def _run(raw, sweep):
+    from paper_2309_04010_b200 import scenarios
+    from paper_2309_04010_b200.config import resolve
+    from paper_2309_04010_b200.stepping import run_outer_inner
+    params = resolve(raw).params
+    problem, policy = scenarios.build(params, sweep=sweep)
+    obs, counters = run_outer_inner(problem, policy)
+    return {"problem": problem, "obs": obs, "counters": counters, "params": params}
+
+
+NECK3D = {"scenario": "necking_3d", "dp": 53.334e-3 / 53, "stretch_per_end": 3.0e-3,
+          "n_outer": 200}
+FSI3D = {"scenario": "fsi_3d", "length": 1.25e-3, "breadth": 1.25e-3, "dp": 0.125e-3 / 8,
+         "energy_pct": 1e-11, "max_inner": 600, "min_inner": 20, "eta": 3e3,
+         "contact_time": 60.0, "t_total": 300.0, "evaporation_rate": 2e-2,
+         "pressure_coeff": 5e4}
+
+
+@pytest.fixture(scope="module")
+def necking_3d_runs():
+    return {s: _run(NECK3D, s) for s in ("serial", "coloured", "tiled")}
+
+
+@pytest.fixture(scope="module")
+def fsi_3d_runs():
+    return {s: _run(FSI3D, s) for s in ("serial", "coloured", "tiled")}
+
+
+def _neck_symmetry(run):
+    st = run["problem"].state
+    disp = st.pos - st.ref_pos
+    gap = _mirror_gap(st.ref_pos, disp, 1, np.array([1.0, -1.0, 1.0]))
+    return gap / np.max(np.abs(disp))
+
+
+def test_necking_3d_smoke_bounds_symmetry_and_neck(necking_3d_runs):
+    run = necking_3d_runs["serial"]
+    assert not run["counters"].cap_hits
+    problem = run["problem"]
+    st = problem.state
+    assert np.all(np.isfinite(st.pos))
+    assert np.all(np.linalg.det(st.def_grad) > 0.0)
+    assert np.all(problem.plastic.alpha >= 0.0)
+    assert np.max(problem.plastic.alpha) > 0.0
+    assert _neck_symmetry(run) <= 1e-6
+    r = np.sqrt(st.pos[:, 1] ** 2 + st.pos[:, 2] ** 2)
+    mid = np.abs(st.ref_pos[:, 0]) < 2e-3
+    end = np.abs(np.abs(st.ref_pos[:, 0]) - 15e-3) < 2e-3
+    assert np.max(r[mid]) < np.max(r[end])
+
+
+def test_necking_3d_parallel_orders_symmetry(necking_3d_runs):
+    gaps = {s: _neck_symmetry(r) for s, r in necking_3d_runs.items()}
+    print("necking_3d transverse mirror asymmetry (rel. to max |u|):", gaps)
+    assert gaps["coloured"] <= 1e-6
+    assert gaps["tiled"] <= 1e-2
+    for s, r in necking_3d_runs.items():
+        assert not r["counters"].cap_hits, s
+
+
+def _fsi_symmetry(run):
+    st = run["problem"].state
+    dz = st.pos[:, 2] - st.ref_pos[:, 2]
+    scale = np.max(np.abs(dz))
+    return max(_mirror_gap(st.ref_pos, dz, a) for a in (0, 1)) / scale
+
+
+def test_fsi_3d_smoke_bounds_and_two_plane_symmetry(fsi_3d_runs):
+    run = fsi_3d_runs["serial"]
+    st = run["problem"].state
+    obs = run["obs"]
+    assert np.all(np.isfinite(st.pos))
+    assert np.all(obs.extras["max_saturation"] <= 0.4 * (1 + 1e-12))
+    assert np.all(st.saturation >= 0.0)
+    assert _fsi_symmetry(run) <= 1e-6
+
+
+def test_fsi_3d_smoke_amplitude_rises_then_decays(fsi_3d_runs):
+    run = fsi_3d_runs["serial"]
+    obs, params = run["obs"], run["params"]
+    amp = np.abs(obs.amplitude)
+    ic = int(np.searchsorted(obs.time, params["contact_time"]))
+    peak = np.max(amp[:ic])
+    assert amp[ic - 1] > 3.0 * amp[1]
+    assert amp[-1] < 0.5 * peak
+    assert np.all(np.diff(amp[ic + 2:]) <= 1e-3 * peak)
+
+
+def test_fsi_3d_parallel_orders_symmetry(fsi_3d_runs):
+    gaps = {s: _fsi_symmetry(r) for s, r in fsi_3d_runs.items()}
+    print("fsi_3d two-plane mirror asymmetry (rel. to max |u_z|):", gaps)
+    assert gaps["coloured"] <= 1e-6
+    assert gaps["tiled"] <= 1e-2

@@ -10,7 +10,10 @@ parity cases, not bench lines), against the CPU oracle on the same inputs:
              the pore-pressure law -- three outer diffusion steps with
              their inner relaxations, fluid mass / saturation <= 1e-10,
              displacement <= 1e-8 (the reference-run tolerances of
-             test_gpu_porous_layer1.py).
+             test_gpu_porous_layer1.py);
+  configs[3] membrane_3d: the same material and wetting on the 3D cantilever
+             plate (40 x 40 x 1 at dp 1/22 in the bench; a 1 x 0.5 x 1 piece
+             of it here, 6292 particles) -- the same three-outer-step run.
 """
 
 import numpy as np
@@ -86,3 +89,46 @@ def test_config1_membrane2d_run_matches_oracle():
     assert rel_err(st.fluid_mass, ref.fluid_mass) < 1e-10
     assert rel_err(st.saturation, ref.saturation) < 1e-10
     assert rel_err(st.pos - st.ref_pos, ref.pos - lat.pos) < 1e-8
+
+
+def _porous_run_vs_oracle(raw, n_outer=3, inner=25):
+    from oracle import oracle as O
+    from oracle.problems import PorousOracle, run_outer_inner as oracle_run
+    from paper_2309_04010_b200 import scenarios
+    from paper_2309_04010_b200.config import resolve
+    from paper_2309_04010_b200.stepping import run_outer_inner
+    base = resolve(raw).params
+    raw = dict(raw, n_outer=n_outer, t_total=n_outer * base["t_total"] / base["n_outer"],
+               max_inner=inner, min_inner=inner)
+    p = resolve(raw).params
+    problem, policy = scenarios.build(p, sweep="serial")
+    obs, counters = run_outer_inner(problem, policy)
+    lat = problem.lattice
+    m = O.Membrane(p["density"], p["diffusivity"], p["pressure_coeff"], p["youngs_modulus"],
+                   p["poisson_ratio"], p["porosity"], p["fluid_density"], p["initial_saturation"])
+    ref = PorousOracle(lat.pos, lat.vol, lat.constrained, lat.contact, m,
+                       p["h_factor"] * p["dp"], (1.0,) * lat.pos.shape[1], p["contact_time"],
+                       p["evaporation_rate"], lat.column_id, len(lat.column_x),
+                       lat.center_column, lat.deflection_axis)
+    rows = oracle_run(ref, policy.dt_outer, n_outer, policy.eta, policy.energy_criterion,
+                      cfl=policy.cfl, max_inner=inner, min_inner=inner)
+    np.testing.assert_array_equal(obs.n_inner, [r["n_inner"] for r in rows])
+    return problem, ref, lat
+
+
+def test_config3_membrane3d_plate_run_matches_oracle():
+    from paper_2309_04010_b200 import lattices
+    from paper_2309_04010_b200.config import resolve
+    full = resolve({"scenario": "membrane_3d"}).params
+    assert abs(lattices.particle_count(full) - 16e6) < 1.5e6       # BASELINE's ~16 M
+    problem, ref, lat = _porous_run_vs_oracle({"scenario": "membrane_3d", "length": 1.0,
+                                               "breadth": 0.5})
+    assert lat.n == 6292
+    st = problem.state
+    assert np.max(ref.fluid_mass) > 0, "water must enter through the top face"
+    assert rel_err(st.fluid_mass, ref.fluid_mass) < 1e-10
+    assert rel_err(st.saturation, ref.saturation) < 1e-10
+    assert rel_err(st.pos - st.ref_pos, ref.pos - lat.pos) < 1e-8
+    # wetting from the top face only: the top layer holds the most water
+    z = lat.pos[:, 2]
+    assert st.fluid_mass[z == z.max()].mean() > st.fluid_mass[z == z.min()].mean()

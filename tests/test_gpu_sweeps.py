@@ -143,6 +143,37 @@ def test_serial_sweep_shared_memory_kernel_is_bit_identical(dim, monkeypatch):
         np.testing.assert_array_equal(x, y)
 
 
+@pytest.mark.parametrize("case", ["block3d", "bar2d", "fsi2d"])
+def test_serial_sweep_multi_cta_kernel_is_bit_identical(case, monkeypatch):
+    """The multi-CTA reference-order kernel (levels spread over the grid, a
+    grid barrier between levels) applies the same operations in the same
+    order as the one-CTA global kernel: bitwise equal state after a loaded
+    run, for the solid in 3D and 2D and for the membrane (simultaneous
+    group solves)."""
+    from paper_2309_04010_b200.config import resolve
+    from paper_2309_04010_b200.scenarios import build
+    from paper_2309_04010_b200.stepping import run_outer_inner
+    raw = {"block3d": {"scenario": "block_3d", "length": 0.4, "width": 0.2, "breadth": 0.2,
+                       "dp": 0.01, "stretch_per_end": 4e-3, "n_outer": 2, "max_inner": 40},
+           "bar2d": {"scenario": "bar_2d", "length": 4.0, "width": 0.8, "dp": 0.025,
+                     "stretch_per_end": 0.02, "n_outer": 2, "max_inner": 60},
+           "fsi2d": {"scenario": "fsi_2d", "length": 2e-3, "t_total": 2.4, "n_outer": 3,
+                     "max_inner": 40}}[case]
+    p = resolve(raw).params
+    monkeypatch.setenv("MTSPH_SERIAL_SMEM", "0")
+    runs = {}
+    for grid in ("1", "0"):
+        monkeypatch.setenv("MTSPH_SERIAL_GRID", grid)
+        problem, policy = build(p, sweep="serial")
+        obs, _ = run_outer_inner(problem, policy)
+        vel = "vel_solid" if case == "fsi2d" else "vel"
+        runs[grid] = (obs.n_inner, [problem.dev.get(f) for f in ("pos", vel, "F")])
+    np.testing.assert_array_equal(runs["1"][0], runs["0"][0])
+    assert np.max(np.abs(runs["1"][1][1])) > 0
+    for x, y in zip(runs["1"][1], runs["0"][1]):
+        np.testing.assert_array_equal(x, y)
+
+
 def test_serial_sweep_shared_memory_kernel_is_bit_identical_porous(monkeypatch):
     """Same for the membrane (anisotropic kernel, simultaneous group solves
     included where the reference groups pairs)."""
