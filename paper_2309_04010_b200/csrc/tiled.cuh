@@ -44,6 +44,12 @@ namespace mtsph {
 #ifndef MTSPH_SWEEP_STAGES32
 #define MTSPH_SWEEP_STAGES32 4
 #endif
+// 1: the pair/coefficient chunks move by TMA bulk copies completing on
+// mbarriers (every thread applies pairs); 0: per-element cp.async by
+// dedicated staging warps (bit-identical)
+#ifndef MTSPH_SWEEP_TMA
+#define MTSPH_SWEEP_TMA 1
+#endif
 template <class R> struct SweepStages { static constexpr int n = MTSPH_SWEEP_STAGES64; };
 template <> struct SweepStages<float> { static constexpr int n = MTSPH_SWEEP_STAGES32; };
 inline int sweep_stages(int rsize) { return rsize == 8 ? MTSPH_SWEEP_STAGES64 : MTSPH_SWEEP_STAGES32; }
@@ -125,12 +131,36 @@ template <> struct Halo<float> {
     static constexpr size_t bytes = 16;
 };
 
+__device__ __forceinline__ void mbar_wait(uint32_t addr, uint32_t parity) {
+    uint32_t ok = 0;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(ok) : "r"(addr), "r"(parity) : "memory");
+    } while (!ok);
+}
+
+// the ring's mbarriers (one per slot, one arrival per phase), once per CTA
+template <int S> __device__ __forceinline__ void mbar_init(uint64_t *mbar) {
+#if MTSPH_SWEEP_TMA
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < S; ++k)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"((uint32_t)__cvta_generic_to_shared(mbar + k))
+                         : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+#else
+    (void)mbar;
+#endif
+}
+
 // One block task (one CTA): stage the halo, apply the sub-colours in
 // direction dir, write the halo back.  FLOW: other SMs write V during the
 // launch (persistent dataflow sweep), so the halo is read through L2.
 template <int D, bool FLOW, class R>
 __device__ __forceinline__ void sweep_task(const TiledArgsT<R> &T, int64_t task, int dir, R half,
-                                           double *smem) {
+                                           double *smem, uint64_t *mbar, uint32_t &gq) {
     using V_t = typename VTR<D, R>::T;
     const int H = T.halo_n[task];
     const int64_t r0 = T.range_off[task], r1 = T.range_off[task + 1];
@@ -155,7 +185,7 @@ __device__ __forceinline__ void sweep_task(const TiledArgsT<R> &T, int64_t task,
     const int64_t s0 = T.sub_off[task];
     const int nsub = (int)(T.sub_off[task + 1] - s0) - 1;
     constexpr int kSweepStages = SweepStages<R>::n;
-    // ring of kSweepStages (pair, coefficient) chunks staged with cp.async
+    // ring of kSweepStages (pair, coefficient) chunks
     R *bd = reinterpret_cast<R *>(hal.end(H));                                 // ring of coefficients
     uint32_t *bp = reinterpret_cast<uint32_t *>(bd + kSweepStages * T.maxsub);  // ring of pairs
     int *ssub = reinterpret_cast<int *>(bp + kSweepStages * T.maxsub);         // sub-colour bounds
@@ -169,6 +199,48 @@ __device__ __forceinline__ void sweep_task(const TiledArgsT<R> &T, int64_t task,
         a = ssub[s];
         b = ssub[s + 1];
     };
+#if MTSPH_SWEEP_TMA
+    // Chunks move by TMA bulk copies (cp.async.bulk, one elected thread per
+    // chunk, completion on the slot's mbarrier), so every thread applies
+    // pairs.  Chunk q of this task is the CTA's chunk gq + q: slot
+    // (gq + q) % S, mbarrier phase parity ((gq + q) / S) & 1.  A slot is
+    // refilled only after the barrier that ends the sub-colour that read it.
+    auto issue = [&](int q) {
+        if (q >= nq) return;
+        const uint32_t c = gq + (uint32_t)q;
+        const int slot = (int)(c % kSweepStages);
+        int a, b;
+        sub_range(q, a, b);
+        const uint32_t nb_pk = (uint32_t)(b - a) * 4u, nb_pd = (uint32_t)(b - a) * (uint32_t)sizeof(R);
+        const uint32_t mb = (uint32_t)__cvta_generic_to_shared(mbar + slot);
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb), "r"(nb_pk + nb_pd)
+                     : "memory");
+        if (nb_pk) {
+            const uint32_t dpd = (uint32_t)__cvta_generic_to_shared(bd + slot * T.maxsub);
+            const uint32_t dpp = (uint32_t)__cvta_generic_to_shared(bp + slot * T.maxsub);
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                         ::"r"(dpd), "l"(T.pd + p0 + a), "r"(nb_pd), "r"(mb) : "memory");
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                         ::"r"(dpp), "l"(T.pairs + p0 + a), "r"(nb_pk), "r"(mb) : "memory");
+        }
+    };
+    if (threadIdx.x == 0)
+        for (int q = 0; q < kSweepStages; ++q) issue(q);
+    for (int l = threadIdx.x; l < H; l += blockDim.x) {
+        const int64_t g = global_of(l);
+        R v[3] = {0, 0, 0};
+        // per-colour launches: halos of one launch are disjoint, read-only here
+        vget(FLOW ? vldcg(V + g) : vldg(V + g), v);
+        hal.init(l, v[0], v[1], D == 3 ? v[2] : R(0), T.inv_m[g]);
+    }
+    __syncthreads();
+    const int npr = (int)blockDim.x;
+    for (int q = 0; q < nq; ++q) {
+        const uint32_t c = gq + (uint32_t)q;
+        const int slot = (int)(c % kSweepStages);
+        mbar_wait((uint32_t)__cvta_generic_to_shared(mbar + slot), (c / kSweepStages) & 1u);
+#else
     // Warp-specialised: the top eighth of the threads (whole warps, at least
     // one) only stage chunks, the rest only apply pairs, so a chunk's copy
     // overlaps the pair updates.  Whole warps: the two roles reach
@@ -220,11 +292,13 @@ __device__ __forceinline__ void sweep_task(const TiledArgsT<R> &T, int64_t task,
             __syncthreads();
             continue;
         }
+        const int slot = q % kSweepStages;
+#endif
         int a0, b0;
         sub_range(q, a0, b0);
         const int cnt = b0 - a0;
-        const R *cd = bd + (q % kSweepStages) * T.maxsub;
-        const uint32_t *cpk = bp + (q % kSweepStages) * T.maxsub;
+        const R *cd = bd + slot * T.maxsub;
+        const uint32_t *cpk = bp + slot * T.maxsub;
         for (int p = threadIdx.x; p < cnt; p += npr) {  // npr % 8 == 0: groups stay quarter warps
             const uint32_t pk = cpk[p];
             if (pk == 0xffffffffu) continue;  // kPadPair
@@ -250,7 +324,13 @@ __device__ __forceinline__ void sweep_task(const TiledArgsT<R> &T, int64_t task,
             hal.template st<D>(lj, bx, by, bz, bi);
         }
         __syncthreads();
+#if MTSPH_SWEEP_TMA
+        if (threadIdx.x == 0) issue(q + kSweepStages);  // slot of sub-colour q is free now
+#endif
     }
+#if MTSPH_SWEEP_TMA
+    gq += (uint32_t)nq;
+#endif
     for (int l = threadIdx.x; l < H; l += blockDim.x) {
         const int64_t g = global_of(l);
         R v[3], im;
@@ -265,8 +345,11 @@ __device__ __forceinline__ void sweep_task(const TiledArgsT<R> &T, int64_t task,
 template <int D, class R = double>
 __global__ void __launch_bounds__(1024) k_sweep_tiled(TiledArgsT<R> T, int64_t t0, int dir, const Ctrl *ctrl) {
     extern __shared__ double smem[];
+    __shared__ __align__(8) uint64_t mbar[SweepStages<R>::n];
     if (ctrl->done) return;
-    sweep_task<D, false, R>(T, t0 + blockIdx.x, dir, R(0.5 * ctrl->dt * ctrl->eta), smem);
+    mbar_init<SweepStages<R>::n>(mbar);
+    uint32_t gq = 0;
+    sweep_task<D, false, R>(T, t0 + blockIdx.x, dir, R(0.5 * ctrl->dt * ctrl->eta), smem, mbar, gq);
 }
 
 // Dataflow schedule of a whole sweep (both passes) in one persistent launch.
@@ -300,7 +383,10 @@ template <int D, class R = double>
 __global__ void __launch_bounds__(1024) k_sweep_flow(TiledArgsT<R> T, TiledFlow F, const Ctrl *ctrl) {
     extern __shared__ double smem[];
     __shared__ int s_w;
+    __shared__ __align__(8) uint64_t mbar[SweepStages<R>::n];
     if (ctrl->done) return;
+    mbar_init<SweepStages<R>::n>(mbar);
+    uint32_t gq = 0;  // chunks this CTA has consumed (ring slot and phase)
     const R half = R(0.5 * ctrl->dt * ctrl->eta);
     for (;;) {
         if (threadIdx.x == 0) s_w = atomicAdd(F.counter, 1);
@@ -320,7 +406,7 @@ __global__ void __launch_bounds__(1024) k_sweep_flow(TiledArgsT<R> T, TiledFlow 
             }
         }
         __syncthreads();
-        sweep_task<D, true, R>(T, t, pass ? -1 : 1, half, smem);
+        sweep_task<D, true, R>(T, t, pass ? -1 : 1, half, smem, mbar, gq);
         __syncthreads();  // every write-back of the halo issued
         if (threadIdx.x == 0) {
             __threadfence();
@@ -699,6 +785,12 @@ inline void build_tiled(const NbhDev &nb, int sh, TiledSched &t, cudaStream_t s)
             for (int c = 0; c < ncol; ++c) {
                 const int32_t start = (int32_t)T.pairs.size();
                 bank_order(sp.data() + cnt[c], sd.data() + cnt[c], cnt[c + 1] - cnt[c], T.pairs, T.pd);
+                // whole 16 B chunks (4 pair words): every sub-colour starts 16 B
+                // aligned in both streams, as the kernel's bulk copies require
+                while ((T.pairs.size() - (size_t)start) % 4) {
+                    T.pairs.push_back(kPadPair);
+                    T.pd.push_back(0.0);
+                }
                 // optional cap on the sub-colour size (whole quarter-warp
                 // groups): a subset of a matching is a matching, so a split
                 // sub-colour is still independent pairs; smaller ring slots

@@ -32,6 +32,12 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--scenario", default="bar_2d")
     ap.add_argument("--length", type=float, default=0.0)
+    ap.add_argument("--width", type=float, default=0.0)
+    ap.add_argument("--breadth", type=float, default=0.0)
+    ap.add_argument("--pre", type=float, default=0.0,
+                    help="first apply this fraction of the yield end displacement "
+                         "(sigma0/E x length) by a slow ramp and relax")
+    ap.add_argument("--pre-ramp", type=int, default=4000)
     ap.add_argument("--checkpoints", default="250,500,1000")
     ap.add_argument("--orders", default="tiled")
     ap.add_argument("--final-criterion", type=float, default=1e-8)
@@ -41,8 +47,9 @@ def main():
     from paper_2309_04010_b200 import scenarios
     from paper_2309_04010_b200.config import resolve
     raw = {"scenario": args.scenario}
-    if args.length:
-        raw["length"] = args.length
+    for k in ("length", "width", "breadth"):
+        if getattr(args, k):
+            raw[k] = getattr(args, k)
     p = resolve(raw).params
     cps = [int(c) for c in args.checkpoints.split(",")]
     orders = ["serial"] + args.orders.split(",")
@@ -55,6 +62,17 @@ def main():
     print(json.dumps({"scenario": args.scenario, "particles": n, "dt_outer": pol.dt_outer,
                       "pull_rate": rate, "eta": pol.eta, "criterion": pol.energy_criterion}),
           flush=True)
+    if args.pre > 0:
+        e_mod = 9 * p["bulk_modulus"] * p["shear_modulus"] / (3 * p["bulk_modulus"] + p["shear_modulus"])
+        disp = args.pre * p["initial_flow_stress"] / e_mod * p["length"]
+        for o in orders:
+            prob, _ = probs[o]
+            t0 = time.perf_counter()
+            prob.dev.set_ramp(disp, args.pre_ramp, args.pre_ramp)
+            r = prob.dev.relax(pol.eta, pol.cfl, args.final_criterion, pol.dt_outer,
+                               max_inner=args.final_max, min_inner=1)
+            print(f"  {o}: pre-stretch {disp:.4g} in {int(r.n_inner)} steps cap_hit {int(r.cap_hit)} "
+                  f"({time.perf_counter() - t0:.1f} s)", flush=True)
     done = {o: 0 for o in orders}
     inner = {o: 0 for o in orders}
     caps = {o: 0 for o in orders}
@@ -83,12 +101,22 @@ def main():
         c_ref = d_ref.get("cp_inv")
         a_ref = d_ref.get("alpha")
         eye = np.eye(u_ref.shape[1])
+        from oracle import oracle as O
+        from paper_2309_04010_b200.scenarios import _necking_materials
+        _, hard = _necking_materials(p)
+        law, hp = hard.device_params()
+        matp = O.material_vector(p["shear_modulus"], p["bulk_modulus"], *hp, law=law)
+
+        def stress(dv):   # Kirchhoff stress of the current state (trial = converged)
+            return O.return_map(dv.get("F"), dv.get("cp_inv"), dv.get("alpha"), matp)[0]
+        t_ref = stress(d_ref)
         row = {"outer": cp, "max_alpha": float(a_ref.max()),
                "plastic_frac": float(np.mean(a_ref > 0)), "inner": dict(inner), "caps": dict(caps)}
         for o in orders[1:]:
             dv = probs[o][0].dev
             u = dv.get("pos") - ref.lattice.pos
             row[o] = {"u": rel(u, u_ref), "F": rel(dv.get("F") - eye, f_ref - eye),
+                      "tau": rel(stress(dv), t_ref),
                       "cp_inv": rel(dv.get("cp_inv") - eye, c_ref - eye) if a_ref.max() > 0 else 0.0,
                       "alpha": rel(dv.get("alpha"), a_ref) if a_ref.max() > 0 else 0.0}
         rows.append(row)
