@@ -57,6 +57,19 @@ def emit(line):
     out.flush()
 
 
+def profile_json(stem):
+    """The newest committed profile summary profiles/<stem>_rNN.json (ncu
+    data cannot be taken inside a timed run)."""
+    import glob
+    paths = sorted(glob.glob(os.path.join(ROOT, "profiles", f"{stem}_r[0-9][0-9].json")))
+    if not paths:
+        return {}, None
+    try:
+        return json.load(open(paths[-1])), os.path.basename(paths[-1])
+    except Exception:
+        return {}, None
+
+
 def load_peaks():
     try:
         with open(PEAKS_PATH) as fh:
@@ -322,13 +335,9 @@ def run_ours(args):
                          "bytes_per_particle": model[name], "achieved_gbs": gbs}
     top = max(classes, key=classes.get)
     k_top = kernels[top]
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "traffic_r01.json")
-    if os.path.exists(tpath):
-        try:
-            traffic = json.load(open(tpath)).get(top)
-        except Exception:
-            traffic = None
+    tr, tsrc = profile_json("traffic")
+    traffic = tr.get(top)
+    lim, lsrc = profile_json("limiters")
     variants = {}
     if not args.no_fp32 and args.sweep == "tiled":
         variants["fp32"] = fp32_variant(dev, args, params, n, d, sz, world, peak)
@@ -352,6 +361,11 @@ def run_ours(args):
         "roofline": {"kernel": top, "bound": "hbm", "achieved": k_top["achieved_gbs"],
                      "peak": peak, "unit": "GB/s",
                      "frac": k_top["achieved_gbs"] / peak, "traffic": traffic,
+                     "traffic_source": tsrc,
+                     "limiter": (lim.get(top) or {}).get("limiter"),
+                     "limiter_pct_of_peak": {k: v for k, v in (lim.get(top) or {}).items()
+                                             if k not in ("ms", "limiter")},
+                     "limiter_source": lsrc,
                      "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"},
         "kernels": kernels,
         "variants": variants,

@@ -231,6 +231,9 @@ enum {
                                     reverse when arg >= 64: colour arg - 64)       */
     MTSPH_PHASE_VMAX = 5,        /* out[0] = max |v|^2 (owned)                       */
     MTSPH_PHASE_AMAX = 6,        /* out[0] = max |v|^2, out[1] = max |a|^2 (free)    */
+    MTSPH_PHASE_SWEEP_ALL = 7,   /* damping, the whole sweep (both passes, every
+                                    colour) in one persistent dataflow launch --
+                                    only for a rank with no ghosts (world size 1) */
 };
 /* Device-controlled multi-rank loop (no host synchronisation per phase):
  * phase_async only enqueues a phase on the solid's stream (the reductions

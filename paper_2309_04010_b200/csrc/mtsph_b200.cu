@@ -982,6 +982,13 @@ template <int D> static void solid_phase_async(mtsph_solid *S, int phase, int ar
         k_solid_vmax<D><<<nb, 256, 0, s>>>(A, phase == MTSPH_PHASE_AMAX ? 1 : 0);
         S->launches += 1;
         break;
+    case MTSPH_PHASE_SWEEP_ALL:
+        if (S->nb.sweep != 3) throw Error(MTSPH_ERR_ARG, "sweep phases need the tiled schedule");
+        if (!S->nb.ghost_internal.empty())
+            for (uint8_t g : S->nb.ghost_internal)
+                if (g) throw Error(MTSPH_ERR_ARG, "the one-launch sweep needs a rank without ghosts");
+        S->launches += launch_tiled_sweep<D>(S->tiled, S->tiled_args(), S->ctrl.p, s);
+        break;
     default:
         throw Error(MTSPH_ERR_ARG, "unknown phase");
     }

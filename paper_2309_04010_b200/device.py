@@ -95,7 +95,8 @@ class DeviceSolid:
     FIELDS_D = {"pos", "vel", "accel", "ref_pos"}
     FIELDS_DD = {"F", "cp_inv"}
 
-    PHASES = {"kick_drift": 1, "stress": 2, "accel": 3, "sweep": 4, "vmax": 5, "amax": 6}
+    PHASES = {"kick_drift": 1, "stress": 2, "accel": 3, "sweep": 4, "vmax": 5, "amax": 6,
+              "sweep_all": 7}
 
     def __init__(self, pos, vol, rho0, constrained, side, mid_mask, h_axes,
                  shear_modulus, bulk_modulus, plastic=True, hardening_law=0,

@@ -282,6 +282,7 @@ class DecomposedSolid:
         self.ramp_left = 0
         self.ncolours = max(dev.colours() for dev in self.devices)
         self.n_global = len(lat.vol)
+        self.nranks = int(nranks)
 
     # -- one inner step --------------------------------------------------
     def step(self, dt, eta):
@@ -352,14 +353,19 @@ class DecomposedSolid:
         for dev in self.devices:
             dev.phase_async("accel")
         g.refresh("vel")
-        nc = self.ncolours
-        for rev in (False, True):
-            for q in range(nc):
-                c = nc - 1 - q if rev else q
-                for dev in self.devices:
-                    dev.phase_async("sweep", c + 64 if rev else c)
-                g.pushback(c)
-                g.refresh("vel")
+        if self.nranks == 1:
+            # one rank, no ghosts: the single-domain persistent dataflow
+            # sweep (one launch, same tasks in the same order per particle)
+            self.devices[0].phase_async("sweep_all")
+        else:
+            nc = self.ncolours
+            for rev in (False, True):
+                for q in range(nc):
+                    c = nc - 1 - q if rev else q
+                    for dev in self.devices:
+                        dev.phase_async("sweep", c + 64 if rev else c)
+                    g.pushback(c)
+                    g.refresh("vel")
         for dev in self.devices:
             dev.phase_async("vmax")
         g.control(1)

@@ -22,8 +22,10 @@ def main():
     ap.add_argument("--n-outer", type=int, default=3)
     ap.add_argument("--sweep", default="tiled")
     ap.add_argument("--fp32", action="store_true")
+    ap.add_argument("--max-inner", type=int, default=0,
+                    help="inner cap (0: the reference's 10 ceil(dt_outer/dt))")
     ap.add_argument("--membrane", action="store_true",
-                    help="the porous film (configs[3]-style, fsi_3d widened to ~10 M particles)")
+                    help="the BASELINE configs[3] plate (membrane_3d, 17.1 M particles)")
     args = ap.parse_args()
     if args.membrane:
         return membrane(args)
@@ -34,7 +36,7 @@ def main():
     dt_outer = base["t_total"] / base["n_outer"]
     raw = {"scenario": "bar_3d", "n_outer": args.n_outer, "t_total": args.n_outer * dt_outer,
            "stretch_per_end": base["stretch_per_end"] * args.n_outer / base["n_outer"],
-           "damping_sweep": args.sweep}
+           "damping_sweep": args.sweep, "max_inner": args.max_inner}
     p = resolve(raw).params
     t0 = time.perf_counter()
     problem, policy = scenarios.build(p, sweep=args.sweep)
@@ -62,13 +64,11 @@ def membrane(args):
     from paper_2309_04010_b200 import scenarios
     from paper_2309_04010_b200.config import resolve
     from paper_2309_04010_b200.stepping import run_outer_inner
-    base = resolve({"scenario": "fsi_3d", "length": 0.14, "breadth": 0.14}).params
+    base = resolve({"scenario": "membrane_3d"}).params
     dt_outer = base["t_total"] / base["n_outer"]
-    # inner loops capped at 300 steps: the film's acoustic step (~2e-7 s)
-    # against its 2.2 s outer step would otherwise allow ~1e8 steps
-    p = resolve({"scenario": "fsi_3d", "length": 0.14, "breadth": 0.14, "n_outer": args.n_outer,
+    p = resolve({"scenario": "membrane_3d", "n_outer": args.n_outer,
                  "t_total": args.n_outer * dt_outer, "damping_sweep": "tiled",
-                 "max_inner": 300}).params
+                 "max_inner": args.max_inner or 300}).params
     t0 = time.perf_counter()
     problem, policy = scenarios.build(p, sweep="tiled")
     setup = time.perf_counter() - t0
@@ -77,7 +77,7 @@ def membrane(args):
     wall = time.perf_counter() - t0
     n = problem.lattice.n
     print(json.dumps({
-        "workload": f"fsi_3d porous film 0.14 x 0.14 x {p['thickness']:g} m, {n} particles, tiled",
+        "workload": f"membrane_3d plate (BASELINE configs[3]) 40 x 40 x 1, {n} particles, tiled",
         "dt_outer": policy.dt_outer, "n_outer": counters.n_outer,
         "n_inner": [int(x) for x in obs.n_inner], "cap_hits": counters.cap_hits,
         "clamp_events": counters.clamp_events, "setup_s": setup, "wall_s": wall,

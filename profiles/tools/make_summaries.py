@@ -111,6 +111,44 @@ def full(path):
     return out
 
 
+LIMIT_UNITS = {"l1_lsu_data_pipe": "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed",
+               "fp64_pipe": "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+               "issue": "smsp__issue_active.avg.pct_of_peak_sustained_active"}
+
+
+def limiters(recs, hbm_gbs=None):
+    """Busiest unit per kernel class (% of peak, time-weighted over the
+    class's launches): the L1/LSU data pipe (global + shared wavefronts), the
+    FP64 pipe, instruction issue, and HBM (the class's DRAM bytes over its
+    time against MEASURED_PEAKS.json hbm_gbs)."""
+    if hbm_gbs is None:
+        try:
+            hbm_gbs = float(json.load(open(os.path.join(os.path.dirname(HERE), "MEASURED_PEAKS.json")))["hbm_gbs"])
+        except Exception:
+            hbm_gbs = 6650.0
+    lim = {}
+    for rec in recs:
+        cls = CLASS_OF.get(rec["kernel"])
+        if cls is None:
+            continue
+        t = float(rec.get("gpu__time_duration.sum", 0.0) or 0.0)
+        e = lim.setdefault(cls, {"ms": 0.0, "bytes": 0.0, **{u: 0.0 for u in LIMIT_UNITS}})
+        e["ms"] += t
+        e["bytes"] += float(rec.get("dram__bytes_read.sum", 0.0) or 0.0) + \
+            float(rec.get("dram__bytes_write.sum", 0.0) or 0.0)
+        for u, key in LIMIT_UNITS.items():
+            e[u] += t * float(rec.get(key, 0.0) or 0.0)
+    for cls, e in lim.items():
+        for u in LIMIT_UNITS:
+            e[u] = round(e[u] / e["ms"], 1) if e["ms"] else 0.0
+        e["hbm"] = round(100.0 * e.pop("bytes") / (e["ms"] * 1e-3) / (hbm_gbs * 1e9), 1) if e["ms"] else 0.0
+        e["limiter"] = max(list(LIMIT_UNITS) + ["hbm"], key=lambda u: e[u])
+    lim["note"] = ("busiest unit per kernel class (% of peak, time-weighted over the class's launches of one "
+                   "inner step) from the ncu --set full capture; hbm = DRAM bytes / time against "
+                   f"MEASURED_PEAKS.json hbm_gbs ({hbm_gbs:g} GB/s)")
+    return lim
+
+
 def main():
     lpath, fpath, tag = sys.argv[1], sys.argv[2], sys.argv[3]
     summ = {"source": os.path.basename(lpath),
@@ -140,6 +178,12 @@ def main():
                        "sweep = all colour launches of both passes); same unit as roofline.achieved x time")
     traffic["source"] = f"ncu_full_{tag}_key.csv"
     json.dump(traffic, open(os.path.join(HERE, f"traffic_{tag}.json"), "w"), indent=1)
+    # the unit that limits each kernel class, from the same capture: the
+    # busiest of the L1/LSU data pipe (global + shared wavefronts), the FP64
+    # pipe, instruction issue and DRAM (time-weighted over the class's launches)
+    lim = limiters(recs)
+    lim["source"] = f"ncu_full_{tag}_key.csv"
+    json.dump(lim, open(os.path.join(HERE, f"limiters_{tag}.json"), "w"), indent=1)
     with open(os.path.join(HERE, f"ncu_full_{tag}_key.csv"), "w", newline="") as f:
         w = csv.writer(f)
         w.writerow(["kernel"] + KEY)
