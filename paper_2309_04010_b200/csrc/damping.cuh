@@ -518,30 +518,25 @@ __global__ void __launch_bounds__(kSerialThreads, 1)
 // through L2 (ld.global.cg) because other SMs wrote them at earlier levels.
 // Bit-identical to k_sweep_serial (tests/test_gpu_sweeps.py).
 
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
-    unsigned v;
-    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
-__device__ __forceinline__ void st_release_u32(unsigned *p, unsigned v) {
-    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
 
-// bar[0]: arrivals (0 between barriers), bar[1]: generation.  The last CTA to
-// arrive resets the count and bumps the generation; the others spin on it.
-__device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned &gen) {
+// Grid barrier on a monotonic arrival counter, zeroed before the launch:
+// barrier k completes when the counter reaches (k + 1) * gridDim.x.  One
+// release-add per CTA and a spin on the same word (no separate reset and
+// release round trips).
+__device__ __forceinline__ void grid_barrier(unsigned long long *cnt, unsigned long long &target) {
     __syncthreads();
+    target += gridDim.x;
     if (threadIdx.x == 0) {
         __threadfence();
-        if (atomicAdd(bar, 1u) == gridDim.x - 1) {
-            atomicExch(bar, 0u);
-            __threadfence();
-            st_release_u32(bar + 1, gen + 1);
-        } else {
-            while (ld_acquire_u32(bar + 1) == gen) __nanosleep(20);
+        asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(cnt) : "memory");
+        while (ld_acquire_u64(cnt) < target) {
         }
     }
-    ++gen;
     __syncthreads();
 }
 
@@ -563,51 +558,69 @@ template <int D> struct GlobalV {
 constexpr int kSerialGridThreads = 256;
 
 template <int D>
-__global__ void __launch_bounds__(kSerialGridThreads)
-    k_sweep_serial_grid(SweepArgs A, const double2 *__restrict__ ent, const double2 *__restrict__ side,
-                        const int64_t *__restrict__ level_ptr, int64_t nlevels, unsigned *bar, const Ctrl *ctrl) {
-    if (ctrl->done) return;  // the same decision on every CTA
+__device__ __forceinline__ void serial_grid_apply(const SweepArgs &A, const double2 *__restrict__ side,
+                                                  const double2 &e, double half) {
     using V_t = typename VT<D>::T;
     V_t *V = reinterpret_cast<V_t *>(A.V);
+    const long long key = __double_as_longlong(e.x);
+    if (key < 0) {
+        const long long code = -2 - key;
+        const int cnt = (int)(code & 0xff);
+        if (cnt) group_solve_entries_acc<D>(side + (code >> 8), cnt, A.inv_m, half, GlobalV<D>{V});
+        else visit_group<D, true>(A, code >> 8, half);
+        return;
+    }
+    const int i = (int)(uint32_t)key, j = (int)(uint32_t)((unsigned long long)key >> 32);
+    const double c = half * e.y;
+    const double ca = c * __ldg(A.inv_m + i), cb = c * __ldg(A.inv_m + j);
+    const double den = 1.0 + ca + cb;
+    V_t vi = vldcg(V + i), vj = vldcg(V + j);
+    double a[3], b[3];
+    vget(vi, a);
+    vget(vj, b);
+#pragma unroll
+    for (int m = 0; m < D; ++m) {
+        const double u = (a[m] - b[m]) / den;
+        a[m] -= ca * u;
+        b[m] += cb * u;
+    }
+    vset(vi, a);
+    vset(vj, b);
+    vst(V + i, vi);
+    vst(V + j, vj);
+}
+
+template <int D>
+__global__ void __launch_bounds__(kSerialGridThreads)
+    k_sweep_serial_grid(SweepArgs A, const double2 *__restrict__ ent, const double2 *__restrict__ side,
+                        const int64_t *__restrict__ level_ptr, int64_t nlevels, unsigned long long *bar,
+                        const Ctrl *ctrl) {
+    if (ctrl->done) return;  // the same decision on every CTA
     const double half = 0.5 * ctrl->dt * ctrl->eta;
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
-    unsigned gen = ld_acquire_u32(bar + 1);  // nobody bumps it before every CTA arrived once
-    const GlobalV<D> GV{V};
+    const double2 none = make_double2(__longlong_as_double(-1ll), 0.0);
+    unsigned long long target = 0;
     for (int pass = 0; pass < 2; ++pass) {
+        auto level = [&](int64_t s) { return pass == 0 ? s : nlevels - 1 - s; };
+        // this thread's first entry of a step (static data: prefetched one
+        // step ahead, across the barrier)
+        auto fetch = [&](int64_t s) {
+            if (s >= nlevels) return none;
+            const int64_t L = level(s), k = __ldg(level_ptr + L) + tid;
+            return k < __ldg(level_ptr + L + 1) ? __ldg(ent + k) : none;
+        };
+        double2 nxt = fetch(0);
         for (int64_t s = 0; s < nlevels; ++s) {
-            const int64_t L = pass == 0 ? s : nlevels - 1 - s;
-            const int64_t k1 = __ldg(level_ptr + L + 1);
-            for (int64_t k = __ldg(level_ptr + L) + tid; k < k1; k += nth) {
-                const double2 e = __ldg(ent + k);
-                const long long key = __double_as_longlong(e.x);
-                if (key < 0) {
-                    const long long code = -2 - key;
-                    const int cnt = (int)(code & 0xff);
-                    if (cnt) group_solve_entries_acc<D>(side + (code >> 8), cnt, A.inv_m, half, GV);
-                    else visit_group<D, true>(A, code >> 8, half);
-                    continue;
-                }
-                const int i = (int)(uint32_t)key, j = (int)(uint32_t)((unsigned long long)key >> 32);
-                const double c = half * e.y;
-                const double ca = c * __ldg(A.inv_m + i), cb = c * __ldg(A.inv_m + j);
-                const double den = 1.0 + ca + cb;
-                V_t vi = vldcg(V + i), vj = vldcg(V + j);
-                double a[3], b[3];
-                vget(vi, a);
-                vget(vj, b);
-#pragma unroll
-                for (int m = 0; m < D; ++m) {
-                    const double u = (a[m] - b[m]) / den;
-                    a[m] -= ca * u;
-                    b[m] += cb * u;
-                }
-                vset(vi, a);
-                vset(vj, b);
-                vst(V + i, vi);
-                vst(V + j, vj);
+            const double2 e = nxt;
+            nxt = fetch(s + 1);
+            if (__double_as_longlong(e.x) != -1ll) {
+                serial_grid_apply<D>(A, side, e, half);
+                const int64_t L = level(s), k1 = __ldg(level_ptr + L + 1);
+                for (int64_t k = __ldg(level_ptr + L) + tid + nth; k < k1; k += nth)
+                    serial_grid_apply<D>(A, side, __ldg(ent + k), half);
             }
-            grid_barrier(bar, gen);
+            grid_barrier(bar, target);
         }
     }
 }
@@ -656,8 +669,7 @@ template <int D> void build_serial_entries(NbhDev &nb, const SweepArgs &A, cudaS
             // level's groups, no more (the barrier's cost grows with the grid)
             const int64_t want = (int64_t)std::ceil(per_level / kSerialGridThreads);
             nb.serial_grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * std::max(per, 1)));
-            nb.serial_bar.alloc(2);
-            nb.serial_bar.zero(s);
+            nb.serial_bar.alloc(1);
         }
         if (!nb.serial_grid) return;
     } else {
@@ -695,6 +707,7 @@ int launch_sweep(const NbhDev &nb, const SweepArgs &A, const int64_t *level_ptr_
     if (nb.sweep == 1) {
         const size_t sm = serial_smem_bytes(nb.n, D, nb.nlevels);
         if (nb.serial_grid > 0 && nb.serial_ent.n) {
+            MT_CUDA(cudaMemsetAsync(nb.serial_bar.p, 0, sizeof(unsigned long long), s));
             k_sweep_serial_grid<D><<<(unsigned)nb.serial_grid, kSerialGridThreads, 0, s>>>(
                 A, nb.serial_ent.p, nb.serial_side.p, level_ptr_d, nb.nlevels, nb.serial_bar.p, ctrl);
             MT_LAUNCH_CHECK();

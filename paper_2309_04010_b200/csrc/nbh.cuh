@@ -102,7 +102,7 @@ struct NbhDev {
     DBuf<double2> serial_ent;    // level-ordered sweep entries (damping.cuh k_serial_entries)
     DBuf<double2> serial_side;   // pair entries of the small simultaneous-solve groups
     int serial_grid = 0;         // CTAs of the multi-CTA serial kernel (0: not used)
-    DBuf<unsigned> serial_bar;   // its grid barrier (arrivals, generation)
+    DBuf<unsigned long long> serial_bar;  // its grid barrier (monotonic arrivals, zeroed per launch)
     // COLOURED: phases (colours) -> tasks -> groups
     std::vector<int64_t> colour_task_ptr;  // ncolours+1 over tasks
     DBuf<int64_t> task_ptr;                // ntasks+1 over groups

@@ -225,7 +225,11 @@ __device__ __forceinline__ void sweep_task(const TiledArgsT<R> &T, int64_t task,
                          ::"r"(dpp), "l"(T.pairs + p0 + a), "r"(nb_pk), "r"(mb) : "memory");
         }
     };
-    if (threadIdx.x == 0)
+    // the issuer is lane 0 of the last warp: sub-colours hold at most
+    // maxsub <= blockDim - 64 pairs, so that warp has no pairs to apply and
+    // the copies stay off the barrier-to-barrier critical path
+    const bool issuer = threadIdx.x == blockDim.x - 32;
+    if (issuer)
         for (int q = 0; q < kSweepStages; ++q) issue(q);
     for (int l = threadIdx.x; l < H; l += blockDim.x) {
         const int64_t g = global_of(l);
@@ -325,7 +329,7 @@ __device__ __forceinline__ void sweep_task(const TiledArgsT<R> &T, int64_t task,
         }
         __syncthreads();
 #if MTSPH_SWEEP_TMA
-        if (threadIdx.x == 0) issue(q + kSweepStages);  // slot of sub-colour q is free now
+        if (issuer) issue(q + kSweepStages);  // slot of sub-colour q is free now
 #endif
     }
 #if MTSPH_SWEEP_TMA
