@@ -341,6 +341,8 @@ def run_ours(args):
     variants = {}
     if not args.no_fp32 and args.sweep == "tiled":
         variants["fp32"] = fp32_variant(dev, args, params, n, d, sz, world, peak)
+    if not args.no_serial and args.sweep == "tiled" and world == 1:
+        variants["serial"] = serial_variant(params, args)
     line = {
         "metric": "inner solid-relaxation particle-steps/sec",
         "value": value, "unit": "particle-steps/s", "n_gpus": world, "steps": args.steps,
@@ -382,6 +384,27 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+
+
+def serial_variant(params, args):
+    """Parity mode at full size: the same workload with the reference's exact
+    damping order (bit-identical to the serial sequence, the multi-CTA
+    level-scheduled kernel), a few steps timed the same way."""
+    t0 = time.perf_counter()
+    dev, lat, _, _ = build_solid(params, "serial")
+    setup = time.perf_counter() - t0
+    eta, cfl = params["eta"], params["cfl"]
+    steps = max(2, min(args.steps, 5))
+    dev.run_steps(1, eta, cfl)
+    t = dev.run_steps(steps, eta, cfl)
+    sz = dev.sizes()
+    out = {"damping_order": "serial (the reference's exact order; multi-CTA level-scheduled kernel)",
+           "value": lat.n * steps / (t["total_ms"] / 1e3), "unit": "particle-steps/s",
+           "ms_per_step": t["total_ms"] / steps, "sweep_ms_per_step": t["sweep_ms"] / steps,
+           "levels": sz["phases"], "groups": sz["ngroups"], "steps": steps, "setup_s": setup,
+           "finite": dev.measure()["finite"]}
+    del dev
+    return out
 
 
 def fp32_variant(dev, args, params, n, d, sz, world, peak):
@@ -680,6 +703,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-fp32", action="store_true", help="skip the fp32 variant")
+    ap.add_argument("--no-serial", action="store_true",
+                    help="skip the reference-order (parity mode) variant")
     ap.add_argument("--mode", default="auto", choices=("auto", "decomposed"),
                     help="auto: N = 1 single domain, N > 1 slab decomposition with NCCL halos; "
                          "decomposed forces the decomposed path (also at N = 1)")

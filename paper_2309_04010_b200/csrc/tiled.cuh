@@ -44,12 +44,16 @@ namespace mtsph {
 #ifndef MTSPH_SWEEP_STAGES32
 #define MTSPH_SWEEP_STAGES32 4
 #endif
-// 1: the pair/coefficient chunks move by TMA bulk copies completing on
-// mbarriers (every thread applies pairs); 0: per-element cp.async by
-// dedicated staging warps (bit-identical)
+// How the pair/coefficient chunks reach shared memory: TMA bulk copies
+// completing on mbarriers (every thread applies pairs), or per-element
+// cp.async by dedicated staging warps.  Bit-identical.  Measured at 10M (3D):
+// fp64 sweep 6.19 -> 5.72 ms with TMA; fp32 3.67 ms with cp.async, 3.83
+// with TMA.  MTSPH_SWEEP_TMA=0 builds cp.async for both.
 #ifndef MTSPH_SWEEP_TMA
 #define MTSPH_SWEEP_TMA 1
 #endif
+template <class R> struct SweepTma { static constexpr bool on = MTSPH_SWEEP_TMA != 0; };
+template <> struct SweepTma<float> { static constexpr bool on = false; };
 template <class R> struct SweepStages { static constexpr int n = MTSPH_SWEEP_STAGES64; };
 template <> struct SweepStages<float> { static constexpr int n = MTSPH_SWEEP_STAGES32; };
 inline int sweep_stages(int rsize) { return rsize == 8 ? MTSPH_SWEEP_STAGES64 : MTSPH_SWEEP_STAGES32; }
@@ -141,8 +145,11 @@ __device__ __forceinline__ void mbar_wait(uint32_t addr, uint32_t parity) {
 }
 
 // the ring's mbarriers (one per slot, one arrival per phase), once per CTA
-template <int S> __device__ __forceinline__ void mbar_init(uint64_t *mbar) {
-#if MTSPH_SWEEP_TMA
+template <int S, class R> __device__ __forceinline__ void mbar_init(uint64_t *mbar) {
+    if constexpr (!SweepTma<R>::on) {
+        (void)mbar;
+        return;
+    }
     if (threadIdx.x == 0) {
         for (int k = 0; k < S; ++k)
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"((uint32_t)__cvta_generic_to_shared(mbar + k))
@@ -150,9 +157,6 @@ template <int S> __device__ __forceinline__ void mbar_init(uint64_t *mbar) {
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
-#else
-    (void)mbar;
-#endif
 }
 
 // One block task (one CTA): stage the halo, apply the sub-colours in
@@ -199,105 +203,8 @@ __device__ __forceinline__ void sweep_task(const TiledArgsT<R> &T, int64_t task,
         a = ssub[s];
         b = ssub[s + 1];
     };
-#if MTSPH_SWEEP_TMA
-    // Chunks move by TMA bulk copies (cp.async.bulk, one elected thread per
-    // chunk, completion on the slot's mbarrier), so every thread applies
-    // pairs.  Chunk q of this task is the CTA's chunk gq + q: slot
-    // (gq + q) % S, mbarrier phase parity ((gq + q) / S) & 1.  A slot is
-    // refilled only after the barrier that ends the sub-colour that read it.
-    auto issue = [&](int q) {
-        if (q >= nq) return;
-        const uint32_t c = gq + (uint32_t)q;
-        const int slot = (int)(c % kSweepStages);
-        int a, b;
-        sub_range(q, a, b);
-        const uint32_t nb_pk = (uint32_t)(b - a) * 4u, nb_pd = (uint32_t)(b - a) * (uint32_t)sizeof(R);
-        const uint32_t mb = (uint32_t)__cvta_generic_to_shared(mbar + slot);
-        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb), "r"(nb_pk + nb_pd)
-                     : "memory");
-        if (nb_pk) {
-            const uint32_t dpd = (uint32_t)__cvta_generic_to_shared(bd + slot * T.maxsub);
-            const uint32_t dpp = (uint32_t)__cvta_generic_to_shared(bp + slot * T.maxsub);
-            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
-                         ::"r"(dpd), "l"(T.pd + p0 + a), "r"(nb_pd), "r"(mb) : "memory");
-            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
-                         ::"r"(dpp), "l"(T.pairs + p0 + a), "r"(nb_pk), "r"(mb) : "memory");
-        }
-    };
-    // the issuer is lane 0 of the last warp: sub-colours hold at most
-    // maxsub <= blockDim - 64 pairs, so that warp has no pairs to apply and
-    // the copies stay off the barrier-to-barrier critical path
-    const bool issuer = threadIdx.x == blockDim.x - 32;
-    if (issuer)
-        for (int q = 0; q < kSweepStages; ++q) issue(q);
-    for (int l = threadIdx.x; l < H; l += blockDim.x) {
-        const int64_t g = global_of(l);
-        R v[3] = {0, 0, 0};
-        // per-colour launches: halos of one launch are disjoint, read-only here
-        vget(FLOW ? vldcg(V + g) : vldg(V + g), v);
-        hal.init(l, v[0], v[1], D == 3 ? v[2] : R(0), T.inv_m[g]);
-    }
-    __syncthreads();
-    const int npr = (int)blockDim.x;
-    for (int q = 0; q < nq; ++q) {
-        const uint32_t c = gq + (uint32_t)q;
-        const int slot = (int)(c % kSweepStages);
-        mbar_wait((uint32_t)__cvta_generic_to_shared(mbar + slot), (c / kSweepStages) & 1u);
-#else
-    // Warp-specialised: the top eighth of the threads (whole warps, at least
-    // one) only stage chunks, the rest only apply pairs, so a chunk's copy
-    // overlaps the pair updates.  Whole warps: the two roles reach
-    // __syncthreads (bar.sync, .aligned) from different call sites, which a
-    // warp may only do if all its lanes take the same one.
-    const int nst = std::max(32, (int)(blockDim.x >> 3) & ~31), npr = (int)blockDim.x - nst;
-    const bool stager = (int)threadIdx.x >= npr;
-    const int st = (int)threadIdx.x - npr;
-    // (stagers) every call commits exactly one (possibly empty) cp.async group
-    auto stage = [&](int q) {
-        if (q < nq) {
-            const int slot = q % kSweepStages;
-            int a, b;
-            sub_range(q, a, b);
-            for (int p = a + st; p < b; p += nst) {
-                const unsigned dpd = (unsigned)__cvta_generic_to_shared(bd + slot * T.maxsub + (p - a));
-                const unsigned dpp = (unsigned)__cvta_generic_to_shared(bp + slot * T.maxsub + (p - a));
-                if (sizeof(R) == 8)
-                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dpd), "l"(T.pd + p0 + p));
-                else
-                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dpd), "l"(T.pd + p0 + p));
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dpp), "l"(T.pairs + p0 + p));
-            }
-        }
-        asm volatile("cp.async.commit_group;\n" ::);
-    };
-    // prefetch distance kSweepStages-1 sub-colours; the first ones stream
-    // in while the halo is gathered
-    if (stager)
-        for (int q = 0; q < kSweepStages - 1; ++q) stage(q);
-    for (int l = threadIdx.x; l < H; l += blockDim.x) {
-        const int64_t g = global_of(l);
-        R v[3] = {0, 0, 0};
-        // per-colour launches: halos of one launch are disjoint, read-only here
-        vget(FLOW ? vldcg(V + g) : vldg(V + g), v);
-        hal.init(l, v[0], v[1], D == 3 ? v[2] : R(0), T.inv_m[g]);
-    }
-    if (stager) asm volatile("cp.async.wait_group %0;\n" ::"n"(kSweepStages - 2));  // chunk 0
-    __syncthreads();
-    // One barrier per sub-colour, at the end of iteration q.  Before it the
-    // stagers have issued chunk q + S - 1 into slot (q - 1) % S (free: every
-    // thread passed the previous barrier, so sub-colour q - 1 is done) and
-    // waited for chunks <= q + 1; after it chunk q + 1 is visible to all and
-    // sub-colour q is complete in the halo.
-    for (int q = 0; q < nq; ++q) {
-        if (stager) {
-            stage(q + kSweepStages - 1);
-            asm volatile("cp.async.wait_group %0;\n" ::"n"(kSweepStages - 2));
-            __syncthreads();
-            continue;
-        }
-        const int slot = q % kSweepStages;
-#endif
+    // the pair updates of sub-colour q from ring slot `slot`, npr lanes
+    auto apply_sub = [&](int q, int slot, int npr) {
         int a0, b0;
         sub_range(q, a0, b0);
         const int cnt = b0 - a0;
@@ -327,14 +234,112 @@ __device__ __forceinline__ void sweep_task(const TiledArgsT<R> &T, int64_t task,
             hal.template st<D>(li, ax, ay, az, ai);
             hal.template st<D>(lj, bx, by, bz, bi);
         }
+    };
+    auto stage_halo = [&]() {
+        for (int l = threadIdx.x; l < H; l += blockDim.x) {
+            const int64_t g = global_of(l);
+            R v[3] = {0, 0, 0};
+            // per-colour launches: halos of one launch are disjoint, read-only here
+            vget(FLOW ? vldcg(V + g) : vldg(V + g), v);
+            hal.init(l, v[0], v[1], D == 3 ? v[2] : R(0), T.inv_m[g]);
+        }
+    };
+    if constexpr (SweepTma<R>::on) {
+        // Chunks move by TMA bulk copies (cp.async.bulk, one elected thread
+        // per chunk, completion on the slot's mbarrier), so every thread
+        // applies pairs.  Chunk q of this task is the CTA's chunk gq + q:
+        // slot (gq + q) % S, mbarrier phase parity ((gq + q) / S) & 1.  A slot
+        // is refilled only after the barrier that ends the sub-colour that
+        // read it.
+        auto issue = [&](int q) {
+            if (q >= nq) return;
+            const uint32_t c = gq + (uint32_t)q;
+            const int slot = (int)(c % kSweepStages);
+            int a, b;
+            sub_range(q, a, b);
+            const uint32_t nb_pk = (uint32_t)(b - a) * 4u, nb_pd = (uint32_t)(b - a) * (uint32_t)sizeof(R);
+            const uint32_t mb = (uint32_t)__cvta_generic_to_shared(mbar + slot);
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb), "r"(nb_pk + nb_pd)
+                         : "memory");
+            if (nb_pk) {
+                const uint32_t dpd = (uint32_t)__cvta_generic_to_shared(bd + slot * T.maxsub);
+                const uint32_t dpp = (uint32_t)__cvta_generic_to_shared(bp + slot * T.maxsub);
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                    ::"r"(dpd), "l"(T.pd + p0 + a), "r"(nb_pd), "r"(mb) : "memory");
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                    ::"r"(dpp), "l"(T.pairs + p0 + a), "r"(nb_pk), "r"(mb) : "memory");
+            }
+        };
+        // the issuer is lane 0 of the last warp: sub-colours hold at most
+        // maxsub <= blockDim - 64 pairs, so that warp has no pairs to apply
+        // and the copies stay off the barrier-to-barrier critical path
+        const bool issuer = threadIdx.x == blockDim.x - 32;
+        if (issuer)
+            for (int q = 0; q < kSweepStages; ++q) issue(q);
+        stage_halo();
         __syncthreads();
-#if MTSPH_SWEEP_TMA
-        if (issuer) issue(q + kSweepStages);  // slot of sub-colour q is free now
-#endif
+        for (int q = 0; q < nq; ++q) {
+            const uint32_t c = gq + (uint32_t)q;
+            const int slot = (int)(c % kSweepStages);
+            mbar_wait((uint32_t)__cvta_generic_to_shared(mbar + slot), (c / kSweepStages) & 1u);
+            apply_sub(q, slot, (int)blockDim.x);
+            __syncthreads();
+            if (issuer) issue(q + kSweepStages);  // slot of sub-colour q is free now
+        }
+        gq += (uint32_t)nq;
+    } else {
+        // Warp-specialised: the top eighth of the threads (whole warps, at
+        // least one) only stage chunks by per-element cp.async, the rest
+        // only apply pairs, so a chunk's copy overlaps the pair updates.
+        // Whole warps: the two roles reach __syncthreads (bar.sync, .aligned)
+        // from different call sites, which a warp may only do if all its
+        // lanes take the same one.
+        const int nst = std::max(32, (int)(blockDim.x >> 3) & ~31), npr = (int)blockDim.x - nst;
+        const bool stager = (int)threadIdx.x >= npr;
+        const int st = (int)threadIdx.x - npr;
+        // (stagers) every call commits exactly one (possibly empty) cp.async group
+        auto stage = [&](int q) {
+            if (q < nq) {
+                const int slot = q % kSweepStages;
+                int a, b;
+                sub_range(q, a, b);
+                for (int p = a + st; p < b; p += nst) {
+                    const unsigned dpd = (unsigned)__cvta_generic_to_shared(bd + slot * T.maxsub + (p - a));
+                    const unsigned dpp = (unsigned)__cvta_generic_to_shared(bp + slot * T.maxsub + (p - a));
+                    if (sizeof(R) == 8)
+                        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dpd), "l"(T.pd + p0 + p));
+                    else
+                        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dpd), "l"(T.pd + p0 + p));
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dpp), "l"(T.pairs + p0 + p));
+                }
+            }
+            asm volatile("cp.async.commit_group;\n" ::);
+        };
+        // prefetch distance kSweepStages-1 sub-colours; the first ones
+        // stream in while the halo is gathered
+        if (stager)
+            for (int q = 0; q < kSweepStages - 1; ++q) stage(q);
+        stage_halo();
+        if (stager) asm volatile("cp.async.wait_group %0;\n" ::"n"(kSweepStages - 2));  // chunk 0
+        __syncthreads();
+        // One barrier per sub-colour, at the end of iteration q.  Before it
+        // the stagers have issued chunk q + S - 1 into slot (q - 1) % S (free:
+        // every thread passed the previous barrier, so sub-colour q - 1 is
+        // done) and waited for chunks <= q + 1; after it chunk q + 1 is
+        // visible to all and sub-colour q is complete in the halo.
+        for (int q = 0; q < nq; ++q) {
+            if (stager) {
+                stage(q + kSweepStages - 1);
+                asm volatile("cp.async.wait_group %0;\n" ::"n"(kSweepStages - 2));
+            } else {
+                apply_sub(q, q % kSweepStages, npr);
+            }
+            __syncthreads();
+        }
     }
-#if MTSPH_SWEEP_TMA
-    gq += (uint32_t)nq;
-#endif
     for (int l = threadIdx.x; l < H; l += blockDim.x) {
         const int64_t g = global_of(l);
         R v[3], im;
@@ -351,7 +356,7 @@ __global__ void __launch_bounds__(1024) k_sweep_tiled(TiledArgsT<R> T, int64_t t
     extern __shared__ double smem[];
     __shared__ __align__(8) uint64_t mbar[SweepStages<R>::n];
     if (ctrl->done) return;
-    mbar_init<SweepStages<R>::n>(mbar);
+    mbar_init<SweepStages<R>::n, R>(mbar);
     uint32_t gq = 0;
     sweep_task<D, false, R>(T, t0 + blockIdx.x, dir, R(0.5 * ctrl->dt * ctrl->eta), smem, mbar, gq);
 }
@@ -389,7 +394,7 @@ __global__ void __launch_bounds__(1024) k_sweep_flow(TiledArgsT<R> T, TiledFlow 
     __shared__ int s_w;
     __shared__ __align__(8) uint64_t mbar[SweepStages<R>::n];
     if (ctrl->done) return;
-    mbar_init<SweepStages<R>::n>(mbar);
+    mbar_init<SweepStages<R>::n, R>(mbar);
     uint32_t gq = 0;  // chunks this CTA has consumed (ring slot and phase)
     const R half = R(0.5 * ctrl->dt * ctrl->eta);
     for (;;) {

@@ -23,8 +23,11 @@ def main():
     ap.add_argument("--sweep", default="tiled")
     ap.add_argument("--steps", type=int, default=1)
     ap.add_argument("--precisions", default="64,32")
+    ap.add_argument("--length", type=float, default=0.0)
     args = ap.parse_args()
-    params = bench.workload_params(args)
+    params = dict(bench.workload_params(args))
+    if args.length:
+        params["length"] = args.length
     dev, lat, _, _ = bench.build_solid(params, args.sweep)
     for bits in [int(b) for b in args.precisions.split(",")]:
         dev.set_precision(bits)

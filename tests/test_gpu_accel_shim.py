@@ -117,6 +117,8 @@ class _ReferenceStep:
             self.vel[self.right] = 0.0
             self.vel[self.left, 0] = -vbc
             self.vel[self.right, 0] = vbc
+        else:
+            self.vel[~self.movable] = 0.0
         self.pos += dt * self.vel
         raw = np.empty_like(self.F)                       # solids.deformation_rate
         self.accel.velocity_gradient_gather(np.ascontiguousarray(self.vel), nb.indptr, nb.idx,

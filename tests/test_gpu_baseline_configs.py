@@ -132,3 +132,50 @@ def test_config3_membrane3d_plate_run_matches_oracle():
     # wetting from the top face only: the top layer holds the most water
     z = lat.pos[:, 2]
     assert st.fluid_mass[z == z.max()].mean() > st.fluid_mass[z == z.min()].mean()
+
+
+def test_config2_slice_serial_trajectory_matches_oracle():
+    """A configs[2] slice at full cross-section (0.2 x 2 x 2 at dp 0.02, 100 k
+    particles; BASELINE material, right end pulled at the BASELINE rate),
+    pre-stretched 0.5 % like the bench so the return map runs its plastic
+    branch: 100 inner steps in the reference's damping order (the multi-CTA
+    serial kernel at this size) against the oracle, every field <= 1e-10
+    (north-star per-step bar)."""
+    from oracle.problems import NeckingOracle
+    from paper_2309_04010_b200 import device, lattices
+    from paper_2309_04010_b200.config import resolve
+    from paper_2309_04010_b200.scenarios import _necking_materials
+    p = resolve({"scenario": "bar_3d", "length": 0.2}).params
+    lat = lattices.build_lattice(p)
+    assert lat.n == 100_000
+    el, hard = _necking_materials(p)
+    law, hp = hard.device_params()
+    gpu = device.DeviceSolid(lat.pos, lat.vol, el.density0, lat.constrained, lat.side,
+                             lat.mid_mask, lat.h_axes, el.shear_modulus, el.bulk_modulus,
+                             plastic=True, hardening_law=law, hard=hp, sweep="serial")
+    disp = p["stretch_per_end"] / p["n_outer"]           # 1e-5 per outer step
+    cpu = NeckingOracle(lat.pos, lat.vol, el.density0, lat.constrained, lat.side < 0,
+                        lat.side > 0, lat.mid_mask, el.shear_modulus, el.bulk_modulus, hp,
+                        float(lat.h_axes[0]), end_disp_per_outer=disp, ramp_steps=50,
+                        hardening_law=law)
+    Fm = np.diag([1.005, 1 - 0.3 * 0.005, 1 - 0.3 * 0.005])
+    for obj in (gpu, cpu):
+        if obj is gpu:
+            gpu.set("F", np.broadcast_to(Fm, (lat.n, 3, 3)))
+            gpu.set("pos", lat.pos @ Fm.T)
+        else:
+            cpu.F[:] = Fm
+            cpu.pos[:] = lat.pos @ Fm.T
+    gpu.set_ramp(disp, 50, 50)
+    cpu.advance_slow(1, 0.01, 0.01)
+    cfl, eta = p["cfl"], p["eta"]
+    for _ in range(100):
+        dt = gpu.stable_dt(cfl)
+        dtc = cpu.stable_time_step(cfl)
+        assert abs(dt - dtc) <= 1e-10 * dtc
+        gpu.relax_step(dt, eta)
+        cpu.relax_step(dtc, eta)
+    for field, ref in (("pos", cpu.pos), ("vel", cpu.vel), ("F", cpu.F), ("alpha", cpu.alpha)):
+        err = rel_err(gpu.get(field), ref)
+        assert err < 1e-10, (field, err)
+    assert np.mean(cpu.alpha > 0) > 0.5, "the slice must be in plastic flow"
