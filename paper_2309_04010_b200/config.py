@@ -20,7 +20,10 @@ out-of-range values raise ConfigError naming the line.
 from __future__ import annotations
 
 import math
+import numbers
 from dataclasses import dataclass, field
+
+import numpy as np
 
 from .errors import ConfigError
 
@@ -229,10 +232,14 @@ def _check_value(key: str, value, line_no=None):
     if spec is None:
         raise ConfigError(f"{at}unknown key {key!r}")
     kind = spec.kind
-    ok_type = (isinstance(value, bool) if kind is bool else
-               isinstance(value, int) and not isinstance(value, bool) if kind is int else
-               isinstance(value, (int, float)) and not isinstance(value, bool) if kind is float else
-               isinstance(value, str))
+    if kind is bool:
+        ok_type = isinstance(value, (bool, np.bool_))
+    elif kind is int:
+        ok_type = isinstance(value, numbers.Integral) and not isinstance(value, (bool, np.bool_))
+    elif kind is float:
+        ok_type = isinstance(value, numbers.Real) and not isinstance(value, (bool, np.bool_))
+    else:
+        ok_type = isinstance(value, str)
     if not ok_type:
         raise ConfigError(f"{at}value {value!r} for key {key!r} is not a valid {kind.__name__}")
     if spec.check is not None and not spec.check(value):
