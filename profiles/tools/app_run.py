@@ -22,6 +22,8 @@ def main():
     ap.add_argument("--n-outer", type=int, default=3)
     ap.add_argument("--sweep", default="tiled")
     ap.add_argument("--fp32", action="store_true")
+    ap.add_argument("--scenario", default="bar_3d", help="bar_3d (configs[2]) or block_3d (configs[4])")
+    ap.add_argument("--length", type=float, default=0.0)
     ap.add_argument("--max-inner", type=int, default=0,
                     help="inner cap (0: the reference's 10 ceil(dt_outer/dt))")
     ap.add_argument("--membrane", action="store_true",
@@ -32,11 +34,13 @@ def main():
     from paper_2309_04010_b200 import scenarios
     from paper_2309_04010_b200.config import resolve
     from paper_2309_04010_b200.stepping import run_outer_inner
-    base = resolve({"scenario": "bar_3d"}).params
+    base = resolve({"scenario": args.scenario}).params
     dt_outer = base["t_total"] / base["n_outer"]
-    raw = {"scenario": "bar_3d", "n_outer": args.n_outer, "t_total": args.n_outer * dt_outer,
+    raw = {"scenario": args.scenario, "n_outer": args.n_outer, "t_total": args.n_outer * dt_outer,
            "stretch_per_end": base["stretch_per_end"] * args.n_outer / base["n_outer"],
            "damping_sweep": args.sweep, "max_inner": args.max_inner}
+    if args.length:
+        raw["length"] = args.length
     p = resolve(raw).params
     t0 = time.perf_counter()
     problem, policy = scenarios.build(p, sweep=args.sweep)
@@ -48,10 +52,12 @@ def main():
     wall = time.perf_counter() - t0
     n = problem.lattice.n
     print(json.dumps({
-        "workload": f"bar_3d (BASELINE configs[2]), {n} particles, {args.sweep} sweep, "
+        "workload": f"{args.scenario} (BASELINE configs[{2 if args.scenario == 'bar_3d' else 4}]), "
+                    f"{n} particles, {args.sweep} sweep, "
                     f"{'fp32 variant' if args.fp32 else 'fp64'}",
         "dt_outer": policy.dt_outer, "energy_criterion": policy.energy_criterion,
         "n_outer": counters.n_outer, "n_inner": [int(x) for x in obs.n_inner],
+        "ek_ratio": [float(x) for x in obs.ek_ratio], "max_inner": p["max_inner"],
         "cap_hits": counters.cap_hits, "setup_s": setup, "wall_s": wall,
         "inner_steps_per_s": counters.n_inner / wall,
         "particle_steps_per_s": n * counters.n_inner / wall,
