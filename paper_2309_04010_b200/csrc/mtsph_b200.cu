@@ -22,6 +22,7 @@
 #include "solid.cuh"
 #include "tiled.cuh"
 #include "gather_csr.cuh"
+#include "window.cuh"
 #include "solid32.cuh"
 #include "layer1.cuh"
 
@@ -234,6 +235,10 @@ struct mtsph_solid {
     // Measured (10M, 3D): SELL 7.4 + 10.0 ms, G=2 5.8 + 7.4, G=4 5.8 + 7.3,
     // G=8 6.9 + 8.7 (stress + accel); MTSPH_GATHER_LANES overrides
     int gather_g = 4;
+    // 3D fp64 opt-in (MTSPH_GATHER_WINDOW=1): shared-memory cell-window
+    // gathers (window.cuh; measured slower than the CSR gathers)
+    WinSched win;
+    DBuf<double> Lacc;  // its stress sums, [d*d][n]
     Ctrl *hc = nullptr;  // pinned mirror
     Mat mat{};
     int nblk = 0;
@@ -292,6 +297,7 @@ struct mtsph_solid {
         A.slice_ptr = nb.slice_ptr.p; A.slice_w = nb.slice_w.p; A.nbr = nb.nbr.p;
         A.indptr = nb.indptr.p; A.csr = nb.csr.p;
         A.perm = nb.perm.p;
+        A.Lacc = win.on ? Lacc.p : nullptr;
         A.part = part.p;
         A.nblk = nblk;
         A.ctrl = ctrl.p;
@@ -317,12 +323,19 @@ struct mtsph_solid {
 
 // neighbour gathers: row-parallel CSR (default, gather_g lanes per particle),
 // SELL (gather_g = 0), or block-tiled shared memory (opt-in, slower)
-template <int D> static void launch_stress_gather(mtsph_solid *S, const SolidArgs &A, cudaStream_t s) {
+// (returns the number of kernels launched)
+template <int D> static int launch_stress_gather(mtsph_solid *S, const SolidArgs &A, cudaStream_t s) {
     const unsigned nb = blocks_for(S->n);
+    if (D == 3 && S->win.on) {
+        if (S->win.ntasks > 0)
+            k_win_stress<<<(unsigned)S->win.ntasks, S->win.threads, win_smem(S->win, 2, 9), s>>>(A, win_args(S->win, S->nb));
+        return 1;
+    }
     if (S->gather_g == 4) k_solid_stress_csr<D, 4><<<nb, 256, 0, s>>>(A);
     else if (S->gather_g == 8) k_solid_stress_csr<D, 8><<<nb, 256, 0, s>>>(A);
     else if (S->gather_g == 2) k_solid_stress_csr<D, 2><<<nb, 256, 0, s>>>(A);
     else k_solid_stress<D, true><<<nb, 256, 0, s>>>(A);
+    return 1;
 }
 // the split return map, instantiated per hardening law
 template <int D> static void launch_rmap(mtsph_solid *S, const SolidArgs &A, cudaStream_t s) {
@@ -330,12 +343,19 @@ template <int D> static void launch_rmap(mtsph_solid *S, const SolidArgs &A, cud
     if (S->mat.law == 1) k_solid_rmap<D, 1><<<nb, 256, 0, s>>>(A);
     else k_solid_rmap<D, 0><<<nb, 256, 0, s>>>(A);
 }
-template <int D> static void launch_accel_gather(mtsph_solid *S, const SolidArgs &A, cudaStream_t s) {
+template <int D> static int launch_accel_gather(mtsph_solid *S, const SolidArgs &A, cudaStream_t s) {
     const unsigned nb = blocks_for(S->n);
+    if (D == 3 && S->win.on) {
+        if (S->win.ntasks > 0)
+            k_win_accel<<<(unsigned)S->win.ntasks, S->win.threads, win_smem(S->win, 3, 3), s>>>(A, win_args(S->win, S->nb));
+        k_solid_kick_part<D><<<nb, 256, 0, s>>>(A);
+        return 2;
+    }
     if (S->gather_g == 4) k_solid_accel_csr<D, 4><<<nb, 256, 0, s>>>(A);
     else if (S->gather_g == 8) k_solid_accel_csr<D, 8><<<nb, 256, 0, s>>>(A);
     else if (S->gather_g == 2) k_solid_accel_csr<D, 2><<<nb, 256, 0, s>>>(A);
     else k_solid_accel<D><<<nb, 256, 0, s>>>(A);
+    return 1;
 }
 
 // one inner step; ev (optional, 6 events) brackets the kernel classes
@@ -350,13 +370,13 @@ template <int D> static int solid_step(mtsph_solid *S, int ctrl_mode, cudaEvent_
     mark(1);
     // split: the neighbour gather runs at low register count / high
     // occupancy, the register-heavy return map element-wise
-    launch_stress_gather<D>(S, A, S->s);
+    int extra = launch_stress_gather<D>(S, A, S->s) - 1;
     launch_rmap<D>(S, A, S->s);
     mark(2);
-    launch_accel_gather<D>(S, A, S->s);
+    extra += launch_accel_gather<D>(S, A, S->s) - 1;
     MT_LAUNCH_CHECK();
     mark(3);
-    int l = 3 + (S->nb.sweep == 3 ? launch_tiled_sweep<D>(S->tiled, S->tiled_args(), S->ctrl.p, S->s)
+    int l = 3 + extra + (S->nb.sweep == 3 ? launch_tiled_sweep<D>(S->tiled, S->tiled_args(), S->ctrl.p, S->s)
                                    : launch_sweep<D>(S->nb, S->sweep_args(), S->level_ptr.p, S->ctrl.p, S->s));
     mark(4);
     k_solid_vmax<D><<<nb, 256, 0, S->s>>>(A, 0);
@@ -555,6 +575,10 @@ extern "C" mtsph_status mtsph_solid_create(const mtsph_solid_desc *dsc, mtsph_so
     setup_mark(S->s, "neighbourhood");
     if (dsc->sweep == 3) build_tiled_auto(S->nb, S->tiled, S->s, dsc->tile);
     setup_mark(S->s, "tiled schedule");
+    // window gathers when asked for (MTSPH_GATHER_WINDOW=1, no CSR / SELL lane count set)
+    if (d == 3 && !std::getenv("MTSPH_GATHER_LANES")) build_window(S->nb, S->win, S->s);
+    if (S->win.on) S->Lacc.alloc((size_t)d * d * n);
+    setup_mark(S->s, "window gathers");
     std::vector<int64_t> perm(n);
     S->nb.perm.download(perm.data(), n, S->s);
     MT_CUDA(cudaStreamSynchronize(S->s));
@@ -875,15 +899,14 @@ template <int D> static void solid_phase(mtsph_solid *S, int phase, int arg, dou
         S->launches += 1;
         break;
     case MTSPH_PHASE_STRESS:
-        launch_stress_gather<D>(S, A, s);
+        S->launches += launch_stress_gather<D>(S, A, s);
         launch_rmap<D>(S, A, s);
-        S->launches += 2;
+        S->launches += 1;
         break;
     case MTSPH_PHASE_ACCEL: {
         S->part.zero(s);
-        launch_accel_gather<D>(S, A, s);
+        S->launches += launch_accel_gather<D>(S, A, s);
         MT_LAUNCH_CHECK();
-        S->launches += 1;
         std::vector<double> h((size_t)2 * S->nblk);
         S->part.download(h.data(), h.size(), s);
         MT_CUDA(cudaStreamSynchronize(s));
@@ -956,13 +979,12 @@ template <int D> static void solid_phase_async(mtsph_solid *S, int phase, int ar
         S->launches += 1;
         break;
     case MTSPH_PHASE_STRESS:
-        launch_stress_gather<D>(S, A, s);
+        S->launches += launch_stress_gather<D>(S, A, s);
         launch_rmap<D>(S, A, s);
-        S->launches += 2;
+        S->launches += 1;
         break;
     case MTSPH_PHASE_ACCEL:
-        launch_accel_gather<D>(S, A, s);
-        S->launches += 1;
+        S->launches += launch_accel_gather<D>(S, A, s);
         break;
     case MTSPH_PHASE_SWEEP: {
         if (S->nb.sweep != 3) throw Error(MTSPH_ERR_ARG, "sweep phases need the tiled schedule");

@@ -250,6 +250,7 @@ struct SolidArgs {
     const int64_t *indptr;   // CSR rows (sorted), for the row-parallel gathers
     const int32_t *csr;
     const int64_t *perm;
+    const double *Lacc;  // window gathers: sum_b V_b (v_b-v_a) (x) gradW [d*d][n] (F updated in k_solid_rmap)
     double *part;    // [3][nblk]: ek, amax2, vmax2
     int nblk;
     Ctrl *ctrl;
@@ -423,6 +424,21 @@ __global__ void __launch_bounds__(256, 2) k_solid_rmap(SolidArgs A) {
     double F[D * D];
 #pragma unroll
     for (int k = 0; k < D * D; ++k) F[k] = A.F[(int64_t)k * n + i];
+    if (A.Lacc) {  // after a window gather: F += dt (sum) B, as the CSR gather's epilogue
+        const double dt = A.ctrl->dt;
+        double acc[D * D], Bm[D * D], L[D * D];
+#pragma unroll
+        for (int k = 0; k < D * D; ++k) {
+            acc[k] = A.Lacc[(int64_t)k * n + i];
+            Bm[k] = A.B[(int64_t)k * n + i];
+        }
+        mm<D>(acc, Bm, L);
+#pragma unroll
+        for (int k = 0; k < D * D; ++k) {
+            F[k] = F[k] + dt * L[k];
+            A.F[(int64_t)k * n + i] = F[k];
+        }
+    }
     solid_stress_point<D, LAW>(A, i, F, nullptr);
 }
 

@@ -74,6 +74,14 @@ def test_necking_trajectory_gather_modes(gold_traj, prefix, lanes, monkeypatch):
     _check_trajectory(gold_traj, prefix)
 
 
+def test_necking_trajectory_window_gathers(gold_traj, monkeypatch):
+    """The 3D bar with the opt-in shared-memory cell-window gathers
+    (window.cuh): same 100-step parity as the CSR gathers."""
+    monkeypatch.delenv("MTSPH_GATHER_LANES", raising=False)
+    monkeypatch.setenv("MTSPH_GATHER_WINDOW", "1")
+    _check_trajectory(gold_traj, "n3_")
+
+
 def _check_trajectory(gold_traj, prefix):
     dev = _device()
     pos, vol, con, side, mid, dp = _neck_inputs(gold_traj, prefix)
