@@ -28,6 +28,66 @@
 
 namespace mtsph {
 
+// ---- chunked index table (C16 kernels) ----------------------------------
+// With G lanes striding a row, each index load is 4 B per lane: G x 4 B per
+// particle, one L1 wavefront per particle and iteration for 16 useful bytes
+// -- 8 of the ~46 (dF/dt) / ~65 (divergence) wavefronts of a warp iteration
+// with 4 lanes.  The chunked copy of the table stores every row in chunks of
+// 4 G entries, permuted so lane l's next four entries (l, G + l, 2 G + l,
+// 3 G + l of the chunk -- the entries it visits anyway, in the same order) are
+// one 16 B word: one index wavefront per particle every four iterations.
+// Rows are padded to whole chunks with -1.  Same visits in the same order on
+// every lane: bit-identical to the CSR walk.
+__global__ void k_chunk_count(int64_t n, const int64_t *__restrict__ indptr, int g, int64_t *cnt) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i > n) return;
+    cnt[i] = i < n ? (indptr[i + 1] - indptr[i] + 4 * g - 1) / (4 * g) : 0;
+}
+__global__ void k_chunk_fill(int64_t n, const int64_t *__restrict__ indptr, const int32_t *__restrict__ csr, int g,
+                             const int64_t *__restrict__ cptr, int32_t *out) {
+    // one thread per (particle, lane): its 16 B words of every chunk
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t i = t / g;
+    const int l = (int)(t % g);
+    if (i >= n) return;
+    const int64_t k0 = indptr[i], len = indptr[i + 1] - k0;
+    const int64_t c0 = cptr[i], nch = cptr[i + 1] - c0;
+    for (int64_t c = 0; c < nch; ++c) {
+        int4 w;
+        int32_t *wp = &w.x;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int64_t e = c * 4 * g + (int64_t)q * g + l;
+            wp[q] = e < len ? csr[k0 + e] : -1;
+        }
+        reinterpret_cast<int4 *>(out)[(c0 + c) * g + l] = w;
+    }
+}
+
+}  // namespace mtsph
+namespace mtsph {
+// build the chunked table for g lanes per particle (MTSPH_GATHER_CHUNKED=0: keep the CSR walk)
+inline void build_chunked(NbhDev &nb, int g, cudaStream_t s) {
+    nb.chunk_g = 0;
+    if (const char *e = std::getenv("MTSPH_GATHER_CHUNKED"); e && e[0] == '0') return;
+    if (g < 2 || nb.n == 0 || nb.nnz == 0) return;
+    const int64_t n = nb.n;
+    DBuf<int64_t> cnt((size_t)n + 1);
+    k_chunk_count<<<blocks_for(n + 1), 256, 0, s>>>(n, nb.indptr.p, g, cnt.p);
+    MT_LAUNCH_CHECK();
+    nb.cptr.alloc((size_t)n + 1);
+    CubTemp tmp;
+    exclusive_scan(tmp, cnt.p, nb.cptr.p, n + 1, s);
+    int64_t total = 0;
+    MT_CUDA(cudaMemcpyAsync(&total, nb.cptr.p + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    MT_CUDA(cudaStreamSynchronize(s));
+    nb.csr16.alloc((size_t)total * 4 * g);
+    k_chunk_fill<<<blocks_for(n * g), 256, 0, s>>>(n, nb.indptr.p, nb.csr.p, g, nb.cptr.p, nb.csr16.p);
+    MT_LAUNCH_CHECK();
+    MT_CUDA(cudaStreamSynchronize(s));
+    nb.chunk_g = g;
+}
+
 template <int G, int K> __device__ __forceinline__ void group_sum(double (&v)[K]) {
 #pragma unroll
     for (int o = G / 2; o > 0; o >>= 1)
@@ -36,7 +96,7 @@ template <int G, int K> __device__ __forceinline__ void group_sum(double (&v)[K]
 }
 
 // dF/dt gather + F update (the split path: the return map runs in k_solid_rmap)
-template <int D, int G>
+template <int D, int G, bool C16 = false>
 __global__ void __launch_bounds__(256, MTSPH_STRESS_CTAS) k_solid_stress_csr(SolidArgs A) {
     using V_t = typename VT<D>::T;
     const Ctrl *c = A.ctrl;
@@ -55,9 +115,7 @@ __global__ void __launch_bounds__(256, MTSPH_STRESS_CTAS) k_solid_stress_csr(Sol
             double xa[3], va[3];
             xget<D>(ldg4(A.XV + i), xa);
             vget(vldg(V + i), va);
-            const int64_t k1 = A.indptr[i + 1];
-            for (int64_t k = A.indptr[i] + sub; k < k1; k += G) {
-                const int32_t b = __ldg(A.csr + k);
+            auto visit = [&](int32_t b) {
                 const double4 xvb = ldg4(A.XV + b);
                 double xb[3], vb[3], rel[D], g[D];
                 xget<D>(xvb, xb);
@@ -72,6 +130,21 @@ __global__ void __launch_bounds__(256, MTSPH_STRESS_CTAS) k_solid_stress_csr(Sol
 #pragma unroll
                     for (int cc = 0; cc < D; ++cc) acc[r * D + cc] += dv * g[cc];
                 }
+            };
+            if constexpr (C16) {
+                const int64_t c0 = A.cptr[i];
+                const int nch = (int)(A.cptr[i + 1] - c0);
+                const int4 *w = reinterpret_cast<const int4 *>(A.csr16) + c0 * G + sub;
+                for (int c = 0; c < nch; ++c, w += G) {
+                    const int4 q = __ldg(w);
+                    if (q.x >= 0) visit(q.x);
+                    if (q.y >= 0) visit(q.y);
+                    if (q.z >= 0) visit(q.z);
+                    if (q.w >= 0) visit(q.w);
+                }
+            } else {
+                const int64_t k1 = A.indptr[i + 1];
+                for (int64_t k = A.indptr[i] + sub; k < k1; k += G) visit(__ldg(A.csr + k));
             }
         }
         group_sum<G>(acc);
@@ -90,7 +163,7 @@ __global__ void __launch_bounds__(256, MTSPH_STRESS_CTAS) k_solid_stress_csr(Sol
 }
 
 // a = 1/rho0 sum_b V_b (T_a + T_b) gradW, v += dt/2 a, E_k and |a|max partials
-template <int D, int G>
+template <int D, int G, bool C16 = false>
 __global__ void __launch_bounds__(256, MTSPH_ACCEL_CTAS) k_solid_accel_csr(SolidArgs A) {
     using V_t = typename VT<D>::T;
     __shared__ double sh[32];
@@ -112,9 +185,7 @@ __global__ void __launch_bounds__(256, MTSPH_ACCEL_CTAS) k_solid_accel_csr(Solid
         if (act) {
             double xa[3];
             xget<D>(ldg4(A.XV + i), xa);
-            const int64_t k1 = A.indptr[i + 1];
-            for (int64_t k = A.indptr[i] + sub; k < k1; k += G) {
-                const int32_t b = __ldg(A.csr + k);
+            auto visit = [&](int32_t b) {
                 double xb[3], Tb[D * D], rel[D], g[D];
                 dload<D>(A.T, n, A.XV, b, Tb, xb);
 #pragma unroll
@@ -124,6 +195,21 @@ __global__ void __launch_bounds__(256, MTSPH_ACCEL_CTAS) k_solid_accel_csr(Solid
                 for (int r = 0; r < D; ++r)
 #pragma unroll
                     for (int cc = 0; cc < D; ++cc) acc[r] = fma(Tb[r * D + cc], g[cc], acc[r]);
+            };
+            if constexpr (C16) {
+                const int64_t c0 = A.cptr[i];
+                const int nch = (int)(A.cptr[i + 1] - c0);
+                const int4 *w = reinterpret_cast<const int4 *>(A.csr16) + c0 * G + sub;
+                for (int c = 0; c < nch; ++c, w += G) {
+                    const int4 q = __ldg(w);
+                    if (q.x >= 0) visit(q.x);
+                    if (q.y >= 0) visit(q.y);
+                    if (q.z >= 0) visit(q.z);
+                    if (q.w >= 0) visit(q.w);
+                }
+            } else {
+                const int64_t k1 = A.indptr[i + 1];
+                for (int64_t k = A.indptr[i] + sub; k < k1; k += G) visit(__ldg(A.csr + k));
             }
         }
         group_sum<G>(acc);

@@ -296,6 +296,7 @@ struct mtsph_solid {
         A.B = nb.B.p; A.G = G.p; A.mass = mass.p; A.rho0 = rho0.p; A.flags = flags.p;
         A.slice_ptr = nb.slice_ptr.p; A.slice_w = nb.slice_w.p; A.nbr = nb.nbr.p;
         A.indptr = nb.indptr.p; A.csr = nb.csr.p;
+        A.cptr = nb.chunk_g ? nb.cptr.p : nullptr; A.csr16 = nb.csr16.p;
         A.perm = nb.perm.p;
         A.Lacc = win.on ? Lacc.p : nullptr;
         A.part = part.p;
@@ -331,7 +332,10 @@ template <int D> static int launch_stress_gather(mtsph_solid *S, const SolidArgs
             k_win_stress<<<(unsigned)S->win.ntasks, S->win.threads, win_smem(S->win, 2, 9), s>>>(A, win_args(S->win, S->nb));
         return 1;
     }
-    if (S->gather_g == 4) k_solid_stress_csr<D, 4><<<nb, 256, 0, s>>>(A);
+    const bool c16 = S->nb.chunk_g == S->gather_g && S->gather_g > 0;
+    if (S->gather_g == 4 && c16) k_solid_stress_csr<D, 4, true><<<nb, 256, 0, s>>>(A);
+    else if (S->gather_g == 2 && c16) k_solid_stress_csr<D, 2, true><<<nb, 256, 0, s>>>(A);
+    else if (S->gather_g == 4) k_solid_stress_csr<D, 4><<<nb, 256, 0, s>>>(A);
     else if (S->gather_g == 8) k_solid_stress_csr<D, 8><<<nb, 256, 0, s>>>(A);
     else if (S->gather_g == 2) k_solid_stress_csr<D, 2><<<nb, 256, 0, s>>>(A);
     else k_solid_stress<D, true><<<nb, 256, 0, s>>>(A);
@@ -351,7 +355,10 @@ template <int D> static int launch_accel_gather(mtsph_solid *S, const SolidArgs 
         k_solid_kick_part<D><<<nb, 256, 0, s>>>(A);
         return 2;
     }
-    if (S->gather_g == 4) k_solid_accel_csr<D, 4><<<nb, 256, 0, s>>>(A);
+    const bool c16 = S->nb.chunk_g == S->gather_g && S->gather_g > 0;
+    if (S->gather_g == 4 && c16) k_solid_accel_csr<D, 4, true><<<nb, 256, 0, s>>>(A);
+    else if (S->gather_g == 2 && c16) k_solid_accel_csr<D, 2, true><<<nb, 256, 0, s>>>(A);
+    else if (S->gather_g == 4) k_solid_accel_csr<D, 4><<<nb, 256, 0, s>>>(A);
     else if (S->gather_g == 8) k_solid_accel_csr<D, 8><<<nb, 256, 0, s>>>(A);
     else if (S->gather_g == 2) k_solid_accel_csr<D, 2><<<nb, 256, 0, s>>>(A);
     else k_solid_accel<D><<<nb, 256, 0, s>>>(A);
@@ -573,6 +580,8 @@ extern "C" mtsph_status mtsph_solid_create(const mtsph_solid_desc *dsc, mtsph_so
         build_nbh(S->nb, n, d, dsc->pos, dsc->vol, dsc->h_axes, dsc->sweep, S->s);
     }
     setup_mark(S->s, "neighbourhood");
+    if (S->gather_g == 2 || S->gather_g == 4) build_chunked(S->nb, S->gather_g, S->s);
+    setup_mark(S->s, "chunked index table");
     if (dsc->sweep == 3) build_tiled_auto(S->nb, S->tiled, S->s, dsc->tile);
     setup_mark(S->s, "tiled schedule");
     // window gathers when asked for (MTSPH_GATHER_WINDOW=1, no CSR / SELL lane count set)

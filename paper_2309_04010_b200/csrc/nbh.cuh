@@ -75,6 +75,11 @@ struct NbhDev {
     int64_t nnz = 0;             // directed entries (2 * pairs)
     DBuf<int64_t> indptr;        // CSR over internal ids
     DBuf<int32_t> csr;
+    // chunked copy for the row-parallel gathers (gather_csr.cuh build_chunked):
+    // chunk offsets per particle and the permuted, padded entries
+    int chunk_g = 0;             // lanes per particle it was built for (0: none)
+    DBuf<int64_t> cptr;
+    DBuf<int32_t> csr16;
     bool want_sell = false;      // SELL-32 only for the opt-in one-lane gathers
     int64_t nslices = 0, sell_size = 0;
     DBuf<int64_t> slice_ptr;

@@ -249,6 +249,8 @@ struct SolidArgs {
     const int32_t *slice_w, *nbr;
     const int64_t *indptr;   // CSR rows (sorted), for the row-parallel gathers
     const int32_t *csr;
+    const int64_t *cptr;     // chunked index table (gather_csr.cuh): chunk offsets, or null
+    const int32_t *csr16;
     const int64_t *perm;
     const double *Lacc;  // window gathers: sum_b V_b (v_b-v_a) (x) gradW [d*d][n] (F updated in k_solid_rmap)
     double *part;    // [3][nblk]: ek, amax2, vmax2
