@@ -43,25 +43,77 @@ __global__ void k_chunk_count(int64_t n, const int64_t *__restrict__ indptr, int
     if (i > n) return;
     cnt[i] = i < n ? (indptr[i + 1] - indptr[i] + 4 * g - 1) / (4 * g) : 0;
 }
+// One thread per particle.  pack: the row is first reordered so the four
+// entries of every window (one 256-bit load of a 4-lane group) have
+// distinct ids mod 4.  Measured (profiles/tools/l1_gather_ubench.cu): the L1
+// returns a 4-lane group's four 32 B records in one cycle when their sector
+// offsets within a 128 B line (id mod 4) differ, whatever lines they are in
+// (a group straddling two lines: 8.5 cycles per warp load, as 8.2 aligned),
+// and serialises equal offsets (four lines at one offset: 32 cycles; random
+// records: 20).  A sorted row's windows break at cell boundaries: offline on
+// the bench lattice 1.55 cycles per window, 1.15 after this reordering.
+// Greedy and local: four queues by id mod 4 in ascending order, a window
+// takes the head of every non-empty queue and fills up from the longest one
+// (mean displacement ~4 entries, so a warp's eight rows still walk memory
+// together).  Packing windows by whole 128 B lines instead (2.38 -> 1.97
+// lines per window) measured no gain (stress 5.32 -> 5.36 ms, accel 5.64 ->
+// 5.65): lines are not what the L1 data stage counts.
+constexpr int kChunkMaxRow = 192;
 __global__ void k_chunk_fill(int64_t n, const int64_t *__restrict__ indptr, const int32_t *__restrict__ csr, int g,
-                             const int64_t *__restrict__ cptr, int32_t *out) {
-    // one thread per (particle, lane): its 16 B words of every chunk
-    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    const int64_t i = t / g;
-    const int l = (int)(t % g);
+                             int pack, const int64_t *__restrict__ cptr, int32_t *out) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const int64_t k0 = indptr[i], len = indptr[i + 1] - k0;
+    const int64_t k0 = indptr[i];
+    const int len = (int)(indptr[i + 1] - k0);
     const int64_t c0 = cptr[i], nch = cptr[i + 1] - c0;
-    for (int64_t c = 0; c < nch; ++c) {
-        int4 w;
-        int32_t *wp = &w.x;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int64_t e = c * 4 * g + (int64_t)q * g + l;
-            wp[q] = e < len ? csr[k0 + e] : -1;
+    int32_t row[kChunkMaxRow];
+    const bool packed = pack && len <= kChunkMaxRow;
+    if (packed) {
+        int cur[4], cnt[4] = {0, 0, 0, 0};
+        for (int e = 0; e < len; ++e) ++cnt[csr[k0 + e] & 3];
+        auto seek = [&](int k, int from) {
+            while (from < len && (csr[k0 + from] & 3) != k) ++from;
+            return from;
+        };
+        for (int k = 0; k < 4; ++k) cur[k] = seek(k, 0);
+        int w = 0;
+        while (w < len) {
+            int32_t take[4];
+            int m = 0;
+            for (int k = 0; k < 4; ++k)
+                if (cnt[k]) {
+                    take[m++] = csr[k0 + cur[k]];
+                    cur[k] = seek(k, cur[k] + 1);
+                    --cnt[k];
+                }
+            while (m < 4 && w + m < len) {  // a queue ran dry: fill up from the longest one
+                int k = 0;
+                for (int q = 1; q < 4; ++q)
+                    if (cnt[q] > cnt[k]) k = q;
+                take[m++] = csr[k0 + cur[k]];
+                cur[k] = seek(k, cur[k] + 1);
+                --cnt[k];
+            }
+            for (int x = 1; x < m; ++x)  // ascending within the window
+                for (int y = x; y > 0 && take[y] < take[y - 1]; --y) {
+                    const int32_t t = take[y];
+                    take[y] = take[y - 1];
+                    take[y - 1] = t;
+                }
+            for (int x = 0; x < m; ++x) row[w++] = take[x];
         }
-        reinterpret_cast<int4 *>(out)[(c0 + c) * g + l] = w;
     }
+    for (int64_t c = 0; c < nch; ++c)
+        for (int l = 0; l < g; ++l) {
+            int4 w;
+            int32_t *wp = &w.x;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int64_t e = c * 4 * g + (int64_t)q * g + l;
+                wp[q] = e < len ? (packed ? row[e] : csr[k0 + e]) : -1;
+            }
+            reinterpret_cast<int4 *>(out)[(c0 + c) * g + l] = w;
+        }
 }
 
 }  // namespace mtsph
@@ -82,7 +134,10 @@ inline void build_chunked(NbhDev &nb, int g, cudaStream_t s) {
     MT_CUDA(cudaMemcpyAsync(&total, nb.cptr.p + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     MT_CUDA(cudaStreamSynchronize(s));
     nb.csr16.alloc((size_t)total * 4 * g);
-    k_chunk_fill<<<blocks_for(n * g), 256, 0, s>>>(n, nb.indptr.p, nb.csr.p, g, nb.cptr.p, nb.csr16.p);
+    // bank-balanced windows for 4 lanes per particle (MTSPH_GATHER_PACK=0: sorted rows)
+    int pack = g == 4 ? 1 : 0;
+    if (const char *e = std::getenv("MTSPH_GATHER_PACK")) pack = e[0] != '0' && g == 4;
+    k_chunk_fill<<<blocks_for(n, 128), 128, 0, s>>>(n, nb.indptr.p, nb.csr.p, g, pack, nb.cptr.p, nb.csr16.p);
     MT_LAUNCH_CHECK();
     MT_CUDA(cudaStreamSynchronize(s));
     nb.chunk_g = g;
