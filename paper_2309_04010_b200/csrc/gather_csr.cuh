@@ -16,14 +16,25 @@
 
 #include "solid.cuh"
 
-// minimum resident CTAs per SM (register caps 85): measured at 10M (3D) accel
-// 7.3 ms at 2 CTAs (92 regs), 6.3 ms at 3, 7.0 ms at 4 (spills); stress is
-// flat from 3 up, and slower when the cap is lifted (1: 7.2 vs 5.8 ms)
+// minimum resident CTAs per SM (register caps 85 / 64): measured at 10M (3D)
+// with the chunked table, accel 5.28 ms at 3 CTAs, 5.23 at 4 (spills), 6.15
+// at 2; stress (with the return map) 5.26 at 3, 5.06 at 4, 6.18 at 2
 #ifndef MTSPH_STRESS_CTAS
-#define MTSPH_STRESS_CTAS 3
+#define MTSPH_STRESS_CTAS 4
 #endif
 #ifndef MTSPH_ACCEL_CTAS
 #define MTSPH_ACCEL_CTAS 3
+#endif
+// Chunks are padded with the particle itself: gradW(0) = 0, so the visit
+// adds exactly zero and a kernel may run four unconditional visits per chunk
+// (1) instead of a test per visit (0; padding of -1 is still honoured).
+// Measured at 10M: accel 5.28 -> 5.18 ms unconditional; stress at 4 CTAs/SM
+// spills with it (6.25 ms), so it keeps the tests.
+#ifndef MTSPH_ACCEL_SELFPAD
+#define MTSPH_ACCEL_SELFPAD 1
+#endif
+#ifndef MTSPH_STRESS_SELFPAD
+#define MTSPH_STRESS_SELFPAD 0
 #endif
 
 namespace mtsph {
@@ -36,8 +47,8 @@ namespace mtsph {
 // 4 G entries, permuted so lane l's next four entries (l, G + l, 2 G + l,
 // 3 G + l of the chunk -- the entries it visits anyway, in the same order) are
 // one 16 B word: one index wavefront per particle every four iterations.
-// Rows are padded to whole chunks with -1.  Same visits in the same order on
-// every lane: bit-identical to the CSR walk.
+// Rows are padded to whole chunks with the particle itself (a visit that
+// adds exactly zero).
 __global__ void k_chunk_count(int64_t n, const int64_t *__restrict__ indptr, int g, int64_t *cnt) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i > n) return;
@@ -110,7 +121,7 @@ __global__ void k_chunk_fill(int64_t n, const int64_t *__restrict__ indptr, cons
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const int64_t e = c * 4 * g + (int64_t)q * g + l;
-                wp[q] = e < len ? (packed ? row[e] : csr[k0 + e]) : -1;
+                wp[q] = e < len ? (packed ? row[e] : csr[k0 + e]) : (int32_t)i;
             }
             reinterpret_cast<int4 *>(out)[(c0 + c) * g + l] = w;
         }
@@ -192,10 +203,10 @@ __global__ void __launch_bounds__(256, MTSPH_STRESS_CTAS) k_solid_stress_csr(Sol
                 const int4 *w = reinterpret_cast<const int4 *>(A.csr16) + c0 * G + sub;
                 for (int c = 0; c < nch; ++c, w += G) {
                     const int4 q = __ldg(w);
-                    if (q.x >= 0) visit(q.x);
-                    if (q.y >= 0) visit(q.y);
-                    if (q.z >= 0) visit(q.z);
-                    if (q.w >= 0) visit(q.w);
+                    if (MTSPH_STRESS_SELFPAD || q.x >= 0) visit(q.x);
+                    if (MTSPH_STRESS_SELFPAD || q.y >= 0) visit(q.y);
+                    if (MTSPH_STRESS_SELFPAD || q.z >= 0) visit(q.z);
+                    if (MTSPH_STRESS_SELFPAD || q.w >= 0) visit(q.w);
                 }
             } else {
                 const int64_t k1 = A.indptr[i + 1];
@@ -257,10 +268,10 @@ __global__ void __launch_bounds__(256, MTSPH_ACCEL_CTAS) k_solid_accel_csr(Solid
                 const int4 *w = reinterpret_cast<const int4 *>(A.csr16) + c0 * G + sub;
                 for (int c = 0; c < nch; ++c, w += G) {
                     const int4 q = __ldg(w);
-                    if (q.x >= 0) visit(q.x);
-                    if (q.y >= 0) visit(q.y);
-                    if (q.z >= 0) visit(q.z);
-                    if (q.w >= 0) visit(q.w);
+                    if (MTSPH_ACCEL_SELFPAD || q.x >= 0) visit(q.x);
+                    if (MTSPH_ACCEL_SELFPAD || q.y >= 0) visit(q.y);
+                    if (MTSPH_ACCEL_SELFPAD || q.z >= 0) visit(q.z);
+                    if (MTSPH_ACCEL_SELFPAD || q.w >= 0) visit(q.w);
                 }
             } else {
                 const int64_t k1 = A.indptr[i + 1];
