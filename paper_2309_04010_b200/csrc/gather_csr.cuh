@@ -25,18 +25,6 @@
 #ifndef MTSPH_ACCEL_CTAS
 #define MTSPH_ACCEL_CTAS 3
 #endif
-// Chunks are padded with the particle itself: gradW(0) = 0, so the visit
-// adds exactly zero and a kernel may run four unconditional visits per chunk
-// (1) instead of a test per visit (0; padding of -1 is still honoured).
-// Measured at 10M: accel 5.28 -> 5.18 ms unconditional; stress at 4 CTAs/SM
-// spills with it (6.25 ms), so it keeps the tests.
-#ifndef MTSPH_ACCEL_SELFPAD
-#define MTSPH_ACCEL_SELFPAD 1
-#endif
-#ifndef MTSPH_STRESS_SELFPAD
-#define MTSPH_STRESS_SELFPAD 0
-#endif
-
 namespace mtsph {
 
 // ---- chunked index table (C16 kernels) ----------------------------------
@@ -47,8 +35,8 @@ namespace mtsph {
 // 4 G entries, permuted so lane l's next four entries (l, G + l, 2 G + l,
 // 3 G + l of the chunk -- the entries it visits anyway, in the same order) are
 // one 16 B word: one index wavefront per particle every four iterations.
-// Rows are padded to whole chunks with the particle itself (a visit that
-// adds exactly zero).
+// Rows are padded to whole chunks with -1: the full chunks run four
+// unconditional visits, the row's last chunk tests each entry (walk_chunks).
 __global__ void k_chunk_count(int64_t n, const int64_t *__restrict__ indptr, int g, int64_t *cnt) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i > n) return;
@@ -121,7 +109,7 @@ __global__ void k_chunk_fill(int64_t n, const int64_t *__restrict__ indptr, cons
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const int64_t e = c * 4 * g + (int64_t)q * g + l;
-                wp[q] = e < len ? (packed ? row[e] : csr[k0 + e]) : (int32_t)i;
+                wp[q] = e < len ? (packed ? row[e] : csr[k0 + e]) : -1;
             }
             reinterpret_cast<int4 *>(out)[(c0 + c) * g + l] = w;
         }
@@ -130,10 +118,11 @@ __global__ void k_chunk_fill(int64_t n, const int64_t *__restrict__ indptr, cons
 }  // namespace mtsph
 namespace mtsph {
 // build the chunked table for g lanes per particle (MTSPH_GATHER_CHUNKED=0: keep the CSR walk)
-inline void build_chunked(NbhDev &nb, int g, cudaStream_t s) {
+// (the solid's kernels have a CSR fallback; the porous ones need the table: required)
+inline void build_chunked(NbhDev &nb, int g, cudaStream_t s, bool required = false) {
     nb.chunk_g = 0;
-    if (const char *e = std::getenv("MTSPH_GATHER_CHUNKED"); e && e[0] == '0') return;
-    if (g < 2 || nb.n == 0 || nb.nnz == 0) return;
+    if (const char *e = std::getenv("MTSPH_GATHER_CHUNKED"); !required && e && e[0] == '0') return;
+    if (g < 2 || nb.n == 0) return;
     const int64_t n = nb.n;
     DBuf<int64_t> cnt((size_t)n + 1);
     k_chunk_count<<<blocks_for(n + 1), 256, 0, s>>>(n, nb.indptr.p, g, cnt.p);
@@ -152,6 +141,35 @@ inline void build_chunked(NbhDev &nb, int g, cudaStream_t s) {
     MT_LAUNCH_CHECK();
     MT_CUDA(cudaStreamSynchronize(s));
     nb.chunk_g = g;
+}
+
+// this lane's entries of particle i's row in the chunked table: four
+// unconditional visits per full 16 B word (the compiler overlaps the next
+// visit's loads with the current one's arithmetic; measured at 10M accel
+// 5.28 -> 5.18 ms against a test per visit), per-entry tests in a partial one
+// (FAST).  !FAST: a test per visit everywhere -- the dF/dt gathers run at a
+// tighter register cap (4 CTAs/SM in fp64), where the overlapped schedule
+// spills (6.25 vs 5.06 ms).
+template <int G, bool FAST, class F>
+__device__ __forceinline__ void walk_chunks(const int64_t *__restrict__ cptr, const int32_t *__restrict__ csr16,
+                                            int64_t i, int sub, F &&visit) {
+    const int64_t c0 = cptr[i];
+    const int nch = (int)(cptr[i + 1] - c0);
+    const int4 *w = reinterpret_cast<const int4 *>(csr16) + c0 * G + sub;
+    for (int c = 0; c < nch; ++c, w += G) {
+        const int4 q = __ldg(w);
+        if (FAST && q.w >= 0) {  // a full word (every one but the row's last few)
+            visit(q.x);
+            visit(q.y);
+            visit(q.z);
+            visit(q.w);
+        } else {
+            if (q.x >= 0) visit(q.x);
+            if (q.y >= 0) visit(q.y);
+            if (q.z >= 0) visit(q.z);
+            if (q.w >= 0) visit(q.w);
+        }
+    }
 }
 
 template <int G, int K> __device__ __forceinline__ void group_sum(double (&v)[K]) {
@@ -198,16 +216,7 @@ __global__ void __launch_bounds__(256, MTSPH_STRESS_CTAS) k_solid_stress_csr(Sol
                 }
             };
             if constexpr (C16) {
-                const int64_t c0 = A.cptr[i];
-                const int nch = (int)(A.cptr[i + 1] - c0);
-                const int4 *w = reinterpret_cast<const int4 *>(A.csr16) + c0 * G + sub;
-                for (int c = 0; c < nch; ++c, w += G) {
-                    const int4 q = __ldg(w);
-                    if (MTSPH_STRESS_SELFPAD || q.x >= 0) visit(q.x);
-                    if (MTSPH_STRESS_SELFPAD || q.y >= 0) visit(q.y);
-                    if (MTSPH_STRESS_SELFPAD || q.z >= 0) visit(q.z);
-                    if (MTSPH_STRESS_SELFPAD || q.w >= 0) visit(q.w);
-                }
+                walk_chunks<G, false>(A.cptr, A.csr16, i, sub, visit);
             } else {
                 const int64_t k1 = A.indptr[i + 1];
                 for (int64_t k = A.indptr[i] + sub; k < k1; k += G) visit(__ldg(A.csr + k));
@@ -263,16 +272,7 @@ __global__ void __launch_bounds__(256, MTSPH_ACCEL_CTAS) k_solid_accel_csr(Solid
                     for (int cc = 0; cc < D; ++cc) acc[r] = fma(Tb[r * D + cc], g[cc], acc[r]);
             };
             if constexpr (C16) {
-                const int64_t c0 = A.cptr[i];
-                const int nch = (int)(A.cptr[i + 1] - c0);
-                const int4 *w = reinterpret_cast<const int4 *>(A.csr16) + c0 * G + sub;
-                for (int c = 0; c < nch; ++c, w += G) {
-                    const int4 q = __ldg(w);
-                    if (MTSPH_ACCEL_SELFPAD || q.x >= 0) visit(q.x);
-                    if (MTSPH_ACCEL_SELFPAD || q.y >= 0) visit(q.y);
-                    if (MTSPH_ACCEL_SELFPAD || q.z >= 0) visit(q.z);
-                    if (MTSPH_ACCEL_SELFPAD || q.w >= 0) visit(q.w);
-                }
+                walk_chunks<G, true>(A.cptr, A.csr16, i, sub, visit);
             } else {
                 const int64_t k1 = A.indptr[i + 1];
                 for (int64_t k = A.indptr[i] + sub; k < k1; k += G) visit(__ldg(A.csr + k));

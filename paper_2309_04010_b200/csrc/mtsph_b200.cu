@@ -266,6 +266,7 @@ struct mtsph_solid {
         A.u = u32.p; A.a = a32.p; A.H = H32.p; A.Hc = Hc32.p; A.alpha = alpha32.p; A.T = T32.p;
         A.B = B32.p; A.G = G32.p; A.mass = mass32.p; A.rho0 = rho032.p; A.flags = flags.p;
         A.indptr = nb.indptr.p; A.csr = nb.csr.p;
+        A.cptr = nb.chunk_g ? nb.cptr.p : nullptr; A.csr16 = nb.csr16.p;
         A.perm = nb.perm.p;
         A.part = part.p;
         A.nblk = nblk;
@@ -402,7 +403,10 @@ template <int D> static int solid_step32(mtsph_solid *S, int ctrl_mode, cudaEven
     mark(0);
     k32_kick_drift<D><<<nb, 256, 0, S->s>>>(A);
     mark(1);
-    switch (S->gather_g32) {
+    const bool c16 = S->nb.chunk_g == S->gather_g32;
+    switch (c16 ? -S->gather_g32 : S->gather_g32) {
+    case -2: k32_stress_csr<D, 2, true><<<nb, 256, 0, S->s>>>(A); break;
+    case -4: k32_stress_csr<D, 4, true><<<nb, 256, 0, S->s>>>(A); break;
     case 2: k32_stress_csr<D, 2><<<nb, 256, 0, S->s>>>(A); break;
     case 8: k32_stress_csr<D, 8><<<nb, 256, 0, S->s>>>(A); break;
     case 16: k32_stress_csr<D, 16><<<nb, 256, 0, S->s>>>(A); break;
@@ -411,7 +415,9 @@ template <int D> static int solid_step32(mtsph_solid *S, int ctrl_mode, cudaEven
     if (S->mat.law == 1) k32_rmap<D, 1><<<nb, 256, 0, S->s>>>(A);
     else k32_rmap<D, 0><<<nb, 256, 0, S->s>>>(A);
     mark(2);
-    switch (S->gather_g32) {
+    switch (c16 ? -S->gather_g32 : S->gather_g32) {
+    case -2: k32_accel_csr<D, 2, true><<<nb, 256, 0, S->s>>>(A); break;
+    case -4: k32_accel_csr<D, 4, true><<<nb, 256, 0, S->s>>>(A); break;
     case 2: k32_accel_csr<D, 2><<<nb, 256, 0, S->s>>>(A); break;
     case 8: k32_accel_csr<D, 8><<<nb, 256, 0, S->s>>>(A); break;
     case 16: k32_accel_csr<D, 16><<<nb, 256, 0, S->s>>>(A); break;

@@ -62,6 +62,8 @@ struct PorousArgs {
     const double *B;
     const uint8_t *flags;
     const int64_t *indptr;   // CSR rows (sorted)
+    const int64_t *cptr;     // chunked index table (gather_csr.cuh build_chunked, kPorLanes lanes)
+    const int32_t *csr16;
     const int32_t *csr;
     const int64_t *perm;
     double *part;
@@ -81,6 +83,12 @@ template <int D> struct PorRM { static constexpr int planes = D == 3 ? 4 : 2; };
         const int64_t i = (int64_t)blockIdx.x * 256 + it * (256 / kPorLanes) + threadIdx.x / kPorLanes; \
         const bool act = i < n;
 #define POR_ROWS_END }
+
+// this lane's neighbours of particle i from the chunked index table (gather_csr.cuh)
+template <bool FAST = true, class F>
+__device__ __forceinline__ void por_walk(const PorousArgs &A, int64_t i, int sub, F &&visit) {
+    walk_chunks<kPorLanes, FAST>(A.cptr, A.csr16, i, sub, visit);
+}
 
 template <int D>
 __global__ void __launch_bounds__(256) k_por_prep(PorousArgs A, int with_amap) {
@@ -134,9 +142,7 @@ __global__ void __launch_bounds__(256) k_por_flux(PorousArgs A, int pack) {
         double xa[3];
         xget<D>(ldg4(A.XV + i), xa);
         const double sa = A.sat[i];
-        const int64_t k1 = A.indptr[i + 1];
-        for (int64_t k = A.indptr[i] + sub; k < k1; k += kPorLanes) {
-            const int32_t b = __ldg(A.csr + k);
+        auto visit = [&](int32_t b) {
             const double4 xvb = ldg4(A.XV + b);
             double xb[3], rel[D], g[D];
             xget<D>(xvb, xb);
@@ -146,7 +152,8 @@ __global__ void __launch_bounds__(256) k_por_flux(PorousArgs A, int pack) {
             const double wgt = A.volc[b] * (sa - A.sat[b]);
 #pragma unroll
             for (int c = 0; c < D; ++c) acc[c] += wgt * g[c];
-        }
+        };
+        por_walk(A, i, sub, visit);
     }
     group_sum<kPorLanes>(acc);
     if (act && sub == 0 && !(A.flags[i] & PF_GHOST)) {
@@ -186,10 +193,8 @@ __global__ void __launch_bounds__(256) k_por_mass(PorousArgs A, double dt, int c
         for (int k = 0; k < D * D; ++k) ama[k] = A.amap[(int64_t)k * n + i];
 #pragma unroll
         for (int k = 0; k < D; ++k) qa[k] = A.q[(int64_t)k * n + i];
-        const int64_t k1 = A.indptr[i + 1];
         const double4 *rm = reinterpret_cast<const double4 *>(A.rm);
-        for (int64_t k = A.indptr[i] + sub; k < k1; k += kPorLanes) {
-            const int32_t b = __ldg(A.csr + k);
+        auto visit = [&](int32_t b) {
             // A_b, q_b, V_b (and X_b in 3D) from the planar record
             double ab[D * D], qb[D], xb[3], vb;
             const double4 p0 = ldg4(rm + b), p1 = ldg4(rm + n + b);
@@ -217,7 +222,8 @@ __global__ void __launch_bounds__(256) k_por_mass(PorousArgs A, double dt, int c
                 acc += (qa[r] + qb[r]) * s;
             }
             rate[0] -= vb * acc;
-        }
+        };
+        por_walk(A, i, sub, visit);
     }
     group_sum<kPorLanes>(rate);
     if (act && sub == 0 && !(A.flags[i] & PF_GHOST)) {
@@ -313,10 +319,8 @@ __global__ void __launch_bounds__(256, 3) k_por_fluxrate(PorousArgs A) {
         xget<D>(ldg4(A.XV + i), xa);
 #pragma unroll
         for (int k = 0; k < D * D; ++k) am[k] = -A.amap[(int64_t)k * n + i];
-        const int64_t k1 = A.indptr[i + 1];
         const double4 *rf = reinterpret_cast<const double4 *>(A.rf);
-        for (int64_t k = A.indptr[i] + sub; k < k1; k += kPorLanes) {
-            const int32_t b = __ldg(A.csr + k);
+        auto visit = [&](int32_t b) {
             const double4 xvb = ldg4(A.XV + b);
             double xb[3], rel[D], g0[D], g[D];
             xget<D>(xvb, xb);
@@ -342,7 +346,8 @@ __global__ void __launch_bounds__(256, 3) k_por_fluxrate(PorousArgs A) {
                 acc[r] += w * vlb[r];
                 acc[D + r] += vb * g[r];
             }
-        }
+        };
+        por_walk(A, i, sub, visit);
     }
     group_sum<kPorLanes>(acc);
     if (act && sub == 0 && !(A.flags[i] & PF_GHOST)) {
@@ -484,9 +489,7 @@ __global__ void __launch_bounds__(256) k_por_stress(PorousArgs A) {
         double xa[3], va[3];
         xget<D>(ldg4(A.XV + i), xa);
         vget(vldg(V + i), va);
-        const int64_t k1 = A.indptr[i + 1];
-        for (int64_t k = A.indptr[i] + sub; k < k1; k += kPorLanes) {
-            const int32_t b = __ldg(A.csr + k);
+        auto visit = [&](int32_t b) {
             const double4 xvb = ldg4(A.XV + b);
             double xb[3], vb[3], rel[D], g[D];
             xget<D>(xvb, xb);
@@ -501,7 +504,8 @@ __global__ void __launch_bounds__(256) k_por_stress(PorousArgs A) {
 #pragma unroll
                 for (int cc = 0; cc < D; ++cc) acc[r * D + cc] += dv * g[cc];
             }
-        }
+        };
+        por_walk<false>(A, i, sub, visit);
     }
     group_sum<kPorLanes>(acc);
     if (act && sub == 0 && !(A.flags[i] & PF_GHOST)) {  // F += dt (acc B)
@@ -535,9 +539,7 @@ __global__ void __launch_bounds__(256) k_por_accel(PorousArgs A) {
     if (act) {
         double xa[3];
         xget<D>(ldg4(A.XV + i), xa);
-        const int64_t k1 = A.indptr[i + 1];
-        for (int64_t k = A.indptr[i] + sub; k < k1; k += kPorLanes) {
-            const int32_t b = __ldg(A.csr + k);
+        auto visit = [&](int32_t b) {
             double xb[3], Tb[D * D], rel[D], g[D];
             dload<D>(A.T, n, A.XV, b, Tb, xb);
 #pragma unroll
@@ -547,7 +549,8 @@ __global__ void __launch_bounds__(256) k_por_accel(PorousArgs A) {
             for (int r = 0; r < D; ++r)
 #pragma unroll
                 for (int cc = 0; cc < D; ++cc) acc[r] = fma(Tb[r * D + cc], g[cc], acc[r]);
-        }
+        };
+        por_walk(A, i, sub, visit);
     }
     group_sum<kPorLanes>(acc);
     if (act && sub == 0 && !(A.flags[i] & PF_GHOST)) {

@@ -63,6 +63,8 @@ struct Solid32Args {
     const uint8_t *flags;
     const int64_t *indptr;
     const int32_t *csr;
+    const int64_t *cptr;     // chunked index table (gather_csr.cuh), or null
+    const int32_t *csr16;
     const int64_t *perm;
     double *part;            // [3][nblk]: ek, amax2, vmax2 (fp64 partials)
     int nblk;
@@ -167,7 +169,7 @@ __global__ void __launch_bounds__(256) k32_kick_drift(Solid32Args A) {
 }
 
 // k_solid_stress_csr in fp32: H += dt (sum_b V_b (v_b - v_a) (x) gradW) B
-template <int D, int G>
+template <int D, int G, bool C16 = false>
 __global__ void __launch_bounds__(256) k32_stress_csr(Solid32Args A) {
     using V_t = typename VTR<D, float>::T;
     const Ctrl *c = A.ctrl;
@@ -186,9 +188,7 @@ __global__ void __launch_bounds__(256) k32_stress_csr(Solid32Args A) {
             float xa[3], va[3];
             xget32<D>(__ldg(A.XV + i), xa);
             vget(vldg(V + i), va);
-            const int64_t k1 = A.indptr[i + 1];
-            for (int64_t k = A.indptr[i] + sub; k < k1; k += G) {
-                const int32_t b = __ldg(A.csr + k);
+            auto visit = [&](int32_t b) {
                 const float4 xvb = __ldg(A.XV + b);
                 float xb[3], vb[3], rel[D], g[D];
                 xget32<D>(xvb, xb);
@@ -203,6 +203,12 @@ __global__ void __launch_bounds__(256) k32_stress_csr(Solid32Args A) {
 #pragma unroll
                     for (int cc = 0; cc < D; ++cc) acc[r * D + cc] += dv * g[cc];
                 }
+            };
+            if constexpr (C16) {
+                walk_chunks<G, false>(A.cptr, A.csr16, i, sub, visit);
+            } else {
+                const int64_t k1 = A.indptr[i + 1];
+                for (int64_t k = A.indptr[i] + sub; k < k1; k += G) visit(__ldg(A.csr + k));
             }
         }
         group_sum32<G>(acc);
@@ -271,7 +277,7 @@ __global__ void __launch_bounds__(256, 2) k32_rmap(Solid32Args A) {
 }
 
 // k_solid_accel_csr in fp32; E_k and |a|max partials in fp64
-template <int D, int G>
+template <int D, int G, bool C16 = false>
 __global__ void __launch_bounds__(256) k32_accel_csr(Solid32Args A) {
     using V_t = typename VTR<D, float>::T;
     __shared__ double sh[32];
@@ -290,9 +296,7 @@ __global__ void __launch_bounds__(256) k32_accel_csr(Solid32Args A) {
         if (act) {
             float xa[3];
             xget32<D>(__ldg(A.XV + i), xa);
-            const int64_t k1 = A.indptr[i + 1];
-            for (int64_t k = A.indptr[i] + sub; k < k1; k += G) {
-                const int32_t b = __ldg(A.csr + k);
+            auto visit = [&](int32_t b) {
                 float xb[3], Tb[D * D], rel[D], g[D];
                 dload32<D>(A.T, n, A.XV, b, Tb, xb);
 #pragma unroll
@@ -302,6 +306,12 @@ __global__ void __launch_bounds__(256) k32_accel_csr(Solid32Args A) {
                 for (int r = 0; r < D; ++r)
 #pragma unroll
                     for (int cc = 0; cc < D; ++cc) acc[r] = fmaf(Tb[r * D + cc], g[cc], acc[r]);
+            };
+            if constexpr (C16) {
+                walk_chunks<G, true>(A.cptr, A.csr16, i, sub, visit);
+            } else {
+                const int64_t k1 = A.indptr[i + 1];
+                for (int64_t k = A.indptr[i] + sub; k < k1; k += G) visit(__ldg(A.csr + k));
             }
         }
         group_sum32<G>(acc);

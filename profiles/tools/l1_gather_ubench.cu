@@ -41,10 +41,11 @@ int main() {
     int *di; cudaMalloc(&di, iters * 32 * 4);
     const char *names[] = {"coalesced (8 full lines)", "8 random aligned quads", "quads straddling 2 lines (16 touches)",
                            "32 random records (32 lines)", "all lanes same record", "4-lane groups: same record per group",
-                           "pairs: 16 random aligned pairs (16 lines)", "8 random lines, lanes permuted across groups"};
+                           "pairs: 16 random aligned pairs (16 lines)", "8 random lines, lanes permuted across groups",
+                           "32 random lines, offset = lane % 4 (bank-balanced groups)", "16 random lines: group = 2 lines x 2 records, offsets distinct", "32 random lines, offsets = 2 x {0,1} per group (2-way)"};
     int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     int clk; cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
-    for (int pat = 0; pat < 8; ++pat) {
+    for (int pat = 0; pat < 11; ++pat) {
         std::vector<int> idx(iters * 32);
         srand(1);
         for (int it = 0; it < iters; ++it) {
@@ -60,6 +61,9 @@ int main() {
                 case 5: v = quad[g] * 4; break;
                 case 6: v = ((rand() % (nrec / 2)) * 2 * ((l & 1) == 0) + 0); if (l & 1) v = idx[it * 32 + l - 1] + 1; break;
                 case 7: v = quad[l % 8] * 4 + (l / 8); break;
+                case 8: v = (rand() % (nrec / 4)) * 4 + s; break;
+                case 9: v = (s & 1) ? idx[it * 32 + l - 1] + 1 : (rand() % (nrec / 4)) * 4 + s; break;
+                case 10: v = (rand() % (nrec / 4)) * 4 + (s & 1); break;
                 }
                 idx[it * 32 + l] = v;
             }
