@@ -179,6 +179,34 @@ template <int G, int K> __device__ __forceinline__ void group_sum(double (&v)[K]
         for (int k = 0; k < K; ++k) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
 }
 
+// Persistent gathers (A.queue != null): the grid is one wave of CTAs; the
+// 256-particle blocks are split into one contiguous range per SM, and a CTA
+// claims the next block of its own SM's range (then of the following SMs'
+// ranges, so the tail is shared).  CTAs resident on one SM thus work on
+// adjacent blocks of the Morton order, whose neighbourhoods overlap: they
+// hit each other's lines in the SM's L1 instead of each streaming its own
+// halo (with the hardware's round-robin block placement an SM's CTAs are
+// ~148 blocks apart).  Returns -1 when every range is exhausted.
+__device__ __forceinline__ int claim_block(const SolidArgs &A, int *s_blk) {
+    __syncthreads();  // every thread has read the previous claim
+    if (threadIdx.x == 0) {
+        unsigned smid;
+        asm("mov.u32 %0, %%smid;" : "=r"(smid));
+        const int nq = A.nq, chunk = A.qchunk, my = (int)(smid % (unsigned)nq);
+        int blk = -1;
+        for (int t = 0; t < nq && blk < 0; ++t) {
+            const int q = my + t < nq ? my + t : my + t - nq;
+            const int len = min(chunk, A.nblk - q * chunk);
+            if (len <= 0 || *reinterpret_cast<volatile int *>(A.queue + q) >= len) continue;
+            const int k = atomicAdd(A.queue + q, 1);
+            if (k < len) blk = q * chunk + k;
+        }
+        *s_blk = blk;
+    }
+    __syncthreads();
+    return *s_blk;
+}
+
 // dF/dt gather + F update (the split path: the return map runs in k_solid_rmap)
 template <int D, int G, bool C16 = false>
 __global__ void __launch_bounds__(256, MTSPH_STRESS_CTAS) k_solid_stress_csr(SolidArgs A) {
@@ -189,8 +217,12 @@ __global__ void __launch_bounds__(256, MTSPH_STRESS_CTAS) k_solid_stress_csr(Sol
     const int64_t n = A.n;
     const int sub = threadIdx.x % G;
     const V_t *V = reinterpret_cast<const V_t *>(A.V);
+    __shared__ int s_blk;
+    const bool persist = A.queue != nullptr;
+    for (int blk = blockIdx.x;;) {
+    if (persist && (blk = claim_block(A, &s_blk)) < 0) break;
     for (int it = 0; it < G; ++it) {
-        const int64_t i = (int64_t)blockIdx.x * 256 + it * (256 / G) + threadIdx.x / G;
+        const int64_t i = (int64_t)blk * 256 + it * (256 / G) + threadIdx.x / G;
         const bool act = i < n && !(A.flags[i] & FL_GHOST);  // uniform over the G lanes
         double acc[D * D];
 #pragma unroll
@@ -235,6 +267,8 @@ __global__ void __launch_bounds__(256, MTSPH_STRESS_CTAS) k_solid_stress_csr(Sol
             for (int k = 0; k < D * D; ++k) A.F[(int64_t)k * n + i] = F[k] + dt * L[k];
         }
     }
+    if (!persist) break;
+    }
 }
 
 // a = 1/rho0 sum_b V_b (T_a + T_b) gradW, v += dt/2 a, E_k and |a|max partials
@@ -247,9 +281,13 @@ __global__ void __launch_bounds__(256, MTSPH_ACCEL_CTAS) k_solid_accel_csr(Solid
     const double dt = c->dt;
     const int64_t n = A.n;
     const int sub = threadIdx.x % G;
+    __shared__ int s_blk;
+    const bool persist = A.queue != nullptr;
+    for (int blk = blockIdx.x;;) {
+    if (persist && (blk = claim_block(A, &s_blk)) < 0) break;
     double ek = 0.0, a2m = 0.0;
     for (int it = 0; it < G; ++it) {
-        const int64_t i = (int64_t)blockIdx.x * 256 + it * (256 / G) + threadIdx.x / G;
+        const int64_t i = (int64_t)blk * 256 + it * (256 / G) + threadIdx.x / G;
         const bool act = i < n && !(A.flags[i] & FL_GHOST);
         // sum_b V_b (T_a + T_b) gradW = sum_b T~_b gradW + T_a G_a, with
         // T~_b = V_b T_b from the divergence record (three 256-bit loads per
@@ -313,8 +351,10 @@ __global__ void __launch_bounds__(256, MTSPH_ACCEL_CTAS) k_solid_accel_csr(Solid
     const double se = block_sum<256>(ek, sh);
     const double sa = block_max<256>(a2m, sh);
     if (threadIdx.x == 0) {
-        A.part[blockIdx.x] = se;
-        A.part[A.nblk + blockIdx.x] = sa;
+        A.part[blk] = se;
+        A.part[A.nblk + blk] = sa;
+    }
+    if (!persist) break;
     }
 }
 

@@ -235,6 +235,10 @@ struct mtsph_solid {
     // Measured (10M, 3D): SELL 7.4 + 10.0 ms, G=2 5.8 + 7.4, G=4 5.8 + 7.3,
     // G=8 6.9 + 8.7 (stress + accel); MTSPH_GATHER_LANES overrides
     int gather_g = 4;
+    // persistent gathers (gather_csr.cuh claim_block): per-SM block counters
+    // (stress, accel), the SM count and the one-wave grids; persist 0 = off
+    DBuf<int> gqueue;
+    int persist = 0, nq = 0, grid_stress = 0, grid_accel = 0;
     // 3D fp64 opt-in (MTSPH_GATHER_WINDOW=1): shared-memory cell-window
     // gathers (window.cuh; measured slower than the CSR gathers)
     WinSched win;
@@ -334,6 +338,15 @@ template <int D> static int launch_stress_gather(mtsph_solid *S, const SolidArgs
         return 1;
     }
     const bool c16 = S->nb.chunk_g == S->gather_g && S->gather_g > 0;
+    if (S->gather_g == 4 && c16 && S->persist && D == 3) {
+        SolidArgs P = A;
+        P.queue = S->gqueue.p;
+        P.nq = S->nq;
+        P.qchunk = (S->nblk + S->nq - 1) / S->nq;
+        MT_CUDA(cudaMemsetAsync(P.queue, 0, sizeof(int) * (size_t)S->nq, s));
+        k_solid_stress_csr<D, 4, true><<<(unsigned)S->grid_stress, 256, 0, s>>>(P);
+        return 1;
+    }
     if (S->gather_g == 4 && c16) k_solid_stress_csr<D, 4, true><<<nb, 256, 0, s>>>(A);
     else if (S->gather_g == 2 && c16) k_solid_stress_csr<D, 2, true><<<nb, 256, 0, s>>>(A);
     else if (S->gather_g == 4) k_solid_stress_csr<D, 4><<<nb, 256, 0, s>>>(A);
@@ -357,6 +370,15 @@ template <int D> static int launch_accel_gather(mtsph_solid *S, const SolidArgs 
         return 2;
     }
     const bool c16 = S->nb.chunk_g == S->gather_g && S->gather_g > 0;
+    if (S->gather_g == 4 && c16 && S->persist && D == 3) {
+        SolidArgs P = A;
+        P.queue = S->gqueue.p + S->nq;
+        P.nq = S->nq;
+        P.qchunk = (S->nblk + S->nq - 1) / S->nq;
+        MT_CUDA(cudaMemsetAsync(P.queue, 0, sizeof(int) * (size_t)S->nq, s));
+        k_solid_accel_csr<D, 4, true><<<(unsigned)S->grid_accel, 256, 0, s>>>(P);
+        return 1;
+    }
     if (S->gather_g == 4 && c16) k_solid_accel_csr<D, 4, true><<<nb, 256, 0, s>>>(A);
     else if (S->gather_g == 2 && c16) k_solid_accel_csr<D, 2, true><<<nb, 256, 0, s>>>(A);
     else if (S->gather_g == 4) k_solid_accel_csr<D, 4><<<nb, 256, 0, s>>>(A);
@@ -638,6 +660,18 @@ extern "C" mtsph_status mtsph_solid_create(const mtsph_solid_desc *dsc, mtsph_so
     MT_LAUNCH_CHECK();
     S->part.alloc((size_t)3 * S->nblk);
     S->part.zero(S->s);
+    if (const char *e = std::getenv("MTSPH_GATHER_PERSIST"); e && e[0] == '1' && d == 3) {
+        int dev = 0, sms = 0, per = 0;
+        MT_CUDA(cudaGetDevice(&dev));
+        MT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        S->nq = sms;
+        S->gqueue.alloc((size_t)2 * sms);
+        MT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, (const void *)k_solid_stress_csr<3, 4, true>, 256, 0));
+        S->grid_stress = sms * per;
+        MT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, (const void *)k_solid_accel_csr<3, 4, true>, 256, 0));
+        S->grid_accel = sms * per;
+        S->persist = 1;
+    }
     S->meas.alloc((size_t)5 * S->nblk);
     if (S->nb.sweep == 1) {
         S->level_ptr.upload(S->nb.level_ptr_h.data(), S->nb.level_ptr_h.size(), S->s);
