@@ -197,17 +197,29 @@ struct KSpec {
 // (1-q/2)^3 w_k: the same value as the form above up to rounding, with
 // fewer FP64 operations in the neighbour loops (9 instead of 13 besides
 // the square root).
+// magnitude factor and scaled separation: gradW = mag * w
 template <int D>
-__device__ __forceinline__ void grad_w(const double *rel, const KSpec &ks, double *g) {
-    double w[D];
+__device__ __forceinline__ double grad_mag(const double *rel, const KSpec &ks, double *w) {
     double q2 = 0.0;
 #pragma unroll
     for (int k = 0; k < D; ++k) { w[k] = rel[k] * ks.inv_h2[k]; q2 = fma(rel[k], w[k], q2); }
     const double q = sqrt(q2);
     const double t = 1.0 - 0.5 * q;
-    const double mag = (q < 2.0) ? ks.pref5 * (t * t * t) : 0.0;
+    return (q < 2.0) ? ks.pref5 * (t * t * t) : 0.0;
+}
+template <int D>
+__device__ __forceinline__ void grad_w(const double *rel, const KSpec &ks, double *g) {
+    double w[D];
+    const double mag = grad_mag<D>(rel, ks, w);
 #pragma unroll
     for (int k = 0; k < D; ++k) g[k] = mag * w[k];
+}
+// gradW from a stored magnitude factor (gather_csr.cuh build_chunked): the
+// same products as grad_w, without the square root and the polynomial
+template <int D>
+__device__ __forceinline__ void grad_w_mag(const double *rel, const KSpec &ks, double mag, double *g) {
+#pragma unroll
+    for (int k = 0; k < D; ++k) g[k] = mag * (rel[k] * ks.inv_h2[k]);
 }
 
 // 32 B accesses.  sm_100 has 256-bit global loads/stores (SASS

@@ -115,12 +115,46 @@ __global__ void k_chunk_fill(int64_t n, const int64_t *__restrict__ indptr, cons
         }
 }
 
+// Per entry of the chunked table, the static magnitude factor of the kernel
+// gradient, gradW_ab = mag_ab (X_b - X_a) / h^2 -- the one-time "precomputed
+// kernel gradient" of the neighbour build in its cheapest form to stream
+// (8 B per entry, a lane's next four in one 32 B word next to its four ids).
+// Computed by grad_mag, the function the gathers would call: the stored
+// gradient is bit-identical to the recomputed one.
+template <int D>
+__global__ void k_chunk_mag(int64_t n, const double4 *__restrict__ XV, KSpec ks, int g,
+                            const int64_t *__restrict__ cptr, const int32_t *__restrict__ csr16, double *mag16) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double xa[3];
+    xget<D>(ldg4(XV + i), xa);
+    const int64_t w0 = cptr[i] * g, w1 = cptr[i + 1] * g;
+    for (int64_t w = w0; w < w1; ++w) {
+        const int4 q = reinterpret_cast<const int4 *>(csr16)[w];
+        const int32_t b[4] = {q.x, q.y, q.z, q.w};
+        double m[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            m[e] = 0.0;
+            if (b[e] >= 0) {
+                double xb[3], rel[D], ww[D];
+                xget<D>(ldg4(XV + b[e]), xb);
+#pragma unroll
+                for (int k = 0; k < D; ++k) rel[k] = xb[k] - xa[k];
+                m[e] = grad_mag<D>(rel, ks, ww);
+            }
+        }
+        reinterpret_cast<double4 *>(mag16)[w] = make_double4(m[0], m[1], m[2], m[3]);
+    }
+}
+
 }  // namespace mtsph
 namespace mtsph {
 // build the chunked table for g lanes per particle (MTSPH_GATHER_CHUNKED=0: keep the CSR walk)
 // (the solid's kernels have a CSR fallback; the porous ones need the table: required)
-inline void build_chunked(NbhDev &nb, int g, cudaStream_t s, bool required = false) {
+inline void build_chunked(NbhDev &nb, int g, cudaStream_t s, bool required = false, bool with_mag = false) {
     nb.chunk_g = 0;
+    nb.mag16.release();
     if (const char *e = std::getenv("MTSPH_GATHER_CHUNKED"); !required && e && e[0] == '0') return;
     if (g < 2 || nb.n == 0) return;
     const int64_t n = nb.n;
@@ -139,37 +173,77 @@ inline void build_chunked(NbhDev &nb, int g, cudaStream_t s, bool required = fal
     if (const char *e = std::getenv("MTSPH_GATHER_PACK")) pack = e[0] != '0' && g == 4;
     k_chunk_fill<<<blocks_for(n, 128), 128, 0, s>>>(n, nb.indptr.p, nb.csr.p, g, pack, nb.cptr.p, nb.csr16.p);
     MT_LAUNCH_CHECK();
+    // stored kernel-gradient magnitudes (MTSPH_GATHER_MAG=0: recompute in the gathers)
+    const char *me = std::getenv("MTSPH_GATHER_MAG");
+    if (with_mag && (required || !(me && me[0] == '0'))) {
+        nb.mag16.alloc((size_t)total * 4 * g);
+        if (nb.d == 2) k_chunk_mag<2><<<blocks_for(n, 128), 128, 0, s>>>(n, nb.XV.p, nb.ks, g, nb.cptr.p, nb.csr16.p, nb.mag16.p);
+        else k_chunk_mag<3><<<blocks_for(n, 128), 128, 0, s>>>(n, nb.XV.p, nb.ks, g, nb.cptr.p, nb.csr16.p, nb.mag16.p);
+        MT_LAUNCH_CHECK();
+    }
     MT_CUDA(cudaStreamSynchronize(s));
     nb.chunk_g = g;
 }
 
-// this lane's entries of particle i's row in the chunked table: four
-// unconditional visits per full 16 B word (the compiler overlaps the next
-// visit's loads with the current one's arithmetic; measured at 10M accel
-// 5.28 -> 5.18 ms against a test per visit), per-entry tests in a partial one
-// (FAST).  !FAST: a test per visit everywhere -- the dF/dt gathers run at a
-// tighter register cap (4 CTAs/SM in fp64), where the overlapped schedule
-// spills (6.25 vs 5.06 ms).
-template <int G, bool FAST, class F>
-__device__ __forceinline__ void walk_chunks(const int64_t *__restrict__ cptr, const int32_t *__restrict__ csr16,
-                                            int64_t i, int sub, F &&visit) {
+// This lane's entries of particle i's row in the chunked table; visit(b, mag)
+// with MAG (the stored gradient magnitudes next to the ids), else visit(b).
+// MODE 0: a test per entry (padding is -1).  The dF/dt gathers run at a
+//   tighter register cap (4 CTAs/SM in fp64), where an overlapped schedule
+//   spills (6.25 vs 5.06 ms).
+// MODE 1: four unconditional visits per full 16 B word -- the compiler
+//   overlaps the next visit's loads with the current one's arithmetic -- and
+//   tests in a partial word (the row's last few).  accel at 10M: 5.28 ms with
+//   tests only, 5.27 so, 5.36 peeled, 5.18 with rows padded by the particle
+//   itself (a zero contribution; no waste on the regular bar, ~10 % wasted
+//   visits on rows of irregular length).
+// MODE 2: peeled -- every chunk but the row's last unconditional, the last
+//   one tested.  The register-heavy porous gathers: outer step (17 M plate)
+//   33.2 ms peeled, 39.5 with MODE 1's two bodies in the loop, 37.1 CSR.
+template <int G, int MODE, bool MAG, class F>
+__device__ __forceinline__ void walk_chunks_any(const int64_t *__restrict__ cptr, const int32_t *__restrict__ csr16,
+                                                const double *__restrict__ mag16, int64_t i, int sub, F &&visit) {
     const int64_t c0 = cptr[i];
     const int nch = (int)(cptr[i + 1] - c0);
     const int4 *w = reinterpret_cast<const int4 *>(csr16) + c0 * G + sub;
-    for (int c = 0; c < nch; ++c, w += G) {
+    const double4 *mw = reinterpret_cast<const double4 *>(mag16) + c0 * G + sub;
+    auto call = [&](int32_t b, double m) {
+        if constexpr (MAG) visit(b, m);
+        else visit(b);
+    };
+    auto full = [&](const int4 &q, const double4 &m) {
+        call(q.x, m.x);
+        call(q.y, m.y);
+        call(q.z, m.z);
+        call(q.w, m.w);
+    };
+    auto tested = [&](const int4 &q, const double4 &m) {
+        if (q.x >= 0) call(q.x, m.x);
+        if (q.y >= 0) call(q.y, m.y);
+        if (q.z >= 0) call(q.z, m.z);
+        if (q.w >= 0) call(q.w, m.w);
+    };
+    const int nfull = MODE == 2 ? nch - 1 : nch;
+    for (int c = 0; c < nfull; ++c, w += G, mw += G) {
         const int4 q = __ldg(w);
-        if (FAST && q.w >= 0) {  // a full word (every one but the row's last few)
-            visit(q.x);
-            visit(q.y);
-            visit(q.z);
-            visit(q.w);
-        } else {
-            if (q.x >= 0) visit(q.x);
-            if (q.y >= 0) visit(q.y);
-            if (q.z >= 0) visit(q.z);
-            if (q.w >= 0) visit(q.w);
-        }
+        const double4 m = MAG ? ldg4(mw) : make_double4(0.0, 0.0, 0.0, 0.0);
+        if (MODE == 2 || (MODE == 1 && q.w >= 0)) full(q, m);
+        else tested(q, m);
     }
+    if (MODE == 2 && nch > 0) {
+        const int4 q = __ldg(w);
+        const double4 m = MAG ? ldg4(mw) : make_double4(0.0, 0.0, 0.0, 0.0);
+        tested(q, m);
+    }
+}
+template <int G, bool FAST, class F>
+__device__ __forceinline__ void walk_chunks(const int64_t *__restrict__ cptr, const int32_t *__restrict__ csr16,
+                                            int64_t i, int sub, F &&visit) {
+    walk_chunks_any<G, FAST ? 1 : 0, false>(cptr, csr16, nullptr, i, sub, visit);
+}
+template <int G, bool FAST, class F>
+__device__ __forceinline__ void walk_chunks_mag(const int64_t *__restrict__ cptr, const int32_t *__restrict__ csr16,
+                                                const double *__restrict__ mag16, int64_t i, int sub, F &&visit) {
+    walk_chunks_any<G, FAST ? 1 : 0, true>(cptr, csr16, mag16, i, sub, visit);
 }
 
 template <int G, int K> __device__ __forceinline__ void group_sum(double (&v)[K]) {
@@ -179,36 +253,8 @@ template <int G, int K> __device__ __forceinline__ void group_sum(double (&v)[K]
         for (int k = 0; k < K; ++k) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
 }
 
-// Persistent gathers (A.queue != null): the grid is one wave of CTAs; the
-// 256-particle blocks are split into one contiguous range per SM, and a CTA
-// claims the next block of its own SM's range (then of the following SMs'
-// ranges, so the tail is shared).  CTAs resident on one SM thus work on
-// adjacent blocks of the Morton order, whose neighbourhoods overlap: they
-// hit each other's lines in the SM's L1 instead of each streaming its own
-// halo (with the hardware's round-robin block placement an SM's CTAs are
-// ~148 blocks apart).  Returns -1 when every range is exhausted.
-__device__ __forceinline__ int claim_block(const SolidArgs &A, int *s_blk) {
-    __syncthreads();  // every thread has read the previous claim
-    if (threadIdx.x == 0) {
-        unsigned smid;
-        asm("mov.u32 %0, %%smid;" : "=r"(smid));
-        const int nq = A.nq, chunk = A.qchunk, my = (int)(smid % (unsigned)nq);
-        int blk = -1;
-        for (int t = 0; t < nq && blk < 0; ++t) {
-            const int q = my + t < nq ? my + t : my + t - nq;
-            const int len = min(chunk, A.nblk - q * chunk);
-            if (len <= 0 || *reinterpret_cast<volatile int *>(A.queue + q) >= len) continue;
-            const int k = atomicAdd(A.queue + q, 1);
-            if (k < len) blk = q * chunk + k;
-        }
-        *s_blk = blk;
-    }
-    __syncthreads();
-    return *s_blk;
-}
-
 // dF/dt gather + F update (the split path: the return map runs in k_solid_rmap)
-template <int D, int G, bool C16 = false>
+template <int D, int G, bool C16 = false, bool MAG = false>
 __global__ void __launch_bounds__(256, MTSPH_STRESS_CTAS) k_solid_stress_csr(SolidArgs A) {
     using V_t = typename VT<D>::T;
     const Ctrl *c = A.ctrl;
@@ -217,12 +263,8 @@ __global__ void __launch_bounds__(256, MTSPH_STRESS_CTAS) k_solid_stress_csr(Sol
     const int64_t n = A.n;
     const int sub = threadIdx.x % G;
     const V_t *V = reinterpret_cast<const V_t *>(A.V);
-    __shared__ int s_blk;
-    const bool persist = A.queue != nullptr;
-    for (int blk = blockIdx.x;;) {
-    if (persist && (blk = claim_block(A, &s_blk)) < 0) break;
     for (int it = 0; it < G; ++it) {
-        const int64_t i = (int64_t)blk * 256 + it * (256 / G) + threadIdx.x / G;
+        const int64_t i = (int64_t)blockIdx.x * 256 + it * (256 / G) + threadIdx.x / G;
         const bool act = i < n && !(A.flags[i] & FL_GHOST);  // uniform over the G lanes
         double acc[D * D];
 #pragma unroll
@@ -231,14 +273,15 @@ __global__ void __launch_bounds__(256, MTSPH_STRESS_CTAS) k_solid_stress_csr(Sol
             double xa[3], va[3];
             xget<D>(ldg4(A.XV + i), xa);
             vget(vldg(V + i), va);
-            auto visit = [&](int32_t b) {
+            auto visit2 = [&](int32_t b, double mag) {
                 const double4 xvb = ldg4(A.XV + b);
                 double xb[3], vb[3], rel[D], g[D];
                 xget<D>(xvb, xb);
                 vget(vldg(V + b), vb);
 #pragma unroll
                 for (int q = 0; q < D; ++q) rel[q] = xb[q] - xa[q];
-                grad_w<D>(rel, A.ks, g);
+                if (MAG) grad_w_mag<D>(rel, A.ks, mag, g);
+                else grad_w<D>(rel, A.ks, g);
                 const double volb = volof<D>(xvb);
 #pragma unroll
                 for (int r = 0; r < D; ++r) {
@@ -247,7 +290,10 @@ __global__ void __launch_bounds__(256, MTSPH_STRESS_CTAS) k_solid_stress_csr(Sol
                     for (int cc = 0; cc < D; ++cc) acc[r * D + cc] += dv * g[cc];
                 }
             };
-            if constexpr (C16) {
+            auto visit = [&](int32_t b) { visit2(b, 0.0); };
+            if constexpr (C16 && MAG) {
+                walk_chunks_mag<G, false>(A.cptr, A.csr16, A.mag16, i, sub, visit2);
+            } else if constexpr (C16) {
                 walk_chunks<G, false>(A.cptr, A.csr16, i, sub, visit);
             } else {
                 const int64_t k1 = A.indptr[i + 1];
@@ -267,12 +313,10 @@ __global__ void __launch_bounds__(256, MTSPH_STRESS_CTAS) k_solid_stress_csr(Sol
             for (int k = 0; k < D * D; ++k) A.F[(int64_t)k * n + i] = F[k] + dt * L[k];
         }
     }
-    if (!persist) break;
-    }
 }
 
 // a = 1/rho0 sum_b V_b (T_a + T_b) gradW, v += dt/2 a, E_k and |a|max partials
-template <int D, int G, bool C16 = false>
+template <int D, int G, bool C16 = false, bool MAG = false>
 __global__ void __launch_bounds__(256, MTSPH_ACCEL_CTAS) k_solid_accel_csr(SolidArgs A) {
     using V_t = typename VT<D>::T;
     __shared__ double sh[32];
@@ -281,13 +325,9 @@ __global__ void __launch_bounds__(256, MTSPH_ACCEL_CTAS) k_solid_accel_csr(Solid
     const double dt = c->dt;
     const int64_t n = A.n;
     const int sub = threadIdx.x % G;
-    __shared__ int s_blk;
-    const bool persist = A.queue != nullptr;
-    for (int blk = blockIdx.x;;) {
-    if (persist && (blk = claim_block(A, &s_blk)) < 0) break;
     double ek = 0.0, a2m = 0.0;
     for (int it = 0; it < G; ++it) {
-        const int64_t i = (int64_t)blk * 256 + it * (256 / G) + threadIdx.x / G;
+        const int64_t i = (int64_t)blockIdx.x * 256 + it * (256 / G) + threadIdx.x / G;
         const bool act = i < n && !(A.flags[i] & FL_GHOST);
         // sum_b V_b (T_a + T_b) gradW = sum_b T~_b gradW + T_a G_a, with
         // T~_b = V_b T_b from the divergence record (three 256-bit loads per
@@ -298,18 +338,22 @@ __global__ void __launch_bounds__(256, MTSPH_ACCEL_CTAS) k_solid_accel_csr(Solid
         if (act) {
             double xa[3];
             xget<D>(ldg4(A.XV + i), xa);
-            auto visit = [&](int32_t b) {
+            auto visit2 = [&](int32_t b, double mag) {
                 double xb[3], Tb[D * D], rel[D], g[D];
                 dload<D>(A.T, n, A.XV, b, Tb, xb);
 #pragma unroll
                 for (int q = 0; q < D; ++q) rel[q] = xb[q] - xa[q];
-                grad_w<D>(rel, A.ks, g);
+                if (MAG) grad_w_mag<D>(rel, A.ks, mag, g);
+                else grad_w<D>(rel, A.ks, g);
 #pragma unroll
                 for (int r = 0; r < D; ++r)
 #pragma unroll
                     for (int cc = 0; cc < D; ++cc) acc[r] = fma(Tb[r * D + cc], g[cc], acc[r]);
             };
-            if constexpr (C16) {
+            auto visit = [&](int32_t b) { visit2(b, 0.0); };
+            if constexpr (C16 && MAG) {
+                walk_chunks_mag<G, true>(A.cptr, A.csr16, A.mag16, i, sub, visit2);
+            } else if constexpr (C16) {
                 walk_chunks<G, true>(A.cptr, A.csr16, i, sub, visit);
             } else {
                 const int64_t k1 = A.indptr[i + 1];
@@ -351,10 +395,8 @@ __global__ void __launch_bounds__(256, MTSPH_ACCEL_CTAS) k_solid_accel_csr(Solid
     const double se = block_sum<256>(ek, sh);
     const double sa = block_max<256>(a2m, sh);
     if (threadIdx.x == 0) {
-        A.part[blk] = se;
-        A.part[A.nblk + blk] = sa;
-    }
-    if (!persist) break;
+        A.part[blockIdx.x] = se;
+        A.part[A.nblk + blockIdx.x] = sa;
     }
 }
 

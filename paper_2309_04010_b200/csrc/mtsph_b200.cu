@@ -235,10 +235,6 @@ struct mtsph_solid {
     // Measured (10M, 3D): SELL 7.4 + 10.0 ms, G=2 5.8 + 7.4, G=4 5.8 + 7.3,
     // G=8 6.9 + 8.7 (stress + accel); MTSPH_GATHER_LANES overrides
     int gather_g = 4;
-    // persistent gathers (gather_csr.cuh claim_block): per-SM block counters
-    // (stress, accel), the SM count and the one-wave grids; persist 0 = off
-    DBuf<int> gqueue;
-    int persist = 0, nq = 0, grid_stress = 0, grid_accel = 0;
     // 3D fp64 opt-in (MTSPH_GATHER_WINDOW=1): shared-memory cell-window
     // gathers (window.cuh; measured slower than the CSR gathers)
     WinSched win;
@@ -301,7 +297,7 @@ struct mtsph_solid {
         A.B = nb.B.p; A.G = G.p; A.mass = mass.p; A.rho0 = rho0.p; A.flags = flags.p;
         A.slice_ptr = nb.slice_ptr.p; A.slice_w = nb.slice_w.p; A.nbr = nb.nbr.p;
         A.indptr = nb.indptr.p; A.csr = nb.csr.p;
-        A.cptr = nb.chunk_g ? nb.cptr.p : nullptr; A.csr16 = nb.csr16.p;
+        A.cptr = nb.chunk_g ? nb.cptr.p : nullptr; A.csr16 = nb.csr16.p; A.mag16 = nb.mag16.p;
         A.perm = nb.perm.p;
         A.Lacc = win.on ? Lacc.p : nullptr;
         A.part = part.p;
@@ -338,16 +334,8 @@ template <int D> static int launch_stress_gather(mtsph_solid *S, const SolidArgs
         return 1;
     }
     const bool c16 = S->nb.chunk_g == S->gather_g && S->gather_g > 0;
-    if (S->gather_g == 4 && c16 && S->persist && D == 3) {
-        SolidArgs P = A;
-        P.queue = S->gqueue.p;
-        P.nq = S->nq;
-        P.qchunk = (S->nblk + S->nq - 1) / S->nq;
-        MT_CUDA(cudaMemsetAsync(P.queue, 0, sizeof(int) * (size_t)S->nq, s));
-        k_solid_stress_csr<D, 4, true><<<(unsigned)S->grid_stress, 256, 0, s>>>(P);
-        return 1;
-    }
-    if (S->gather_g == 4 && c16) k_solid_stress_csr<D, 4, true><<<nb, 256, 0, s>>>(A);
+    if (S->gather_g == 4 && c16 && A.mag16) k_solid_stress_csr<D, 4, true, true><<<nb, 256, 0, s>>>(A);
+    else if (S->gather_g == 4 && c16) k_solid_stress_csr<D, 4, true><<<nb, 256, 0, s>>>(A);
     else if (S->gather_g == 2 && c16) k_solid_stress_csr<D, 2, true><<<nb, 256, 0, s>>>(A);
     else if (S->gather_g == 4) k_solid_stress_csr<D, 4><<<nb, 256, 0, s>>>(A);
     else if (S->gather_g == 8) k_solid_stress_csr<D, 8><<<nb, 256, 0, s>>>(A);
@@ -370,15 +358,7 @@ template <int D> static int launch_accel_gather(mtsph_solid *S, const SolidArgs 
         return 2;
     }
     const bool c16 = S->nb.chunk_g == S->gather_g && S->gather_g > 0;
-    if (S->gather_g == 4 && c16 && S->persist && D == 3) {
-        SolidArgs P = A;
-        P.queue = S->gqueue.p + S->nq;
-        P.nq = S->nq;
-        P.qchunk = (S->nblk + S->nq - 1) / S->nq;
-        MT_CUDA(cudaMemsetAsync(P.queue, 0, sizeof(int) * (size_t)S->nq, s));
-        k_solid_accel_csr<D, 4, true><<<(unsigned)S->grid_accel, 256, 0, s>>>(P);
-        return 1;
-    }
+    // (the stored gradient magnitudes cost the divergence gather registers: 5.27 -> 5.45 ms)
     if (S->gather_g == 4 && c16) k_solid_accel_csr<D, 4, true><<<nb, 256, 0, s>>>(A);
     else if (S->gather_g == 2 && c16) k_solid_accel_csr<D, 2, true><<<nb, 256, 0, s>>>(A);
     else if (S->gather_g == 4) k_solid_accel_csr<D, 4><<<nb, 256, 0, s>>>(A);
@@ -608,7 +588,7 @@ extern "C" mtsph_status mtsph_solid_create(const mtsph_solid_desc *dsc, mtsph_so
         build_nbh(S->nb, n, d, dsc->pos, dsc->vol, dsc->h_axes, dsc->sweep, S->s);
     }
     setup_mark(S->s, "neighbourhood");
-    if (S->gather_g == 2 || S->gather_g == 4) build_chunked(S->nb, S->gather_g, S->s);
+    if (S->gather_g == 2 || S->gather_g == 4) build_chunked(S->nb, S->gather_g, S->s, false, S->gather_g == 4);
     setup_mark(S->s, "chunked index table");
     if (dsc->sweep == 3) build_tiled_auto(S->nb, S->tiled, S->s, dsc->tile);
     setup_mark(S->s, "tiled schedule");
@@ -660,18 +640,6 @@ extern "C" mtsph_status mtsph_solid_create(const mtsph_solid_desc *dsc, mtsph_so
     MT_LAUNCH_CHECK();
     S->part.alloc((size_t)3 * S->nblk);
     S->part.zero(S->s);
-    if (const char *e = std::getenv("MTSPH_GATHER_PERSIST"); e && e[0] == '1' && d == 3) {
-        int dev = 0, sms = 0, per = 0;
-        MT_CUDA(cudaGetDevice(&dev));
-        MT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        S->nq = sms;
-        S->gqueue.alloc((size_t)2 * sms);
-        MT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, (const void *)k_solid_stress_csr<3, 4, true>, 256, 0));
-        S->grid_stress = sms * per;
-        MT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, (const void *)k_solid_accel_csr<3, 4, true>, 256, 0));
-        S->grid_accel = sms * per;
-        S->persist = 1;
-    }
     S->meas.alloc((size_t)5 * S->nblk);
     if (S->nb.sweep == 1) {
         S->level_ptr.upload(S->nb.level_ptr_h.data(), S->nb.level_ptr_h.size(), S->s);

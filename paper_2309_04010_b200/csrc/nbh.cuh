@@ -80,6 +80,7 @@ struct NbhDev {
     int chunk_g = 0;             // lanes per particle it was built for (0: none)
     DBuf<int64_t> cptr;
     DBuf<int32_t> csr16;
+    DBuf<double> mag16;          // per entry of csr16: the kernel-gradient magnitude factor (0 for padding)
     bool want_sell = false;      // SELL-32 only for the opt-in one-lane gathers
     int64_t nslices = 0, sell_size = 0;
     DBuf<int64_t> slice_ptr;

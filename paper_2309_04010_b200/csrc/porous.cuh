@@ -64,6 +64,7 @@ struct PorousArgs {
     const int64_t *indptr;   // CSR rows (sorted)
     const int64_t *cptr;     // chunked index table (gather_csr.cuh build_chunked, kPorLanes lanes)
     const int32_t *csr16;
+    const double *mag16;     // stored kernel-gradient magnitude factors per entry of csr16
     const int32_t *csr;
     const int64_t *perm;
     double *part;
@@ -74,6 +75,10 @@ struct PorousArgs {
 };
 
 constexpr int kPorLanes = 4;
+// dF/dt gather from the stored gradient magnitudes (1) or recomputed (0)
+#ifndef MTSPH_POR_STRESS_MAG
+#define MTSPH_POR_STRESS_MAG 1
+#endif
 template <int D> struct PorRM { static constexpr int planes = D == 3 ? 4 : 2; };
 
 // particle of round `it` for this lane, its lane within the group
@@ -87,7 +92,12 @@ template <int D> struct PorRM { static constexpr int planes = D == 3 ? 4 : 2; };
 // this lane's neighbours of particle i from the chunked index table (gather_csr.cuh)
 template <bool FAST = true, class F>
 __device__ __forceinline__ void por_walk(const PorousArgs &A, int64_t i, int sub, F &&visit) {
-    walk_chunks<kPorLanes, FAST>(A.cptr, A.csr16, i, sub, visit);
+    walk_chunks_any<kPorLanes, FAST ? 2 : 0, false>(A.cptr, A.csr16, nullptr, i, sub, visit);
+}
+// the same with the stored gradient magnitudes: visit(b, mag)
+template <bool FAST = true, class F>
+__device__ __forceinline__ void por_walk_mag(const PorousArgs &A, int64_t i, int sub, F &&visit) {
+    walk_chunks_any<kPorLanes, FAST ? 2 : 0, true>(A.cptr, A.csr16, A.mag16, i, sub, visit);
 }
 
 template <int D>
@@ -142,6 +152,8 @@ __global__ void __launch_bounds__(256) k_por_flux(PorousArgs A, int pack) {
         double xa[3];
         xget<D>(ldg4(A.XV + i), xa);
         const double sa = A.sat[i];
+        // (light gather, one record per neighbour: streaming the stored gradient
+        // magnitudes as well measured slower, outer step 33.2 -> 40.2 ms at 17 M)
         auto visit = [&](int32_t b) {
             const double4 xvb = ldg4(A.XV + b);
             double xb[3], rel[D], g[D];
@@ -474,7 +486,7 @@ __global__ void __launch_bounds__(256) k_por_gsum(PorousArgs A, double *G) {
 }
 
 template <int D>
-__global__ void __launch_bounds__(256) k_por_stress(PorousArgs A) {
+__global__ void __launch_bounds__(256, 3) k_por_stress(PorousArgs A) {
     using V_t = typename VT<D>::T;
     Ctrl *c = A.ctrl;
     if (c->done) return;
@@ -489,14 +501,15 @@ __global__ void __launch_bounds__(256) k_por_stress(PorousArgs A) {
         double xa[3], va[3];
         xget<D>(ldg4(A.XV + i), xa);
         vget(vldg(V + i), va);
-        auto visit = [&](int32_t b) {
+        auto visit = [&](int32_t b, double mag) {
             const double4 xvb = ldg4(A.XV + b);
             double xb[3], vb[3], rel[D], g[D];
             xget<D>(xvb, xb);
             vget(vldg(V + b), vb);
 #pragma unroll
             for (int q = 0; q < D; ++q) rel[q] = xb[q] - xa[q];
-            grad_w<D>(rel, A.ks, g);
+            if (MTSPH_POR_STRESS_MAG) grad_w_mag<D>(rel, A.ks, mag, g);
+            else grad_w<D>(rel, A.ks, g);
             const double volb = volof<D>(xvb);
 #pragma unroll
             for (int r = 0; r < D; ++r) {
@@ -505,7 +518,8 @@ __global__ void __launch_bounds__(256) k_por_stress(PorousArgs A) {
                 for (int cc = 0; cc < D; ++cc) acc[r * D + cc] += dv * g[cc];
             }
         };
-        por_walk<false>(A, i, sub, visit);
+        if (MTSPH_POR_STRESS_MAG) por_walk_mag<false>(A, i, sub, visit);
+        else por_walk<false>(A, i, sub, [&](int32_t b) { visit(b, 0.0); });
     }
     group_sum<kPorLanes>(acc);
     if (act && sub == 0 && !(A.flags[i] & PF_GHOST)) {  // F += dt (acc B)
@@ -521,7 +535,7 @@ __global__ void __launch_bounds__(256) k_por_stress(PorousArgs A) {
 
 
 template <int D>
-__global__ void __launch_bounds__(256) k_por_accel(PorousArgs A) {
+__global__ void __launch_bounds__(256, 3) k_por_accel(PorousArgs A) {
     using V_t = typename VT<D>::T;
     __shared__ double sh[32];
     const Ctrl *c = A.ctrl;

@@ -38,7 +38,7 @@ struct mtsph_porous {
         A.mass_l = mass_l.p; A.sat = sat.p; A.pres = pres.p; A.J = J.p; A.rho_lf = rho_lf.p;
         A.mix = mix.p; A.inv_mix = inv_mix.p; A.volc = volc.p; A.coeff = coeff.p; A.amap = amap.p;
         A.mrate = mrate.p; A.T = T.p; A.G = G.p; A.rm = rm.p; A.rf = rf.p; A.B = nb.B.p; A.flags = flags.p; A.indptr = nb.indptr.p;
-        A.csr = nb.csr.p; A.cptr = nb.cptr.p; A.csr16 = nb.csr16.p; A.perm = nb.perm.p; A.part = part.p; A.nblk = nblk;
+        A.csr = nb.csr.p; A.cptr = nb.cptr.p; A.csr16 = nb.csr16.p; A.mag16 = nb.mag16.p; A.perm = nb.perm.p; A.part = part.p; A.nblk = nblk;
         A.ctrl = ctrl.p; A.ks = nb.ks; A.m = m;
         return A;
     }
@@ -135,7 +135,7 @@ extern "C" mtsph_status mtsph_porous_create(const mtsph_porous_desc *dsc, mtsph_
     } else {
         build_nbh(P->nb, n, d, dsc->pos, dsc->vol, dsc->h_axes, dsc->sweep, P->s);
     }
-    build_chunked(P->nb, kPorLanes, P->s, true);
+    build_chunked(P->nb, kPorLanes, P->s, true, true);
     if (dsc->sweep == 3) build_tiled_auto(P->nb, P->tiled, P->s, dsc->tile);
     std::vector<int64_t> perm(n);
     P->nb.perm.download(perm.data(), n, P->s);

@@ -251,8 +251,7 @@ struct SolidArgs {
     const int32_t *csr;
     const int64_t *cptr;     // chunked index table (gather_csr.cuh): chunk offsets, or null
     const int32_t *csr16;
-    int *queue;              // persistent gathers: per-SM block counters (gather_csr.cuh claim_block), or null
-    int nq, qchunk;
+    const double *mag16;     // per entry of csr16: kernel-gradient magnitude factor, or null
     const int64_t *perm;
     const double *Lacc;  // window gathers: sum_b V_b (v_b-v_a) (x) gradW [d*d][n] (F updated in k_solid_rmap)
     double *part;    // [3][nblk]: ek, amax2, vmax2
