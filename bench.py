@@ -157,11 +157,15 @@ def algorithmic_bytes(d, nnz_pp, pairs_pp, groups_pp, sweep="tiled", w=8):
     else:
         # v r/w + X|vol + 1/m, per pair and pass: two int32 ids + group pointer
         sweep_b = 2 * vec + xv + w + 2 * (8 * pairs_pp + 8 * groups_pp)
+    # fp64: the dF/dt gather streams the stored kernel-gradient magnitude
+    # factor of every table entry (8 B; the north star's precomputed kernel
+    # gradients in their smallest form) instead of recomputing it
+    stored_grad = 8 * nnz_pp if w == 8 else 0.0
     return {
         # v r/w, a, x (displacement in fp32) r/w, flags
         "kick_drift": 2 * vec + vec + 2 * vec + 1,
-        # X|V0, v, csr, B, F r/w, C_p^-1 r/w, alpha r/w, T write
-        "stress": xv + vec + 4 * nnz_pp + ten + 2 * ten + 2 * ten + 2 * w + ten,
+        # X|V0, v, csr (+ stored gradient magnitudes), B, F r/w, C_p^-1 r/w, alpha r/w, T write
+        "stress": xv + vec + 4 * nnz_pp + stored_grad + ten + 2 * ten + 2 * ten + 2 * w + ten,
         # X|V0, T, csr, rho0, flags, mass, v r/w, a write, static sum V gradW
         "accel": xv + ten + 4 * nnz_pp + w + 1 + w + 2 * vec + vec + vec,
         "sweep": sweep_b,
@@ -333,8 +337,11 @@ def run_ours(args):
         gbs = model[name] * n / per_step_s / 1e9 if per_step_s > 0 else 0.0
         kernels[name] = {"ms_per_step": tms / args.steps, "share": tms / ms if ms else 0.0,
                          "bytes_per_particle": model[name], "achieved_gbs": gbs}
+    kernels["stress"]["of_which_stored_gradient_magnitudes"] = 8 * sz["nnz"] / n
     top = max(classes, key=classes.get)
     k_top = kernels[top]
+    step_bytes = sum(model[k] for k in classes)
+    step_gbs = step_bytes * n / (ms / 1e3 / args.steps) / 1e9
     tr, tsrc = profile_json("traffic")
     traffic = tr.get(top)
     lim, lsrc = profile_json("limiters")
@@ -364,6 +371,8 @@ def run_ours(args):
                      "peak": peak, "unit": "GB/s",
                      "frac": k_top["achieved_gbs"] / peak, "traffic": traffic,
                      "traffic_source": tsrc,
+                     "whole_step": {"bytes_per_particle": step_bytes, "achieved": step_gbs,
+                                    "frac": step_gbs / peak},
                      "limiter": (lim.get(top) or {}).get("limiter"),
                      "limiter_pct_of_peak": {k: v for k, v in (lim.get(top) or {}).items()
                                              if k not in ("ms", "limiter")},
