@@ -74,6 +74,44 @@ def test_necking_trajectory_gather_modes(gold_traj, prefix, lanes, monkeypatch):
     _check_trajectory(gold_traj, prefix)
 
 
+@pytest.mark.parametrize("knob", ["MTSPH_GATHER_CHUNKED", "MTSPH_GATHER_PACK", "MTSPH_GATHER_MAG"])
+@pytest.mark.parametrize("prefix", ["n2_", "n3_"])
+def test_necking_trajectory_index_table_modes(gold_traj, prefix, knob, monkeypatch):
+    """The chunked index table of the row-parallel gathers (gather_csr.cuh)
+    with each of its parts switched off in turn -- the plain CSR walk, sorted
+    instead of bank-balanced windows, recomputed instead of stored gradient
+    magnitudes -- holds the same 100-step bar (the default, everything on,
+    is covered above)."""
+    monkeypatch.delenv("MTSPH_GATHER_LANES", raising=False)
+    monkeypatch.setenv(knob, "0")
+    _check_trajectory(gold_traj, prefix)
+
+
+def test_stored_gradient_magnitudes_are_bit_identical(gold_traj, monkeypatch):
+    """The stored kernel-gradient magnitudes come from the function the
+    gather would call (grad_mag), so the dF/dt gather that reads them gives
+    bitwise the state of the one that recomputes them."""
+    dev = _device()
+    pos, vol, con, side, mid, dp = _neck_inputs(gold_traj, "n3_")
+
+    def run():
+        s = dev.DeviceSolid(pos, vol, 7850.0, con, side, mid, [1.35 * dp] * 3,
+                            80.1938e9, 164.21e9, plastic=True, hardening_law=0,
+                            hard=(450e6, 715e6, 16.93, 129.24e6), sweep="tiled")
+        s.set_ramp(1.2e-4 / 4, 20, 20)
+        for _ in range(40):
+            s.relax_step(s.stable_dt(0.6), 1e4)
+        return {f: s.get(f).copy() for f in ("pos", "vel", "F", "alpha")}
+
+    monkeypatch.delenv("MTSPH_GATHER_LANES", raising=False)
+    monkeypatch.delenv("MTSPH_GATHER_MAG", raising=False)
+    a = run()
+    monkeypatch.setenv("MTSPH_GATHER_MAG", "0")
+    b = run()
+    for f in a:
+        np.testing.assert_array_equal(a[f], b[f], err_msg=f)
+
+
 def test_necking_trajectory_window_gathers(gold_traj, monkeypatch):
     """The 3D bar with the opt-in shared-memory cell-window gathers
     (window.cuh): same 100-step parity as the CSR gathers."""
