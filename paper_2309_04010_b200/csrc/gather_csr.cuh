@@ -254,22 +254,17 @@ template <int G, int K> __device__ __forceinline__ void group_sum(double (&v)[K]
 }
 
 // dF/dt gather + F update (the split path: the return map runs in k_solid_rmap)
-// WIDE: the block's G passes of 256 / G particles run side by side in one CTA
-// of G x 256 threads (one CTA per SM) instead of one after the other in a
-// 256-thread CTA, so the 256 consecutive particles of the Morton order that
-// an SM works on at a time are one compact neighbourhood sharing its L1.
-template <int D, int G, bool C16 = false, bool MAG = false, bool WIDE = false>
-__global__ void __launch_bounds__(WIDE ? G * 256 : 256, WIDE ? 1 : MTSPH_STRESS_CTAS) k_solid_stress_csr(SolidArgs A) {
+template <int D, int G, bool C16 = false, bool MAG = false>
+__global__ void __launch_bounds__(256, MTSPH_STRESS_CTAS) k_solid_stress_csr(SolidArgs A) {
     using V_t = typename VT<D>::T;
     const Ctrl *c = A.ctrl;
     if (c->done) return;
     const double dt = c->dt;
     const int64_t n = A.n;
-    const int tid = WIDE ? threadIdx.x & 255 : threadIdx.x;
-    const int sub = tid % G;
+    const int sub = threadIdx.x % G;
     const V_t *V = reinterpret_cast<const V_t *>(A.V);
-    for (int it = WIDE ? threadIdx.x >> 8 : 0; it < (WIDE ? (int)(threadIdx.x >> 8) + 1 : G); ++it) {
-        const int64_t i = (int64_t)blockIdx.x * 256 + it * (256 / G) + tid / G;
+    for (int it = 0; it < G; ++it) {
+        const int64_t i = (int64_t)blockIdx.x * 256 + it * (256 / G) + threadIdx.x / G;
         const bool act = i < n && !(A.flags[i] & FL_GHOST);  // uniform over the G lanes
         double acc[D * D];
 #pragma unroll
@@ -321,19 +316,18 @@ __global__ void __launch_bounds__(WIDE ? G * 256 : 256, WIDE ? 1 : MTSPH_STRESS_
 }
 
 // a = 1/rho0 sum_b V_b (T_a + T_b) gradW, v += dt/2 a, E_k and |a|max partials
-template <int D, int G, bool C16 = false, bool MAG = false, bool WIDE = false>
-__global__ void __launch_bounds__(WIDE ? G * 256 : 256, WIDE ? 1 : MTSPH_ACCEL_CTAS) k_solid_accel_csr(SolidArgs A) {
+template <int D, int G, bool C16 = false, bool MAG = false>
+__global__ void __launch_bounds__(256, MTSPH_ACCEL_CTAS) k_solid_accel_csr(SolidArgs A) {
     using V_t = typename VT<D>::T;
     __shared__ double sh[32];
     const Ctrl *c = A.ctrl;
     if (c->done) return;  // uniform across the grid
     const double dt = c->dt;
     const int64_t n = A.n;
-    const int tid = WIDE ? threadIdx.x & 255 : threadIdx.x;
-    const int sub = tid % G;
+    const int sub = threadIdx.x % G;
     double ek = 0.0, a2m = 0.0;
-    for (int it = WIDE ? threadIdx.x >> 8 : 0; it < (WIDE ? (int)(threadIdx.x >> 8) + 1 : G); ++it) {
-        const int64_t i = (int64_t)blockIdx.x * 256 + it * (256 / G) + tid / G;
+    for (int it = 0; it < G; ++it) {
+        const int64_t i = (int64_t)blockIdx.x * 256 + it * (256 / G) + threadIdx.x / G;
         const bool act = i < n && !(A.flags[i] & FL_GHOST);
         // sum_b V_b (T_a + T_b) gradW = sum_b T~_b gradW + T_a G_a, with
         // T~_b = V_b T_b from the divergence record (three 256-bit loads per
@@ -360,7 +354,7 @@ __global__ void __launch_bounds__(WIDE ? G * 256 : 256, WIDE ? 1 : MTSPH_ACCEL_C
             if constexpr (C16 && MAG) {
                 walk_chunks_mag<G, true>(A.cptr, A.csr16, A.mag16, i, sub, visit2);
             } else if constexpr (C16) {
-                walk_chunks<G, !WIDE>(A.cptr, A.csr16, i, sub, visit);
+                walk_chunks<G, true>(A.cptr, A.csr16, i, sub, visit);
             } else {
                 const int64_t k1 = A.indptr[i + 1];
                 for (int64_t k = A.indptr[i] + sub; k < k1; k += G) visit(__ldg(A.csr + k));
@@ -398,8 +392,8 @@ __global__ void __launch_bounds__(WIDE ? G * 256 : 256, WIDE ? 1 : MTSPH_ACCEL_C
             }
         }
     }
-    const double se = block_sum<WIDE ? G * 256 : 256>(ek, sh);
-    const double sa = block_max<WIDE ? G * 256 : 256>(a2m, sh);
+    const double se = block_sum<256>(ek, sh);
+    const double sa = block_max<256>(a2m, sh);
     if (threadIdx.x == 0) {
         A.part[blockIdx.x] = se;
         A.part[A.nblk + blockIdx.x] = sa;

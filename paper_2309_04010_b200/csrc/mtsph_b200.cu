@@ -235,7 +235,6 @@ struct mtsph_solid {
     // Measured (10M, 3D): SELL 7.4 + 10.0 ms, G=2 5.8 + 7.4, G=4 5.8 + 7.3,
     // G=8 6.9 + 8.7 (stress + accel); MTSPH_GATHER_LANES overrides
     int gather_g = 4;
-    int wide = 0;  // MTSPH_GATHER_WIDE: bit 0 the dF/dt gather, bit 1 the divergence gather in 1024-thread CTAs
     // 3D fp64 opt-in (MTSPH_GATHER_WINDOW=1): shared-memory cell-window
     // gathers (window.cuh; measured slower than the CSR gathers)
     WinSched win;
@@ -335,8 +334,7 @@ template <int D> static int launch_stress_gather(mtsph_solid *S, const SolidArgs
         return 1;
     }
     const bool c16 = S->nb.chunk_g == S->gather_g && S->gather_g > 0;
-    if (S->gather_g == 4 && c16 && A.mag16 && S->wide) k_solid_stress_csr<D, 4, true, true, true><<<nb, 1024, 0, s>>>(A);
-    else if (S->gather_g == 4 && c16 && A.mag16) k_solid_stress_csr<D, 4, true, true><<<nb, 256, 0, s>>>(A);
+    if (S->gather_g == 4 && c16 && A.mag16) k_solid_stress_csr<D, 4, true, true><<<nb, 256, 0, s>>>(A);
     else if (S->gather_g == 4 && c16) k_solid_stress_csr<D, 4, true><<<nb, 256, 0, s>>>(A);
     else if (S->gather_g == 2 && c16) k_solid_stress_csr<D, 2, true><<<nb, 256, 0, s>>>(A);
     else if (S->gather_g == 4) k_solid_stress_csr<D, 4><<<nb, 256, 0, s>>>(A);
@@ -361,8 +359,7 @@ template <int D> static int launch_accel_gather(mtsph_solid *S, const SolidArgs 
     }
     const bool c16 = S->nb.chunk_g == S->gather_g && S->gather_g > 0;
     // (the stored gradient magnitudes cost the divergence gather registers: 5.27 -> 5.45 ms)
-    if (S->gather_g == 4 && c16 && (S->wide & 2)) k_solid_accel_csr<D, 4, true, false, true><<<nb, 1024, 0, s>>>(A);
-    else if (S->gather_g == 4 && c16) k_solid_accel_csr<D, 4, true><<<nb, 256, 0, s>>>(A);
+    if (S->gather_g == 4 && c16) k_solid_accel_csr<D, 4, true><<<nb, 256, 0, s>>>(A);
     else if (S->gather_g == 2 && c16) k_solid_accel_csr<D, 2, true><<<nb, 256, 0, s>>>(A);
     else if (S->gather_g == 4) k_solid_accel_csr<D, 4><<<nb, 256, 0, s>>>(A);
     else if (S->gather_g == 8) k_solid_accel_csr<D, 8><<<nb, 256, 0, s>>>(A);
@@ -566,7 +563,6 @@ extern "C" mtsph_status mtsph_solid_create(const mtsph_solid_desc *dsc, mtsph_so
     // measured 2D 10M fp64 4.99 -> 4.94 ms/step, fp32 3.14 -> 2.95
     S->gather_g = d == 2 ? 2 : 4;
     S->gather_g32 = d == 2 ? 2 : 4;
-    if (const char *e = std::getenv("MTSPH_GATHER_WIDE")) S->wide = std::atoi(e) & 3;
     if (const char *e = std::getenv("MTSPH_GATHER_LANES")) {
         const int g = std::atoi(e);
         if (g != 0 && g != 2 && g != 4 && g != 8) throw Error(MTSPH_ERR_ARG, "MTSPH_GATHER_LANES: 0, 2, 4 or 8");
