@@ -27,6 +27,8 @@ the per-phase reductions still return to the host.
 from __future__ import annotations
 
 import math
+import os
+import time
 
 import numpy as np
 
@@ -246,7 +248,57 @@ def stable_dt(h, sound, cfl, vmax2, amax2):
     return cfl * dt
 
 
-class DecomposedSolid:
+class _GraphedStep:
+    """CUDA-graph capture of one rank's inner step for the device-controlled
+    loops: the phases (kernels on the problem's stream), the pack / unpack
+    kernels, the grouped NCCL send/recv of every halo exchange and the NCCL
+    all-gather + control kernel, recorded once and replayed per step.  Every
+    kernel reads dt, the ramp counter and the done flag from the device control
+    block, so a replay is the same step the eager enqueue would issue, without
+    the ~40 phase calls and ~35 exchange calls from Python per step.  Only for
+    TorchGroup on the device (NCCL); a capture that fails -- a torch / NCCL
+    build that cannot capture the exchange -- falls back to the eager enqueue.
+    MTSPH_DECOMP_GRAPH=0 disables it."""
+
+    _graph = None          # None: not tried, False: unavailable
+    graph_replays = 0      # steps issued by replay (their launches are not in dev.launches())
+    graph_launches = 0     # library launches of one captured step
+    issue_s = 0.0          # host seconds spent issuing steps in relax_device
+    issue_steps = 0
+
+    def _issue_step(self):
+        import os
+        g = self.group
+        if self._graph is None:
+            self._graph = False
+            if getattr(g, "on_device", False) and os.environ.get("MTSPH_DECOMP_GRAPH", "1") != "0":
+                torch = g.torch
+                dev = self.devices[0]
+                # first step eagerly: lazily created exchange / control buffers
+                # and NCCL's own first-use setup must not happen inside a capture
+                self._step_async()
+                try:
+                    graph = torch.cuda.CUDAGraph()
+                    l0 = dev.launches()
+                    with torch.cuda.graph(graph, stream=g.stream, capture_error_mode="thread_local"):
+                        self._step_async()
+                    self.graph_launches = dev.launches() - l0
+                    self._graph = graph
+                except Exception as e:  # noqa: BLE001 -- any capture failure means "no graph"
+                    import warnings
+                    warnings.warn(f"decomposed step: CUDA graph capture unavailable ({type(e).__name__}: {e}); "
+                                  "enqueueing the phases eagerly")
+                    torch.cuda.synchronize()
+                return
+        if self._graph:
+            with g.torch.cuda.stream(g.stream):
+                self._graph.replay()
+            self.graph_replays += 1
+        else:
+            self._step_async()
+
+
+class DecomposedSolid(_GraphedStep):
     """A necking-type solid split into x-slabs (tiled damping sweep)."""
 
     def __init__(self, lat, elastic, hardening, nranks, ranks=None, group="local",
@@ -353,9 +405,12 @@ class DecomposedSolid:
         for dev in self.devices:
             dev.phase_async("accel")
         g.refresh("vel")
-        if self.nranks == 1:
+        if self.nranks == 1 and os.environ.get("MTSPH_DECOMP_COLOURS", "0") != "1":
             # one rank, no ghosts: the single-domain persistent dataflow
-            # sweep (one launch, same tasks in the same order per particle)
+            # sweep (one launch, same tasks in the same order per particle).
+            # MTSPH_DECOMP_COLOURS=1 keeps the multi-rank sequence (a launch,
+            # push-back and refresh per colour and pass) for measuring its
+            # issue cost on one GPU.
             self.devices[0].phase_async("sweep_all")
         else:
             nc = self.ncolours
@@ -386,8 +441,11 @@ class DecomposedSolid:
             dev.phase_async("amax")
         self.group.control(0)
         while True:
+            t_issue = time.perf_counter()
             for _ in range(max(int(check_every), 1)):
-                self._step_async()
+                self._issue_step()
+            self.issue_s += time.perf_counter() - t_issue   # host time to issue the steps (no sync inside)
+            self.issue_steps += max(int(check_every), 1)
             states = [dev.loop_state() for dev in self.devices]
             if all(done for done, _ in states):
                 break
@@ -408,7 +466,7 @@ class DecomposedSolid:
         return out
 
 
-class DecomposedPorous:
+class DecomposedPorous(_GraphedStep):
     """A porous membrane (PorousProblem) split into x-slabs: the outer
     diffusion step and the inner relaxation as device phases separated by
     ghost exchanges, with the host-side control of DecomposedSolid.relax.
@@ -558,8 +616,11 @@ class DecomposedPorous:
             dev.phase_async("amax")
         self.group.control(0)
         while True:
+            t_issue = time.perf_counter()
             for _ in range(max(int(check_every), 1)):
-                self._step_async()
+                self._issue_step()
+            self.issue_s += time.perf_counter() - t_issue   # host time to issue the steps (no sync inside)
+            self.issue_steps += max(int(check_every), 1)
             states = [dev.loop_state() for dev in self.devices]
             if all(done for done, _ in states):
                 break

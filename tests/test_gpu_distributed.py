@@ -138,6 +138,10 @@ def test_nccl_group_single_rank_device_loop():
         dec.advance_slow()
         n, ek, cap, _ = dec.relax_device(eta, cfl, 0.0, 1.0, fixed_steps=steps, check_every=5)
         assert n == steps
+        # the step was captured in a CUDA graph (phases + NCCL all-gather +
+        # control kernel) after its first eager issue, and replayed
+        assert dec._graph, "graph capture of the decomposed step failed"
+        assert dec.graph_replays == steps - 1 and dec.graph_launches > 0
         dev = dec.devices[0]
         for f, w in want.items():
             got = dev.get(f)
