@@ -224,6 +224,13 @@ __device__ __forceinline__ void walk_chunks_any(const int64_t *__restrict__ cptr
     };
     const int nfull = MODE == 2 ? nch - 1 : nch;
     for (int c = 0; c < nfull; ++c, w += G, mw += G) {
+        // the table words are a pure stream from DRAM, and a chunk's first
+        // visit needs its word at once: hint them into L1 two chunks ahead
+        // (stress 4.78 -> 4.68 ms, accel 5.27 -> 5.22; holding the next word
+        // in registers instead spills, and prefetching the records the next
+        // word names costs the data stage as much as loading them: 7.3 ms)
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(w + 2 * G));
+        if (MAG) asm volatile("prefetch.global.L1 [%0];" ::"l"(mw + 2 * G));
         const int4 q = __ldg(w);
         const double4 m = MAG ? ldg4(mw) : make_double4(0.0, 0.0, 0.0, 0.0);
         if (MODE == 2 || (MODE == 1 && q.w >= 0)) full(q, m);
