@@ -92,14 +92,18 @@ def test_config1_membrane2d_run_matches_oracle():
 
 
 def _porous_run_vs_oracle(raw, n_outer=3, inner=25):
+    """inner: a fixed inner-step count per outer step, or None for the
+    reference driver's own protocol (exit on the E_k criterion, capped at
+    10 ceil(dt_outer / dt) inner steps, stepping.py:158)."""
     from oracle import oracle as O
     from oracle.problems import PorousOracle, run_outer_inner as oracle_run
     from paper_2309_04010_b200 import scenarios
     from paper_2309_04010_b200.config import resolve
     from paper_2309_04010_b200.stepping import run_outer_inner
     base = resolve(raw).params
-    raw = dict(raw, n_outer=n_outer, t_total=n_outer * base["t_total"] / base["n_outer"],
-               max_inner=inner, min_inner=inner)
+    raw = dict(raw, n_outer=n_outer, t_total=n_outer * base["t_total"] / base["n_outer"])
+    if inner is not None:
+        raw.update(max_inner=inner, min_inner=inner)
     p = resolve(raw).params
     problem, policy = scenarios.build(p, sweep="serial")
     obs, counters = run_outer_inner(problem, policy)
@@ -111,9 +115,28 @@ def _porous_run_vs_oracle(raw, n_outer=3, inner=25):
                        p["evaporation_rate"], lat.column_id, len(lat.column_x),
                        lat.center_column, lat.deflection_axis)
     rows = oracle_run(ref, policy.dt_outer, n_outer, policy.eta, policy.energy_criterion,
-                      cfl=policy.cfl, max_inner=inner, min_inner=inner)
+                      cfl=policy.cfl, max_inner=inner or 0, min_inner=inner or 1)
     np.testing.assert_array_equal(obs.n_inner, [r["n_inner"] for r in rows])
     return problem, ref, lat
+
+
+@pytest.mark.parametrize("raw,n", [({"scenario": "membrane_2d"}, 8080),
+                                   ({"scenario": "membrane_3d", "length": 1.0, "breadth": 0.5}, 6292)])
+def test_membrane_configs_reference_protocol(raw, n):
+    """BASELINE configs[1] (the whole 2D strip) and the configs[3] plate piece
+    through the reference driver's own protocol -- every outer diffusion step
+    followed by an inner loop that runs to the kinetic-energy criterion or the
+    reference's cap of 10 ceil(dt_outer / dt) steps (90 per outer step on the
+    strip), not a fixed short count: the same inner-step counts as the oracle,
+    fluid mass and saturation <= 1e-10, displacement <= 1e-8 after four outer
+    steps."""
+    problem, ref, lat = _porous_run_vs_oracle(raw, n_outer=4, inner=None)
+    assert lat.n == n
+    st = problem.state
+    assert np.max(ref.fluid_mass) > 0
+    assert rel_err(st.fluid_mass, ref.fluid_mass) < 1e-10
+    assert rel_err(st.saturation, ref.saturation) < 1e-10
+    assert rel_err(st.pos - st.ref_pos, ref.pos - lat.pos) < 1e-8
 
 
 def test_config3_membrane3d_plate_run_matches_oracle():
