@@ -22,6 +22,10 @@
 #ifndef MTSPH_STRESS_CTAS
 #define MTSPH_STRESS_CTAS 4
 #endif
+// dF/dt gather: a test per visit (0) or unconditional visits per full word (1)
+#ifndef MTSPH_STRESS_FAST
+#define MTSPH_STRESS_FAST 0
+#endif
 #ifndef MTSPH_ACCEL_CTAS
 #define MTSPH_ACCEL_CTAS 3
 #endif
@@ -299,9 +303,9 @@ __global__ void __launch_bounds__(256, MTSPH_STRESS_CTAS) k_solid_stress_csr(Sol
             };
             auto visit = [&](int32_t b) { visit2(b, 0.0); };
             if constexpr (C16 && MAG) {
-                walk_chunks_mag<G, false>(A.cptr, A.csr16, A.mag16, i, sub, visit2);
+                walk_chunks_mag<G, MTSPH_STRESS_FAST != 0>(A.cptr, A.csr16, A.mag16, i, sub, visit2);
             } else if constexpr (C16) {
-                walk_chunks<G, false>(A.cptr, A.csr16, i, sub, visit);
+                walk_chunks<G, MTSPH_STRESS_FAST != 0>(A.cptr, A.csr16, i, sub, visit);
             } else {
                 const int64_t k1 = A.indptr[i + 1];
                 for (int64_t k = A.indptr[i] + sub; k < k1; k += G) visit(__ldg(A.csr + k));
