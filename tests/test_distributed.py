@@ -190,3 +190,36 @@ def test_single_rank_plans_equal_full_plans(nranks):
             for k in da:
                 assert np.array_equal(da[k], db[k]), (r, name, k)
         assert np.array_equal(grid, g2) and np.array_equal(owner, o2)
+
+
+def test_graphed_step_falls_back_to_eager_issue_off_device(monkeypatch):
+    """distributed._GraphedStep: without a device-resident (NCCL) group the
+    decomposed step is never captured -- every issue is the eager enqueue --
+    and MTSPH_DECOMP_GRAPH=0 gives the same on any group."""
+    from paper_2309_04010_b200.distributed import _GraphedStep
+
+    class Group:
+        on_device = False
+
+    class Loop(_GraphedStep):
+        def __init__(self, group):
+            self.group = group
+            self.devices = []
+            self.steps = 0
+
+        def _step_async(self):
+            self.steps += 1
+
+    loop = Loop(Group())
+    for _ in range(5):
+        loop._issue_step()
+    assert loop.steps == 5 and loop._graph is False and loop.graph_replays == 0
+
+    class DeviceGroup:
+        on_device = True
+
+    monkeypatch.setenv("MTSPH_DECOMP_GRAPH", "0")
+    loop = Loop(DeviceGroup())
+    for _ in range(3):
+        loop._issue_step()
+    assert loop.steps == 3 and loop._graph is False
