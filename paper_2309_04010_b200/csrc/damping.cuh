@@ -665,10 +665,16 @@ template <int D> void build_serial_entries(NbhDev &nb, const SweepArgs &A, cudaS
             MT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
             MT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sweep_serial_grid<D>,
                                                                   kSerialGridThreads, 0));
-            // every CTA must be resident (grid barrier); enough CTAs for a
-            // level's groups, no more (the barrier's cost grows with the grid)
-            const int64_t want = (int64_t)std::ceil(per_level / kSerialGridThreads);
-            nb.serial_grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * std::max(per, 1)));
+            // every CTA must be resident (grid barrier).  Two threads per group
+            // of an average level, so that the fuller levels still give a
+            // thread one entry (entries of one thread are dependent L2 round
+            // trips), at most one CTA per SM (the barrier's cost grows with
+            // the grid).  Measured on a 2 M slice (6469 levels): 24 CTAs
+            // 67.3 ms per sweep, 48 52.0, 96 43.4, 148 43.3, 296 48.4.
+            const int64_t want = (int64_t)std::ceil(2.0 * per_level / kSerialGridThreads);
+            nb.serial_grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, std::min<int64_t>(sms, (int64_t)sms * std::max(per, 1))));
+            if (const char *ce = getenv("MTSPH_SERIAL_GRID_CTAS"))  // tuning override (still all co-resident)
+                nb.serial_grid = (int)std::max<int64_t>(1, std::min<int64_t>(atoi(ce), (int64_t)sms * std::max(per, 1)));
             nb.serial_bar.alloc(1);
         }
         if (!nb.serial_grid) return;
