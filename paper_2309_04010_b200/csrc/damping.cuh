@@ -528,11 +528,18 @@ __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long
 // barrier k completes when the counter reaches (k + 1) * gridDim.x.  One
 // release-add per CTA and a spin on the same word (no separate reset and
 // release round trips).
+#ifndef MTSPH_GRID_BARRIER_FENCE
+#define MTSPH_GRID_BARRIER_FENCE 0
+#endif
 __device__ __forceinline__ void grid_barrier(unsigned long long *cnt, unsigned long long &target) {
     __syncthreads();
     target += gridDim.x;
     if (threadIdx.x == 0) {
+#if MTSPH_GRID_BARRIER_FENCE
         __threadfence();
+#endif
+        // release at gpu scope is cumulative: it orders the CTA's writes that
+        // the barrier above made happen-before this thread
         asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(cnt) : "memory");
         while (ld_acquire_u64(cnt) < target) {
         }
