@@ -70,6 +70,26 @@ def profile_json(stem):
         return {}, None
 
 
+def on_chip_roofline(on_chip, kernels, n, sms=148, sm_mhz=1965.0):
+    """The neighbour kernels against the L1 / shared-memory data stage
+    (128 B per clock per SM, the unit ncu shows them bound by): bytes it must
+    move per particle (gathered records, table words, halo records) over the
+    class's time, against sms x 128 B x the SM clock."""
+    peak = sms * 128 * sm_mhz * 1e6 / 1e9   # GB/s
+    out = {"peak": peak, "unit": "GB/s", "per_class": {}}
+    tot_b, tot_ms = 0.0, 0.0
+    for name, b in on_chip.items():
+        ms = kernels[name]["ms_per_step"]
+        gbs = b * n / (ms / 1e3) / 1e9 if ms > 0 else 0.0
+        out["per_class"][name] = {"bytes_per_particle": b, "achieved": gbs, "frac": gbs / peak}
+        tot_b += b
+        tot_ms += ms
+    out["neighbour_kernels"] = {"bytes_per_particle": tot_b,
+                                "achieved": tot_b * n / (tot_ms / 1e3) / 1e9 if tot_ms > 0 else 0.0}
+    out["neighbour_kernels"]["frac"] = out["neighbour_kernels"]["achieved"] / peak
+    return out
+
+
 def load_peaks():
     try:
         with open(PEAKS_PATH) as fh:
@@ -338,6 +358,14 @@ def run_ours(args):
         kernels[name] = {"ms_per_step": tms / args.steps, "share": tms / ms if ms else 0.0,
                          "bytes_per_particle": model[name], "achieved_gbs": gbs}
     kernels["stress"]["of_which_stored_gradient_magnitudes"] = 8 * sz["nnz"] / n
+    # the neighbour kernels' real bound: the SM's L1 / shared-memory data
+    # stage (128 B per clock per SM).  Bytes it must move per particle: the
+    # gathered records (64 B dF/dt, 96 B divergence) and table words per
+    # neighbour visit; per pair update of the sweep (two passes) the 12 B
+    # ring entry and both halo records read and written (4 x 32 B)
+    nnz_pp, pairs_pp = sz["nnz"] / n, sz["npairs"] / n
+    on_chip = {"stress": (64 + 4 + 8) * nnz_pp, "accel": (96 + 4) * nnz_pp,
+               "sweep": 2 * (12 + 4 * 32) * pairs_pp}
     top = max(classes, key=classes.get)
     k_top = kernels[top]
     step_bytes = sum(model[k] for k in classes)
@@ -373,6 +401,7 @@ def run_ours(args):
                      "traffic_source": tsrc,
                      "whole_step": {"bytes_per_particle": step_bytes, "achieved": step_gbs,
                                     "frac": step_gbs / peak},
+                     "on_chip_data_stage": on_chip_roofline(on_chip, kernels, n),
                      "limiter": (lim.get(top) or {}).get("limiter"),
                      "limiter_pct_of_peak": {k: v for k, v in (lim.get(top) or {}).items()
                                              if k not in ("ms", "limiter")},

@@ -24,6 +24,18 @@ def test_algorithmic_bytes_fp64_and_fp32():
     assert abs((m64["accel"] - m32["accel"]) - (4 * 4 + 4 * 9 + 4 + 4 + 4 * 3 * 4)) < 1e-9
 
 
+def test_on_chip_roofline_accounts_per_class_and_total():
+    import bench
+    k = {"stress": {"ms_per_step": 4.0}, "accel": {"ms_per_step": 5.0}, "sweep": {"ms_per_step": 6.0}}
+    oc = {"stress": 6000.0, "accel": 8000.0, "sweep": 11000.0}
+    r = bench.on_chip_roofline(oc, k, 10_000_000)
+    assert abs(r["peak"] - 148 * 128 * 1.965) < 1e-6          # GB/s
+    assert abs(r["per_class"]["accel"]["achieved"] - 8000.0 * 1e7 / 5e-3 / 1e9) < 1e-6
+    tot = r["neighbour_kernels"]
+    assert abs(tot["achieved"] - 25000.0 * 1e7 / 15e-3 / 1e9) < 1e-6
+    assert 0 < tot["frac"] < 1
+
+
 def test_outer_bytes_counts_index_per_gather_pass():
     import bench
     a, b = bench.outer_bytes(3, 70.0), bench.outer_bytes(3, 71.0)
