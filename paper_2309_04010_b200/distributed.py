@@ -258,7 +258,9 @@ class _GraphedStep:
     the ~40 phase calls and ~35 exchange calls from Python per step.  Only for
     TorchGroup on the device (NCCL); a capture that fails -- a torch / NCCL
     build that cannot capture the exchange -- falls back to the eager enqueue.
-    MTSPH_DECOMP_GRAPH=0 disables it."""
+    MTSPH_DECOMP_GRAPH=1 / 0 forces it on / off; unset, it is on for a single
+    rank and off for several (the graph with point-to-point NCCL nodes has not
+    run on more than one GPU yet)."""
 
     _graph = None          # None: not tried, False: unavailable
     graph_replays = 0      # steps issued by replay (their launches are not in dev.launches())
@@ -271,7 +273,13 @@ class _GraphedStep:
         g = self.group
         if self._graph is None:
             self._graph = False
-            if getattr(g, "on_device", False) and os.environ.get("MTSPH_DECOMP_GRAPH", "1") != "0":
+            # default: on for a single rank (exercised on hardware), and for
+            # several ranks only on request -- the graph with point-to-point
+            # NCCL nodes has never run on more than one GPU in this repository
+            want = os.environ.get("MTSPH_DECOMP_GRAPH")
+            if want is None:
+                want = "1" if getattr(self, "nranks", 1) == 1 else "0"
+            if getattr(g, "on_device", False) and want != "0":
                 torch = g.torch
                 dev = self.devices[0]
                 # first step eagerly: lazily created exchange / control buffers
@@ -481,6 +489,7 @@ class DecomposedPorous(_GraphedStep):
     def __init__(self, lat, model, contact_time, evaporation_rate, nranks, ranks=None,
                  group="local", dist=None, tensor_device="cpu"):
         from .device import DevicePorous
+        self.nranks = int(nranks)
         ranks = list(range(nranks)) if ranks is None else list(ranks)
         self.plans, self.grid, self.owner = make_plans(
             lat.pos, lat.h_axes, nranks, ranks=None if group in ("local", "local_device") else ranks)
