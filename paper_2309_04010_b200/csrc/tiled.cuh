@@ -193,15 +193,22 @@ __device__ __forceinline__ void sweep_task(const TiledArgsT<R> &T, int64_t task,
     R *bd = reinterpret_cast<R *>(hal.end(H));                                 // ring of coefficients
     uint32_t *bp = reinterpret_cast<uint32_t *>(bd + kSweepStages * T.maxsub);  // ring of pairs
     int *ssub = reinterpret_cast<int *>(bp + kSweepStages * T.maxsub);         // sub-colour bounds
-    for (int k = threadIdx.x; k <= nsub; k += blockDim.x) ssub[k] = T.sub[s0 + k];
+    // one word per sub-colour: first pair (low 20 bits) | pair count << 20, so
+    // the loop reads one shared-memory word per warp and iteration, not two
+    // (a task holds < 2^20 pair slots, a sub-colour < 2^12)
+    for (int k = threadIdx.x; k < nsub; k += blockDim.x) {
+        const int a = T.sub[s0 + k], b = T.sub[s0 + k + 1];
+        ssub[k] = a | ((b - a) << 20);
+    }
     __syncthreads();
     // dir 1: sub-colours ascending, -1: descending.  (Merging the last
     // forward and first reverse colour into one launch was measured slower.)
     const int nq = nsub;
     auto sub_range = [&](int q, int &a, int &b) {
         const int s = dir > 0 ? q : nsub - 1 - q;
-        a = ssub[s];
-        b = ssub[s + 1];
+        const int w = ssub[s];
+        a = w & 0xfffff;
+        b = a + (int)((unsigned)w >> 20);
     };
     // the pair updates of sub-colour q from ring slot `slot`, npr lanes
     auto apply_sub = [&](int q, int slot, int npr) {
@@ -887,6 +894,9 @@ inline void build_tiled(const NbhDev &nb, int sh, TiledSched &t, cudaStream_t s)
         t.max_halo = std::max(t.max_halo, T.halo);
         t.max_ranges = std::max(t.max_ranges, (int)T.ranges.size());
         for (size_t k = 0; k + 1 < T.sub.size(); ++k) t.maxsub = std::max(t.maxsub, T.sub[k + 1] - T.sub[k]);
+        // the kernel packs a sub-colour's first pair (20 bits) and count (12 bits) into one word
+        if (T.pairs.size() >= (size_t(1) << 20) || t.maxsub >= (1 << 12))
+            throw Error(1, "tiled sweep: block too large for the packed sub-colour bounds");
         t.max_nsub = std::max(t.max_nsub, (int)T.sub.size() - 1);
         t.nsub_total += (int64_t)T.sub.size() - 1;
     }
