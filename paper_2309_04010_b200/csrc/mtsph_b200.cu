@@ -255,7 +255,8 @@ struct mtsph_solid {
     DBuf<unsigned char> V32;
     TiledArgsT<float> tiled_args32() {
         TiledArgsT<float> A{tiled.range_off.p, tiled.ranges.p, tiled.halo_n.p, tiled.pair_off.p, tiled.pairs.p,
-                            pd32.p, tiled.sub_off.p, tiled.sub.p, inv_m32.p, V32.p, tiled.maxsub};
+                            pd32.p, tiled.sub_off.p, tiled.sub.p, inv_m32.p, V32.p, tiled.maxsub,
+                            tiled.hid_off.p, tiled.hid.p};
         return A;
     }
     Solid32Args args32() {
@@ -280,7 +281,7 @@ struct mtsph_solid {
     }
     TiledArgs tiled_args() {
         TiledArgs A{tiled.range_off.p, tiled.ranges.p, tiled.halo_n.p, tiled.pair_off.p, tiled.pairs.p,
-                    tiled.pd.p, tiled.sub_off.p, tiled.sub.p, inv_m.p, V.p, tiled.maxsub};
+                    tiled.pd.p, tiled.sub_off.p, tiled.sub.p, inv_m.p, V.p, tiled.maxsub, tiled.hid_off.p, tiled.hid.p};
         return A;
     }
     ~mtsph_solid() {

@@ -70,7 +70,7 @@ template <int D> static int porous_step(mtsph_porous *P, int mode) {
     if (P->nb.sweep == 3) {
         TiledArgs T{P->tiled.range_off.p, P->tiled.ranges.p, P->tiled.halo_n.p, P->tiled.pair_off.p,
                     P->tiled.pairs.p, P->tiled.pd.p, P->tiled.sub_off.p, P->tiled.sub.p, P->inv_mix.p, P->V.p,
-                    P->tiled.maxsub};
+                    P->tiled.maxsub, P->tiled.hid_off.p, P->tiled.hid.p};
         l += launch_tiled_sweep<D>(P->tiled, T, P->ctrl.p, P->s);
     } else {
         l += launch_sweep<D>(P->nb, P->sweep_args(), P->level_ptr.p, P->ctrl.p, P->s);
@@ -302,7 +302,7 @@ template <int D> static void porous_phase(mtsph_porous *P, int phase, int arg, d
         const int64_t t0 = t.colour_ptr[c], t1 = t.colour_ptr[c + 1];
         if (t1 > t0) {
             TiledArgs T{t.range_off.p, t.ranges.p, t.halo_n.p, t.pair_off.p, t.pairs.p, t.pd.p, t.sub_off.p,
-                        t.sub.p, P->inv_mix.p, P->V.p, t.maxsub};
+                        t.sub.p, P->inv_mix.p, P->V.p, t.maxsub, t.hid_off.p, t.hid.p};
             k_sweep_tiled<D><<<(unsigned)(t1 - t0), t.threads, tiled_smem_bytes(t, D), s>>>(T, t0, dir, P->ctrl.p);
         }
         break;
