@@ -265,8 +265,8 @@ template <int G, int K> __device__ __forceinline__ void group_sum(double (&v)[K]
 }
 
 // dF/dt gather + F update (the split path: the return map runs in k_solid_rmap)
-template <int D, int G, bool C16 = false, bool MAG = false>
-__global__ void __launch_bounds__(256, MTSPH_STRESS_CTAS) k_solid_stress_csr(SolidArgs A) {
+template <int D, int G, bool C16 = false, bool MAG = false, int TW = 1, int NP = 1>
+__global__ void __launch_bounds__(256 * TW, TW == 1 ? MTSPH_STRESS_CTAS : 1) k_solid_stress_csr(SolidArgs A) {
     using V_t = typename VT<D>::T;
     const Ctrl *c = A.ctrl;
     if (c->done) return;
@@ -274,8 +274,8 @@ __global__ void __launch_bounds__(256, MTSPH_STRESS_CTAS) k_solid_stress_csr(Sol
     const int64_t n = A.n;
     const int sub = threadIdx.x % G;
     const V_t *V = reinterpret_cast<const V_t *>(A.V);
-    for (int it = 0; it < G; ++it) {
-        const int64_t i = (int64_t)blockIdx.x * 256 + it * (256 / G) + threadIdx.x / G;
+    for (int it = 0; it < G * NP; ++it) {
+        const int64_t i = (int64_t)blockIdx.x * (256 * TW * NP) + it * (256 * TW / G) + threadIdx.x / G;
         const bool act = i < n && !(A.flags[i] & FL_GHOST);  // uniform over the G lanes
         double acc[D * D];
 #pragma unroll
@@ -327,8 +327,12 @@ __global__ void __launch_bounds__(256, MTSPH_STRESS_CTAS) k_solid_stress_csr(Sol
 }
 
 // a = 1/rho0 sum_b V_b (T_a + T_b) gradW, v += dt/2 a, E_k and |a|max partials
-template <int D, int G, bool C16 = false, bool MAG = false>
-__global__ void __launch_bounds__(256, MTSPH_ACCEL_CTAS) k_solid_accel_csr(SolidArgs A) {
+// TW: 1 = a 256-thread CTA works through its 256 particles 64 at a time (three
+// such CTAs per SM, from blocks far apart); 3 = one 768-thread CTA per SM
+// works through 768 particles 192 consecutive ones at a time, so the
+// particles in flight on an SM are one compact neighbourhood in its L1
+template <int D, int G, bool C16 = false, bool MAG = false, int TW = 1, int NP = 1>
+__global__ void __launch_bounds__(256 * TW, TW == 1 ? MTSPH_ACCEL_CTAS : 1) k_solid_accel_csr(SolidArgs A) {
     using V_t = typename VT<D>::T;
     __shared__ double sh[32];
     const Ctrl *c = A.ctrl;
@@ -337,8 +341,8 @@ __global__ void __launch_bounds__(256, MTSPH_ACCEL_CTAS) k_solid_accel_csr(Solid
     const int64_t n = A.n;
     const int sub = threadIdx.x % G;
     double ek = 0.0, a2m = 0.0;
-    for (int it = 0; it < G; ++it) {
-        const int64_t i = (int64_t)blockIdx.x * 256 + it * (256 / G) + threadIdx.x / G;
+    for (int it = 0; it < G * NP; ++it) {
+        const int64_t i = (int64_t)blockIdx.x * (256 * TW * NP) + it * (256 * TW / G) + threadIdx.x / G;
         const bool act = i < n && !(A.flags[i] & FL_GHOST);
         // sum_b V_b (T_a + T_b) gradW = sum_b T~_b gradW + T_a G_a, with
         // T~_b = V_b T_b from the divergence record (three 256-bit loads per
@@ -403,11 +407,17 @@ __global__ void __launch_bounds__(256, MTSPH_ACCEL_CTAS) k_solid_accel_csr(Solid
             }
         }
     }
-    const double se = block_sum<256>(ek, sh);
-    const double sa = block_max<256>(a2m, sh);
-    if (threadIdx.x == 0) {
-        A.part[blockIdx.x] = se;
-        A.part[A.nblk + blockIdx.x] = sa;
+    const double se = block_sum<256 * TW>(ek, sh);
+    const double sa = block_max<256 * TW>(a2m, sh);
+    // a wide CTA covers TW NP of the 256-particle blocks the partial rows are
+    // laid out for: its sums go to the first of their slots, zeros to the rest
+    // (the control kernel reduces all nblk slots)
+    if (threadIdx.x < TW * NP) {
+        const int64_t slot = (int64_t)blockIdx.x * (TW * NP) + threadIdx.x;
+        if (slot < A.nblk) {
+            A.part[slot] = threadIdx.x == 0 ? se : 0.0;
+            A.part[A.nblk + slot] = threadIdx.x == 0 ? sa : 0.0;
+        }
     }
 }
 

@@ -235,6 +235,9 @@ struct mtsph_solid {
     // Measured (10M, 3D): SELL 7.4 + 10.0 ms, G=2 5.8 + 7.4, G=4 5.8 + 7.3,
     // G=8 6.9 + 8.7 (stress + accel); MTSPH_GATHER_LANES overrides
     int gather_g = 4;
+    // passes per wide gather CTA (0: the 256-thread kernels); set at setup from
+    // the particle count, MTSPH_ACCEL_WIDE / MTSPH_STRESS_WIDE override (0, 2, 4, 8 / 0, 4)
+    int accel_np = 0, stress_np = 0;
     // 3D fp64 opt-in (MTSPH_GATHER_WINDOW=1): shared-memory cell-window
     // gathers (window.cuh; measured slower than the CSR gathers)
     WinSched win;
@@ -335,7 +338,8 @@ template <int D> static int launch_stress_gather(mtsph_solid *S, const SolidArgs
         return 1;
     }
     const bool c16 = S->nb.chunk_g == S->gather_g && S->gather_g > 0;
-    if (S->gather_g == 4 && c16 && A.mag16) k_solid_stress_csr<D, 4, true, true><<<nb, 256, 0, s>>>(A);
+    if (S->gather_g == 4 && c16 && A.mag16 && S->stress_np == 4) k_solid_stress_csr<D, 4, true, true, 4, 4><<<(unsigned)((S->n + 4095) / 4096), 1024, 0, s>>>(A);
+    else if (S->gather_g == 4 && c16 && A.mag16) k_solid_stress_csr<D, 4, true, true><<<nb, 256, 0, s>>>(A);
     else if (S->gather_g == 4 && c16) k_solid_stress_csr<D, 4, true><<<nb, 256, 0, s>>>(A);
     else if (S->gather_g == 2 && c16) k_solid_stress_csr<D, 2, true><<<nb, 256, 0, s>>>(A);
     else if (S->gather_g == 4) k_solid_stress_csr<D, 4><<<nb, 256, 0, s>>>(A);
@@ -360,7 +364,14 @@ template <int D> static int launch_accel_gather(mtsph_solid *S, const SolidArgs 
     }
     const bool c16 = S->nb.chunk_g == S->gather_g && S->gather_g > 0;
     // (the stored gradient magnitudes cost the divergence gather registers: 5.27 -> 5.45 ms)
-    if (S->gather_g == 4 && c16) k_solid_accel_csr<D, 4, true><<<nb, 256, 0, s>>>(A);
+    // large problems: one 768-thread CTA per SM working through 768 NP
+    // particles 192 consecutive ones at a time (gather_csr.cuh); accel_np is
+    // chosen at setup so that the grid still has several waves
+    const int anp = S->accel_np;
+    if (S->gather_g == 4 && c16 && anp == 8) k_solid_accel_csr<D, 4, true, false, 3, 8><<<(unsigned)((S->n + 6143) / 6144), 768, 0, s>>>(A);
+    else if (S->gather_g == 4 && c16 && anp == 4) k_solid_accel_csr<D, 4, true, false, 3, 4><<<(unsigned)((S->n + 3071) / 3072), 768, 0, s>>>(A);
+    else if (S->gather_g == 4 && c16 && anp == 2) k_solid_accel_csr<D, 4, true, false, 3, 2><<<(unsigned)((S->n + 1535) / 1536), 768, 0, s>>>(A);
+    else if (S->gather_g == 4 && c16) k_solid_accel_csr<D, 4, true><<<nb, 256, 0, s>>>(A);
     else if (S->gather_g == 2 && c16) k_solid_accel_csr<D, 2, true><<<nb, 256, 0, s>>>(A);
     else if (S->gather_g == 4) k_solid_accel_csr<D, 4><<<nb, 256, 0, s>>>(A);
     else if (S->gather_g == 8) k_solid_accel_csr<D, 8><<<nb, 256, 0, s>>>(A);
@@ -641,6 +652,25 @@ extern "C" mtsph_status mtsph_solid_create(const mtsph_solid_desc *dsc, mtsph_so
     MT_LAUNCH_CHECK();
     S->part.alloc((size_t)3 * S->nblk);
     S->part.zero(S->s);
+    if (d == 3 && S->gather_g == 4) {
+        // wide gather CTAs need several waves of them: >= 8 CTAs per SM
+        int dev = 0, sms = 0;
+        MT_CUDA(cudaGetDevice(&dev));
+        MT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        const int64_t per_sm = n / std::max(sms, 1);
+        S->accel_np = per_sm >= 8 * 6144 ? 8 : per_sm >= 8 * 3072 ? 4 : per_sm >= 8 * 1536 ? 2 : 0;
+        S->stress_np = per_sm >= 8 * 4096 ? 4 : 0;
+        if (const char *e = std::getenv("MTSPH_ACCEL_WIDE")) {
+            const int v = std::atoi(e);
+            if (v != 0 && v != 2 && v != 4 && v != 8) throw Error(MTSPH_ERR_ARG, "MTSPH_ACCEL_WIDE: 0, 2, 4 or 8");
+            S->accel_np = v;
+        }
+        if (const char *e = std::getenv("MTSPH_STRESS_WIDE")) {
+            const int v = std::atoi(e);
+            if (v != 0 && v != 4) throw Error(MTSPH_ERR_ARG, "MTSPH_STRESS_WIDE: 0 or 4");
+            S->stress_np = v;
+        }
+    }
     S->meas.alloc((size_t)5 * S->nblk);
     if (S->nb.sweep == 1) {
         S->level_ptr.upload(S->nb.level_ptr_h.data(), S->nb.level_ptr_h.size(), S->s);

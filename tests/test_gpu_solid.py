@@ -87,6 +87,17 @@ def test_necking_trajectory_index_table_modes(gold_traj, prefix, knob, monkeypat
     _check_trajectory(gold_traj, prefix)
 
 
+def test_necking_trajectory_wide_gather_ctas(gold_traj, monkeypatch):
+    """The wide gather CTAs large problems use (768 / 1024 threads working
+    through consecutive particles, several passes per CTA; forced here on the
+    small 3D bar): the same 100-step bar, including E_k and the step size
+    from their block partials."""
+    monkeypatch.delenv("MTSPH_GATHER_LANES", raising=False)
+    monkeypatch.setenv("MTSPH_ACCEL_WIDE", "8")
+    monkeypatch.setenv("MTSPH_STRESS_WIDE", "4")
+    _check_trajectory(gold_traj, "n3_")
+
+
 def test_stored_gradient_magnitudes_are_bit_identical(gold_traj, monkeypatch):
     """The stored kernel-gradient magnitudes come from the function the
     gather would call (grad_mag), so the dF/dt gather that reads them gives
